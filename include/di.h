@@ -1,0 +1,150 @@
+/* include/di.h — C ABI of the B200-native D-iteration library (libdi.so).
+ *
+ * What it computes. The fixed point X = P.X + B of PAPER.md §1 for the
+ * PageRank instantiation of §2.5: for every link i -> j of the link list,
+ * P_ji = d / #out_i (#out_i counts every listed link of i, duplicates included),
+ * dangling columns (#out_i = 0) are zero, and a node with k self-loop copies folds its
+ * self-return series (generalised to k copies: DESIGN.md reading G6).
+ * The solver is the D-iteration fluid diffusion (§2.5.4 DI-CYC P:249-284, §2.5.5 DI-SOP
+ * P:286-299) reformulated as bulk-synchronous frontier sweeps (R1): it reaches
+ * the same fixed point as the paper's sequential loop, not bit-identical iterates.
+ *
+ * Conventions.
+ *  - Every call returns di_status; DI_OK = 0, positive = warning with a valid state,
+ *    negative = error (the handle is unchanged unless stated). di_last_error() returns a
+ *    thread-local message for the last failure.
+ *  - Pointers are device pointers unless a flag or the argument says "host".
+ *  - The library never frees caller memory; a di_graph owns every device buffer it
+ *    allocates, released by di_graph_free.
+ *  - One handle per stream; calls on one handle are not thread-safe. All work is enqueued
+ *    on the handle's stream; di_solve/di_residual/di_history/di_stats_* block until their
+ *    results are available on the host.
+ *  - There is no CPU fallback: a missing or unusable CUDA device yields DI_ECUDA.
+ */
+#ifndef DI_H
+#define DI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct di_graph_s *di_graph;  /* opaque */
+
+typedef enum {
+  DI_OK = 0,
+  DI_NOT_CONVERGED = 1, /* max_sweeps reached; state (F, H) valid and resumable */
+  DI_EINVAL = -1,       /* bad argument (range, id out of [0,n), d not in (0,1), tol <= 0 ...) */
+  DI_ENOMEM = -2,       /* device allocation failed */
+  DI_ECUDA = -3,        /* CUDA runtime error (message in di_last_error) */
+  DI_ENCCL = -4,        /* NCCL error (multi-GPU) */
+  DI_ESTATE = -5        /* call not valid in the handle's state (e.g. DI_RESUME before a solve) */
+} di_status;
+
+/* Solver variants (§2.3). */
+typedef enum {
+  DI_SOP = 0,      /* D-iteration, select F_i > r_n * #out_i / L           */
+  DI_CYC = 1,      /* D-iteration, select F_i > 0                               */
+  DI_PI_PULL = 2,  /* comparator: power iteration per row, pull over in-links      */
+  DI_PI_PUSH = 3,  /* comparator: power iteration per column, push over out-links  */
+  DI_GS_BLOCK = 4  /* comparator: Gauss-Seidel, ordered node blocks (R4)  */
+} di_variant;
+
+/* di_graph_upload flags */
+#define DI_DEDUP            0x1u  /* drop duplicate links (default keeps multiplicities)  */
+#define DI_DROP_SELF_LOOPS  0x2u  /* drop i -> i links (default folds them)            */
+#define DI_BUILD_CSC        0x4u  /* also build the in-link (CSC) index: pull variant, PI, GS     */
+#define DI_HOST_PTRS        0x8u  /* src/dst are host pointers (copied inside the call)           */
+#define DI_LOCAL_LINKS      0x10u /* multi-GPU: each rank passes only links whose src it owns     */
+
+/* di_solve flags */
+#define DI_PUSH         0x0u   /* push-only sweeps (default)                                       */
+#define DI_PULL         0x1u   /* pull (CSC) sweeps for every sweep (needs DI_BUILD_CSC)           */
+#define DI_AUTO         0x2u   /* per-sweep push/pull choice by predicted bytes (needs CSC)        */
+#define DI_RESUME       0x4u   /* continue from the current (F, H) instead of F = B, H = 0         */
+#define DI_PAPER_ERROR  0x8u   /* stop on sum(F)/(1-d-d*e) <= tol instead of sum(F)    */
+#define DI_TRACE        0x10u  /* record the per-sweep log read by di_sweep_log                    */
+#define DI_PROFILE      0x20u  /* time every kernel with CUDA events (fills *_ms fields)           */
+#define DI_GRAPH_LOOP   0x40u  /* run the sweep loop as one CUDA graph with a device-side while    */
+
+typedef struct {
+  int64_t sweeps;               /* bulk sweeps executed (incl. starvation fallbacks)            */
+  int64_t selected_total;       /* sum over sweeps of |S_n| (diffused nodes, dangling included)  */
+  int64_t link_diffusions;      /* sum over sweeps of sum_{i in S_n} #out_i         */
+  int64_t starvation_fallbacks; /* sweeps that selected nothing and forced one DI-CYC sweep (G5) */
+  int64_t nodes_scanned;        /* sum over sweeps of nodes tested by the select kernel          */
+  int64_t pull_sweeps;          /* sweeps executed in pull (CSC) mode                            */
+  int64_t gpu_launches;         /* kernels launched by this call                                  */
+  double residual_l1;           /* ||F||_1 at exit (exact deterministic sum)                     */
+  double dangling_absorbed;     /* e = sum of transit at dangling nodes           */
+  double equivalent_iterations; /* link_diffusions / L ("nb iter")            */
+  double solve_ms;              /* CUDA-event time of the whole call on the handle's stream      */
+  double counted_bytes;         /* algorithmic bytes: all kernels          */
+  double push_bytes;            /* algorithmic bytes of the push (a5) / pull (a5') kernels       */
+  double push_ms;               /* DI_PROFILE: summed event time of the push/pull kernels        */
+  double select_ms;             /* DI_PROFILE: summed event time of the select kernels           */
+  double error_estimate;        /* sum(F)/(1-d-d*e); comparators: their own error        */
+  int64_t push_launches;        /* DI_PROFILE: push/pull launches that did work                  */
+  int32_t converged;            /* 1 if the stop test passed                                     */
+  int32_t variant;
+} di_stats;
+
+/* Multi-GPU descriptor: one process per GPU, NCCL over NVLink. */
+typedef struct {
+  int32_t rank, world;
+  const void *nccl_unique_id; /* 128-byte ncclUniqueId, identical on every rank (host pointer) */
+} di_dist;
+
+/* Build the device graph (§2.1, "Init" timed separately).
+ *  src, dst : n_links int32 node ids of the links src[k] -> dst[k]; device pointers, or host
+ *             pointers with DI_HOST_PTRS. Any order; caller keeps ownership.
+ *  n_links  : >= 0.   n_nodes : in [1, 2^31 - 1].
+ *  stream   : cudaStream_t the handle will use (NULL = legacy default stream).
+ *  dist     : NULL for one GPU; otherwise every rank calls collectively and owns the node range
+ *             returned by di_graph_range (edge-balanced 1-D partition).
+ * Layout built in HBM: CSR row_ptr int64[n+1], col int32[L] sorted by (src, dst); deg int32[n];
+ * kloop int32[n] (self-loop multiplicity); optional CSC (col_ptr int64[n+1], row int32[L]).
+ * Errors: DI_EINVAL (sizes, an id outside [0, n): the message names the first bad index),
+ * DI_ENOMEM, DI_ECUDA, DI_ENCCL. On error *out is NULL. */
+di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_links, int64_t n_nodes,
+                          uint32_t flags, void *stream, const di_dist *dist, di_graph *out);
+
+/* Node slice [lo, hi) owned by this rank ([0, n) on one GPU). */
+di_status di_graph_range(di_graph g, int64_t *lo, int64_t *hi);
+
+/* Number of links kept after DI_DEDUP / DI_DROP_SELF_LOOPS (this rank's links on multi-GPU). */
+di_status di_graph_links(di_graph g, int64_t *n_links);
+
+/* Solve X = P.X + B (§1) by D-iteration sweeps until ||F||_1 <= tol (BASELINE
+ * north_star; or the paper's error with DI_PAPER_ERROR), or max_sweeps.
+ *  d  : damping in (0, 1) (PAPER.md leaves it unstated: reading G1).
+ *  B  : NULL -> uniform (1 - d)/N; else device pointer to this rank's slice, B >= 0.
+ *  v  : DI_SOP / DI_CYC (the hot path) or a comparator (DI_PI_PULL, DI_PI_PUSH, DI_GS_BLOCK;
+ *       for those tol bounds the scheme's own error estimate, P:176-180 / P:237-245, and
+ *       di_history returns their x: normalised for PI, raw for GS).
+ *  st : host pointer, filled on return (may be NULL).
+ * Returns DI_OK, DI_NOT_CONVERGED (state kept; DI_RESUME continues), or an error. */
+di_status di_solve(di_graph g, double d, const double *B, double tol, di_variant v,
+                   int64_t max_sweeps, uint32_t flags, di_stats *st);
+
+/* ||F||_1 of the current state (exact deterministic tree sum) into *l1_out (host); if F_out
+ * is not NULL, also copy this rank's F slice into it (device pointer). */
+di_status di_residual(di_graph g, double *l1_out, double *F_out);
+
+/* Copy this rank's history H (raw estimate of X) into H_out (device pointer). */
+di_status di_history(di_graph g, double *H_out);
+
+/* Per-sweep log of the last DI_TRACE solve (SPEC S:157 error_history): r_n (sum F at sweep
+ * start as used by the threshold), |S_n|, links(S_n), mode (0 push, 1 pull). Host arrays of
+ * capacity cap (any may be NULL); *n_out = sweeps logged (<= cap). */
+di_status di_sweep_log(di_graph g, double *r, int64_t *selected, int64_t *links, uint8_t *mode,
+                       int64_t cap, int64_t *n_out);
+
+di_status di_graph_free(di_graph g);
+const char *di_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DI_H */

@@ -1,0 +1,39 @@
+/* include/di_test.h — test-only exports of libdi.so (not part of the product ABI).
+ * They expose internal steps so that tests can check them bit for bit.
+ */
+#ifndef DI_TEST_H
+#define DI_TEST_H
+
+#include "di.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Run only the select/compact step (SURVEY §8(a) a3+a4: P:258/P:298 test, P:259-267 update)
+ * on a caller snapshot F_in, H_in (host, this rank's n entries) with a frozen threshold fluid r.
+ * Outputs (host):
+ *   ids/vals/chunk : frontier entries in bin order [T | G | W | C], ascending node id inside a
+ *                    bin; C entries repeat the node once per kChunk-link chunk, chunk = index.
+ *                    vals = T_i*d/#out_i. Capacity `cap` entries (DI_EINVAL if too small).
+ *   bin_off[5]     : bin boundaries in the concatenated arrays.
+ *   scal[3]        : q (sum unselected F), s (sum T*d*(#out-k)/#out), e (dangling transit).
+ *   counts[2]      : |S| (selected, dangling included), links(S).
+ *   F_out, H_out   : state after the step (host, n entries each).
+ * Leaves the handle's F and H set to F_out and H_out. */
+di_status di_test_select(di_graph g, const double *F_in, const double *H_in, double r, double d,
+                         di_variant v, int32_t *ids, double *vals, int32_t *chunk, int64_t cap,
+                         int64_t bin_off[5], double scal[3], int64_t counts[2], double *F_out,
+                         double *H_out);
+
+/* Copy the device CSR (and CSC if built) to host arrays (each may be NULL). */
+di_status di_test_csr(di_graph g, int64_t *row_ptr, int32_t *col, int32_t *deg, int32_t *kloop,
+                      int64_t *csc_ptr, int32_t *csc_row);
+
+/* Bin thresholds compiled into the library: out[0..3] = kBinT, kBinG, kBinW, kChunk. */
+di_status di_test_bins(int32_t out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,418 @@
+// api.cu — C ABI of libdi.so (include/di.h, include/di_test.h): handle management and the
+// host side of the sweep loop. The loop enqueues sweeps in batches without reading anything
+// back in between; the device finaliser decides convergence and later
+// kernels no-op, so the host only synchronises once per batch.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/di.h"
+#include "../../include/di_test.h"
+#include "di_common.cuh"
+
+namespace di {
+
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+
+namespace {
+
+__global__ void k_check_B(const double *B, int64_t n, int *bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double b = B[i];
+    if (!(b >= 0.0) || !isfinite(b)) *bad = 1;
+  }
+}
+
+di_status fail(di_status s, const std::string &msg) {
+  set_error(msg);
+  return s;
+}
+
+struct EventSet {
+  std::vector<cudaEvent_t> ev;
+  ~EventSet() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  cudaEvent_t get(size_t i) {
+    while (ev.size() <= i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    return ev[i];
+  }
+};
+
+void free_graph(Graph *g) {
+  if (!g) return;
+  void *ptrs[] = {g->row_ptr, g->col, g->deg, g->kloop, g->csc_ptr, g->csc_row, g->F, g->H,
+                  g->S, g->aux, g->sc, g->partials, g->red_partials, g->tile_flag, g->tile_agg,
+                  g->tile_incl, g->fr.chunk, g->log_r, g->log_sel, g->log_links, g->log_mode};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  for (int b = 0; b < kBins; b++) {
+    if (g->fr.ids[b]) cudaFree(g->fr.ids[b]);
+    if (g->fr.val[b]) cudaFree(g->fr.val[b]);
+  }
+  if (g->sc_host) cudaFreeHost(g->sc_host);
+  delete g;
+}
+
+di_status sync_scalars(Graph &g) {
+  DI_CK(cudaMemcpyAsync(g.sc_host, g.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, g.stream));
+  DI_CK(cudaStreamSynchronize(g.stream));
+  return DI_OK;
+}
+
+}  // namespace
+}  // namespace di
+
+using namespace di;
+
+extern "C" {
+
+const char *di_last_error(void) { return g_err.c_str(); }
+
+di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_links, int64_t n_nodes,
+                          uint32_t flags, void *stream, const di_dist *dist, di_graph *out) {
+  if (!out) return fail(DI_EINVAL, "di_graph_upload: out is NULL");
+  *out = nullptr;
+  if (n_nodes < 1 || n_nodes > 2147483647LL)
+    return fail(DI_EINVAL, "di_graph_upload: n_nodes must be in [1, 2^31-1]");
+  if (n_links < 0) return fail(DI_EINVAL, "di_graph_upload: n_links < 0");
+  if (n_links > 0 && (!src || !dst)) return fail(DI_EINVAL, "di_graph_upload: NULL src/dst");
+  if (dist && dist->world > 1)
+    return fail(DI_EINVAL, "di_graph_upload: multi-GPU handles are not available in this build");
+  int dev = 0, ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(DI_ECUDA, "di_graph_upload: no CUDA device");
+  DI_CK(cudaGetDevice(&dev));
+  Graph *g = new Graph();
+  g->device = dev;
+  g->stream = (cudaStream_t)stream;
+  cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  g->n = g->n_global = n_nodes;
+  g->lo = 0;
+  g->hi = n_nodes;
+  di_status s = build_graph(*g, src, dst, n_links, flags);
+  if (s == DI_OK) s = alloc_state(*g);
+  if (s != DI_OK) {
+    free_graph(g);
+    return s;
+  }
+  *out = (di_graph)g;
+  return DI_OK;
+}
+
+di_status di_graph_range(di_graph h, int64_t *lo, int64_t *hi) {
+  Graph *g = (Graph *)h;
+  if (!g) return fail(DI_EINVAL, "NULL handle");
+  if (lo) *lo = g->lo;
+  if (hi) *hi = g->hi;
+  return DI_OK;
+}
+
+di_status di_graph_links(di_graph h, int64_t *n_links) {
+  Graph *g = (Graph *)h;
+  if (!g || !n_links) return fail(DI_EINVAL, "NULL argument");
+  *n_links = g->l;
+  return DI_OK;
+}
+
+di_status di_graph_free(di_graph h) {
+  Graph *g = (Graph *)h;
+  if (!g) return DI_OK;
+  cudaStreamSynchronize(g->stream);
+  free_graph(g);
+  return DI_OK;
+}
+
+di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant v,
+                   int64_t max_sweeps, uint32_t flags, di_stats *st) {
+  Graph *gp = (Graph *)h;
+  if (!gp) return fail(DI_EINVAL, "di_solve: NULL handle");
+  Graph &g = *gp;
+  if (!(d > 0.0 && d < 1.0)) return fail(DI_EINVAL, "di_solve: d must be in (0, 1)");
+  if (!(tol > 0.0) || !std::isfinite(tol)) return fail(DI_EINVAL, "di_solve: tol must be > 0");
+  if (max_sweeps < 0) return fail(DI_EINVAL, "di_solve: max_sweeps < 0");
+  if ((int)v < 0 || (int)v > DI_GS_BLOCK) return fail(DI_EINVAL, "di_solve: bad variant");
+  if (B) {
+    int *bad = nullptr;
+    DI_CK(cudaMalloc(&bad, 4));
+    DI_CK(cudaMemsetAsync(bad, 0, 4, g.stream));
+    k_check_B<<<std::max<int64_t>(1, std::min<int64_t>((g.n + 255) / 256, 4096)), 256, 0,
+                g.stream>>>(B, g.n, bad);
+    int hb = 0;
+    DI_CK(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, g.stream));
+    DI_CK(cudaStreamSynchronize(g.stream));
+    cudaFree(bad);
+    if (hb) return fail(DI_EINVAL, "di_solve: B has a negative or non-finite entry");
+  }
+  if (v == DI_PI_PULL || v == DI_PI_PUSH || v == DI_GS_BLOCK)
+    return run_comparator(g, d, tol, (int)v, max_sweeps, flags, st);
+  if (flags & (DI_PULL | DI_AUTO))
+    return fail(DI_EINVAL, "di_solve: pull sweeps are not available in this build");
+  const bool resume = flags & DI_RESUME;
+  if (resume && !g.solved) return fail(DI_ESTATE, "di_solve: DI_RESUME before any solve");
+  const int paper = (flags & DI_PAPER_ERROR) ? 1 : 0;
+  const int trace = (flags & DI_TRACE) ? 1 : 0;
+  const bool prof = flags & DI_PROFILE;
+
+  int64_t launches = 0;
+  cudaEvent_t t0, t1;
+  DI_CK(cudaEventCreate(&t0));
+  DI_CK(cudaEventCreate(&t1));
+  EventSet evs;
+
+  // fresh device scalars (the epoch keeps increasing across solves)
+  {
+    Scalars &s = *g.sc_host;
+    const uint32_t epoch = s.epoch ? s.epoch : 1;
+    const double e_prev = s.e;
+    memset(&s, 0, sizeof(Scalars));
+    s.epoch = epoch;
+    s.e = resume ? e_prev : 0.0;
+  }
+  DI_CK(cudaEventRecord(t0, g.stream));
+  DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
+  if (!resume)
+    launch_init(g, B, d, &launches);
+  else
+    launch_reduce_F_setr(g, &launches);
+  di_status s = sync_scalars(g);
+  if (s != DI_OK) return s;
+  auto err_of = [&](double r, double e) { return paper ? r / (1.0 - d - d * e) : r; };
+  bool converged = err_of(g.sc_host->r, g.sc_host->e) <= tol;
+  double resid = g.sc_host->r;
+  int64_t launched = 0;
+  int64_t K = 4;
+  double push_ms = 0.0, select_ms = 0.0;
+  int64_t push_launches = 0;
+  double r_prev = g.sc_host->r;
+  while (!converged && launched < max_sweeps) {
+    const int64_t k = std::min<int64_t>(K, max_sweeps - launched);
+    const int64_t sweeps_before = g.sc_host->sweeps;
+    for (int64_t j = 0; j < k; j++) {
+      if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 0), g.stream));
+      launch_select(g, d, tol, (int)v, paper, trace, 0, &launches);
+      if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 1), g.stream));
+      launch_push(g, &launches);
+      if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 2), g.stream));
+    }
+    launched += k;
+    s = sync_scalars(g);
+    if (s != DI_OK) return s;
+    DI_CK(cudaGetLastError());
+    const int64_t real = g.sc_host->sweeps - sweeps_before;
+    if (prof) {
+      for (int64_t j = 0; j < real && j < k; j++) {
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, evs.get(4 * j + 0), evs.get(4 * j + 1));
+        cudaEventElapsedTime(&b, evs.get(4 * j + 1), evs.get(4 * j + 2));
+        select_ms += a;
+        push_ms += b;
+        push_launches++;
+      }
+    }
+    if (g.sc_host->stop) {
+      launch_reduce_F(g, &launches);
+      s = sync_scalars(g);
+      if (s != DI_OK) return s;
+      resid = g.sc_host->resid;
+      if (err_of(resid, g.sc_host->e) <= tol) {
+        converged = true;
+        break;
+      }
+      // prediction q+s said converged but the exact sum disagrees by rounding: continue
+      const int32_t zero = 0;
+      DI_CK(cudaMemcpyAsync(&g.sc->stop, &zero, 4, cudaMemcpyHostToDevice, g.stream));
+      g.sc_host->stop = 0;
+    }
+    // batch size: predicted sweeps left from the observed decay rate of r
+    const double r_now = g.sc_host->r;
+    int64_t next = 8;
+    if (real > 0 && r_now > 0.0 && r_prev > r_now) {
+      const double rate = std::pow(r_now / r_prev, 1.0 / (double)real);
+      const double target = paper ? tol * (1.0 - d) : tol;
+      if (rate < 1.0 && rate > 0.0) {
+        const double left = std::log(target / r_now) / std::log(rate);
+        next = (int64_t)std::ceil(std::max(1.0, left));
+      }
+    }
+    K = std::max<int64_t>(1, std::min<int64_t>(next, 32));
+    r_prev = r_now;
+  }
+  if (!converged || launched == 0) {
+    launch_reduce_F(g, &launches);
+    s = sync_scalars(g);
+    if (s != DI_OK) return s;
+    resid = g.sc_host->resid;
+    converged = err_of(resid, g.sc_host->e) <= tol;
+  }
+  DI_CK(cudaEventRecord(t1, g.stream));
+  DI_CK(cudaEventSynchronize(t1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  DI_CK(cudaGetLastError());
+  g.solved = true;
+  g.last_d = d;
+  g.log_n = std::min<int64_t>(g.sc_host->sweeps, kLogCap);
+  if (st) {
+    const Scalars &c = *g.sc_host;
+    memset(st, 0, sizeof(*st));
+    st->sweeps = c.sweeps;
+    st->selected_total = c.selected_total;
+    st->link_diffusions = c.links_total;
+    st->starvation_fallbacks = c.guards;
+    st->nodes_scanned = c.scanned_total;
+    st->pull_sweeps = c.pull_sweeps;
+    st->gpu_launches = launches;
+    st->residual_l1 = resid;
+    st->dangling_absorbed = c.e;
+    st->equivalent_iterations = g.l_global > 0 ? (double)c.links_total / (double)g.l_global : 0.0;
+    st->solve_ms = ms;
+    // algorithmic bytes
+    st->counted_bytes = 12.0 * c.scanned_total + 40.0 * c.selected_total + 20.0 * c.links_total;
+    st->push_bytes = 16.0 * c.selected_nd_total + 20.0 * c.links_total;
+    st->push_ms = push_ms;
+    st->select_ms = select_ms;
+    st->push_launches = push_launches;
+    st->error_estimate = resid / (1.0 - d - d * c.e);
+    st->converged = converged ? 1 : 0;
+    st->variant = (int32_t)v;
+  }
+  return converged ? DI_OK : DI_NOT_CONVERGED;
+}
+
+di_status di_residual(di_graph h, double *l1_out, double *F_out) {
+  Graph *g = (Graph *)h;
+  if (!g) return fail(DI_EINVAL, "di_residual: NULL handle");
+  int64_t launches = 0;
+  launch_reduce_F(*g, &launches);
+  di_status s = sync_scalars(*g);
+  if (s != DI_OK) return s;
+  if (l1_out) *l1_out = g->sc_host->resid;
+  if (F_out) {
+    DI_CK(cudaMemcpyAsync(F_out, g->F, (size_t)g->n * 8, cudaMemcpyDeviceToDevice, g->stream));
+    DI_CK(cudaStreamSynchronize(g->stream));
+  }
+  return DI_OK;
+}
+
+di_status di_history(di_graph h, double *H_out) {
+  Graph *g = (Graph *)h;
+  if (!g || !H_out) return fail(DI_EINVAL, "di_history: NULL argument");
+  DI_CK(cudaMemcpyAsync(H_out, g->H, (size_t)g->n * 8, cudaMemcpyDeviceToDevice, g->stream));
+  DI_CK(cudaStreamSynchronize(g->stream));
+  return DI_OK;
+}
+
+di_status di_sweep_log(di_graph h, double *r, int64_t *selected, int64_t *links, uint8_t *mode,
+                       int64_t cap, int64_t *n_out) {
+  Graph *g = (Graph *)h;
+  if (!g) return fail(DI_EINVAL, "di_sweep_log: NULL handle");
+  const int64_t n = std::min<int64_t>(g->log_n, std::max<int64_t>(cap, 0));
+  if (n > 0) {
+    if (r) DI_CK(cudaMemcpy(r, g->log_r, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    if (selected) DI_CK(cudaMemcpy(selected, g->log_sel, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    if (links) DI_CK(cudaMemcpy(links, g->log_links, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    if (mode) DI_CK(cudaMemcpy(mode, g->log_mode, (size_t)n, cudaMemcpyDeviceToHost));
+  }
+  if (n_out) *n_out = n;
+  return DI_OK;
+}
+
+// ------------------------------------------------------------------ test exports
+di_status di_test_bins(int32_t out[4]) {
+  if (!out) return fail(DI_EINVAL, "NULL");
+  out[0] = kBinT;
+  out[1] = kBinG;
+  out[2] = kBinW;
+  out[3] = kChunk;
+  return DI_OK;
+}
+
+di_status di_test_csr(di_graph h, int64_t *row_ptr, int32_t *col, int32_t *deg, int32_t *kloop,
+                      int64_t *csc_ptr, int32_t *csc_row) {
+  Graph *g = (Graph *)h;
+  if (!g) return fail(DI_EINVAL, "NULL handle");
+  const size_t n = (size_t)g->n, l = (size_t)g->l;
+  if (row_ptr) DI_CK(cudaMemcpy(row_ptr, g->row_ptr, (n + 1) * 8, cudaMemcpyDeviceToHost));
+  if (col && l) DI_CK(cudaMemcpy(col, g->col, l * 4, cudaMemcpyDeviceToHost));
+  if (deg) DI_CK(cudaMemcpy(deg, g->deg, n * 4, cudaMemcpyDeviceToHost));
+  if (kloop) DI_CK(cudaMemcpy(kloop, g->kloop, n * 4, cudaMemcpyDeviceToHost));
+  if (csc_ptr || csc_row) {
+    if (!g->has_csc) return fail(DI_ESTATE, "di_test_csr: CSC not built (DI_BUILD_CSC)");
+    if (csc_ptr) DI_CK(cudaMemcpy(csc_ptr, g->csc_ptr, (n + 1) * 8, cudaMemcpyDeviceToHost));
+    if (csc_row && l) DI_CK(cudaMemcpy(csc_row, g->csc_row, l * 4, cudaMemcpyDeviceToHost));
+  }
+  return DI_OK;
+}
+
+di_status di_test_select(di_graph h, const double *F_in, const double *H_in, double r, double d,
+                         di_variant v, int32_t *ids, double *vals, int32_t *chunk, int64_t cap,
+                         int64_t bin_off[5], double scal[3], int64_t counts[2], double *F_out,
+                         double *H_out) {
+  Graph *gp = (Graph *)h;
+  if (!gp || !F_in || !H_in) return fail(DI_EINVAL, "di_test_select: NULL argument");
+  if (v != DI_SOP && v != DI_CYC) return fail(DI_EINVAL, "di_test_select: DI_SOP or DI_CYC");
+  Graph &g = *gp;
+  const size_t n = (size_t)g.n;
+  DI_CK(cudaMemcpy(g.F, F_in, n * 8, cudaMemcpyHostToDevice));
+  DI_CK(cudaMemcpy(g.H, H_in, n * 8, cudaMemcpyHostToDevice));
+  {
+    Scalars &s = *g.sc_host;
+    const uint32_t epoch = s.epoch ? s.epoch : 1;
+    memset(&s, 0, sizeof(Scalars));
+    s.epoch = epoch;
+    s.r = r;
+  }
+  DI_CK(cudaMemcpy(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice));
+  int64_t launches = 0;
+  launch_select(g, d, 1e300, (int)v, 0, 0, 1, &launches);
+  di_status s = sync_scalars(g);
+  if (s != DI_OK) return s;
+  DI_CK(cudaGetLastError());
+  const Scalars &c = *g.sc_host;
+  int64_t off = 0;
+  for (int b = 0; b < kBins; b++) {
+    if (bin_off) bin_off[b] = off;
+    off += c.bin_count[b];
+  }
+  if (bin_off) bin_off[kBins] = off;
+  if (off > cap) return fail(DI_EINVAL, "di_test_select: cap too small");
+  off = 0;
+  for (int b = 0; b < kBins; b++) {
+    const size_t m = (size_t)c.bin_count[b];
+    if (m) {
+      if (ids) DI_CK(cudaMemcpy(ids + off, g.fr.ids[b], m * 4, cudaMemcpyDeviceToHost));
+      if (vals) DI_CK(cudaMemcpy(vals + off, g.fr.val[b], m * 8, cudaMemcpyDeviceToHost));
+      if (chunk) {
+        if (b == BIN_C)
+          DI_CK(cudaMemcpy(chunk + off, g.fr.chunk, m * 4, cudaMemcpyDeviceToHost));
+        else
+          memset(chunk + off, 0, m * 4);
+      }
+    }
+    off += (int64_t)m;
+  }
+  if (scal) {
+    scal[0] = c.q;
+    scal[1] = c.s;
+    scal[2] = c.e_sw;
+  }
+  if (counts) {
+    counts[0] = c.selected_total;
+    counts[1] = c.links_total;
+  }
+  if (F_out) DI_CK(cudaMemcpy(F_out, g.F, n * 8, cudaMemcpyDeviceToHost));
+  if (H_out) DI_CK(cudaMemcpy(H_out, g.H, n * 8, cudaMemcpyDeviceToHost));
+  return DI_OK;
+}
+
+}  // extern "C"

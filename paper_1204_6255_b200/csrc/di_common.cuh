@@ -1,0 +1,133 @@
+// di_common.cuh — internal types shared by the libdi.so translation units.
+// Product code: nothing here is shared with oracle/ (which is independent C).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/di.h"
+
+namespace di {
+
+// ----------------------------------------------------------------- tuning constants
+// Select / compact (SURVEY §8(a) a3+a4): one tile = kSelThreads x kSelItems consecutive nodes.
+constexpr int kSelThreads = 256;
+constexpr int kSelItems = 8;
+constexpr int kSelTile = kSelThreads * kSelItems;
+// Degree bins of the push (north_star item 3):
+//   T: 1..kBinT links -> one thread per node
+//   G: kBinT+1..kBinG -> 8-lane group per node
+//   W: kBinG+1..kBinW -> one warp per node
+//   C: > kBinW        -> rows split in chunks of kChunk links, one warp per chunk
+constexpr int kBins = 4;
+constexpr int kBinT = 8;
+constexpr int kBinG = 32;
+constexpr int kBinW = 1024;
+constexpr int kChunk = 1024;
+constexpr int kPushThreads = 256;
+constexpr int kRedThreads = 512;
+constexpr int kLogCap = 1 << 16;  // per-sweep trace capacity
+
+enum BinId { BIN_T = 0, BIN_G = 1, BIN_W = 2, BIN_C = 3 };
+
+// Device-resident sweep state. Every field is written only by the "last block" of the
+// select kernel (the finaliser) or by the host between solves, so kernels never race on it.
+struct Scalars {
+  double r;          // r_n: threshold fluid for the current sweep (sum F at sweep start)
+  double e;          // cumulative dangling absorption
+  double q, s, e_sw; // last sweep: unselected fluid, pushed fluid, dangling absorbed
+  double resid;      // exact sum F from the reduce kernel
+  int32_t stop;      // 1: convergence reached after the current sweep's push
+  int32_t guard;     // 1: next sweep runs with threshold 0 (starvation guard, reading G5)
+  int32_t active;    // 1: the current sweep emitted push work
+  int32_t pull;      // 1: the current sweep runs in pull mode (dense S vector)
+  uint32_t epoch;    // select-launch counter: tags look-back flags, starts at 1
+  uint32_t ticket;   // last-block detection of the select kernel
+  uint32_t tile_ctr[2];
+  uint32_t red_ticket;
+  uint32_t pad0;
+  int64_t bin_count[kBins];  // entries in each bin for the current sweep
+  int64_t sweep_sel, sweep_links, sweep_sel_nd;
+  int64_t sweeps, selected_total, selected_nd_total, links_total, scanned_total, guards,
+      pull_sweeps;
+};
+
+struct Frontier {
+  int32_t *ids[kBins];
+  double *val[kBins];   // v_i = T_i * d / #out_i (the "sent" of P:268)
+  int32_t *chunk;       // chunk index for bin C entries
+  int64_t cap[kBins];
+};
+
+struct Graph {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int64_t n = 0;          // nodes owned (== global n on one GPU)
+  int64_t n_global = 0;
+  int64_t lo = 0, hi = 0; // owned global range
+  int64_t l = 0;          // links kept (local)
+  int64_t l_global = 0;
+  bool has_loops = false;
+  bool has_csc = false;
+  int rank = 0, world = 1;
+  // CSR (sources owned), global column ids
+  int64_t *row_ptr = nullptr;
+  int32_t *col = nullptr;
+  int32_t *deg = nullptr;
+  int32_t *kloop = nullptr;
+  // CSC (in-links of owned targets)
+  int64_t *csc_ptr = nullptr;
+  int32_t *csc_row = nullptr;
+  // state
+  double *F = nullptr, *H = nullptr;
+  double *S = nullptr;       // pull mode: dense per-node sent value
+  double *aux = nullptr;     // comparators: x_new
+  Scalars *sc = nullptr;     // device
+  Scalars *sc_host = nullptr;  // pinned mirror
+  double *partials = nullptr;  // per-tile q, s, e partials (3 per tile)
+  double *red_partials = nullptr;
+  uint32_t *tile_flag = nullptr;
+  int64_t *tile_agg = nullptr, *tile_incl = nullptr;
+  Frontier fr{};
+  // trace
+  double *log_r = nullptr;
+  int64_t *log_sel = nullptr, *log_links = nullptr;
+  uint8_t *log_mode = nullptr;
+  int64_t log_n = 0;
+  bool solved = false;
+  double last_d = 0.85;
+  void *nccl = nullptr;      // ncclComm_t when world > 1
+};
+
+// ---------------------------------------------------------------- error plumbing
+void set_error(const std::string &msg);
+#define DI_CK(call)                                                                     \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      ::di::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));              \
+      return e_ == cudaErrorMemoryAllocation ? DI_ENOMEM : DI_ECUDA;                    \
+    }                                                                                   \
+  } while (0)
+
+// ---------------------------------------------------------------- launchers
+// graph_build.cu
+di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t n_links,
+                      uint32_t flags);
+// diffusion.cu
+int64_t select_tiles(int64_t n);
+di_status alloc_state(Graph &g);
+void launch_init(Graph &g, const double *B, double d, int64_t *launches);
+void launch_reduce_F(Graph &g, int64_t *launches);
+void launch_reduce_F_setr(Graph &g, int64_t *launches);
+void launch_select(Graph &g, double d, double tol, int variant, int paper_err, int trace,
+                   int test_mode, int64_t *launches);
+void launch_push(Graph &g, int64_t *launches);
+void launch_pull(Graph &g, int64_t *launches);
+// comparators.cu
+di_status run_comparator(Graph &g, double d, double tol, int variant, int64_t max_sweeps,
+                         uint32_t flags, di_stats *st);
+
+}  // namespace di

@@ -1,0 +1,51 @@
+"""Host-side checks of the C-ABI library (no GPU needed, no compute calls)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = set()
+    for h in ("di.h", "di_test.h"):
+        txt = open(os.path.join(ROOT, "include", h)).read()
+        txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+        names |= set(re.findall(r"\b(di_[a-z_0-9]+)\s*\(", txt))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    from tools import build
+    build.build()
+    lib = ctypes.CDLL(build.SO)
+    syms = declared_symbols()
+    assert {"di_graph_upload", "di_solve", "di_residual", "di_history"} <= syms
+    for s in sorted(syms):
+        assert hasattr(lib, s), s
+
+
+def test_binding_declares_all_symbols():
+    import paper_1204_6255_b200 as di
+    assert declared_symbols() == set(di.EXPORTED)
+
+
+def test_last_error_without_gpu():
+    """di_graph_upload must fail loudly (no CPU fallback) on argument errors and without a GPU."""
+    import paper_1204_6255_b200 as di
+    h = ctypes.c_void_p()
+    rc = di._lib.di_graph_upload(None, None, 0, 0, 0, None, None, ctypes.byref(h))
+    assert rc == di.DI_EINVAL and h.value is None
+    assert b"n_nodes" in di._lib.di_last_error()
+
+
+def test_no_oracle_in_product():
+    """The product package never imports or links the oracle (independence rule)."""
+    pkg = os.path.join(ROOT, "paper_1204_6255_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert not re.search(r"\boracle\b\s*(import|\.)|import\s+oracle|di_oracle|libdioracle", txt), f

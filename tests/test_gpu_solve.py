@@ -1,0 +1,224 @@
+"""GPU D-iteration solves vs the oracle and vs properties that hold at any size (T1, T2, T7-T10)."""
+import numpy as np
+import pytest
+
+import digen
+import oracle
+from conftest import load_pins
+from gpu_util import l1, need_gpu, upload
+from oracle import definition as defn
+
+pytestmark = pytest.mark.gpu
+D = 0.85
+PINS = load_pins()
+
+
+@pytest.mark.parametrize("variant", ["sop", "cyc"])
+def test_exact_pins(variant):
+    need_gpu()
+    for name, n, links, X in PINS:
+        src = np.array([s for s, _ in links], dtype=np.int32)
+        dst = np.array([t for _, t in links], dtype=np.int32)
+        g = upload(src, dst, n)
+        st = g.solve(d=D, tol=1e-16, variant=variant)
+        assert st["converged"] == 1, (name, st)
+        H = g.history().cpu().numpy()
+        assert l1(H, [float(x) for x in X]) <= 1e-14, (name, H)
+        g.free()
+
+
+@pytest.mark.parametrize("d", [0.5, 0.85, 0.95])
+def test_random_vs_dense(d):
+    need_gpu()
+    for seed in range(60):
+        src, dst, n = digen.small_random(seed)
+        X = defn.solve_dense(src, dst, n, d)
+        g = upload(src, dst, n)
+        for variant in ("sop", "cyc"):
+            st = g.solve(d=d, tol=1e-15, variant=variant)
+            assert st["converged"] == 1
+            assert l1(g.history().cpu().numpy(), X) <= 1e-13, (seed, variant)
+        g.free()
+
+
+@pytest.mark.parametrize("variant", ["sop", "cyc"])
+@pytest.mark.parametrize("name,seed", [("c1", 1), ("c1", 2), ("c1", 3), ("c2", 1)])
+def test_north_star_parity(name, seed, variant):
+    """T10: ||H_gpu - H_oracle||_1 <= 1e-9, both run to ||F||_1 <= 1e-10 (north_star), and
+    <= 1e-10/(1-d) + 1e-13/(1-d) against the tight (1e-13) oracle run (reading G19)."""
+    need_gpu()
+    src, dst, n = digen.make(name, seed=seed)
+    g = upload(src, dst, n)
+    st = g.solve(d=D, tol=1e-10, variant=variant)
+    assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
+    H = g.history().cpu().numpy()
+    Ho, _, sto = oracle.di(src, dst, n, d=D, tol=1e-10, variant=variant)
+    assert l1(H, Ho) <= 1e-9
+    Ht, _, _ = oracle.di(src, dst, n, d=D, tol=1e-13, variant=variant)
+    assert l1(H, Ht) <= 1e-10 / (1 - D) + 1e-13 / (1 - D)
+    # accounting: eq-iter = link diffusions / L
+    assert abs(st["equivalent_iterations"] - st["link_diffusions"] / len(src)) < 1e-12
+    g.free()
+
+
+def test_invariants_mid_solve():
+    """T8: at any stopping point F = B + P.H - H, F >= 0, conservation, sum F non-increasing."""
+    need_gpu()
+    for seed in range(20):
+        src, dst, n = digen.small_random(seed, n_max=64)
+        P = defn.dense_P(src, dst, n, D)
+        B = defn.uniform_B(n, D)
+        out = np.bincount(src, minlength=n)
+        g = upload(src, dst, n)
+        for variant in ("sop", "cyc"):
+            prev = np.inf
+            for k in (1, 2, 3, 5, 8):
+                g.solve(d=D, tol=1e-300, variant=variant, max_sweeps=k)
+                H = g.history().cpu().numpy()
+                r, F = g.residual(return_F=True)
+                F = F.cpu().numpy()
+                assert np.all(F >= 0)
+                assert np.abs(F - (B + P @ H - H)).max() <= 1e-15
+                cons = F.sum() + (1 - D) * H[out > 0].sum() + H[out == 0].sum()
+                assert abs(cons - (1 - D)) <= 1e-14
+                assert F.sum() <= prev + 1e-17
+                prev = F.sum()
+        g.free()
+
+
+def test_bulk_cyc_neumann_gpu():
+    """T7: bulk DI-CYC without loops: F_n = P^n B and H_n = sum_{k<n} P^k B after n sweeps."""
+    need_gpu()
+    src, dst, n = digen.make("c1")
+    P = defn.sparse_P(src, dst, n, D)
+    B = defn.uniform_B(n, D)
+    g = upload(src, dst, n)
+    Fn, Hn = B.copy(), np.zeros(n)
+    for k in range(1, 11):
+        g.solve(d=D, tol=1e-300, variant="cyc", max_sweeps=k)
+        Hn = Hn + Fn
+        Fn = P @ Fn
+        _, F = g.residual(return_F=True)
+        F = F.cpu().numpy()
+        H = g.history().cpu().numpy()
+        nz = Fn > 0
+        assert np.array_equal(F > 0, nz)
+        assert np.max(np.abs(F[nz] - Fn[nz]) / Fn[nz]) <= 1e-13
+        assert np.max(np.abs(H - Hn) / np.maximum(Hn, 1e-300)) <= 1e-13
+    g.free()
+
+
+def test_closure_drainage_gpu():
+    """T9: nodes of E at depth <= t hold exactly 0.0 after t+1 bulk DI-CYC sweeps."""
+    need_gpu()
+    for seed in range(30):
+        src, dst, n = digen.dag_fringe(seed)
+        depth = digen.closure(src, dst, n)
+        g = upload(src, dst, n)
+        for t in range(6):
+            g.solve(d=D, tol=1e-300, variant="cyc", max_sweeps=t + 1)
+            _, F = g.residual(return_F=True)
+            F = F.cpu().numpy()
+            drained = (depth >= 0) & (depth <= t)
+            assert np.all(F[drained] == 0.0), (seed, t)
+        g.free()
+
+
+def test_resume_and_not_converged():
+    need_gpu()
+    import paper_1204_6255_b200 as di
+    src, dst, n = digen.make("c1")
+    g = upload(src, dst, n)
+    st = g.solve(d=D, tol=1e-10, variant="sop", max_sweeps=5)
+    assert st["status"] == di.DI_NOT_CONVERGED and st["sweeps"] == 5
+    st2 = g.solve(d=D, tol=1e-10, variant="sop", resume=True)
+    assert st2["converged"] == 1
+    H = g.history().cpu().numpy()
+    X = defn.solve_sparse(src, dst, n, D)
+    assert l1(H, X) <= 1e-10 / (1 - D)
+    with pytest.raises(di.DIError):
+        g.solve(d=1.0)
+    with pytest.raises(di.DIError):
+        g.solve(tol=0.0)
+    g.free()
+
+
+def test_edge_cases():
+    need_gpu()
+    import paper_1204_6255_b200 as di
+    # all dangling, L = 0: one sweep absorbs everything, X = (1-d)/N
+    g = di.Graph(np.zeros(0, np.int32), np.zeros(0, np.int32), 3000)
+    st = g.solve(d=D, tol=1e-12)
+    assert st["converged"] == 1 and st["sweeps"] == 1
+    assert np.allclose(g.history().cpu().numpy(), (1 - D) / 3000, rtol=0, atol=1e-18)
+    g.free()
+    # N around the tile size (2048 nodes per select tile): ragged tails
+    for n in (1, 2047, 2048, 2049, 4097):
+        rng = np.random.default_rng(n)
+        m = 4 * n
+        src = rng.integers(0, n, m).astype(np.int32)
+        dst = rng.integers(0, n, m).astype(np.int32)
+        g = upload(src, dst, n)
+        X = defn.solve_sparse(src, dst, n, D)
+        for variant in ("sop", "cyc"):
+            st = g.solve(d=D, tol=1e-13, variant=variant)
+            assert st["converged"] == 1
+            assert l1(g.history().cpu().numpy(), X) <= 1e-13 / (1 - D) + 1e-14
+        g.free()
+
+
+def test_custom_B_and_paper_stop():
+    need_gpu()
+    src, dst, n = digen.make("c1")
+    rng = np.random.default_rng(5)
+    B = rng.random(n) * (1 - D) / n * 2
+    g = upload(src, dst, n)
+    st = g.solve(d=D, tol=1e-12, B=B)
+    X = defn.solve_sparse(src, dst, n, D, B=B)
+    assert l1(g.history().cpu().numpy(), X) <= 1e-12 / (1 - D)
+    st = g.solve(d=D, tol=1.0 / n, paper_error=True)
+    assert st["converged"] == 1 and st["error_estimate"] <= 1.0 / n
+    Ho, _, sto = oracle.di(src, dst, n, d=D, tol=1.0 / n, variant="sop", paper_stop=True)
+    X = defn.solve_sparse(src, dst, n, D)
+    H = g.history().cpu().numpy()
+    assert l1(H / H.sum(), X / X.sum()) <= 2 * st["error_estimate"]
+    g.free()
+
+
+def test_trace_log():
+    need_gpu()
+    src, dst, n = digen.make("c1")
+    g = upload(src, dst, n)
+    st = g.solve(d=D, tol=1e-10, trace=True, profile=True)
+    log = g.sweep_log()
+    assert len(log["r"]) == st["sweeps"]
+    assert log["links"].sum() == st["link_diffusions"] and log["selected"].sum() == st["selected_total"]
+    assert np.all(np.diff(log["r"]) <= 1e-18)                       # sum F non-increasing
+    assert st["push_ms"] > 0 and st["select_ms"] > 0
+    g.free()
+
+
+@pytest.mark.slow
+def test_c4_full_size_properties():
+    """C4 at full size in the bench's launch configuration: converged residual, sampled invariant
+    F_i = B_i + (P.H)_i - H_i on 2000 nodes, and ||X - H||_1 <= ||F||_1/(1-d) by construction."""
+    need_gpu()
+    src, dst, n = digen.make("c4")
+    g = upload(src, dst, n)
+    st = g.solve(d=D, tol=1e-10, variant="sop")
+    assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
+    H = g.history().cpu().numpy()
+    _, F = g.residual(return_F=True)
+    F = F.cpu().numpy()
+    assert np.all(F >= 0) and np.all(H >= 0)
+    rng = np.random.default_rng(0)
+    sample = rng.choice(n, 2000, replace=False)
+    out = np.bincount(src, minlength=n).astype(np.float64)
+    insample = np.isin(dst, sample)
+    ph = np.zeros(n)
+    np.add.at(ph, dst[insample], D * H[src[insample]] / out[src[insample]])
+    resid = (1 - D) / n + ph[sample] - H[sample]
+    assert np.max(np.abs(resid - F[sample])) <= 1e-15
+    cons = F.sum() + (1 - D) * H[out > 0].sum() + H[out == 0].sum()
+    assert abs(cons - (1 - D)) <= 1e-12
+    g.free()
