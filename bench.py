@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""bench.py — D-iteration (arXiv:1204.6255) hot path on B200: GTEPS and time-to-||F||_1 <= 1e-10.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--variant sop] [--impl ours|reference]
+
+A step is one whole solve of the hot path: F = B, H = 0, DI-SOP bulk sweeps
+(select/compact + degree-binned push) until ||F||_1 <= 1e-10, on the graph resident in HBM (the
+device CSR build a0 is "Init", timed separately as in PAPER.md P:61-63, and inside `e2e`).
+value = link diffusions / solve time (GTEPS = 1e9 link-diffusions/s, all ranks).
+The default workload is BASELINE.json configs[3] (C4: R-MAT N=2^24, L~268M, the largest
+single-GPU configuration). Inputs (col 1.07 GB, F/H 134 MB each) exceed the 126 MB L2, and L2
+is additionally flushed (512 MiB write) before every timed step.
+
+--impl reference times the CPU oracle (oracle/, sequential DI-SOP exactly as PAPER.md §2.5.5)
+on a bounded sample of the same workload (the first cycles of the solve), on this host.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "link-diffusions/sec (GTEPS) and time-to-||F||_1<=1e-10; % HBM roofline"
+UNIT = "GTEPS"
+D = 0.85
+TOL = 1e-10
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel="k_push"):
+    """Per-launch dram bytes of the push kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        return t.get(kernel)
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/di_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        try:
+            rows = [l.strip().split(", ") for l in open(self.path) if l.strip()]
+        except Exception:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def make_graph(cfg, seed):
+    import digen
+    t = time.time()
+    src, dst, n = digen.make(cfg, seed=seed)
+    return src, dst, n, time.time() - t
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------------ our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1204_6255_b200 as di
+
+    src, dst, n, gen_s = make_graph(args.config, args.seed)
+    L = len(src)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- a0 build ("Init"), device pointers
+    s_d = torch.from_numpy(src).to(dev)
+    t_d = torch.from_numpy(dst).to(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    g = di.Graph(s_d, t_d, n, stream=stream)
+    torch.cuda.synchronize()
+    init_ms = (time.perf_counter() - t0) * 1e3
+    del s_d, t_d
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def one(profile):
+        flush.fill_(1)                                   # L2 flush (> 126 MB L2) outside the event pair
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        st = g.solve(d=D, tol=TOL, variant=args.variant, profile=profile)
+        ev1.record(stream)
+        ev1.synchronize()
+        assert st["converged"] == 1, st
+        return st, ev0.elapsed_time(ev1)
+
+    for _ in range(args.warmup):
+        one(False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stats, times = [], []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            st, ms = one(True)
+            stats.append(st)
+            times.append(ms)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    tot_ms = sum(times)
+    links = sum(s["link_diffusions"] for s in stats)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        lk = torch.tensor([links], dtype=torch.float64, device=dev)
+        dist.all_reduce(lk)
+        links = float(lk.item())
+    value = links / (tot_ms * 1e-3) / 1e9
+    ms_per_step = tot_ms / args.steps
+
+    # ---- roofline of the dominant kernel (push, a5): algorithmic bytes / event time
+    peak, peak_src = peaks()
+    push_bytes = sum(s["push_bytes"] for s in stats)
+    push_ms = sum(s["push_ms"] for s in stats)
+    push_launches = sum(s["push_launches"] for s in stats)
+    sel_ms = sum(s["select_ms"] for s in stats)
+    achieved = push_bytes / (push_ms * 1e-3) / 1e9 if push_ms > 0 else 0.0
+    tr = ncu_traffic()
+    counted = sum(s["counted_bytes"] for s in stats)
+    roofline = {"bound": "hbm", "kernel": "k_push (a5, degree-binned fp64 RED push)",
+                "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": tr,
+                "peak_source": peak_src,
+                "bytes_per_launch": push_bytes / max(push_launches, 1),
+                "avg_launch_ms": push_ms / max(push_launches, 1),
+                "push_share_of_step": round(push_ms / tot_ms, 4) if tot_ms else None,
+                "select_share_of_step": round(sel_ms / tot_ms, 4) if tot_ms else None,
+                "whole_solve_counted_GBps": round(counted / (tot_ms * 1e-3) / 1e9, 1)}
+
+    # ---- e2e through the C ABI with host buffers (H2D of the link list, build, solve, D2H of H)
+    src_p = torch.from_numpy(src).pin_memory()
+    dst_p = torch.from_numpy(dst).pin_memory()
+    H_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    e2e_ms, e2e_links = [], 0
+    g.free()
+    torch.cuda.empty_cache()
+    for k in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gh = di.Graph(src_p, dst_p, n, stream=stream)     # DI_HOST_PTRS: H2D inside the call
+        st = gh.solve(d=D, tol=TOL, variant=args.variant)
+        H = gh.history()
+        H_host.copy_(H, non_blocking=True)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) * 1e3
+        gh.free()
+        del H
+        if k > 0:                                        # first e2e iteration is a warm-up
+            e2e_ms.append(dt)
+            e2e_links += st["link_diffusions"]
+    e2e_val = e2e_links / (sum(e2e_ms) * 1e-3) / 1e9 if e2e_ms else None
+
+    # ---- CPU oracle baseline (rank 0, N=1): bounded sample = first cycles of the same solve
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(src, dst, n, args)
+
+    clocks = clk.summary()
+    gpu_launches = sum(s["gpu_launches"] for s in stats)
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded R-MAT + repair, digen; stands in for uk-2007-05 / gr0.California)",
+        "config": {"workload": f"{args.config}: " + __import__("digen").CONFIGS[args.config].note,
+                   "n": n, "links": L, "variant": "DI-" + args.variant.upper(), "d": D,
+                   "tol_l1_fluid": TOL, "seed": args.seed,
+                   "l2": "inputs > 126 MB L2 and 512 MiB L2 flush before each step",
+                   "parallelism": "1-D node range" if world > 1 else "single GPU",
+                   "init_build_ms": round(init_ms, 1), "generator_s": round(gen_s, 1)},
+        "time_to_tol_ms": round(ms_per_step, 3),
+        "sweeps": stats[-1]["sweeps"], "equivalent_iterations": round(stats[-1]["equivalent_iterations"], 2),
+        "residual_l1": stats[-1]["residual_l1"],
+        "hbm_frac_counted_whole_solve": round(counted / (tot_ms * 1e-3) / 1e9 / peak, 4),
+        "roofline": roofline,
+        "e2e": {"value": round(e2e_val, 3) if e2e_val else None, "unit": UNIT, "ms_per_step": round(statistics.mean(e2e_ms), 2) if e2e_ms else None,
+                "h2d_bytes_per_step": 8 * L, "d2h_bytes_per_step": 8 * n,
+                "includes": "pinned host link list -> di_graph_upload(DI_HOST_PTRS) build -> di_solve -> H to host"},
+        "gpu_launches": gpu_launches,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(src, dst, n, args, budget_cycles=None):
+    """Sequential oracle DI-SOP (§2.5.5) on this host, 1 thread, bounded to the first
+    `cycles` cycles of the same workload (adjacency build excluded, as the paper's Init)."""
+    import oracle
+    cycles = budget_cycles or args.cpu_cycles
+    H, F, st = oracle.di(src, dst, n, d=D, tol=TOL, variant=args.variant, max_cycles=cycles)
+    secs = st["solve_seconds"]
+    return {"value": round(st["diffusions"] / secs / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {st['cycles']} sequential DI-{args.variant.upper()} cycles of {args.config} "
+                      f"({st['diffusions']} link diffusions, {secs:.1f} s, loop only)",
+            "seconds": round(secs, 2)}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    src, dst, n, _ = make_graph(args.config, args.seed)
+    import oracle
+    vals, times, last = [], [], None
+    for k in range(args.warmup + args.steps):
+        cb = cpu_baseline(src, dst, n, args)
+        if k >= args.warmup:
+            vals.append(cb["value"])
+            times.append(cb["seconds"] * 1e3)
+            last = cb
+    value = statistics.mean(vals)
+    out = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(statistics.mean(times), 1), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": f"{args.config}: " + __import__("digen").CONFIGS[args.config].note,
+                      "variant": "DI-" + args.variant.upper(), "d": D, "tol_l1_fluid": TOL},
+           "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": last["sample"]},
+           "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--variant", default="sop", choices=["sop", "cyc"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-cycles", type=int, default=12)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -38,7 +38,8 @@ class Stats(ctypes.Structure):
     _fields_ = [("cycles", ctypes.c_int64), ("diffusions", ctypes.c_int64),
                 ("guard_sweeps", ctypes.c_int64), ("selected", ctypes.c_int64),
                 ("converged", ctypes.c_int64), ("residual", ctypes.c_double),
-                ("e", ctypes.c_double), ("eq_iter", ctypes.c_double)]
+                ("e", ctypes.c_double), ("eq_iter", ctypes.c_double),
+                ("solve_seconds", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -25,6 +25,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <time.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -37,7 +38,15 @@ typedef struct {
   double residual;           /* sum F at exit (DI) / last error estimate (PI, PI', GS)       */
   double e;                  /* dangling absorbed mass                        */
   double eq_iter;            /* diffusions / L [G12]                                         */
+  double solve_seconds;      /* wall time of the iteration loop only (adjacency build excluded,
+                                as the paper times "Init" separately)                */
 } orc_stats;
+
+static double now_seconds(void) {
+  struct timespec t;
+  clock_gettime(CLOCK_MONOTONIC, &t);
+  return (double)t.tv_sec + 1e-9 * (double)t.tv_nsec;
+}
 
 /* ------------------------------------------------------------------ adjacency */
 typedef struct {
@@ -156,6 +165,7 @@ int orc_di(const int32_t *src, const int32_t *dst, int64_t L, int64_t N, double 
   for (int64_t i = 0; i < N; i++) { H[i] = 0.0; F[i] = B ? B[i] : (1 - d) / N; }
   int64_t diff = 0, sel = 0;
   int rc = 1;
+  double t_start = now_seconds();
   for (;;) {
     double r = sum_seq(F, N);
     if (r_hist && st->cycles < hist_cap) r_hist[st->cycles] = r;
@@ -168,6 +178,7 @@ int orc_di(const int32_t *src, const int32_t *dst, int64_t L, int64_t N, double 
     if (s == 0) { di_cycle(&g, F, H, &e, d, 0, 0.0, &diff, &sel); st->guard_sweeps++; }
     st->cycles++;
   }
+  st->solve_seconds = now_seconds() - t_start;
   st->converged = (rc == 0);
   st->diffusions = diff; st->selected = sel; st->e = e;
   st->eq_iter = L > 0 ? (double)diff / (double)L : 0.0;
