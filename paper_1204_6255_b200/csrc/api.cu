@@ -2,7 +2,9 @@
 // host side of the sweep loop. The loop enqueues sweeps in batches without reading anything
 // back in between; the device finaliser decides convergence and later
 // kernels no-op, so the host only synchronises once per batch.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -49,13 +51,14 @@ struct EventSet {
 void free_graph(Graph *g) {
   if (!g) return;
   void *ptrs[] = {g->row_ptr, g->col, g->deg, g->kloop, g->csc_ptr, g->csc_row, g->F, g->H,
-                  g->S, g->aux, g->sc, g->partials, g->red_partials, g->tile_flag, g->tile_agg,
-                  g->tile_incl, g->fr.chunk, g->log_r, g->log_sel, g->log_links, g->log_mode};
+                  g->S, g->aux, g->sc, g->partials, g->ipartials, g->red_partials,
+                  g->log_r, g->log_sel, g->log_links, g->log_mode};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (int b = 0; b < kBins; b++) {
-    if (g->fr.ids[b]) cudaFree(g->fr.ids[b]);
-    if (g->fr.val[b]) cudaFree(g->fr.val[b]);
+    void *q[] = {g->fr.ent[b], g->fr.id[b]};
+    for (void *p : q)
+      if (p) cudaFree(p);
   }
   if (g->sc_host) cudaFreeHost(g->sc_host);
   delete g;
@@ -97,6 +100,8 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
   g->n = g->n_global = n_nodes;
   g->lo = 0;
   g->hi = n_nodes;
+  if (const char *e = getenv("DI_RED_HINT")) g->red_hint = atoi(e);
+  if (const char *e = getenv("DI_PUSH_OCC")) g->push_occ = atoi(e);
   di_status s = build_graph(*g, src, dst, n_links, flags);
   if (s == DI_OK) s = alloc_state(*g);
   if (s != DI_OK) {
@@ -175,6 +180,11 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     memset(&s, 0, sizeof(Scalars));
     s.epoch = epoch;
     s.e = resume ? e_prev : 0.0;
+    s.d = d;
+    s.tol = tol;
+    s.variant = (int32_t)v;
+    s.paper_err = paper;
+    s.trace = trace;
   }
   DI_CK(cudaEventRecord(t0, g.stream));
   DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
@@ -197,7 +207,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     const int64_t sweeps_before = g.sc_host->sweeps;
     for (int64_t j = 0; j < k; j++) {
       if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 0), g.stream));
-      launch_select(g, d, tol, (int)v, paper, trace, 0, &launches);
+      launch_select(g, 0, &launches);
       if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 1), g.stream));
       launch_push(g, &launches);
       if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 2), g.stream));
@@ -371,10 +381,14 @@ di_status di_test_select(di_graph h, const double *F_in, const double *H_in, dou
     memset(&s, 0, sizeof(Scalars));
     s.epoch = epoch;
     s.r = r;
+    s.d = d;
+    s.tol = 1e300;
+    s.variant = (int32_t)v;
   }
   DI_CK(cudaMemcpy(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice));
   int64_t launches = 0;
-  launch_select(g, d, 1e300, (int)v, 0, 0, 1, &launches);
+  launch_select(g, 1, &launches);
+  launch_finalize(g, &launches);
   di_status s = sync_scalars(g);
   if (s != DI_OK) return s;
   DI_CK(cudaGetLastError());
@@ -386,20 +400,34 @@ di_status di_test_select(di_graph h, const double *F_in, const double *H_in, dou
   }
   if (bin_off) bin_off[kBins] = off;
   if (off > cap) return fail(DI_EINVAL, "di_test_select: cap too small");
+  // bin contents, sorted by (node id, chunk) inside each bin (the tile order inside a bin is
+  // the reservation order and carries no meaning)
+  std::vector<int64_t> rp((size_t)g.n + 1);
+  DI_CK(cudaMemcpy(rp.data(), g.row_ptr, ((size_t)g.n + 1) * 8, cudaMemcpyDeviceToHost));
   off = 0;
   for (int b = 0; b < kBins; b++) {
     const size_t m = (size_t)c.bin_count[b];
+    std::vector<Entry> ent(m);
+    std::vector<int32_t> eid(m);
     if (m) {
-      if (ids) DI_CK(cudaMemcpy(ids + off, g.fr.ids[b], m * 4, cudaMemcpyDeviceToHost));
-      if (vals) DI_CK(cudaMemcpy(vals + off, g.fr.val[b], m * 8, cudaMemcpyDeviceToHost));
-      if (chunk) {
-        if (b == BIN_C)
-          DI_CK(cudaMemcpy(chunk + off, g.fr.chunk, m * 4, cudaMemcpyDeviceToHost));
-        else
-          memset(chunk + off, 0, m * 4);
-      }
+      DI_CK(cudaMemcpy(ent.data(), g.fr.ent[b], m * sizeof(Entry), cudaMemcpyDeviceToHost));
+      DI_CK(cudaMemcpy(eid.data(), g.fr.id[b], m * 4, cudaMemcpyDeviceToHost));
     }
-    off += (int64_t)m;
+    std::vector<size_t> order(m);
+    for (size_t k = 0; k < m; k++) order[k] = k;
+    std::sort(order.begin(), order.end(), [&](size_t x, size_t y) {
+      if (eid[x] != eid[y]) return eid[x] < eid[y];
+      return (ent[x].bl & kBegMask) < (ent[y].bl & kBegMask);
+    });
+    for (size_t k = 0; k < m; k++) {
+      const size_t slot = order[k];
+      const int32_t id = eid[slot];
+      const int64_t beg = (int64_t)(ent[slot].bl & kBegMask);
+      if (ids) ids[off] = id;
+      if (vals) vals[off] = ent[slot].v;
+      if (chunk) chunk[off] = (int32_t)((beg - rp[id]) / kChunk);
+      off++;
+    }
   }
   if (scal) {
     scal[0] = c.q;

@@ -13,7 +13,7 @@ namespace di {
 // ----------------------------------------------------------------- tuning constants
 // Select / compact (SURVEY §8(a) a3+a4): one tile = kSelThreads x kSelItems consecutive nodes.
 constexpr int kSelThreads = 256;
-constexpr int kSelItems = 8;
+constexpr int kSelItems = 4;
 constexpr int kSelTile = kSelThreads * kSelItems;
 // Degree bins of the push (north_star item 3):
 //   T: 1..kBinT links -> one thread per node
@@ -33,31 +33,45 @@ enum BinId { BIN_T = 0, BIN_G = 1, BIN_W = 2, BIN_C = 3 };
 
 // Device-resident sweep state. Every field is written only by the "last block" of the
 // select kernel (the finaliser) or by the host between solves, so kernels never race on it.
-struct Scalars {
+struct __align__(256) Scalars {
   double r;          // r_n: threshold fluid for the current sweep (sum F at sweep start)
   double e;          // cumulative dangling absorption
   double q, s, e_sw; // last sweep: unselected fluid, pushed fluid, dangling absorbed
   double resid;      // exact sum F from the reduce kernel
+  double d, tol;     // solve parameters (device-resident: kernels take constant arguments)
+  int32_t variant, paper_err, trace, pad1;
   int32_t stop;      // 1: convergence reached after the current sweep's push
   int32_t guard;     // 1: next sweep runs with threshold 0 (starvation guard, reading G5)
   int32_t active;    // 1: the current sweep emitted push work
   int32_t pull;      // 1: the current sweep runs in pull mode (dense S vector)
   uint32_t epoch;    // select-launch counter: tags look-back flags, starts at 1
   uint32_t ticket;   // last-block detection of the select kernel
-  uint32_t tile_ctr[2];
   uint32_t red_ticket;
   uint32_t pad0;
-  int64_t bin_count[kBins];  // entries in each bin for the current sweep
+  int64_t bin_count[kBins];  // entries in each bin for the current sweep (read by the push)
+  unsigned long long bin_fill[kBins][32];  // reservation counters (one 256-B line each)
   int64_t sweep_sel, sweep_links, sweep_sel_nd;
   int64_t sweeps, selected_total, selected_nd_total, links_total, scanned_total, guards,
       pull_sweeps;
 };
 
+// One push work item: a row (or a kChunk-link chunk of a hub row) of a selected node.
+// bl = first link index (48 bits) | number of links (16 bits); v = T_i*d/#out_i ("sent").
+struct __align__(16) Entry {
+  uint64_t bl;
+  double v;
+};
+constexpr int kLenShift = 48;
+constexpr uint64_t kBegMask = (1ull << kLenShift) - 1;
+
+// Frontier: one contiguous array per degree bin. Each select tile reserves a contiguous range
+// of a bin with one atomicAdd and writes its entries there in ascending node order; the order
+// of tiles inside a bin is the (nondeterministic) reservation order, which the push does not
+// depend on (its fp64 atomics are order-nondeterministic anyway).
 struct Frontier {
-  int32_t *ids[kBins];
-  double *val[kBins];   // v_i = T_i * d / #out_i (the "sent" of P:268)
-  int32_t *chunk;       // chunk index for bin C entries
-  int64_t cap[kBins];
+  Entry *ent[kBins];
+  int32_t *id[kBins];            // node id of each entry (self-loop test, tests)
+  int64_t cap[kBins];            // static capacity: rows (chunks for C) with a degree in the bin
 };
 
 struct Graph {
@@ -71,6 +85,8 @@ struct Graph {
   int64_t l_global = 0;
   bool has_loops = false;
   bool has_csc = false;
+  int push_occ = 4;         // k_push min blocks per SM (DI_PUSH_OCC)
+  int red_hint = 1;         // L2 evict_last hint on the push's REDs into F (DI_RED_HINT=0 disables)
   int rank = 0, world = 1;
   // CSR (sources owned), global column ids
   int64_t *row_ptr = nullptr;
@@ -87,9 +103,9 @@ struct Graph {
   Scalars *sc = nullptr;     // device
   Scalars *sc_host = nullptr;  // pinned mirror
   double *partials = nullptr;  // per-tile q, s, e partials (3 per tile)
+  int64_t *ipartials = nullptr;  // per-tile selected, selected non-dangling, links
+  int64_t ntiles = 0;
   double *red_partials = nullptr;
-  uint32_t *tile_flag = nullptr;
-  int64_t *tile_agg = nullptr, *tile_incl = nullptr;
   Frontier fr{};
   // trace
   double *log_r = nullptr;
@@ -122,9 +138,9 @@ di_status alloc_state(Graph &g);
 void launch_init(Graph &g, const double *B, double d, int64_t *launches);
 void launch_reduce_F(Graph &g, int64_t *launches);
 void launch_reduce_F_setr(Graph &g, int64_t *launches);
-void launch_select(Graph &g, double d, double tol, int variant, int paper_err, int trace,
-                   int test_mode, int64_t *launches);
+void launch_select(Graph &g, int test_mode, int64_t *launches);
 void launch_push(Graph &g, int64_t *launches);
+void launch_finalize(Graph &g, int64_t *launches);
 void launch_pull(Graph &g, int64_t *launches);
 // comparators.cu
 di_status run_comparator(Graph &g, double d, double tol, int variant, int64_t max_sweeps,

@@ -1,40 +1,59 @@
-// diffusion.cu — the D-iteration hot path on sm_100a (SURVEY §8(a) a1-a5).
+// diffusion.cu — the D-iteration hot path on sm_100a (SURVEY §8(a) a1-a6).
 //
 // One bulk-synchronous sweep n (R1) is two kernels:
 //   k_select  (a2+a3+a4): for every node i, test F_i against the DI-SOP threshold
 //             (r_n/L)*#out_i (literal order, reading G4) or 0 (DI-CYC);
 //             for selected i: T_i = F_i, or F_i*#out_i/(#out_i - k_i*d) with k_i self-loops
 //             (reading G6); H_i += T_i; F_i = 0; dangling: e += T_i
-//             (P:266-267); else emit (i, v_i = T_i*d/#out_i) into the degree bin of #out_i.
-//             Emission order is deterministic (ascending i inside each bin) through a
-//             single-pass decoupled look-back scan over tiles. The same pass reduces
-//             q = sum of unselected F and s = sum T_i*d*(#out_i-k_i)/#out_i, so that
-//             r_{n+1} = q + s is known when the sweep ends (a2) without another pass over F.
+//             (P:266-267); else emit the row (first link, #out_i, v_i = T_i*d/#out_i) into the
+//             degree bin of #out_i. A tile reserves its range of each bin with one atomicAdd
+//             and writes its entries in ascending node order (no inter-block waiting). The
+//             same pass writes per-tile partial sums of q = sum of unselected F and
+//             s = sum T_i*d*(#out_i-k_i)/#out_i, so r_{n+1} = q + s is known when the sweep
+//             ends (a2) without another pass over F.
 //   k_push    (a5): F_j += v_i for every link i -> j, j != i, fp64 RED atomics,
-//             degree-binned: CTA-chunk / warp / 8-lane group / thread per node.
-// The last block of k_select finalises the sweep (deterministic fixed-order reductions,
-// convergence test, starvation guard G5), so the host never has to read anything between
-// sweeps: kernels of later sweeps no-op once `stop` is set.
+//             degree-binned: hub chunks and W rows one warp each, G rows one 8-lane group,
+//             T rows one thread. Its last block finalises the sweep (a6): fixed-order
+//             reduction of the partials, r_{n+1}, the stop test, the starvation guard (G5).
+// All solve parameters live in device memory (Scalars), so the sweep is a fixed pair of
+// launches with constant arguments (CUDA-graph capturable); once `stop` is set both kernels
+// return immediately, so the host can enqueue sweeps ahead without reading anything back.
+#include <vector>
+
 #include "di_common.cuh"
 
 namespace di {
 namespace {
 
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// streaming read of the column index array: read once per sweep, do not pollute L1/L2
+// streaming read of the column index array: read once per sweep, keep it out of L1 and make
+// it the first L2 eviction candidate so that F stays resident
 __device__ __forceinline__ int32_t ld_col(const int32_t *p, uint64_t pol) {
   int32_t v;
   asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
                : "=r"(v)
                : "l"(p), "l"(pol));
   return v;
+}
+__device__ __forceinline__ int4 ld_col4(const int32_t *p, uint64_t pol) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void red_add_f64_hint(double *p, double v, uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
+               : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
@@ -114,125 +133,62 @@ int reduce_grid(int64_t n, int sms) {
 }
 
 // -------------------------------------------------------- select + compact (a2-a4)
-struct SelectArgs {
+struct SweepArgs {
   double *F, *H;
   const int32_t *deg, *kloop;
+  const int64_t *row_ptr;
+  const int32_t *col;
   int64_t n;            // owned nodes
+  int64_t lo;           // global id of local node 0
   int64_t ntiles;
-  double L_total;       // global link count, as double (threshold r/L)
-  double d, tol;
-  int variant, paper_err, trace, test_mode;
+  double L_total;       // global link count (threshold r/L)
   Scalars *sc;
   Frontier fr;
-  double *partials;     // 3 per tile
-  uint32_t *tflag;
-  int64_t *tagg, *tincl;  // kBins per tile
+  double *partials;     // 3 per select tile
+  int64_t *ipartials;   // 4 per select tile
   double *log_r;
   int64_t *log_sel, *log_links;
   uint8_t *log_mode;
+  int test_mode;
+  int red_hint;         // 1: REDs into F carry an L2 evict_last policy
 };
 
-// Decoupled look-back (single-pass scan): warp 0 of tile `tile` obtains the exclusive
-// prefix of the 4 bin counts. Flags are tagged with the select-launch epoch so they never
-// need resetting: flag = epoch << 2 | {1: aggregate ready, 2: inclusive prefix ready}.
-__device__ __forceinline__ void lookback(const SelectArgs &a, int64_t tile, uint32_t epoch,
-                                         const int64_t agg[kBins], int64_t excl[kBins]) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t tag = epoch << 2;
-  if (tile == 0) {
-    if (lane < kBins) a.tincl[lane] = agg[lane];
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release_u32(a.tflag, tag | 2u);
-#pragma unroll
-    for (int b = 0; b < kBins; b++) excl[b] = 0;
-    return;
-  }
-  if (lane < kBins) a.tagg[tile * kBins + lane] = agg[lane];
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) st_release_u32(a.tflag + tile, tag | 1u);
-  int64_t run[kBins] = {0, 0, 0, 0};
-  int64_t pred = tile - 1;
-  while (true) {
-    const int64_t idx = pred - lane;
-    uint32_t f = tag | 2u;
-    if (idx >= 0) {
-      do {
-        f = ld_acquire_u32(a.tflag + idx);
-      } while ((f & ~3u) != tag || (f & 3u) == 0);
-    }
-    const bool isP = (f & 3u) == 2u;
-    const uint32_t pm = __ballot_sync(0xffffffffu, isP);
-    const int stop_lane = pm ? (__ffs(pm) - 1) : 32;
-    int64_t v[kBins] = {0, 0, 0, 0};
-    if (idx >= 0 && lane <= stop_lane) {
-      const int64_t *src = (lane == stop_lane) ? (a.tincl + idx * kBins) : (a.tagg + idx * kBins);
-#pragma unroll
-      for (int b = 0; b < kBins; b++) v[b] = __ldcg(src + b);
-    }
-#pragma unroll
-    for (int b = 0; b < kBins; b++) run[b] += warp_sum(v[b]);
-    if (pm) break;
-    pred -= 32;
-  }
-  if (lane < kBins) {
-    int64_t mine = 0;
-#pragma unroll
-    for (int b = 0; b < kBins; b++)
-      if (b == lane) mine = run[b] + agg[b];
-    a.tincl[tile * kBins + lane] = mine;
-  }
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) st_release_u32(a.tflag + tile, tag | 2u);
-#pragma unroll
-  for (int b = 0; b < kBins; b++) excl[b] = run[b];
-}
-
+// One tile = kSelTile consecutive nodes; thread t owns kSelItems consecutive nodes.
 template <bool LOOPS>
-__global__ void __launch_bounds__(kSelThreads) k_select(const SelectArgs a) {
+__global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
   constexpr int NW = kSelThreads / 32;
-  __shared__ uint32_t s_tile;
   __shared__ int s_wcnt[NW][kBins];
-  __shared__ int64_t s_excl[kBins];
   __shared__ double s_red[NW][3];
   __shared__ int64_t s_links[NW];
   __shared__ int s_sel[NW], s_selnd[NW];
-  __shared__ bool s_last;
+  __shared__ unsigned long long s_res[kBins];
 
   Scalars *sc = a.sc;
-  if (!a.test_mode && sc->stop) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) sc->active = 0;
-    return;
-  }
-  const uint32_t epoch = sc->epoch;
-  const int par = epoch & 1;
-  if (threadIdx.x == 0) s_tile = atomicAdd(&sc->tile_ctr[par], 1u);
-  __syncthreads();
-  const int64_t tile = s_tile;
+  if (!a.test_mode && sc->stop) return;
+  const int64_t tile = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double r = sc->r;
-  const bool cyc = (a.variant == DI_CYC) || sc->guard;
-  const double d = a.d;
+  const double d = sc->d;
+  const bool cyc = (sc->variant == DI_CYC) || sc->guard;
   const double t = (a.L_total > 0.0) ? r / a.L_total : 0.0;  // r/L once (G3, G4)
   const int64_t base = tile * (int64_t)kSelTile + (int64_t)threadIdx.x * kSelItems;
+  const bool full = base + kSelItems <= a.n;
 
   double f[kSelItems];
   int o[kSelItems];
   int kl[kSelItems];
-  if (base + kSelItems <= a.n) {
+  if (full) {
     const double2 *F2 = reinterpret_cast<const double2 *>(a.F + base);
 #pragma unroll
     for (int j = 0; j < kSelItems / 2; j++) {
-      double2 x = F2[j];
+      const double2 x = F2[j];
       f[2 * j] = x.x;
       f[2 * j + 1] = x.y;
     }
     const int4 *D4 = reinterpret_cast<const int4 *>(a.deg + base);
 #pragma unroll
     for (int j = 0; j < kSelItems / 4; j++) {
-      int4 x = D4[j];
+      const int4 x = D4[j];
       o[4 * j] = x.x;
       o[4 * j + 1] = x.y;
       o[4 * j + 2] = x.z;
@@ -242,7 +198,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const SelectArgs a) {
       const int4 *K4 = reinterpret_cast<const int4 *>(a.kloop + base);
 #pragma unroll
       for (int j = 0; j < kSelItems / 4; j++) {
-        int4 x = K4[j];
+        const int4 x = K4[j];
         kl[4 * j] = x.x;
         kl[4 * j + 1] = x.y;
         kl[4 * j + 2] = x.z;
@@ -263,57 +219,154 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const SelectArgs a) {
     for (int j = 0; j < kSelItems; j++) kl[j] = 0;
   }
 
-  double v[kSelItems];
-  uint32_t selmask = 0;
+  // ---- pass 1: the selection test (P:258 / P:298) and the bin counts
+  uint32_t selmask = 0, dangmask = 0;
   int cnt[kBins] = {0, 0, 0, 0};
-  double q = 0.0, s = 0.0, e = 0.0;
-  int64_t links = 0;
-  int nsel = 0, nsel_nd = 0;
+  double q = 0.0;
 #pragma unroll
   for (int j = 0; j < kSelItems; j++) {
     const int64_t i = base + j;
-    v[j] = 0.0;
     if (i >= a.n) continue;
-    const double od = (double)o[j];
-    const double thr = cyc ? 0.0 : __dmul_rn(t, od);  // (r/L)*out[i]
-    if (f[j] > thr) {                                   // strict '>'
-      double T = f[j];
-      if (LOOPS && kl[j] > 0)                           // P:259-263 with k copies (G6)
-        T = __ddiv_rn(__dmul_rn(f[j], od), __dsub_rn(od, __dmul_rn((double)kl[j], d)));
-      a.H[i] = __dadd_rn(a.H[i], T);
-      a.F[i] = 0.0;                                     // P:265
-      nsel++;
+    const double thr = cyc ? 0.0 : __dmul_rn(t, (double)o[j]);  // (r/L)*out[i]
+    if (f[j] > thr) {                                             // strict '>'
       if (o[j] == 0) {
-        e = __dadd_rn(e, T);                            // P:266-267
+        dangmask |= 1u << j;
       } else {
-        const double Td = __dmul_rn(T, d);
-        v[j] = __ddiv_rn(Td, od);                       // sent = transit*d/out[i]
-        s = __dadd_rn(s, __ddiv_rn(__dmul_rn(Td, (double)(o[j] - kl[j])), od));
-        links += o[j];
-        nsel_nd++;
-        const int b = bin_of(o[j]);
-        cnt[b] += (b == BIN_C) ? (o[j] + kChunk - 1) / kChunk : 1;
         selmask |= 1u << j;
+        const int b = bin_of(o[j]);
+        const int inc = (b == BIN_C) ? (o[j] + kChunk - 1) / kChunk : 1;
+#pragma unroll
+        for (int bb = 0; bb < kBins; bb++) cnt[bb] += (bb == b) ? inc : 0;  // no local memory
       }
     } else {
       q = __dadd_rn(q, f[j]);
     }
   }
+  // ---- pass 2a: move the fluid of selected nodes into H; independent of the bin
+  //      reservation, so its loads and fp64 divisions overlap the reservation latency
+  const uint32_t anysel = selmask | dangmask;
+  double v[kSelItems];
+  int64_t rb[kSelItems];
+  double s = 0.0, e = 0.0;
+  int64_t links = 0;
+  int nsel = 0, nsel_nd = 0;
+  if (anysel) {
+    double h[kSelItems];
+    if (full) {
+      const double2 *H2 = reinterpret_cast<const double2 *>(a.H + base);
+      const longlong2 *R2 = reinterpret_cast<const longlong2 *>(a.row_ptr + base);
+#pragma unroll
+      for (int j = 0; j < kSelItems / 2; j++) {
+        const double2 x = H2[j];
+        h[2 * j] = x.x;
+        h[2 * j + 1] = x.y;
+      }
+      if (selmask) {
+#pragma unroll
+        for (int j = 0; j < kSelItems / 2; j++) {
+          const longlong2 x = R2[j];
+          rb[2 * j] = x.x;
+          rb[2 * j + 1] = x.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kSelItems; j++) {
+        h[j] = (anysel >> j & 1u) ? a.H[base + j] : 0.0;
+        rb[j] = (selmask >> j & 1u) ? a.row_ptr[base + j] : 0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kSelItems; j++) {
+      v[j] = 0.0;
+      if (!(anysel & (1u << j))) continue;
+      const int64_t i = base + j;
+      const double od = (double)o[j];
+      double T = f[j];
+      if (LOOPS && kl[j] > 0)                           // P:259-263 with k copies (G6)
+        T = __ddiv_rn(__dmul_rn(f[j], od), __dsub_rn(od, __dmul_rn((double)kl[j], d)));
+      a.H[i] = __dadd_rn(h[j], T);
+      a.F[i] = 0.0;                                     // P:265
+      nsel++;
+      if (o[j] == 0) {
+        e = __dadd_rn(e, T);                            // P:266-267
+      } else {
+        v[j] = __ddiv_rn(__dmul_rn(T, d), od);          // sent = transit*d/out[i]
+        s = __dadd_rn(s, __dmul_rn(v[j], (double)(o[j] - kl[j])));  // fluid leaving i
+        links += o[j];
+        nsel_nd++;
+      }
+    }
+  }
 
-  // ---- block-wide exclusive scan of the 4 bin counts
+  // ---- block-wide exclusive scan of the 4 bin counts, one reservation per bin
   int incl[kBins];
 #pragma unroll
   for (int b = 0; b < kBins; b++) {
     int x = cnt[b];
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, x, off);
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
       if (lane >= off) x += y;
     }
     incl[b] = x;
     if (lane == 31) s_wcnt[warp][b] = x;
   }
-  // ---- block reductions of q, s, e, links, selected (fixed order)
+  __syncthreads();
+  int pos[kBins];
+#pragma unroll
+  for (int b = 0; b < kBins; b++) {
+    int we = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) {
+      const int c = s_wcnt[w][b];
+      we += (w < warp) ? c : 0;
+      tot += c;
+    }
+    pos[b] = we + incl[b] - cnt[b];
+    if (threadIdx.x == b)
+      s_res[b] = tot ? atomicAdd(&sc->bin_fill[b][0], (unsigned long long)tot) : 0ull;
+  }
+  __syncthreads();
+
+  // ---- pass 2b: emit the rows into the reserved ranges, ascending node id inside each bin
+  if (selmask) {
+    int64_t slot[kBins];
+#pragma unroll
+    for (int b = 0; b < kBins; b++) slot[b] = (int64_t)s_res[b] + pos[b];
+#pragma unroll
+    for (int j = 0; j < kSelItems; j++) {
+      if (!(selmask & (1u << j))) continue;
+      const int32_t i = (int32_t)(base + j);
+      const int b = bin_of(o[j]);
+      if (b != BIN_C) {
+        Entry en;
+        en.bl = (uint64_t)rb[j] | ((uint64_t)o[j] << kLenShift);
+        en.v = v[j];
+#pragma unroll
+        for (int bb = 0; bb < BIN_C; bb++) {
+          if (bb == b) {
+            a.fr.ent[bb][slot[bb]] = en;
+            a.fr.id[bb][slot[bb]] = i;
+            slot[bb]++;
+          }
+        }
+      } else {
+        const int nch = (o[j] + kChunk - 1) / kChunk;
+        for (int c = 0; c < nch; c++) {
+          const int len = min(kChunk, o[j] - c * kChunk);
+          Entry en;
+          en.bl = (uint64_t)(rb[j] + (int64_t)c * kChunk) | ((uint64_t)len << kLenShift);
+          en.v = v[j];
+          a.fr.ent[BIN_C][slot[BIN_C] + c] = en;
+          a.fr.id[BIN_C][slot[BIN_C] + c] = i;
+        }
+        slot[BIN_C] += nch;
+      }
+    }
+  }
+
+  // ---- block partials (fixed order), reduced by the sweep finaliser
   q = warp_sum(q);
   s = warp_sum(s);
   e = warp_sum(e);
@@ -329,36 +382,11 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const SelectArgs a) {
     s_selnd[warp] = nsel_nd;
   }
   __syncthreads();
-  int texcl[kBins];
-  int64_t agg[kBins];
-#pragma unroll
-  for (int b = 0; b < kBins; b++) {
-    int we = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < NW; w++) {
-      const int c = s_wcnt[w][b];
-      we += (w < warp) ? c : 0;
-      tot += c;
-    }
-    texcl[b] = we + incl[b] - cnt[b];
-    agg[b] = tot;
-  }
-  if (warp == 0) {
-    int64_t ex[kBins];
-    lookback(a, tile, epoch, agg, ex);
-    if (lane == 0) {
-#pragma unroll
-      for (int b = 0; b < kBins; b++) s_excl[b] = ex[b];
-      if (tile == a.ntiles - 1) {
-#pragma unroll
-        for (int b = 0; b < kBins; b++) sc->bin_count[b] = ex[b] + agg[b];
-      }
-    }
-  }
-  if (threadIdx.x == 32) {
+  if (threadIdx.x == 0) {
     double tq = 0.0, ts = 0.0, te = 0.0;
     int64_t tl = 0;
     int tsel = 0, tnd = 0;
+#pragma unroll
     for (int w = 0; w < NW; w++) {
       tq += s_red[w][0];
       ts += s_red[w][1];
@@ -370,206 +398,268 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const SelectArgs a) {
     a.partials[tile * 3 + 0] = tq;
     a.partials[tile * 3 + 1] = ts;
     a.partials[tile * 3 + 2] = te;
-    if (tl) atomicAdd((unsigned long long *)&sc->sweep_links, (unsigned long long)tl);
-    if (tsel) atomicAdd((unsigned long long *)&sc->sweep_sel, (unsigned long long)tsel);
-    if (tnd) atomicAdd((unsigned long long *)&sc->sweep_sel_nd, (unsigned long long)tnd);
+    reinterpret_cast<longlong2 *>(a.ipartials)[2 * tile] = make_longlong2(tsel, tnd);
+    reinterpret_cast<longlong2 *>(a.ipartials)[2 * tile + 1] = make_longlong2(tl, 0);
   }
-  __syncthreads();
+}
 
-  // ---- emit (i, v_i) in ascending i inside each bin
-  if (selmask) {
-    int64_t pos[kBins];
-#pragma unroll
-    for (int b = 0; b < kBins; b++) pos[b] = s_excl[b] + texcl[b];
-#pragma unroll
-    for (int j = 0; j < kSelItems; j++) {
-      if (!(selmask & (1u << j))) continue;
-      const int32_t i = (int32_t)(base + j);
-      const int b = bin_of(o[j]);
-      if (b != BIN_C) {
-        a.fr.ids[b][pos[b]] = i;
-        a.fr.val[b][pos[b]] = v[j];
-        pos[b]++;
-      } else {
-        const int nch = (o[j] + kChunk - 1) / kChunk;
-        for (int c = 0; c < nch; c++) {
-          a.fr.ids[BIN_C][pos[BIN_C] + c] = i;
-          a.fr.val[BIN_C][pos[BIN_C] + c] = v[j];
-          a.fr.chunk[pos[BIN_C] + c] = c;
-        }
-        pos[BIN_C] += nch;
-      }
-    }
-  }
-
-  // ---- last block finalises the sweep
-  __threadfence();
-  if (threadIdx.x == 0) s_last = atomicAdd(&sc->ticket, 1u) == (uint32_t)(a.ntiles - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
+// --------------------------------------------------------------- sweep finaliser (a6)
+// Executed by one whole block after every select tile has finished (the last push block, or
+// k_finalize in test mode). Fixed-order reduction of the per-tile partials.
+__device__ void finalize_sweep(const SweepArgs &a, int nthreads) {
+  __shared__ double s_fin[32][3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ long long s_ifin[32][3];
   double aq = 0.0, as = 0.0, ae = 0.0;
-  for (int64_t tt = threadIdx.x; tt < a.ntiles; tt += kSelThreads) {
+  long long c_sel = 0, c_nd = 0, c_lk = 0;
+#pragma unroll 4
+  for (int64_t tt = threadIdx.x; tt < a.ntiles; tt += nthreads) {
     aq += __ldcg(a.partials + tt * 3 + 0);
     as += __ldcg(a.partials + tt * 3 + 1);
     ae += __ldcg(a.partials + tt * 3 + 2);
+    const longlong2 c01 = __ldcg(reinterpret_cast<const longlong2 *>(a.ipartials) + 2 * tt);
+    const longlong2 c23 = __ldcg(reinterpret_cast<const longlong2 *>(a.ipartials) + 2 * tt + 1);
+    c_sel += c01.x;
+    c_nd += c01.y;
+    c_lk += c23.x;
   }
   aq = warp_sum(aq);
   as = warp_sum(as);
   ae = warp_sum(ae);
+  c_sel = warp_sum(c_sel);
+  c_nd = warp_sum(c_nd);
+  c_lk = warp_sum(c_lk);
   if (lane == 0) {
-    s_red[warp][0] = aq;
-    s_red[warp][1] = as;
-    s_red[warp][2] = ae;
+    s_fin[warp][0] = aq;
+    s_fin[warp][1] = as;
+    s_fin[warp][2] = ae;
+    s_ifin[warp][0] = c_sel;
+    s_ifin[warp][1] = c_nd;
+    s_ifin[warp][2] = c_lk;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double tq = 0.0, ts = 0.0, te = 0.0;
-    for (int w = 0; w < NW; w++) {
-      tq += s_red[w][0];
-      ts += s_red[w][1];
-      te += s_red[w][2];
-    }
-    volatile Scalars *vs = sc;
-    const int64_t sel = vs->sweep_sel, lk = vs->sweep_links, nd = vs->sweep_sel_nd;
-    const int64_t sw = vs->sweeps;
-    if (a.trace && sw < kLogCap) {
-      a.log_r[sw] = r;
-      a.log_sel[sw] = sel;
-      a.log_links[sw] = lk;
-      a.log_mode[sw] = 0;
-    }
-    const double r_next = tq + ts;   // r_{n+1} = q_n + s_n (a2)
-    const double e_tot = vs->e + te;
-    vs->e = e_tot;
-    vs->q = tq;
-    vs->s = ts;
-    vs->e_sw = te;
-    vs->r = r_next;
-    vs->sweeps = sw + 1;
-    vs->selected_total = vs->selected_total + sel;
-    vs->selected_nd_total = vs->selected_nd_total + nd;
-    vs->links_total = vs->links_total + lk;
-    vs->scanned_total = vs->scanned_total + a.n;
-    if (cyc && a.variant != DI_CYC) vs->guards = vs->guards + 1;
-    const double err = a.paper_err ? r_next / (1.0 - d - d * e_tot) : r_next;
-    const int stop = err <= a.tol;
-    vs->stop = stop;
-    vs->guard = (sel == 0 && !stop && a.variant == DI_SOP) ? 1 : 0;
-    int64_t tot = 0;
-    for (int b = 0; b < kBins; b++) tot += vs->bin_count[b];
-    vs->active = tot > 0;
-    vs->sweep_sel = 0;
-    vs->sweep_links = 0;
-    vs->sweep_sel_nd = 0;
-    vs->tile_ctr[par ^ 1] = 0;
-    vs->ticket = 0;
-    vs->epoch = epoch + 1;
+  if (threadIdx.x != 0) return;
+  double tq = 0.0, ts = 0.0, te = 0.0;
+  int64_t sel = 0, nd = 0, lk = 0;
+  for (int w = 0; w < nthreads / 32; w++) {
+    tq += s_fin[w][0];
+    ts += s_fin[w][1];
+    te += s_fin[w][2];
+    sel += s_ifin[w][0];
+    nd += s_ifin[w][1];
+    lk += s_ifin[w][2];
   }
+  volatile Scalars *vs = a.sc;
+  const int64_t sw = vs->sweeps;
+  const double d = vs->d, r = vs->r;
+  const int variant = vs->variant;
+  const bool guarded = vs->guard && variant != DI_CYC;
+  if (vs->trace && sw < kLogCap) {
+    a.log_r[sw] = r;
+    a.log_sel[sw] = sel;
+    a.log_links[sw] = lk;
+    a.log_mode[sw] = 0;
+  }
+  const double r_next = tq + ts;  // r_{n+1} = q_n + s_n (a2)
+  const double e_tot = vs->e + te;
+  vs->e = e_tot;
+  vs->q = tq;
+  vs->s = ts;
+  vs->e_sw = te;
+  vs->r = r_next;
+  vs->sweeps = sw + 1;
+  vs->selected_total = vs->selected_total + sel;
+  vs->selected_nd_total = vs->selected_nd_total + nd;
+  vs->links_total = vs->links_total + lk;
+  vs->scanned_total = vs->scanned_total + a.n;
+  if (guarded) vs->guards = vs->guards + 1;
+  const double err = vs->paper_err ? r_next / (1.0 - d - d * e_tot) : r_next;
+  const int stop = err <= vs->tol;
+  vs->stop = stop;
+  vs->guard = (sel == 0 && !stop && variant == DI_SOP) ? 1 : 0;
+  for (int b = 0; b < kBins; b++) {
+    vs->bin_count[b] = (int64_t)vs->bin_fill[b][0];
+    vs->bin_fill[b][0] = 0;
+  }
+  vs->ticket = 0;
+}
+
+__global__ void __launch_bounds__(kPushThreads) k_finalize(const SweepArgs a) {
+  finalize_sweep(a, kPushThreads);
+}
+
+// Static capacity of every bin (rows, or chunks for C) from the degrees, per select tile.
+__global__ void __launch_bounds__(kSelThreads) k_tile_caps(const int32_t *__restrict__ deg,
+                                                           int64_t n, int32_t *__restrict__ cap,
+                                                           int64_t ntiles) {
+  __shared__ int s_c[kBins];
+  if (threadIdx.x < kBins) s_c[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kSelTile;
+  int c[kBins] = {0, 0, 0, 0};
+  for (int k = threadIdx.x; k < kSelTile; k += kSelThreads) {
+    const int64_t i = base + k;
+    if (i >= n) break;
+    const int o = deg[i];
+    if (o == 0) continue;
+    const int b = bin_of(o);
+    const int inc = (b == BIN_C) ? (o + kChunk - 1) / kChunk : 1;
+#pragma unroll
+    for (int bb = 0; bb < kBins; bb++) c[bb] += (bb == b) ? inc : 0;
+  }
+#pragma unroll
+  for (int b = 0; b < kBins; b++) {
+    const int x = warp_sum(c[b]);
+    if ((threadIdx.x & 31) == 0 && x) atomicAdd(&s_c[b], x);
+  }
+  __syncthreads();
+  if (threadIdx.x < kBins) cap[(int64_t)threadIdx.x * ntiles + blockIdx.x] = s_c[threadIdx.x];
 }
 
 // ------------------------------------------------------------------ push (a5)
-struct PushArgs {
-  Frontier fr;
-  const int64_t *row_ptr;
-  const int32_t *col;
-  double *F;
-  int64_t lo;  // global id of local node 0 (self-loop test compares global ids)
-  Scalars *sc;
-};
-
-// one warp walks links [beg, end) of node gi, adding v to each target
-__device__ __forceinline__ void warp_row(const int32_t *__restrict__ col, double *__restrict__ F,
-                                         int64_t beg, int64_t end, int32_t gi, double v, int lane,
-                                         uint64_t pol) {
-  int64_t k = beg + lane;
-  for (; k + 96 < end; k += 128) {
-    const int32_t j0 = ld_col(col + k, pol), j1 = ld_col(col + k + 32, pol);
-    const int32_t j2 = ld_col(col + k + 64, pol), j3 = ld_col(col + k + 96, pol);
-    if (j0 != gi) red_add_f64(F + j0, v);
-    if (j1 != gi) red_add_f64(F + j1, v);
-    if (j2 != gi) red_add_f64(F + j2, v);
-    if (j3 != gi) red_add_f64(F + j3, v);
-  }
-  for (; k < end; k += 32) {
-    const int32_t j = ld_col(col + k, pol);
-    if (j != gi) red_add_f64(F + j, v);
+// Column ids are read as aligned int4 groups (one LSU instruction per 4 links); elements of a
+// group outside [beg, end) are masked. The col array carries 8 elements of tail padding.
+// Each valid target j != i receives v with a fire-and-forget RED.
+template <bool LOOPS>
+__device__ __forceinline__ void red_group(double *__restrict__ F, int4 x, int64_t p0, int64_t beg,
+                                          int64_t end, int32_t gi, double v, uint64_t fpol) {
+  const int32_t jj[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    const int64_t p = p0 + c;
+    if (p >= beg && p < end && (!LOOPS || jj[c] != gi)) red_add_f64_hint(F + jj[c], v, fpol);
   }
 }
 
-__global__ void __launch_bounds__(kPushThreads) k_push(const PushArgs a) {
+// rows of > kBinG links (bins W and C): one warp per row, entries walked in order (warp-uniform
+// broadcast loads, prefetched one ahead), 2 int4 groups (8 links) per lane in flight.
+template <bool LOOPS>
+__device__ __forceinline__ void push_rows_warp(const SweepArgs &a, int b, int64_t u0, int64_t u1,
+                                               int lane, uint64_t pol, uint64_t fpol) {
+  if (u0 >= u1) return;
+  const Entry *__restrict__ ent = a.fr.ent[b];
+  const int32_t *__restrict__ col = a.col;
+  double *__restrict__ F = a.F;
+  Entry nx = ent[u0];
+  for (int64_t u = u0; u < u1; u++) {
+    const Entry en = nx;
+    if (u + 1 < u1) nx = ent[u + 1];
+    const int32_t gi = LOOPS ? (int32_t)(a.fr.id[b][u] + a.lo) : -1;
+    const int64_t beg = (int64_t)(en.bl & kBegMask);
+    const int64_t end = beg + (int64_t)(en.bl >> kLenShift);
+    const int64_t a0 = beg & ~3ll;
+    const int nvec = (int)((end - a0 + 3) >> 2);
+    for (int vb = 0; vb < nvec; vb += 64) {
+      const int v0 = vb + lane, v1 = vb + 32 + lane;
+      int4 x0 = make_int4(0, 0, 0, 0), x1 = make_int4(0, 0, 0, 0);
+      if (v0 < nvec) x0 = ld_col4(col + a0 + 4 * (int64_t)v0, pol);
+      if (v1 < nvec) x1 = ld_col4(col + a0 + 4 * (int64_t)v1, pol);
+      if (v0 < nvec) red_group<LOOPS>(F, x0, a0 + 4 * (int64_t)v0, beg, end, gi, en.v, fpol);
+      if (v1 < nvec) red_group<LOOPS>(F, x1, a0 + 4 * (int64_t)v1, beg, end, gi, en.v, fpol);
+    }
+  }
+}
+
+template <bool LOOPS, int MINB>
+__global__ void __launch_bounds__(kPushThreads, MINB) k_push(const SweepArgs a) {
+  __shared__ bool s_last;
   Scalars *sc = a.sc;
-  if (!sc->active) return;
+  if (sc->stop) return;
   const uint64_t pol = policy_evict_first();
+  const uint64_t fpol = a.red_hint ? policy_evict_last() : policy_evict_normal();
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * (kPushThreads / 32);
   const int64_t w = (int64_t)blockIdx.x * (kPushThreads / 32) + (threadIdx.x >> 5);
-  const int64_t *__restrict__ rp = a.row_ptr;
+  const int32_t *__restrict__ col = a.col;
   double *__restrict__ F = a.F;
-  // ---- bin C: hub rows, fixed-size chunks of kChunk links, one warp per chunk
+  int64_t U[kBins];
+#pragma unroll
+  for (int b = 0; b < kBins; b++) U[b] = (int64_t)sc->bin_fill[b][0];
+  // ---- bins C (hub chunks) and W: warp per row
+  push_rows_warp<LOOPS>(a, BIN_C, w * U[BIN_C] / W, (w + 1) * U[BIN_C] / W, lane, pol, fpol);
+  push_rows_warp<LOOPS>(a, BIN_W, w * U[BIN_W] / W, (w + 1) * U[BIN_W] / W, lane, pol, fpol);
+  // ---- bin G (9..32 links): 8-lane group per row, 4 rows per warp step; <= 9 int4 groups
   {
-    const int64_t U = sc->bin_count[BIN_C];
-    const int64_t u0 = w * U / W, u1 = (w + 1) * U / W;
-    for (int64_t u = u0; u < u1; u++) {
-      const int32_t i = a.fr.ids[BIN_C][u];
-      const double v = a.fr.val[BIN_C][u];
-      const int64_t beg = rp[i] + (int64_t)a.fr.chunk[u] * kChunk;
-      const int64_t end = min(beg + (int64_t)kChunk, rp[i + 1]);
-      warp_row(a.col, F, beg, end, (int32_t)(i + a.lo), v, lane, pol);
-    }
-  }
-  // ---- bin W: one warp per node
-  {
-    const int64_t U = sc->bin_count[BIN_W];
-    const int64_t u0 = w * U / W, u1 = (w + 1) * U / W;
-    for (int64_t u = u0; u < u1; u++) {
-      const int32_t i = a.fr.ids[BIN_W][u];
-      const double v = a.fr.val[BIN_W][u];
-      warp_row(a.col, F, rp[i], rp[i + 1], (int32_t)(i + a.lo), v, lane, pol);
-    }
-  }
-  // ---- bin G: 8-lane group per node, 4 nodes per warp step
-  {
-    const int64_t U = sc->bin_count[BIN_G];
-    const int64_t u0 = w * U / W, u1 = (w + 1) * U / W;
+    const int64_t u0 = w * U[BIN_G] / W, u1 = (w + 1) * U[BIN_G] / W;
     const int sub = lane & 7;
     for (int64_t u = u0 + (lane >> 3); u < u1; u += 4) {
-      const int32_t i = a.fr.ids[BIN_G][u];
-      const double v = a.fr.val[BIN_G][u];
-      const int32_t gi = (int32_t)(i + a.lo);
-      const int64_t end = rp[i + 1];
-      for (int64_t k = rp[i] + sub; k < end; k += 8) {
-        const int32_t j = ld_col(a.col + k, pol);
-        if (j != gi) red_add_f64(F + j, v);
-      }
+      const Entry en = a.fr.ent[BIN_G][u];
+      const int32_t gi = LOOPS ? (int32_t)(a.fr.id[BIN_G][u] + a.lo) : -1;
+      const int64_t beg = (int64_t)(en.bl & kBegMask);
+      const int64_t end = beg + (int64_t)(en.bl >> kLenShift);
+      const int64_t a0 = beg & ~3ll;
+      const int nvec = (int)((end - a0 + 3) >> 2);
+      int4 x0 = make_int4(0, 0, 0, 0), x1 = make_int4(0, 0, 0, 0);
+      if (sub < nvec) x0 = ld_col4(col + a0 + 4 * sub, pol);
+      if (sub + 8 < nvec) x1 = ld_col4(col + a0 + 4 * (sub + 8), pol);
+      if (sub < nvec) red_group<LOOPS>(F, x0, a0 + 4 * sub, beg, end, gi, en.v, fpol);
+      if (sub + 8 < nvec) red_group<LOOPS>(F, x1, a0 + 4 * (sub + 8), beg, end, gi, en.v, fpol);
     }
   }
-  // ---- bin T: one thread per node
+  // ---- bin T (1..8 links): one thread per row; <= 3 int4 groups
   {
-    const int64_t U = sc->bin_count[BIN_T];
-    const int64_t u0 = w * U / W, u1 = (w + 1) * U / W;
+    const int64_t u0 = w * U[BIN_T] / W, u1 = (w + 1) * U[BIN_T] / W;
     for (int64_t u = u0 + lane; u < u1; u += 32) {
-      const int32_t i = a.fr.ids[BIN_T][u];
-      const double v = a.fr.val[BIN_T][u];
-      const int32_t gi = (int32_t)(i + a.lo);
-      const int64_t beg = rp[i], end = rp[i + 1];
-      int32_t js[kBinT];
-#pragma unroll
-      for (int k = 0; k < kBinT; k++) js[k] = (beg + k < end) ? ld_col(a.col + beg + k, pol) : gi;
-#pragma unroll
-      for (int k = 0; k < kBinT; k++)
-        if (js[k] != gi) red_add_f64(F + js[k], v);
+      const Entry en = a.fr.ent[BIN_T][u];
+      const int32_t gi = LOOPS ? (int32_t)(a.fr.id[BIN_T][u] + a.lo) : -1;
+      const int64_t beg = (int64_t)(en.bl & kBegMask);
+      const int64_t end = beg + (int64_t)(en.bl >> kLenShift);
+      const int64_t a0 = beg & ~3ll;
+      const int nvec = (int)((end - a0 + 3) >> 2);
+      const int4 x0 = ld_col4(col + a0, pol);
+      int4 x1 = make_int4(0, 0, 0, 0), x2 = make_int4(0, 0, 0, 0);
+      if (nvec > 1) x1 = ld_col4(col + a0 + 4, pol);
+      if (nvec > 2) x2 = ld_col4(col + a0 + 8, pol);
+      red_group<LOOPS>(F, x0, a0, beg, end, gi, en.v, fpol);
+      if (nvec > 1) red_group<LOOPS>(F, x1, a0 + 4, beg, end, gi, en.v, fpol);
+      if (nvec > 2) red_group<LOOPS>(F, x2, a0 + 8, beg, end, gi, en.v, fpol);
     }
   }
+  // ---- the last block to finish finalises the sweep
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  finalize_sweep(a, kPushThreads);
 }
 
-int push_grid(const Graph &g) {
+template <bool LOOPS, int MINB>
+void launch_push_t(const Graph &g, const SweepArgs &a) {
   static int occ = 0;
   if (occ == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push, kPushThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push<LOOPS, MINB>, kPushThreads, 0);
     if (occ < 1) occ = 1;
   }
-  return g.num_sms * occ;
+  k_push<LOOPS, MINB><<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a);
+}
+
+SweepArgs sweep_args(Graph &g, int test_mode) {
+  SweepArgs a;
+  a.F = g.F;
+  a.H = g.H;
+  a.deg = g.deg;
+  a.kloop = g.kloop;
+  a.row_ptr = g.row_ptr;
+  a.col = g.col;
+  a.n = g.n;
+  a.lo = g.lo;
+  a.ntiles = select_tiles(g.n);
+  a.L_total = (double)g.l_global;
+  a.sc = g.sc;
+  a.fr = g.fr;
+  a.partials = g.partials;
+  a.ipartials = g.ipartials;
+  a.log_r = g.log_r;
+  a.log_sel = g.log_sel;
+  a.log_links = g.log_links;
+  a.log_mode = g.log_mode;
+  a.test_mode = test_mode;
+  a.red_hint = g.red_hint;
+  return a;
 }
 
 }  // namespace
@@ -587,24 +677,26 @@ di_status alloc_state(Graph &g) {
   DI_CK(cudaMemset(g.sc, 0, sizeof(Scalars)));
   DI_CK(cudaMallocHost(&g.sc_host, sizeof(Scalars)));
   memset(g.sc_host, 0, sizeof(Scalars));
-  g.sc_host->epoch = 1;
-  DI_CK(cudaMemcpy(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice));
   DI_CK(cudaMalloc(&g.partials, (size_t)nt * 3 * 8));
+  DI_CK(cudaMalloc(&g.ipartials, (size_t)nt * 4 * 8));
   const int rg = reduce_grid(n, g.num_sms);
   DI_CK(cudaMalloc(&g.red_partials, (size_t)rg * 8));
-  DI_CK(cudaMalloc(&g.tile_flag, (size_t)nt * 4));
-  DI_CK(cudaMemset(g.tile_flag, 0, (size_t)nt * 4));
-  DI_CK(cudaMalloc(&g.tile_agg, (size_t)nt * kBins * 8));
-  DI_CK(cudaMalloc(&g.tile_incl, (size_t)nt * kBins * 8));
+  // frontier: per-bin capacity = rows (chunks for C) whose static degree falls in the bin
+  g.ntiles = nt;
+  int32_t *cap = nullptr;
+  DI_CK(cudaMalloc(&cap, (size_t)nt * kBins * 4));
+  k_tile_caps<<<(unsigned)nt, kSelThreads>>>(g.deg, n, cap, nt);
+  std::vector<int32_t> hcap((size_t)nt * kBins);
+  DI_CK(cudaMemcpy(hcap.data(), cap, (size_t)nt * kBins * 4, cudaMemcpyDeviceToHost));
+  cudaFree(cap);
   for (int b = 0; b < kBins; b++) {
-    int64_t cap = n;
-    if (b == BIN_C) cap = n + g.l / kChunk + 1;
-    if (cap < 1) cap = 1;
-    g.fr.cap[b] = cap;
-    DI_CK(cudaMalloc(&g.fr.ids[b], (size_t)cap * 4));
-    DI_CK(cudaMalloc(&g.fr.val[b], (size_t)cap * 8));
+    int64_t acc = 0;
+    for (int64_t t = 0; t < nt; t++) acc += hcap[(size_t)b * nt + t];
+    g.fr.cap[b] = acc;
+    const size_t cap_b = (size_t)std::max<int64_t>(acc, 1);
+    DI_CK(cudaMalloc(&g.fr.ent[b], cap_b * sizeof(Entry)));
+    DI_CK(cudaMalloc(&g.fr.id[b], cap_b * 4));
   }
-  DI_CK(cudaMalloc(&g.fr.chunk, (size_t)g.fr.cap[BIN_C] * 4));
   DI_CK(cudaMalloc(&g.log_r, (size_t)kLogCap * 8));
   DI_CK(cudaMalloc(&g.log_sel, (size_t)kLogCap * 8));
   DI_CK(cudaMalloc(&g.log_links, (size_t)kLogCap * 8));
@@ -633,32 +725,8 @@ void launch_reduce_F_setr(Graph &g, int64_t *launches) {
   *launches += 1;
 }
 
-void launch_select(Graph &g, double d, double tol, int variant, int paper_err, int trace,
-                   int test_mode, int64_t *launches) {
-  SelectArgs a;
-  a.F = g.F;
-  a.H = g.H;
-  a.deg = g.deg;
-  a.kloop = g.kloop;
-  a.n = g.n;
-  a.ntiles = select_tiles(g.n);
-  a.L_total = (double)g.l_global;
-  a.d = d;
-  a.tol = tol;
-  a.variant = variant;
-  a.paper_err = paper_err;
-  a.trace = trace;
-  a.test_mode = test_mode;
-  a.sc = g.sc;
-  a.fr = g.fr;
-  a.partials = g.partials;
-  a.tflag = g.tile_flag;
-  a.tagg = g.tile_agg;
-  a.tincl = g.tile_incl;
-  a.log_r = g.log_r;
-  a.log_sel = g.log_sel;
-  a.log_links = g.log_links;
-  a.log_mode = g.log_mode;
+void launch_select(Graph &g, int test_mode, int64_t *launches) {
+  const SweepArgs a = sweep_args(g, test_mode);
   if (g.has_loops)
     k_select<true><<<(unsigned)a.ntiles, kSelThreads, 0, g.stream>>>(a);
   else
@@ -667,14 +735,19 @@ void launch_select(Graph &g, double d, double tol, int variant, int paper_err, i
 }
 
 void launch_push(Graph &g, int64_t *launches) {
-  PushArgs a;
-  a.fr = g.fr;
-  a.row_ptr = g.row_ptr;
-  a.col = g.col;
-  a.F = g.F;
-  a.lo = g.lo;
-  a.sc = g.sc;
-  k_push<<<push_grid(g), kPushThreads, 0, g.stream>>>(a);
+  const SweepArgs a = sweep_args(g, 0);
+  if (g.has_loops)
+    launch_push_t<true, 4>(g, a);
+  else if (g.push_occ >= 6)
+    launch_push_t<false, 6>(g, a);
+  else
+    launch_push_t<false, 4>(g, a);
+  *launches += 1;
+}
+
+void launch_finalize(Graph &g, int64_t *launches) {
+  const SweepArgs a = sweep_args(g, 1);
+  k_finalize<<<1, kPushThreads, 0, g.stream>>>(a);
   *launches += 1;
 }
 

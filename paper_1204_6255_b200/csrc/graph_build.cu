@@ -182,7 +182,9 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   g.l_global = Lk;
   const size_t LkS = (size_t)(Lk > 0 ? Lk : 1);
   DI_CK(cudaMalloc(&g.row_ptr, ((size_t)n + 1) * 8));
-  DI_CK(cudaMalloc(&g.col, LkS * 4));
+  // +8 elements of padding: the push reads whole aligned int4 groups around each row
+  DI_CK(cudaMalloc(&g.col, (LkS + 8) * 4));
+  DI_CK(cudaMemsetAsync(g.col + LkS, 0, 8 * 4, st));
   DI_CK(cudaMalloc(&g.deg, (size_t)n * 4));
   DI_CK(cudaMalloc(&g.kloop, (size_t)n * 4));
   DI_CK(cudaMemsetAsync(g.kloop, 0, (size_t)n * 4, st));
