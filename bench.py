@@ -136,7 +136,7 @@ def run_ours(args):
     t_d = torch.from_numpy(dst).to(dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    g = di.Graph(s_d, t_d, n, stream=stream)
+    g = di.Graph(s_d, t_d, n, build_csc=True, stream=stream)
     torch.cuda.synchronize()
     init_ms = (time.perf_counter() - t0) * 1e3
     del s_d, t_d
@@ -148,7 +148,7 @@ def run_ours(args):
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        st = g.solve(d=D, tol=TOL, variant=args.variant, profile=profile)
+        st = g.solve(d=D, tol=TOL, variant=args.variant, profile=profile, mode=args.mode)
         ev1.record(stream)
         ev1.synchronize()
         assert st["converged"] == 1, st
@@ -189,7 +189,7 @@ def run_ours(args):
     achieved = push_bytes / (push_ms * 1e-3) / 1e9 if push_ms > 0 else 0.0
     tr = ncu_traffic()
     counted = sum(s["counted_bytes"] for s in stats)
-    roofline = {"bound": "hbm", "kernel": "k_push (a5, degree-binned fp64 RED push)",
+    roofline = {"bound": "hbm", "kernel": "k_push + k_pull (a5/a5': diffusion of the frontier's fluid)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": tr,
                 "peak_source": peak_src,
@@ -209,8 +209,8 @@ def run_ours(args):
     for k in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        gh = di.Graph(src_p, dst_p, n, stream=stream)     # DI_HOST_PTRS: H2D inside the call
-        st = gh.solve(d=D, tol=TOL, variant=args.variant)
+        gh = di.Graph(src_p, dst_p, n, build_csc=True, stream=stream)  # DI_HOST_PTRS: H2D inside
+        st = gh.solve(d=D, tol=TOL, variant=args.variant, mode=args.mode)
         H = gh.history()
         H_host.copy_(H, non_blocking=True)
         torch.cuda.synchronize()
@@ -236,7 +236,7 @@ def run_ours(args):
         "data": "synthetic (seeded R-MAT + repair, digen; stands in for uk-2007-05 / gr0.California)",
         "config": {"workload": f"{args.config}: " + __import__("digen").CONFIGS[args.config].note,
                    "n": n, "links": L, "variant": "DI-" + args.variant.upper(), "d": D,
-                   "tol_l1_fluid": TOL, "seed": args.seed,
+                   "tol_l1_fluid": TOL, "seed": args.seed, "sweep_mode": args.mode,
                    "l2": "inputs > 126 MB L2 and 512 MiB L2 flush before each step",
                    "parallelism": "1-D node range" if world > 1 else "single GPU",
                    "init_build_ms": round(init_ms, 1), "generator_s": round(gen_s, 1)},
@@ -304,6 +304,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4")
     ap.add_argument("--variant", default="sop", choices=["sop", "cyc"])
+    ap.add_argument("--mode", default="auto", choices=["push", "pull", "auto"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)

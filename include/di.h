@@ -57,6 +57,9 @@ typedef enum {
 #define DI_BUILD_CSC        0x4u  /* also build the in-link (CSC) index: pull variant, PI, GS     */
 #define DI_HOST_PTRS        0x8u  /* src/dst are host pointers (copied inside the call)           */
 #define DI_LOCAL_LINKS      0x10u /* multi-GPU: each rank passes only links whose src it owns     */
+#define DI_NO_REORDER       0x20u /* keep the caller's node numbering internally (default relabels
+                                     by descending in-degree for L2 locality; results are always
+                                     returned in the caller's numbering)                          */
 
 /* di_solve flags */
 #define DI_PUSH         0x0u   /* push-only sweeps (default)                                       */

@@ -26,7 +26,11 @@ di_status di_test_select(di_graph g, const double *F_in, const double *H_in, dou
                          int64_t bin_off[5], double scal[3], int64_t counts[2], double *F_out,
                          double *H_out);
 
-/* Copy the device CSR (and CSC if built) to host arrays (each may be NULL). */
+/* Internal numbering: old_of[k] = caller id of internal node k (identity with DI_NO_REORDER). */
+di_status di_test_perm(di_graph g, int32_t *old_of);
+
+/* Copy the device CSR (and CSC if built), in the internal numbering, to host arrays
+ * (each may be NULL). */
 di_status di_test_csr(di_graph g, int64_t *row_ptr, int32_t *col, int32_t *deg, int32_t *kloop,
                       int64_t *csc_ptr, int32_t *csc_row);
 

@@ -30,7 +30,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 DI_OK, DI_NOT_CONVERGED = 0, 1
 DI_EINVAL, DI_ENOMEM, DI_ECUDA, DI_ENCCL, DI_ESTATE = -1, -2, -3, -4, -5
 VARIANTS = {"sop": 0, "cyc": 1, "pi": 2, "pi_pull": 2, "pi_push": 3, "pi_col": 3, "gs": 4, "gs_block": 4}
-DEDUP, DROP_SELF_LOOPS, BUILD_CSC, HOST_PTRS, LOCAL_LINKS = 0x1, 0x2, 0x4, 0x8, 0x10
+DEDUP, DROP_SELF_LOOPS, BUILD_CSC, HOST_PTRS, LOCAL_LINKS, NO_REORDER = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 PUSH, PULL, AUTO, RESUME, PAPER_ERROR, TRACE, PROFILE, GRAPH_LOOP = 0x0, 0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
 
 
@@ -79,12 +79,14 @@ _lib.di_test_select.restype = _ci
 _lib.di_test_select.argtypes = [_vp, _vp, _vp, _dbl, _dbl, _ci, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
 _lib.di_test_csr.restype = _ci
 _lib.di_test_csr.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp]
+_lib.di_test_perm.restype = _ci
+_lib.di_test_perm.argtypes = [_vp, _vp]
 _lib.di_test_bins.restype = _ci
 _lib.di_test_bins.argtypes = [_vp]
 
 EXPORTED = ["di_graph_upload", "di_graph_range", "di_graph_links", "di_solve", "di_residual",
             "di_history", "di_sweep_log", "di_graph_free", "di_last_error",
-            "di_test_select", "di_test_csr", "di_test_bins"]
+            "di_test_select", "di_test_csr", "di_test_bins", "di_test_perm"]
 
 
 class DIError(RuntimeError):
@@ -116,11 +118,11 @@ class Graph:
     (device pointers) or host arrays / CPU tensors (copied with DI_HOST_PTRS)."""
 
     def __init__(self, src, dst, n, dedup=False, drop_self_loops=False, build_csc=False,
-                 stream=None):
+                 reorder=True, stream=None):
         torch = _torch()
         self.n = int(n)
         flags = (DEDUP if dedup else 0) | (DROP_SELF_LOOPS if drop_self_loops else 0) | \
-                (BUILD_CSC if build_csc else 0)
+                (BUILD_CSC if build_csc else 0) | (0 if reorder else NO_REORDER)
         keep = []
         if isinstance(src, torch.Tensor) and src.is_cuda:
             s = src.to(torch.int32).contiguous()
@@ -221,6 +223,11 @@ class Graph:
         if csc:
             out.update(csc_ptr=cp, csc_row=cr)
         return out
+
+    def test_perm(self):
+        old_of = np.empty(self.n, dtype=np.int32)
+        _check(_lib.di_test_perm(self._h, old_of.ctypes.data))
+        return old_of
 
     def test_select(self, F, H, r, d=0.85, variant="sop"):
         F = np.ascontiguousarray(F, dtype=np.float64)

@@ -28,6 +28,19 @@ __global__ void k_check_B(const double *B, int64_t n, int *bad) {
   }
 }
 
+// out[k] = in[idx[k]] (idx = NULL: plain copy)
+__global__ void k_gather(double *__restrict__ out, const double *__restrict__ in,
+                         const int32_t *__restrict__ idx, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = in[idx ? idx[k] : k];
+}
+
+void gather(const Graph &g, double *out, const double *in, const int32_t *idx) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((g.n + 255) / 256, 16 * g.num_sms));
+  k_gather<<<grid, 256, 0, g.stream>>>(out, in, idx, g.n);
+}
+
 di_status fail(di_status s, const std::string &msg) {
   set_error(msg);
   return s;
@@ -51,6 +64,7 @@ struct EventSet {
 void free_graph(Graph *g) {
   if (!g) return;
   void *ptrs[] = {g->row_ptr, g->col, g->deg, g->kloop, g->csc_ptr, g->csc_row, g->F, g->H,
+                  g->new_of, g->old_of, g->Bperm, g->xfer,
                   g->S, g->aux, g->sc, g->partials, g->ipartials, g->red_partials,
                   g->log_r, g->log_sel, g->log_links, g->log_mode};
   for (void *p : ptrs)
@@ -60,6 +74,8 @@ void free_graph(Graph *g) {
     for (void *p : q)
       if (p) cudaFree(p);
   }
+  for (int b = 0; b < kPullBins; b++)
+    if (g->pe[b]) cudaFree(g->pe[b]);
   if (g->sc_host) cudaFreeHost(g->sc_host);
   delete g;
 }
@@ -102,8 +118,11 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
   g->hi = n_nodes;
   if (const char *e = getenv("DI_RED_HINT")) g->red_hint = atoi(e);
   if (const char *e = getenv("DI_PUSH_OCC")) g->push_occ = atoi(e);
+  if (const char *e = getenv("DI_AUTO_RATIO")) g->auto_ratio = atof(e);
+  if (const char *e = getenv("DI_STRIPES")) g->stripes = atoi(e);
   di_status s = build_graph(*g, src, dst, n_links, flags);
   if (s == DI_OK) s = alloc_state(*g);
+  if (s == DI_OK) s = alloc_pull(*g);
   if (s != DI_OK) {
     free_graph(g);
     return s;
@@ -158,8 +177,9 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   }
   if (v == DI_PI_PULL || v == DI_PI_PUSH || v == DI_GS_BLOCK)
     return run_comparator(g, d, tol, (int)v, max_sweeps, flags, st);
-  if (flags & (DI_PULL | DI_AUTO))
-    return fail(DI_EINVAL, "di_solve: pull sweeps are not available in this build");
+  const int mode = (flags & DI_PULL) ? MODE_PULL : ((flags & DI_AUTO) ? MODE_AUTO : MODE_PUSH);
+  if (mode != MODE_PUSH && !g.has_csc)
+    return fail(DI_EINVAL, "di_solve: DI_PULL / DI_AUTO need the CSC (upload with DI_BUILD_CSC)");
   const bool resume = flags & DI_RESUME;
   if (resume && !g.solved) return fail(DI_ESTATE, "di_solve: DI_RESUME before any solve");
   const int paper = (flags & DI_PAPER_ERROR) ? 1 : 0;
@@ -185,11 +205,20 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     s.variant = (int32_t)v;
     s.paper_err = paper;
     s.trace = trace;
+    s.mode = mode;
+    s.pull_thr = (int64_t)(g.auto_ratio * (double)g.l_global);
   }
   DI_CK(cudaEventRecord(t0, g.stream));
   DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
+  const double *Bint = B;
+  if (B && g.reordered) {   // B arrives in the caller's numbering
+    if (!g.Bperm) DI_CK(cudaMalloc(&g.Bperm, (size_t)g.n * 8));
+    gather(g, g.Bperm, B, g.old_of);
+    launches++;
+    Bint = g.Bperm;
+  }
   if (!resume)
-    launch_init(g, B, d, &launches);
+    launch_init(g, Bint, d, &launches);
   else
     launch_reduce_F_setr(g, &launches);
   di_status s = sync_scalars(g);
@@ -209,7 +238,8 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
       if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 0), g.stream));
       launch_select(g, 0, &launches);
       if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 1), g.stream));
-      launch_push(g, &launches);
+      if (mode != MODE_PULL) launch_push(g, &launches);
+      if (mode != MODE_PUSH) launch_pull(g, &launches);
       if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 2), g.stream));
     }
     launched += k;
@@ -308,7 +338,10 @@ di_status di_residual(di_graph h, double *l1_out, double *F_out) {
   if (s != DI_OK) return s;
   if (l1_out) *l1_out = g->sc_host->resid;
   if (F_out) {
-    DI_CK(cudaMemcpyAsync(F_out, g->F, (size_t)g->n * 8, cudaMemcpyDeviceToDevice, g->stream));
+    if (g->reordered)
+      gather(*g, F_out, g->F, g->new_of);
+    else
+      DI_CK(cudaMemcpyAsync(F_out, g->F, (size_t)g->n * 8, cudaMemcpyDeviceToDevice, g->stream));
     DI_CK(cudaStreamSynchronize(g->stream));
   }
   return DI_OK;
@@ -317,7 +350,10 @@ di_status di_residual(di_graph h, double *l1_out, double *F_out) {
 di_status di_history(di_graph h, double *H_out) {
   Graph *g = (Graph *)h;
   if (!g || !H_out) return fail(DI_EINVAL, "di_history: NULL argument");
-  DI_CK(cudaMemcpyAsync(H_out, g->H, (size_t)g->n * 8, cudaMemcpyDeviceToDevice, g->stream));
+  if (g->reordered)
+    gather(*g, H_out, g->H, g->new_of);
+  else
+    DI_CK(cudaMemcpyAsync(H_out, g->H, (size_t)g->n * 8, cudaMemcpyDeviceToDevice, g->stream));
   DI_CK(cudaStreamSynchronize(g->stream));
   return DI_OK;
 }
@@ -347,6 +383,17 @@ di_status di_test_bins(int32_t out[4]) {
   return DI_OK;
 }
 
+di_status di_test_perm(di_graph h, int32_t *old_of) {
+  Graph *g = (Graph *)h;
+  if (!g || !old_of) return fail(DI_EINVAL, "NULL argument");
+  if (!g->reordered) {
+    for (int64_t k = 0; k < g->n; k++) old_of[k] = (int32_t)k;
+    return DI_OK;
+  }
+  DI_CK(cudaMemcpy(old_of, g->old_of, (size_t)g->n * 4, cudaMemcpyDeviceToHost));
+  return DI_OK;
+}
+
 di_status di_test_csr(di_graph h, int64_t *row_ptr, int32_t *col, int32_t *deg, int32_t *kloop,
                       int64_t *csc_ptr, int32_t *csc_row) {
   Graph *g = (Graph *)h;
@@ -373,8 +420,21 @@ di_status di_test_select(di_graph h, const double *F_in, const double *H_in, dou
   if (v != DI_SOP && v != DI_CYC) return fail(DI_EINVAL, "di_test_select: DI_SOP or DI_CYC");
   Graph &g = *gp;
   const size_t n = (size_t)g.n;
-  DI_CK(cudaMemcpy(g.F, F_in, n * 8, cudaMemcpyHostToDevice));
-  DI_CK(cudaMemcpy(g.H, H_in, n * 8, cudaMemcpyHostToDevice));
+  std::vector<int32_t> old_of;
+  if (g.reordered) {
+    old_of.resize(n);
+    DI_CK(cudaMemcpy(old_of.data(), g.old_of, n * 4, cudaMemcpyDeviceToHost));
+    std::vector<double> Fi(n), Hi(n);
+    for (size_t k = 0; k < n; k++) {
+      Fi[k] = F_in[old_of[k]];
+      Hi[k] = H_in[old_of[k]];
+    }
+    DI_CK(cudaMemcpy(g.F, Fi.data(), n * 8, cudaMemcpyHostToDevice));
+    DI_CK(cudaMemcpy(g.H, Hi.data(), n * 8, cudaMemcpyHostToDevice));
+  } else {
+    DI_CK(cudaMemcpy(g.F, F_in, n * 8, cudaMemcpyHostToDevice));
+    DI_CK(cudaMemcpy(g.H, H_in, n * 8, cudaMemcpyHostToDevice));
+  }
   {
     Scalars &s = *g.sc_host;
     const uint32_t epoch = s.epoch ? s.epoch : 1;
@@ -413,17 +473,19 @@ di_status di_test_select(di_graph h, const double *F_in, const double *H_in, dou
       DI_CK(cudaMemcpy(ent.data(), g.fr.ent[b], m * sizeof(Entry), cudaMemcpyDeviceToHost));
       DI_CK(cudaMemcpy(eid.data(), g.fr.id[b], m * 4, cudaMemcpyDeviceToHost));
     }
+    std::vector<int32_t> uid(m);   // caller's numbering
+    for (size_t k = 0; k < m; k++) uid[k] = g.reordered ? old_of[eid[k]] : eid[k];
     std::vector<size_t> order(m);
     for (size_t k = 0; k < m; k++) order[k] = k;
     std::sort(order.begin(), order.end(), [&](size_t x, size_t y) {
-      if (eid[x] != eid[y]) return eid[x] < eid[y];
+      if (uid[x] != uid[y]) return uid[x] < uid[y];
       return (ent[x].bl & kBegMask) < (ent[y].bl & kBegMask);
     });
     for (size_t k = 0; k < m; k++) {
       const size_t slot = order[k];
       const int32_t id = eid[slot];
       const int64_t beg = (int64_t)(ent[slot].bl & kBegMask);
-      if (ids) ids[off] = id;
+      if (ids) ids[off] = uid[slot];
       if (vals) vals[off] = ent[slot].v;
       if (chunk) chunk[off] = (int32_t)((beg - rp[id]) / kChunk);
       off++;
@@ -438,8 +500,14 @@ di_status di_test_select(di_graph h, const double *F_in, const double *H_in, dou
     counts[0] = c.selected_total;
     counts[1] = c.links_total;
   }
-  if (F_out) DI_CK(cudaMemcpy(F_out, g.F, n * 8, cudaMemcpyDeviceToHost));
-  if (H_out) DI_CK(cudaMemcpy(H_out, g.H, n * 8, cudaMemcpyDeviceToHost));
+  std::vector<double> Fo(n), Ho(n);
+  DI_CK(cudaMemcpy(Fo.data(), g.F, n * 8, cudaMemcpyDeviceToHost));
+  DI_CK(cudaMemcpy(Ho.data(), g.H, n * 8, cudaMemcpyDeviceToHost));
+  for (size_t k = 0; k < n; k++) {
+    const size_t u = g.reordered ? (size_t)old_of[k] : k;
+    if (F_out) F_out[u] = Fo[k];
+    if (H_out) H_out[u] = Ho[k];
+  }
   return DI_OK;
 }
 

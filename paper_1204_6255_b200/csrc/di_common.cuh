@@ -31,6 +31,23 @@ constexpr int kLogCap = 1 << 16;  // per-sweep trace capacity
 
 enum BinId { BIN_T = 0, BIN_G = 1, BIN_W = 2, BIN_C = 3 };
 
+// Pull (CSC) variant, SURVEY §8(a) a5': static bins of target rows by in-degree.
+//   P0: 1..kPullT in-links -> one thread per row
+//   P1: ..kPullG           -> 8-lane group per row
+//   P2: ..kPullChunk       -> one warp per row
+//   P3: > kPullChunk       -> rows split in kPullChunk chunks, one warp each (partial sums
+//                             added with an fp64 atomic; every other row is a plain RMW)
+constexpr int kPullBins = 4;
+constexpr int kPullT = 8;
+constexpr int kPullG = 128;
+constexpr int kPullChunk = 8192;
+struct __align__(16) PullEntry {
+  int64_t beg;   // first in-link (csc_row index)
+  int32_t len;   // in-links in this entry
+  int32_t j;     // target node (local id)
+};
+enum SweepMode { MODE_PUSH = 0, MODE_PULL = 1, MODE_AUTO = 2 };
+
 // Device-resident sweep state. Every field is written only by the "last block" of the
 // select kernel (the finaliser) or by the host between solves, so kernels never race on it.
 struct __align__(256) Scalars {
@@ -39,7 +56,9 @@ struct __align__(256) Scalars {
   double q, s, e_sw; // last sweep: unselected fluid, pushed fluid, dangling absorbed
   double resid;      // exact sum F from the reduce kernel
   double d, tol;     // solve parameters (device-resident: kernels take constant arguments)
-  int32_t variant, paper_err, trace, pad1;
+  int32_t variant, paper_err, trace, mode;  // mode: SweepMode
+  int64_t pull_thr;  // DI_AUTO: a sweep with more than pull_thr links runs in pull mode
+  unsigned long long fill_links[32];  // DI_AUTO: links of the current frontier (own line)
   int32_t stop;      // 1: convergence reached after the current sweep's push
   int32_t guard;     // 1: next sweep runs with threshold 0 (starvation guard, reading G5)
   int32_t active;    // 1: the current sweep emitted push work
@@ -88,6 +107,12 @@ struct Graph {
   int push_occ = 4;         // k_push min blocks per SM (DI_PUSH_OCC)
   int red_hint = 1;         // L2 evict_last hint on the push's REDs into F (DI_RED_HINT=0 disables)
   int rank = 0, world = 1;
+  // locality relabelling: internal id = new_of[user id]; user id = old_of[internal id]
+  bool reordered = false;
+  int stripes = 4096;        // relabelling stripes (DI_STRIPES; 1 = plain degree order)
+  int32_t *new_of = nullptr, *old_of = nullptr;
+  double *Bperm = nullptr;   // B in internal order (custom B)
+  double *xfer = nullptr;    // scratch for permuted copies
   // CSR (sources owned), global column ids
   int64_t *row_ptr = nullptr;
   int32_t *col = nullptr;
@@ -96,6 +121,10 @@ struct Graph {
   // CSC (in-links of owned targets)
   int64_t *csc_ptr = nullptr;
   int32_t *csc_row = nullptr;
+  // pull variant: static row entries per in-degree bin
+  PullEntry *pe[kPullBins] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t pe_count[kPullBins] = {0, 0, 0, 0};
+  double auto_ratio = 0.35; // DI_AUTO threshold on links(S_n)/L (DI_AUTO_RATIO)
   // state
   double *F = nullptr, *H = nullptr;
   double *S = nullptr;       // pull mode: dense per-node sent value
@@ -142,6 +171,7 @@ void launch_select(Graph &g, int test_mode, int64_t *launches);
 void launch_push(Graph &g, int64_t *launches);
 void launch_finalize(Graph &g, int64_t *launches);
 void launch_pull(Graph &g, int64_t *launches);
+di_status alloc_pull(Graph &g);
 // comparators.cu
 di_status run_comparator(Graph &g, double d, double tol, int variant, int64_t max_sweeps,
                          uint32_t flags, di_stats *st);

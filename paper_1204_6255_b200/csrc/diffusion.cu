@@ -151,6 +151,10 @@ struct SweepArgs {
   uint8_t *log_mode;
   int test_mode;
   int red_hint;         // 1: REDs into F carry an L2 evict_last policy
+  double *S;            // pull variant: dense sent value per node (0 if not diffused)
+  const int32_t *csc_row;
+  PullEntry *pe[kPullBins];
+  int64_t pe_count[kPullBins];
 };
 
 // One tile = kSelTile consecutive nodes; thread t owns kSelItems consecutive nodes.
@@ -170,6 +174,8 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
   const double r = sc->r;
   const double d = sc->d;
   const bool cyc = (sc->variant == DI_CYC) || sc->guard;
+  const int mode = sc->mode;
+  const bool emit = mode != MODE_PULL, dense = mode != MODE_PUSH;
   const double t = (a.L_total > 0.0) ? r / a.L_total : 0.0;  // r/L once (G3, G4)
   const int64_t base = tile * (int64_t)kSelTile + (int64_t)threadIdx.x * kSelItems;
   const bool full = base + kSelItems <= a.n;
@@ -247,6 +253,8 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
   const uint32_t anysel = selmask | dangmask;
   double v[kSelItems];
   int64_t rb[kSelItems];
+#pragma unroll
+  for (int j = 0; j < kSelItems; j++) v[j] = 0.0;
   double s = 0.0, e = 0.0;
   int64_t links = 0;
   int nsel = 0, nsel_nd = 0;
@@ -298,6 +306,20 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
       }
     }
   }
+  // pull variant: dense S (v_i for diffused non-dangling nodes, 0 elsewhere), read by k_pull
+  if (dense) {
+    if (full) {
+      double2 *S2 = reinterpret_cast<double2 *>(a.S + base);
+#pragma unroll
+      for (int j = 0; j < kSelItems / 2; j++)
+        S2[j] = make_double2((selmask >> (2 * j) & 1u) ? v[2 * j] : 0.0,
+                             (selmask >> (2 * j + 1) & 1u) ? v[2 * j + 1] : 0.0);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kSelItems; j++)
+        if (base + j < a.n) a.S[base + j] = (selmask >> j & 1u) ? v[j] : 0.0;
+    }
+  }
 
   // ---- block-wide exclusive scan of the 4 bin counts, one reservation per bin
   int incl[kBins];
@@ -325,12 +347,12 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
     }
     pos[b] = we + incl[b] - cnt[b];
     if (threadIdx.x == b)
-      s_res[b] = tot ? atomicAdd(&sc->bin_fill[b][0], (unsigned long long)tot) : 0ull;
+      s_res[b] = (tot && emit) ? atomicAdd(&sc->bin_fill[b][0], (unsigned long long)tot) : 0ull;
   }
   __syncthreads();
 
   // ---- pass 2b: emit the rows into the reserved ranges, ascending node id inside each bin
-  if (selmask) {
+  if (selmask && emit) {
     int64_t slot[kBins];
 #pragma unroll
     for (int b = 0; b < kBins; b++) slot[b] = (int64_t)s_res[b] + pos[b];
@@ -399,6 +421,7 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
     a.partials[tile * 3 + 1] = ts;
     a.partials[tile * 3 + 2] = te;
     reinterpret_cast<longlong2 *>(a.ipartials)[2 * tile] = make_longlong2(tsel, tnd);
+    if (mode == MODE_AUTO && tl) atomicAdd(&sc->fill_links[0], (unsigned long long)tl);
     reinterpret_cast<longlong2 *>(a.ipartials)[2 * tile + 1] = make_longlong2(tl, 0);
   }
 }
@@ -454,12 +477,16 @@ __device__ void finalize_sweep(const SweepArgs &a, int nthreads) {
   const double d = vs->d, r = vs->r;
   const int variant = vs->variant;
   const bool guarded = vs->guard && variant != DI_CYC;
+  const int mode = vs->mode;
+  const bool pulled = mode == MODE_PULL || (mode == MODE_AUTO && lk > vs->pull_thr);
   if (vs->trace && sw < kLogCap) {
     a.log_r[sw] = r;
     a.log_sel[sw] = sel;
     a.log_links[sw] = lk;
-    a.log_mode[sw] = 0;
+    a.log_mode[sw] = pulled ? 1 : 0;
   }
+  if (pulled) vs->pull_sweeps = vs->pull_sweeps + 1;
+  vs->fill_links[0] = 0;
   const double r_next = tq + ts;  // r_{n+1} = q_n + s_n (a2)
   const double e_tot = vs->e + te;
   vs->e = e_tot;
@@ -531,19 +558,21 @@ __device__ __forceinline__ void red_group(double *__restrict__ F, int4 x, int64_
   }
 }
 
-// rows of > kBinG links (bins W and C): one warp per row, entries walked in order (warp-uniform
-// broadcast loads, prefetched one ahead), 2 int4 groups (8 links) per lane in flight.
+// rows of > kBinG links (bins W and C): one warp per row. Entries are dealt round-robin
+// (u = w, w + W, ...): rows of similar size cluster in a bin (tile order, hubs first after the
+// relabelling), so contiguous ranges would load-imbalance. Warp-uniform broadcast entry loads,
+// prefetched one ahead; 2 int4 groups (8 links) per lane in flight.
 template <bool LOOPS>
-__device__ __forceinline__ void push_rows_warp(const SweepArgs &a, int b, int64_t u0, int64_t u1,
-                                               int lane, uint64_t pol, uint64_t fpol) {
-  if (u0 >= u1) return;
+__device__ __forceinline__ void push_rows_warp(const SweepArgs &a, int b, int64_t w, int64_t W,
+                                               int64_t U, int lane, uint64_t pol, uint64_t fpol) {
+  if (w >= U) return;
   const Entry *__restrict__ ent = a.fr.ent[b];
   const int32_t *__restrict__ col = a.col;
   double *__restrict__ F = a.F;
-  Entry nx = ent[u0];
-  for (int64_t u = u0; u < u1; u++) {
+  Entry nx = ent[w];
+  for (int64_t u = w; u < U; u += W) {
     const Entry en = nx;
-    if (u + 1 < u1) nx = ent[u + 1];
+    if (u + W < U) nx = ent[u + W];
     const int32_t gi = LOOPS ? (int32_t)(a.fr.id[b][u] + a.lo) : -1;
     const int64_t beg = (int64_t)(en.bl & kBegMask);
     const int64_t end = beg + (int64_t)(en.bl >> kLenShift);
@@ -565,6 +594,8 @@ __global__ void __launch_bounds__(kPushThreads, MINB) k_push(const SweepArgs a) 
   __shared__ bool s_last;
   Scalars *sc = a.sc;
   if (sc->stop) return;
+  const int mode = sc->mode;
+  if (mode == MODE_AUTO && (int64_t)sc->fill_links[0] > sc->pull_thr) return;  // k_pull's sweep
   const uint64_t pol = policy_evict_first();
   const uint64_t fpol = a.red_hint ? policy_evict_last() : policy_evict_normal();
   const int lane = threadIdx.x & 31;
@@ -576,13 +607,13 @@ __global__ void __launch_bounds__(kPushThreads, MINB) k_push(const SweepArgs a) 
 #pragma unroll
   for (int b = 0; b < kBins; b++) U[b] = (int64_t)sc->bin_fill[b][0];
   // ---- bins C (hub chunks) and W: warp per row
-  push_rows_warp<LOOPS>(a, BIN_C, w * U[BIN_C] / W, (w + 1) * U[BIN_C] / W, lane, pol, fpol);
-  push_rows_warp<LOOPS>(a, BIN_W, w * U[BIN_W] / W, (w + 1) * U[BIN_W] / W, lane, pol, fpol);
+  push_rows_warp<LOOPS>(a, BIN_C, w, W, U[BIN_C], lane, pol, fpol);
+  push_rows_warp<LOOPS>(a, BIN_W, w, W, U[BIN_W], lane, pol, fpol);
   // ---- bin G (9..32 links): 8-lane group per row, 4 rows per warp step; <= 9 int4 groups
   {
-    const int64_t u0 = w * U[BIN_G] / W, u1 = (w + 1) * U[BIN_G] / W;
     const int sub = lane & 7;
-    for (int64_t u = u0 + (lane >> 3); u < u1; u += 4) {
+    const int64_t u1 = U[BIN_G];
+    for (int64_t u = 4 * w + (lane >> 3); u < u1; u += 4 * W) {
       const Entry en = a.fr.ent[BIN_G][u];
       const int32_t gi = LOOPS ? (int32_t)(a.fr.id[BIN_G][u] + a.lo) : -1;
       const int64_t beg = (int64_t)(en.bl & kBegMask);
@@ -598,8 +629,8 @@ __global__ void __launch_bounds__(kPushThreads, MINB) k_push(const SweepArgs a) 
   }
   // ---- bin T (1..8 links): one thread per row; <= 3 int4 groups
   {
-    const int64_t u0 = w * U[BIN_T] / W, u1 = (w + 1) * U[BIN_T] / W;
-    for (int64_t u = u0 + lane; u < u1; u += 32) {
+    const int64_t u1 = U[BIN_T];
+    for (int64_t u = 32 * w + lane; u < u1; u += 32 * W) {
       const Entry en = a.fr.ent[BIN_T][u];
       const int32_t gi = LOOPS ? (int32_t)(a.fr.id[BIN_T][u] + a.lo) : -1;
       const int64_t beg = (int64_t)(en.bl & kBegMask);
@@ -615,7 +646,120 @@ __global__ void __launch_bounds__(kPushThreads, MINB) k_push(const SweepArgs a) 
       if (nvec > 2) red_group<LOOPS>(F, x2, a0 + 8, beg, end, gi, en.v, fpol);
     }
   }
-  // ---- the last block to finish finalises the sweep
+  // ---- the last block to finish finalises the sweep (DI_AUTO: k_pull, launched next, does)
+  if (mode != MODE_PUSH) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  finalize_sweep(a, kPushThreads);
+}
+
+// ------------------------------------------------------------------ pull (a5')
+// F_j += sum_{i in in(j), i != j} S_i over the CSC, no atomics except for the partial sums of
+// chunked hub rows. Deterministic for every row below kPullChunk in-links.
+__device__ __forceinline__ double sum_group(const double *__restrict__ S, int4 x, int64_t p0,
+                                            int64_t beg, int64_t end, int32_t j) {
+  const int32_t ii[4] = {x.x, x.y, x.z, x.w};
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    const int64_t p = p0 + c;
+    if (p >= beg && p < end && ii[c] != j) acc += __ldg(S + ii[c]);
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(kPushThreads) k_pull(const SweepArgs a) {
+  __shared__ bool s_last;
+  Scalars *sc = a.sc;
+  if (sc->stop) return;
+  const int mode = sc->mode;
+  const bool work = mode == MODE_PULL || (int64_t)sc->fill_links[0] > sc->pull_thr;
+  if (work) {
+    const uint64_t pol = policy_evict_first();
+    const int lane = threadIdx.x & 31;
+    const int64_t W = (int64_t)gridDim.x * (kPushThreads / 32);
+    const int64_t w = (int64_t)blockIdx.x * (kPushThreads / 32) + (threadIdx.x >> 5);
+    const int32_t *__restrict__ row = a.csc_row;
+    const double *__restrict__ S = a.S;
+    double *__restrict__ F = a.F;
+    // ---- P3 / P2: warp per row or hub chunk
+    for (int b = kPullBins - 1; b >= 2; b--) {
+      const int64_t U = a.pe_count[b];
+      for (int64_t u = w; u < U; u += W) {   // round-robin: rows are sorted by size
+        const PullEntry en = a.pe[b][u];
+        const int64_t beg = en.beg, end = en.beg + en.len, a0 = beg & ~3ll;
+        const int nvec = (int)((end - a0 + 3) >> 2);
+        double acc = 0.0;
+        for (int vb = 0; vb < nvec; vb += 64) {
+          const int v0 = vb + lane, v1 = vb + 32 + lane;
+          int4 x0 = make_int4(0, 0, 0, 0), x1 = make_int4(0, 0, 0, 0);
+          if (v0 < nvec) x0 = ld_col4(row + a0 + 4 * (int64_t)v0, pol);
+          if (v1 < nvec) x1 = ld_col4(row + a0 + 4 * (int64_t)v1, pol);
+          if (v0 < nvec) acc += sum_group(S, x0, a0 + 4 * (int64_t)v0, beg, end, en.j);
+          if (v1 < nvec) acc += sum_group(S, x1, a0 + 4 * (int64_t)v1, beg, end, en.j);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) {
+          if (b == 3)
+            atomicAdd(F + en.j, acc);
+          else
+            F[en.j] += acc;
+        }
+      }
+    }
+    // ---- P1: 8-lane group per row (warp-uniform loop, 4 rows per step)
+    {
+      const int64_t U = a.pe_count[1];
+      const int64_t u1 = U;
+      const int sub = lane & 7;
+      for (int64_t ub = 4 * w; ub < u1; ub += 4 * W) {
+        const int64_t u = ub + (lane >> 3);
+        double acc = 0.0;
+        PullEntry en;
+        en.j = -1;
+        if (u < u1) {
+          en = a.pe[1][u];
+          const int64_t beg = en.beg, end = en.beg + en.len, a0 = beg & ~3ll;
+          const int nvec = (int)((end - a0 + 3) >> 2);
+          for (int vb = sub; vb < nvec; vb += 16) {
+            int4 x0 = ld_col4(row + a0 + 4 * (int64_t)vb, pol);
+            int4 x1 = make_int4(0, 0, 0, 0);
+            if (vb + 8 < nvec) x1 = ld_col4(row + a0 + 4 * (int64_t)(vb + 8), pol);
+            acc += sum_group(S, x0, a0 + 4 * (int64_t)vb, beg, end, en.j);
+            if (vb + 8 < nvec) acc += sum_group(S, x1, a0 + 4 * (int64_t)(vb + 8), beg, end, en.j);
+          }
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        if (sub == 0 && u < u1) F[en.j] += acc;
+      }
+    }
+    // ---- P0: one thread per row (<= kPullT in-links, <= 3 int4 groups)
+    {
+      const int64_t U = a.pe_count[0];
+      for (int64_t u = 32 * w + lane; u < U; u += 32 * W) {
+        const PullEntry en = a.pe[0][u];
+        const int64_t beg = en.beg, end = en.beg + en.len, a0 = beg & ~3ll;
+        const int nvec = (int)((end - a0 + 3) >> 2);
+        const int4 x0 = ld_col4(row + a0, pol);
+        int4 x1 = make_int4(0, 0, 0, 0), x2 = make_int4(0, 0, 0, 0);
+        if (nvec > 1) x1 = ld_col4(row + a0 + 4, pol);
+        if (nvec > 2) x2 = ld_col4(row + a0 + 8, pol);
+        double acc = sum_group(S, x0, a0, beg, end, en.j);
+        if (nvec > 1) acc += sum_group(S, x1, a0 + 4, beg, end, en.j);
+        if (nvec > 2) acc += sum_group(S, x2, a0 + 8, beg, end, en.j);
+        F[en.j] += acc;
+      }
+    }
+  }
+  // ---- the last block to finish finalises the sweep (pull and auto modes)
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -659,6 +803,12 @@ SweepArgs sweep_args(Graph &g, int test_mode) {
   a.log_mode = g.log_mode;
   a.test_mode = test_mode;
   a.red_hint = g.red_hint;
+  a.S = g.S;
+  a.csc_row = g.csc_row;
+  for (int b = 0; b < kPullBins; b++) {
+    a.pe[b] = g.pe[b];
+    a.pe_count[b] = g.pe_count[b];
+  }
   return a;
 }
 
@@ -743,6 +893,45 @@ void launch_push(Graph &g, int64_t *launches) {
   else
     launch_push_t<false, 4>(g, a);
   *launches += 1;
+}
+
+void launch_pull(Graph &g, int64_t *launches) {
+  const SweepArgs a = sweep_args(g, 0);
+  static int occ = 0;
+  if (occ == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pull, kPushThreads, 0);
+    if (occ < 1) occ = 1;
+  }
+  k_pull<<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a);
+  *launches += 1;
+}
+
+// Static pull entries from the CSC (built once per graph, on the host from col_ptr).
+di_status alloc_pull(Graph &g) {
+  if (!g.has_csc || g.pe[0]) return DI_OK;
+  const int64_t n = g.n;
+  std::vector<int64_t> cp((size_t)n + 1);
+  DI_CK(cudaMemcpy(cp.data(), g.csc_ptr, ((size_t)n + 1) * 8, cudaMemcpyDeviceToHost));
+  std::vector<PullEntry> e[kPullBins];
+  for (int64_t j = 0; j < n; j++) {
+    const int64_t beg = cp[j], len = cp[j + 1] - cp[j];
+    if (len == 0) continue;
+    const int b = len <= kPullT ? 0 : (len <= kPullG ? 1 : (len <= kPullChunk ? 2 : 3));
+    if (b < 3) {
+      e[b].push_back(PullEntry{beg, (int32_t)len, (int32_t)j});
+    } else {
+      for (int64_t c = 0; c < len; c += kPullChunk)
+        e[3].push_back(PullEntry{beg + c, (int32_t)std::min<int64_t>(kPullChunk, len - c), (int32_t)j});
+    }
+  }
+  for (int b = 0; b < kPullBins; b++) {
+    g.pe_count[b] = (int64_t)e[b].size();
+    DI_CK(cudaMalloc(&g.pe[b], std::max<size_t>(e[b].size(), 1) * sizeof(PullEntry)));
+    if (!e[b].empty())
+      DI_CK(cudaMemcpy(g.pe[b], e[b].data(), e[b].size() * sizeof(PullEntry), cudaMemcpyHostToDevice));
+  }
+  DI_CK(cudaMalloc(&g.S, (size_t)std::max<int64_t>(n, 1) * 8));
+  return DI_OK;
 }
 
 void launch_finalize(Graph &g, int64_t *launches) {

@@ -14,16 +14,56 @@
 namespace di {
 namespace {
 
+// id validation (first bad link index) and, for the locality relabelling, in-degrees
+__global__ void k_validate(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                           int64_t L, int64_t n, unsigned long long *__restrict__ bad,
+                           uint32_t *__restrict__ indeg) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = src[k], t = dst[k];
+    if (s < 0 || s >= n || t < 0 || t >= n)
+      atomicMin(bad, (unsigned long long)k);
+    else if (indeg)
+      atomicAdd(indeg + t, 1u);
+  }
+}
+
+// sort key for the relabelling: descending in-degree (ties: ascending id, radix sort is stable)
+__global__ void k_perm_keys(const uint32_t *__restrict__ indeg, int64_t n, uint32_t *__restrict__ key,
+                            int32_t *__restrict__ iota) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    key[i] = 0xFFFFFFFFu - indeg[i];
+    iota[i] = (int32_t)i;
+  }
+}
+
+// rank r (0 = largest in-degree) -> internal id: rank r goes to stripe r % P at position r / P,
+// stripes laid out contiguously. Nodes of similar rank share L2 lines (hot lines are fully hot)
+// while the P hottest nodes sit in P different lines / L2 slices (no single hot slice for the
+// push's REDs).
+__global__ void k_place(const int32_t *__restrict__ sorted_old, int64_t n, int64_t P,
+                        int32_t *__restrict__ new_of, int32_t *__restrict__ old_of) {
+  const int64_t M = n / P, rem = n % P;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = r % P, idx = r / P;
+    const int64_t k = s * M + (s < rem ? s : rem) + idx;
+    const int32_t o = sorted_old[r];
+    new_of[o] = (int32_t)k;
+    old_of[k] = o;
+  }
+}
+
 __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
-                            int64_t L, int64_t n, int b, uint64_t *__restrict__ keys,
-                            unsigned long long *__restrict__ bad) {
+                            int64_t L, int b, const int32_t *__restrict__ new_of,
+                            uint64_t *__restrict__ keys) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
        k += (int64_t)gridDim.x * blockDim.x) {
     int32_t s = src[k], t = dst[k];
-    if (s < 0 || s >= n || t < 0 || t >= n) {
-      atomicMin(bad, (unsigned long long)k);
-      s = 0;
-      t = 0;
+    if (new_of) {
+      s = new_of[s];
+      t = new_of[t];
     }
     keys[k] = ((uint64_t)(uint32_t)s << b) | (uint64_t)(uint32_t)t;
   }
@@ -124,9 +164,18 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   unsigned long long init_bad = ~0ull;
   DI_CK(cudaMemcpyAsync(badb.p, &init_bad, 8, cudaMemcpyHostToDevice, st));
   uint64_t *ka = (uint64_t *)keys_a.p, *kb = (uint64_t *)keys_b.p;
+  const bool reorder = !(flags & DI_NO_REORDER);
+  // keys_b doubles as the in-degree scratch (n uint32 <= 8L bytes unless L tiny: separate buf)
+  DevBuf indeg_b;
+  uint32_t *indeg = nullptr;
+  if (reorder) {
+    DI_CK(cudaMalloc(&indeg_b.p, (size_t)n * 4));
+    DI_CK(cudaMemsetAsync(indeg_b.p, 0, (size_t)n * 4, st));
+    indeg = (uint32_t *)indeg_b.p;
+  }
   if (L > 0)
-    k_make_keys<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, n, b, ka,
-                                                  (unsigned long long *)badb.p);
+    k_validate<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, n, (unsigned long long *)badb.p,
+                                                 indeg);
   unsigned long long bad = 0;
   DI_CK(cudaMemcpyAsync(&bad, badb.p, 8, cudaMemcpyDeviceToHost, st));
   DI_CK(cudaStreamSynchronize(st));
@@ -144,6 +193,33 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
               ")");
     return DI_EINVAL;
   }
+  // ---- locality relabelling: node ids sorted by descending in-degree, so the
+  //      hot push targets (and, R-MAT being correlated, the hot pull sources) share L2 lines
+  if (reorder) {
+    DevBuf kin, kout, vin;
+    DI_CK(cudaMalloc(&kin.p, (size_t)n * 4));
+    DI_CK(cudaMalloc(&kout.p, (size_t)n * 4));
+    DI_CK(cudaMalloc(&vin.p, (size_t)n * 4));
+    DevBuf sorted;
+    DI_CK(cudaMalloc(&sorted.p, (size_t)n * 4));
+    DI_CK(cudaMalloc(&g.old_of, (size_t)n * 4));
+    DI_CK(cudaMalloc(&g.new_of, (size_t)n * 4));
+    k_perm_keys<<<grid_for(n, sms), 256, 0, st>>>(indeg, n, (uint32_t *)kin.p, (int32_t *)vin.p);
+    size_t pb = 0;
+    DI_CK(cub::DeviceRadixSort::SortPairs(nullptr, pb, (uint32_t *)kin.p, (uint32_t *)kout.p,
+                                          (int32_t *)vin.p, (int32_t *)sorted.p, (int64_t)n, 0, 32,
+                                          st));
+    DevBuf ptmp;
+    DI_CK(cudaMalloc(&ptmp.p, pb));
+    DI_CK(cub::DeviceRadixSort::SortPairs(ptmp.p, pb, (uint32_t *)kin.p, (uint32_t *)kout.p,
+                                          (int32_t *)vin.p, (int32_t *)sorted.p, (int64_t)n, 0, 32,
+                                          st));
+    const int64_t P = std::max<int64_t>(1, std::min<int64_t>(g.stripes, n));
+    k_place<<<grid_for(n, sms), 256, 0, st>>>((const int32_t *)sorted.p, n, P, g.new_of, g.old_of);
+    g.reordered = true;
+  }
+  if (L > 0) k_make_keys<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, b, g.new_of, ka);
+  DI_CK(cudaStreamSynchronize(st));
   dsrc.~DevBuf();
   dsrc.p = nullptr;
   ddst.~DevBuf();
@@ -210,7 +286,8 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
       DI_CK(cub::DeviceRadixSort::SortKeys(tmp.p, sb, ka, kb, (int64_t)Lk, 0, 2 * b, st));
     }
     DI_CK(cudaMalloc(&g.csc_ptr, ((size_t)n + 1) * 8));
-    DI_CK(cudaMalloc(&g.csc_row, LkS * 4));
+    DI_CK(cudaMalloc(&g.csc_row, (LkS + 8) * 4));
+    DI_CK(cudaMemsetAsync(g.csc_row + LkS, 0, 8 * 4, st));
     k_csr_from_sorted<<<grid_for(Lk + 1, sms), 256, 0, st>>>(kb, Lk, n, b, g.csc_ptr, g.csc_row,
                                                             nullptr);
     g.has_csc = true;

@@ -13,7 +13,7 @@ def test_builder_random(dedup, drop_self):
     need_gpu()
     for seed in range(40):
         src, dst, n = digen.small_random(seed, n_max=300)
-        g = upload(src, dst, n, dedup=dedup, drop_self_loops=drop_self, build_csc=True)
+        g = upload(src, dst, n, dedup=dedup, drop_self_loops=drop_self, build_csc=True, reorder=False)
         ref = csr_reference(src, dst, n, dedup, drop_self)
         got = g.test_csr(csc=True)
         assert g.n_links == len(ref["col"])
@@ -30,7 +30,7 @@ def test_builder_configs(name):
     need_gpu()
     src, dst, n = digen.make(name)
     perm = np.random.default_rng(0).permutation(len(src))   # builder must not rely on input order
-    g = upload(src[perm], dst[perm], n, build_csc=True)
+    g = upload(src[perm], dst[perm], n, build_csc=True, reorder=False)
     got = g.test_csr(csc=True)
     ref = csr_reference(src, dst, n)
     for k in ("row_ptr", "col", "deg", "kloop"):
@@ -42,7 +42,7 @@ def test_builder_host_pointers_and_edges():
     need_gpu()
     import paper_1204_6255_b200 as di
     src, dst, n = digen.small_random(3, n_max=50)
-    g = di.Graph(src, dst, n)                     # host arrays -> DI_HOST_PTRS path
+    g = di.Graph(src, dst, n, reorder=False)      # host arrays -> DI_HOST_PTRS path
     ref = csr_reference(src, dst, n)
     assert np.array_equal(g.test_csr()["col"], ref["col"])
     g.free()
@@ -53,3 +53,30 @@ def test_builder_host_pointers_and_edges():
     with pytest.raises(di.DIError) as ei:
         di.Graph(np.array([0, 5], np.int32), np.array([1, 1], np.int32), 3)
     assert ei.value.status == di.DI_EINVAL and "link 1" in str(ei.value)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_reorder_relabelling(name):
+    """Default upload relabels nodes by descending in-degree (stable): the internal CSR equals the
+    reference CSR of the relabelled link list, byte for byte."""
+    need_gpu()
+    src, dst, n = digen.make(name)
+    g = upload(src, dst, n, build_csc=True)
+    old_of = g.test_perm()
+    indeg = np.bincount(dst, minlength=n)
+    ranked = np.argsort(-indeg, kind="stable")           # rank r -> caller id
+    P = min(4096, n)                                     # stripes: rank r -> stripe r % P, slot r // P
+    r = np.arange(n)
+    M, rem = n // P, n % P
+    s_ = r % P
+    k = s_ * M + np.minimum(s_, rem) + r // P
+    expect = np.empty(n, np.int64)
+    expect[k] = ranked
+    assert np.array_equal(old_of, expect.astype(np.int32))
+    new_of = np.empty(n, np.int64)
+    new_of[old_of] = np.arange(n)
+    ref = csr_reference(new_of[src], new_of[dst], n)
+    got = g.test_csr(csc=True)
+    for k in ("row_ptr", "col", "deg", "kloop"):
+        assert np.array_equal(got[k], ref[k]), k
+    g.free()

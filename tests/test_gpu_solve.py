@@ -27,29 +27,36 @@ def test_exact_pins(variant):
         g.free()
 
 
+MODES = ["push", "pull", "auto"]
+
+
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("d", [0.5, 0.85, 0.95])
-def test_random_vs_dense(d):
+def test_random_vs_dense(d, mode):
     need_gpu()
     for seed in range(60):
         src, dst, n = digen.small_random(seed)
         X = defn.solve_dense(src, dst, n, d)
-        g = upload(src, dst, n)
+        g = upload(src, dst, n, build_csc=True)
         for variant in ("sop", "cyc"):
-            st = g.solve(d=d, tol=1e-15, variant=variant)
+            st = g.solve(d=d, tol=1e-15, variant=variant, mode=mode)
             assert st["converged"] == 1
             assert l1(g.history().cpu().numpy(), X) <= 1e-13, (seed, variant)
         g.free()
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("variant", ["sop", "cyc"])
 @pytest.mark.parametrize("name,seed", [("c1", 1), ("c1", 2), ("c1", 3), ("c2", 1)])
-def test_north_star_parity(name, seed, variant):
+def test_north_star_parity(name, seed, variant, mode):
     """T10: ||H_gpu - H_oracle||_1 <= 1e-9, both run to ||F||_1 <= 1e-10 (north_star), and
     <= 1e-10/(1-d) + 1e-13/(1-d) against the tight (1e-13) oracle run (reading G19)."""
     need_gpu()
     src, dst, n = digen.make(name, seed=seed)
-    g = upload(src, dst, n)
-    st = g.solve(d=D, tol=1e-10, variant=variant)
+    g = upload(src, dst, n, build_csc=True)
+    st = g.solve(d=D, tol=1e-10, variant=variant, mode=mode)
+    if mode == "pull":
+        assert st["pull_sweeps"] == st["sweeps"]
     assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
     H = g.history().cpu().numpy()
     Ho, _, sto = oracle.di(src, dst, n, d=D, tol=1e-10, variant=variant)
@@ -61,7 +68,8 @@ def test_north_star_parity(name, seed, variant):
     g.free()
 
 
-def test_invariants_mid_solve():
+@pytest.mark.parametrize("mode", MODES)
+def test_invariants_mid_solve(mode):
     """T8: at any stopping point F = B + P.H - H, F >= 0, conservation, sum F non-increasing."""
     need_gpu()
     for seed in range(20):
@@ -69,11 +77,11 @@ def test_invariants_mid_solve():
         P = defn.dense_P(src, dst, n, D)
         B = defn.uniform_B(n, D)
         out = np.bincount(src, minlength=n)
-        g = upload(src, dst, n)
+        g = upload(src, dst, n, build_csc=True)
         for variant in ("sop", "cyc"):
             prev = np.inf
             for k in (1, 2, 3, 5, 8):
-                g.solve(d=D, tol=1e-300, variant=variant, max_sweeps=k)
+                g.solve(d=D, tol=1e-300, variant=variant, max_sweeps=k, mode=mode)
                 H = g.history().cpu().numpy()
                 r, F = g.residual(return_F=True)
                 F = F.cpu().numpy()
@@ -86,16 +94,17 @@ def test_invariants_mid_solve():
         g.free()
 
 
-def test_bulk_cyc_neumann_gpu():
+@pytest.mark.parametrize("mode", MODES)
+def test_bulk_cyc_neumann_gpu(mode):
     """T7: bulk DI-CYC without loops: F_n = P^n B and H_n = sum_{k<n} P^k B after n sweeps."""
     need_gpu()
     src, dst, n = digen.make("c1")
     P = defn.sparse_P(src, dst, n, D)
     B = defn.uniform_B(n, D)
-    g = upload(src, dst, n)
+    g = upload(src, dst, n, build_csc=True)
     Fn, Hn = B.copy(), np.zeros(n)
     for k in range(1, 11):
-        g.solve(d=D, tol=1e-300, variant="cyc", max_sweeps=k)
+        g.solve(d=D, tol=1e-300, variant="cyc", max_sweeps=k, mode=mode)
         Hn = Hn + Fn
         Fn = P @ Fn
         _, F = g.residual(return_F=True)
@@ -108,15 +117,16 @@ def test_bulk_cyc_neumann_gpu():
     g.free()
 
 
-def test_closure_drainage_gpu():
+@pytest.mark.parametrize("mode", MODES)
+def test_closure_drainage_gpu(mode):
     """T9: nodes of E at depth <= t hold exactly 0.0 after t+1 bulk DI-CYC sweeps."""
     need_gpu()
     for seed in range(30):
         src, dst, n = digen.dag_fringe(seed)
         depth = digen.closure(src, dst, n)
-        g = upload(src, dst, n)
+        g = upload(src, dst, n, build_csc=True)
         for t in range(6):
-            g.solve(d=D, tol=1e-300, variant="cyc", max_sweeps=t + 1)
+            g.solve(d=D, tol=1e-300, variant="cyc", max_sweeps=t + 1, mode=mode)
             _, F = g.residual(return_F=True)
             F = F.cpu().numpy()
             drained = (depth >= 0) & (depth <= t)
@@ -152,16 +162,19 @@ def test_edge_cases():
     assert st["converged"] == 1 and st["sweeps"] == 1
     assert np.allclose(g.history().cpu().numpy(), (1 - D) / 3000, rtol=0, atol=1e-18)
     g.free()
-    # N around the tile size (2048 nodes per select tile): ragged tails
-    for n in (1, 2047, 2048, 2049, 4097):
+    # N around the select tile size (1024 nodes per tile): ragged tails; hub rows > chunk sizes
+    for n in (1, 1023, 1024, 1025, 4097, 20000):
         rng = np.random.default_rng(n)
         m = 4 * n
         src = rng.integers(0, n, m).astype(np.int32)
         dst = rng.integers(0, n, m).astype(np.int32)
-        g = upload(src, dst, n)
+        if n == 20000:   # one out-hub (push bin C) and one in-hub (pull bin P3)
+            src = np.concatenate([src, np.zeros(15000, np.int32), np.arange(1, 12001, dtype=np.int32)])
+            dst = np.concatenate([dst, np.arange(1, 15001, dtype=np.int32), np.full(12000, 7, np.int32)])
+        g = upload(src, dst, n, build_csc=True)
         X = defn.solve_sparse(src, dst, n, D)
-        for variant in ("sop", "cyc"):
-            st = g.solve(d=D, tol=1e-13, variant=variant)
+        for variant, mode in (("sop", "push"), ("cyc", "push"), ("sop", "pull"), ("sop", "auto")):
+            st = g.solve(d=D, tol=1e-13, variant=variant, mode=mode)
             assert st["converged"] == 1
             assert l1(g.history().cpu().numpy(), X) <= 1e-13 / (1 - D) + 1e-14
         g.free()
@@ -188,9 +201,11 @@ def test_custom_B_and_paper_stop():
 def test_trace_log():
     need_gpu()
     src, dst, n = digen.make("c1")
-    g = upload(src, dst, n)
-    st = g.solve(d=D, tol=1e-10, trace=True, profile=True)
+    g = upload(src, dst, n, build_csc=True)
+    st = g.solve(d=D, tol=1e-10, trace=True, profile=True, mode="auto")
     log = g.sweep_log()
+    assert log["mode"].sum() == st["pull_sweeps"] > 0
+    assert np.all((log["links"] > int(0.35 * len(src))) == (log["mode"] == 1))
     assert len(log["r"]) == st["sweeps"]
     assert log["links"].sum() == st["link_diffusions"] and log["selected"].sum() == st["selected_total"]
     assert np.all(np.diff(log["r"]) <= 1e-18)                       # sum F non-increasing
@@ -204,9 +219,9 @@ def test_c4_full_size_properties():
     F_i = B_i + (P.H)_i - H_i on 2000 nodes, and ||X - H||_1 <= ||F||_1/(1-d) by construction."""
     need_gpu()
     src, dst, n = digen.make("c4")
-    g = upload(src, dst, n)
-    st = g.solve(d=D, tol=1e-10, variant="sop")
-    assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
+    g = upload(src, dst, n, build_csc=True)
+    st = g.solve(d=D, tol=1e-10, variant="sop", mode="auto")
+    assert st["converged"] == 1 and st["residual_l1"] <= 1e-10 and 0 < st["pull_sweeps"] < st["sweeps"]
     H = g.history().cpu().numpy()
     _, F = g.residual(return_F=True)
     F = F.cpu().numpy()
