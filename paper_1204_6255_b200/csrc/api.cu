@@ -74,8 +74,11 @@ void free_graph(Graph *g) {
     for (void *p : q)
       if (p) cudaFree(p);
   }
-  for (int b = 0; b < kPullBins; b++)
+  for (int b = 0; b < kPullBins; b++) {
     if (g->pe[b]) cudaFree(g->pe[b]);
+    if (g->re[b]) cudaFree(g->re[b]);
+  }
+  if (g->cmp_partials) cudaFree(g->cmp_partials);
   if (g->sc_host) cudaFreeHost(g->sc_host);
   delete g;
 }

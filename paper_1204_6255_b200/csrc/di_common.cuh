@@ -124,6 +124,9 @@ struct Graph {
   // pull variant: static row entries per in-degree bin
   PullEntry *pe[kPullBins] = {nullptr, nullptr, nullptr, nullptr};
   int64_t pe_count[kPullBins] = {0, 0, 0, 0};
+  PullEntry *re[kPullBins] = {nullptr, nullptr, nullptr, nullptr};  // PI' static out-rows
+  int64_t re_count[kPullBins] = {0, 0, 0, 0};
+  double *cmp_partials = nullptr;
   double auto_ratio = 0.35; // DI_AUTO threshold on links(S_n)/L (DI_AUTO_RATIO)
   // state
   double *F = nullptr, *H = nullptr;

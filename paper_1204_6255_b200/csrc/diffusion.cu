@@ -21,59 +21,10 @@
 #include <vector>
 
 #include "di_common.cuh"
+#include "kern_util.cuh"
 
 namespace di {
 namespace {
-
-// streaming read of the column index array: read once per sweep, keep it out of L1 and make
-// it the first L2 eviction candidate so that F stays resident
-__device__ __forceinline__ int32_t ld_col(const int32_t *p, uint64_t pol) {
-  int32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
-               : "=r"(v)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ int4 ld_col4(const int32_t *p, uint64_t pol) {
-  int4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ uint64_t policy_evict_normal() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void red_add_f64_hint(double *p, double v, uint64_t pol) {
-  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void red_add_f64(double *p, double v) {
-  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
-
-template <typename T>
-__device__ __forceinline__ T warp_sum(T x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
-}
-
-__device__ __forceinline__ int bin_of(int o) {
-  return o <= kBinT ? BIN_T : (o <= kBinG ? BIN_G : (o <= kBinW ? BIN_W : BIN_C));
-}
 
 // ------------------------------------------------------------------ init (a1)
 __global__ void k_init(double *__restrict__ F, double *__restrict__ H, const double *__restrict__ B,
