@@ -122,9 +122,14 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    nid = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_1204_6255_b200.dist import nccl_rendezvous
+        _, _, nid = nccl_rendezvous()
+        args.mode = "push"                   # the partitioned sweep is push-only
     import paper_1204_6255_b200 as di
+    part = dict(rank=rank, world=world, nccl_id=nid) if world > 1 else dict(build_csc=True)
 
     src, dst, n, gen_s = make_graph(args.config, args.seed)
     L = len(src)
@@ -136,7 +141,7 @@ def run_ours(args):
     t_d = torch.from_numpy(dst).to(dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    g = di.Graph(s_d, t_d, n, build_csc=True, stream=stream)
+    g = di.Graph(s_d, t_d, n, stream=stream, **part)
     torch.cuda.synchronize()
     init_ms = (time.perf_counter() - t0) * 1e3
     del s_d, t_d
@@ -169,26 +174,23 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     tot_ms = sum(times)
-    links = sum(s["link_diffusions"] for s in stats)
+    links = sum(s["link_diffusions"] for s in stats)   # global: the partitioned stats are allreduced
     if world > 1:
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
-        lk = torch.tensor([links], dtype=torch.float64, device=dev)
-        dist.all_reduce(lk)
-        links = float(lk.item())
     value = links / (tot_ms * 1e-3) / 1e9
     ms_per_step = tot_ms / args.steps
 
     # ---- roofline of the dominant kernel (push, a5): algorithmic bytes / event time
     peak, peak_src = peaks()
-    push_bytes = sum(s["push_bytes"] for s in stats)
+    push_bytes = sum(s["push_bytes"] for s in stats) / world   # per GPU (stats are global)
     push_ms = sum(s["push_ms"] for s in stats)
     push_launches = sum(s["push_launches"] for s in stats)
     sel_ms = sum(s["select_ms"] for s in stats)
     achieved = push_bytes / (push_ms * 1e-3) / 1e9 if push_ms > 0 else 0.0
     tr = ncu_traffic()
-    counted = sum(s["counted_bytes"] for s in stats)
+    counted = sum(s["counted_bytes"] for s in stats) / world
     roofline = {"bound": "hbm", "kernel": "k_push + k_pull (a5/a5': diffusion of the frontier's fluid)",
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": tr,
@@ -202,14 +204,15 @@ def run_ours(args):
     # ---- e2e through the C ABI with host buffers (H2D of the link list, build, solve, D2H of H)
     src_p = torch.from_numpy(src).pin_memory()
     dst_p = torch.from_numpy(dst).pin_memory()
-    H_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    n_local = g.n_local
+    H_host = torch.empty(n_local, dtype=torch.float64).pin_memory()
     e2e_ms, e2e_links = [], 0
     g.free()
     torch.cuda.empty_cache()
     for k in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        gh = di.Graph(src_p, dst_p, n, build_csc=True, stream=stream)  # DI_HOST_PTRS: H2D inside
+        gh = di.Graph(src_p, dst_p, n, stream=stream, **part)  # DI_HOST_PTRS: H2D inside
         st = gh.solve(d=D, tol=TOL, variant=args.variant, mode=args.mode)
         H = gh.history()
         H_host.copy_(H, non_blocking=True)
@@ -232,13 +235,15 @@ def run_ours(args):
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic (seeded R-MAT + repair, digen; stands in for uk-2007-05 / gr0.California)",
         "config": {"workload": f"{args.config}: " + __import__("digen").CONFIGS[args.config].note,
                    "n": n, "links": L, "variant": "DI-" + args.variant.upper(), "d": D,
                    "tol_l1_fluid": TOL, "seed": args.seed, "sweep_mode": args.mode,
                    "l2": "inputs > 126 MB L2 and 512 MiB L2 flush before each step",
-                   "parallelism": "1-D node range" if world > 1 else "single GPU",
+                   "parallelism": f"1-D node range x{world}, NCCL (id, value) exchange" if world > 1
+                   else "single GPU",
                    "init_build_ms": round(init_ms, 1), "generator_s": round(gen_s, 1)},
         "time_to_tol_ms": round(ms_per_step, 3),
         "sweeps": stats[-1]["sweeps"], "equivalent_iterations": round(stats[-1]["equivalent_iterations"], 2),
@@ -246,9 +251,12 @@ def run_ours(args):
         "hbm_frac_counted_whole_solve": round(counted / (tot_ms * 1e-3) / 1e9 / peak, 4),
         "roofline": roofline,
         "e2e": {"value": round(e2e_val, 3) if e2e_val else None, "unit": UNIT, "ms_per_step": round(statistics.mean(e2e_ms), 2) if e2e_ms else None,
-                "h2d_bytes_per_step": 8 * L, "d2h_bytes_per_step": 8 * n,
+                "h2d_bytes_per_step": 8 * L, "d2h_bytes_per_step": 8 * n_local,
                 "includes": "pinned host link list -> di_graph_upload(DI_HOST_PTRS) build -> di_solve -> H to host"},
         "gpu_launches": gpu_launches,
+        "exchange": ({"bytes_per_step_per_gpu": sum(s["exchange_bytes"] for s in stats) / len(stats),
+                      "ms_per_step": sum(s["exchange_ms"] for s in stats) / len(stats)}
+                     if world > 1 else None),
         "clocks": clocks,
         "cpu_baseline": cpu,
     }

@@ -91,21 +91,49 @@ typedef struct {
   int64_t push_launches;        /* DI_PROFILE: push/pull launches that did work                  */
   int32_t converged;            /* 1 if the stop test passed                                     */
   int32_t variant;
+  double exchange_bytes;        /* multi-GPU: bytes this rank sent (12 per (remote id, sweep))    */
+  int64_t exchange_entries;     /* multi-GPU: (remote id, value) entries this rank sent           */
+  double exchange_ms;           /* multi-GPU, DI_PROFILE: event time of list exchange + apply     */
 } di_stats;
 
-/* Multi-GPU descriptor: one process per GPU, NCCL over NVLink. */
+/* In-process rank group: `world` emulated ranks, one host thread each, sharing one GPU. The
+ * collectives become host barriers plus device-to-device copies (no kernel waits for another
+ * rank). Used to run and test the partitioned path on a single GPU. */
+typedef struct di_group_s *di_group;
+
+/* Multi-GPU descriptor: one process per GPU with NCCL over NVLink/NVSwitch, or
+ * one host thread per rank with a di_group. Every rank passes the FULL link list; rank g then
+ * owns the node range [lo_g, hi_g) returned by di_graph_range (1-D, contiguous in the caller's
+ * numbering, balanced on 20 B per link + 12 B per node), and each sweep exchanges the fluid sent
+ * to remote targets as (id, value) lists (12 B per distinct remote target per sweep). */
 typedef struct {
-  int32_t rank, world;
-  const void *nccl_unique_id; /* 128-byte ncclUniqueId, identical on every rank (host pointer) */
+  int32_t rank, world;        /* 0 <= rank < world <= 16                                        */
+  const void *nccl_unique_id; /* 128-byte ncclUniqueId, identical on every rank (host pointer),
+                                 from di_nccl_unique_id on one rank; NULL with a group            */
+  di_group group;             /* in-process group from di_group_create, else NULL                */
 } di_dist;
+
+/* Fill out128 (host, 128 bytes) with a fresh ncclUniqueId (call on one rank, broadcast the bytes,
+ * e.g. with torch.distributed). NCCL is loaded at run time (libnccl.so.2, the copy torch loaded).
+ * Errors: DI_ENCCL if NCCL cannot be loaded. */
+di_status di_nccl_unique_id(void *out128);
+/* Create / free an in-process group of `world` ranks (1..16). di_group_free fails with
+ * DI_ESTATE while graphs built on the group are alive. */
+di_status di_group_create(int32_t world, di_group *out);
+di_status di_group_free(di_group grp);
+/* Mark the group failed: every rank blocked in (or later entering) a group collective returns
+ * DI_ESTATE instead of waiting for a rank that will not arrive. Call when one rank's call
+ * failed; the group's graphs can then only be freed. */
+di_status di_group_abort(di_group grp);
 
 /* Build the device graph (§2.1, "Init" timed separately).
  *  src, dst : n_links int32 node ids of the links src[k] -> dst[k]; device pointers, or host
  *             pointers with DI_HOST_PTRS. Any order; caller keeps ownership.
  *  n_links  : >= 0.   n_nodes : in [1, 2^31 - 1].
  *  stream   : cudaStream_t the handle will use (NULL = legacy default stream).
- *  dist     : NULL for one GPU; otherwise every rank calls collectively and owns the node range
- *             returned by di_graph_range (edge-balanced 1-D partition).
+ *  dist     : NULL for one GPU; otherwise every rank calls collectively with the same link list
+ *             and owns the node range returned by di_graph_range (1-D partition).
+ *             Partitioned graphs: no DI_BUILD_CSC / DI_LOCAL_LINKS (DI_EINVAL), n_nodes >= world.
  * Layout built in HBM: CSR row_ptr int64[n+1], col int32[L] sorted by (src, dst); deg int32[n];
  * kloop int32[n] (self-loop multiplicity); optional CSC (col_ptr int64[n+1], row int32[L]).
  * Errors: DI_EINVAL (sizes, an id outside [0, n): the message names the first bad index),
@@ -127,12 +155,15 @@ di_status di_graph_links(di_graph g, int64_t *n_links);
  *       for those tol bounds the scheme's own error estimate, P:176-180 / P:237-245, and
  *       di_history returns their x: normalised for PI, raw for GS).
  *  st : host pointer, filled on return (may be NULL).
+ * Partitioned graph: collective; DI_SOP / DI_CYC with push sweeps only; B is this rank's slice
+ * [lo, hi) in the caller's numbering; the stats are global (identical on every rank).
  * Returns DI_OK, DI_NOT_CONVERGED (state kept; DI_RESUME continues), or an error. */
 di_status di_solve(di_graph g, double d, const double *B, double tol, di_variant v,
                    int64_t max_sweeps, uint32_t flags, di_stats *st);
 
 /* ||F||_1 of the current state (exact deterministic tree sum) into *l1_out (host); if F_out
- * is not NULL, also copy this rank's F slice into it (device pointer). */
+ * is not NULL, also copy this rank's F slice into it (device pointer). Collective on a
+ * partitioned graph (the global sum). */
 di_status di_residual(di_graph g, double *l1_out, double *F_out);
 
 /* Copy this rank's history H (raw estimate of X) into H_out (device pointer). */

@@ -46,6 +46,8 @@ class Stats(ctypes.Structure):
         ("push_ms", ctypes.c_double), ("select_ms", ctypes.c_double),
         ("error_estimate", ctypes.c_double), ("push_launches", ctypes.c_int64),
         ("converged", ctypes.c_int32), ("variant", ctypes.c_int32),
+        ("exchange_bytes", ctypes.c_double), ("exchange_entries", ctypes.c_int64),
+        ("exchange_ms", ctypes.c_double),
     ]
 
     def as_dict(self):
@@ -53,7 +55,8 @@ class Stats(ctypes.Structure):
 
 
 class Dist(ctypes.Structure):
-    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p)]
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
+                ("group", ctypes.c_void_p)]
 
 
 _vp, _i64, _u32, _dbl, _ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_double, ctypes.c_int
@@ -75,6 +78,14 @@ _lib.di_graph_free.restype = _ci
 _lib.di_graph_free.argtypes = [_vp]
 _lib.di_last_error.restype = ctypes.c_char_p
 _lib.di_last_error.argtypes = []
+_lib.di_nccl_unique_id.restype = _ci
+_lib.di_nccl_unique_id.argtypes = [_vp]
+_lib.di_group_create.restype = _ci
+_lib.di_group_create.argtypes = [ctypes.c_int32, ctypes.POINTER(_vp)]
+_lib.di_group_abort.restype = _ci
+_lib.di_group_abort.argtypes = [_vp]
+_lib.di_group_free.restype = _ci
+_lib.di_group_free.argtypes = [_vp]
 _lib.di_test_select.restype = _ci
 _lib.di_test_select.argtypes = [_vp, _vp, _vp, _dbl, _dbl, _ci, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
 _lib.di_test_csr.restype = _ci
@@ -86,6 +97,7 @@ _lib.di_test_bins.argtypes = [_vp]
 
 EXPORTED = ["di_graph_upload", "di_graph_range", "di_graph_links", "di_solve", "di_residual",
             "di_history", "di_sweep_log", "di_graph_free", "di_last_error",
+            "di_nccl_unique_id", "di_group_create", "di_group_free", "di_group_abort",
             "di_test_select", "di_test_csr", "di_test_bins", "di_test_perm"]
 
 
@@ -113,12 +125,51 @@ def _stream_ptr(stream):
     return stream.cuda_stream
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (di_nccl_unique_id); create on one rank, broadcast the bytes."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.di_nccl_unique_id(buf))
+    return buf.raw
+
+
+class LocalGroup:
+    """In-process group of `world` emulated ranks on one GPU (di_group): one host thread per rank,
+    each building its own Graph(..., rank=r, group=this) and calling solve() concurrently."""
+
+    def __init__(self, world):
+        h = _vp()
+        _check(_lib.di_group_create(int(world), ctypes.byref(h)))
+        self._h = h
+        self.world = int(world)
+
+    def abort(self):
+        """Wake every rank blocked in a group collective (they fail with DI_ESTATE)."""
+        if getattr(self, "_h", None):
+            _check(_lib.di_group_abort(self._h))
+
+    def free(self):
+        if getattr(self, "_h", None):
+            _check(_lib.di_group_free(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class Graph:
     """Device graph handle (di_graph). src/dst: link list i -> j as int32, either CUDA tensors
-    (device pointers) or host arrays / CPU tensors (copied with DI_HOST_PTRS)."""
+    (device pointers) or host arrays / CPU tensors (copied with DI_HOST_PTRS).
+
+    Partitioned: pass rank/world and either nccl_id (bytes from nccl_unique_id(),
+    one process per GPU) or group (a LocalGroup, one thread per emulated rank). Every rank passes
+    the full link list and owns the node range self.range(); history()/residual(return_F) are
+    that rank's slice, residual() and solve() are collective."""
 
     def __init__(self, src, dst, n, dedup=False, drop_self_loops=False, build_csc=False,
-                 reorder=True, stream=None):
+                 reorder=True, stream=None, rank=0, world=1, nccl_id=None, group=None):
         torch = _torch()
         self.n = int(n)
         flags = (DEDUP if dedup else 0) | (DROP_SELF_LOOPS if drop_self_loops else 0) | \
@@ -147,13 +198,22 @@ class Graph:
             ps = pt = None
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         h = _vp()
-        _check(_lib.di_graph_upload(ps, pt, m, self.n, flags, self.stream.cuda_stream, None,
-                                    ctypes.byref(h)))
+        dist = None
+        self._group = group
+        if int(world) > 1:
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+            dist = Dist(int(rank), int(world),
+                        ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None,
+                        group._h if group is not None else None)
+        _check(_lib.di_graph_upload(ps, pt, m, self.n, flags, self.stream.cuda_stream,
+                                    ctypes.byref(dist) if dist is not None else None, ctypes.byref(h)))
         del keep
         self._h = h
         lk = _i64()
         _check(_lib.di_graph_links(self._h, ctypes.byref(lk)))
         self.n_links = int(lk.value)
+        self.lo, self.hi = self.range()
+        self.n_local = self.hi - self.lo
 
     # -------------------------------------------------------------- solve
     def solve(self, d=0.85, tol=1e-10, variant="sop", max_sweeps=100_000, B=None, resume=False,
@@ -180,14 +240,14 @@ class Graph:
 
     def history(self):
         torch = _torch()
-        H = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        H = torch.empty(self.n_local, dtype=torch.float64, device=self.device)
         _check(_lib.di_history(self._h, H.data_ptr()))
         return H
 
     def residual(self, return_F=False):
         torch = _torch()
         l1 = _dbl()
-        F = torch.empty(self.n, dtype=torch.float64, device=self.device) if return_F else None
+        F = torch.empty(self.n_local, dtype=torch.float64, device=self.device) if return_F else None
         _check(_lib.di_residual(self._h, ctypes.byref(l1), F.data_ptr() if F is not None else None))
         return (l1.value, F) if return_F else l1.value
 

@@ -11,6 +11,7 @@
 
 #include "../../include/di.h"
 #include "../../include/di_test.h"
+#include "comm.cuh"
 #include "di_common.cuh"
 
 namespace di {
@@ -80,6 +81,11 @@ void free_graph(Graph *g) {
   }
   if (g->cmp_partials) cudaFree(g->cmp_partials);
   if (g->sc_host) cudaFreeHost(g->sc_host);
+  free_dist(*g);
+  if (g->group) {
+    std::lock_guard<std::mutex> lk(g->group->m);
+    g->group->handles--;
+  }
   delete g;
 }
 
@@ -98,6 +104,38 @@ extern "C" {
 
 const char *di_last_error(void) { return g_err.c_str(); }
 
+di_status di_nccl_unique_id(void *out128) {
+  if (!out128) return fail(DI_EINVAL, "di_nccl_unique_id: NULL argument");
+  return nccl_unique_id(out128);
+}
+
+di_status di_group_create(int32_t world, di_group *out) {
+  if (!out) return fail(DI_EINVAL, "di_group_create: NULL argument");
+  *out = nullptr;
+  if (world < 1 || world > kMaxWorld)
+    return fail(DI_EINVAL, "di_group_create: world must be in [1, " + std::to_string(kMaxWorld) + "]");
+  *out = (di_group) new Group(world);
+  return DI_OK;
+}
+
+di_status di_group_abort(di_group grp) {
+  Group *g = (Group *)grp;
+  if (!g) return fail(DI_EINVAL, "di_group_abort: NULL group");
+  g->abort();
+  return DI_OK;
+}
+
+di_status di_group_free(di_group grp) {
+  Group *g = (Group *)grp;
+  if (!g) return DI_OK;
+  {
+    std::lock_guard<std::mutex> lk(g->m);
+    if (g->handles > 0) return fail(DI_ESTATE, "di_group_free: graphs of this group are still alive");
+  }
+  delete g;
+  return DI_OK;
+}
+
 di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_links, int64_t n_nodes,
                           uint32_t flags, void *stream, const di_dist *dist, di_graph *out) {
   if (!out) return fail(DI_EINVAL, "di_graph_upload: out is NULL");
@@ -106,8 +144,24 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
     return fail(DI_EINVAL, "di_graph_upload: n_nodes must be in [1, 2^31-1]");
   if (n_links < 0) return fail(DI_EINVAL, "di_graph_upload: n_links < 0");
   if (n_links > 0 && (!src || !dst)) return fail(DI_EINVAL, "di_graph_upload: NULL src/dst");
-  if (dist && dist->world > 1)
-    return fail(DI_EINVAL, "di_graph_upload: multi-GPU handles are not available in this build");
+  const int world = dist ? dist->world : 1;
+  Group *grp = dist ? (Group *)dist->group : nullptr;
+  const int rank = dist ? dist->rank : 0;
+  if (world < 1 || world > kMaxWorld)
+    return fail(DI_EINVAL, "di_graph_upload: dist->world must be in [1, " +
+                               std::to_string(kMaxWorld) + "]");
+  if (rank < 0 || rank >= world) return fail(DI_EINVAL, "di_graph_upload: dist->rank out of range");
+  if (world > 1) {
+    if (n_nodes < world) return fail(DI_EINVAL, "di_graph_upload: fewer nodes than ranks");
+    if (flags & (DI_BUILD_CSC | DI_LOCAL_LINKS))
+      return fail(DI_EINVAL, "di_graph_upload: DI_BUILD_CSC and DI_LOCAL_LINKS are single-GPU / "
+                             "not available on a partitioned graph (every rank passes the full link "
+                             "list; sweeps are push-only)");
+    if (!grp && !dist->nccl_unique_id)
+      return fail(DI_EINVAL, "di_graph_upload: dist needs an NCCL unique id or a di_group");
+    if (grp && grp->world != world)
+      return fail(DI_EINVAL, "di_graph_upload: dist->world differs from the group's size");
+  }
   int dev = 0, ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(DI_ECUDA, "di_graph_upload: no CUDA device");
@@ -119,6 +173,23 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
   g->n = g->n_global = n_nodes;
   g->lo = 0;
   g->hi = n_nodes;
+  g->rank = rank;
+  g->world = world;
+  if (world > 1) {  // the communicator first: ncclCommInitRank is collective
+    Comm *c = nullptr;
+    di_status cs = grp ? make_group_comm(grp, rank, &c)
+                       : make_nccl_comm(dist->nccl_unique_id, rank, world, &c);
+    if (cs != DI_OK) {
+      delete g;
+      return cs;
+    }
+    g->comm = c;
+    if (grp) {
+      g->group = grp;
+      std::lock_guard<std::mutex> lk(g->group->m);
+      g->group->handles++;
+    }
+  }
   if (const char *e = getenv("DI_RED_HINT")) g->red_hint = atoi(e);
   if (const char *e = getenv("DI_PUSH_OCC")) g->push_occ = atoi(e);
   if (const char *e = getenv("DI_AUTO_RATIO")) g->auto_ratio = atof(e);
@@ -126,6 +197,7 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
   di_status s = build_graph(*g, src, dst, n_links, flags);
   if (s == DI_OK) s = alloc_state(*g);
   if (s == DI_OK) s = alloc_pull(*g);
+  if (s == DI_OK && world > 1) s = alloc_dist(*g);
   if (s != DI_OK) {
     free_graph(g);
     return s;
@@ -177,6 +249,20 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     DI_CK(cudaStreamSynchronize(g.stream));
     cudaFree(bad);
     if (hb) return fail(DI_EINVAL, "di_solve: B has a negative or non-finite entry");
+  }
+  if (g.world > 1) {
+    if (v != DI_SOP && v != DI_CYC)
+      return fail(DI_EINVAL, "di_solve: a partitioned graph runs DI_SOP / DI_CYC only");
+    if (flags & (DI_PULL | DI_AUTO | DI_GRAPH_LOOP))
+      return fail(DI_EINVAL, "di_solve: a partitioned graph runs push sweeps only");
+    if ((flags & DI_RESUME) && !g.solved) return fail(DI_ESTATE, "di_solve: DI_RESUME before any solve");
+    const double *Bint = B;
+    if (B && g.reordered) {  // caller's slice [lo, hi) in the caller's numbering
+      if (!g.Bperm) DI_CK(cudaMalloc(&g.Bperm, (size_t)g.n * 8));
+      gather(g, g.Bperm, B - g.lo, g.old_of + g.lo);
+      Bint = g.Bperm;
+    }
+    return solve_dist(g, d, Bint, tol, (int)v, max_sweeps, flags, st);
   }
   if (v == DI_PI_PULL || v == DI_PI_PUSH || v == DI_GS_BLOCK)
     return run_comparator(g, d, tol, (int)v, max_sweeps, flags, st);
@@ -335,14 +421,21 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
 di_status di_residual(di_graph h, double *l1_out, double *F_out) {
   Graph *g = (Graph *)h;
   if (!g) return fail(DI_EINVAL, "di_residual: NULL handle");
-  int64_t launches = 0;
-  launch_reduce_F(*g, &launches);
-  di_status s = sync_scalars(*g);
-  if (s != DI_OK) return s;
-  if (l1_out) *l1_out = g->sc_host->resid;
+  if (g->world > 1) {  // collective: the global sum
+    double l1 = 0.0;
+    di_status s = dist_residual(*g, &l1);
+    if (s != DI_OK) return s;
+    if (l1_out) *l1_out = l1;
+  } else {
+    int64_t launches = 0;
+    launch_reduce_F(*g, &launches);
+    di_status s = sync_scalars(*g);
+    if (s != DI_OK) return s;
+    if (l1_out) *l1_out = g->sc_host->resid;
+  }
   if (F_out) {
     if (g->reordered)
-      gather(*g, F_out, g->F, g->new_of);
+      gather(*g, F_out, g->F - g->lo, g->new_of + g->lo);
     else
       DI_CK(cudaMemcpyAsync(F_out, g->F, (size_t)g->n * 8, cudaMemcpyDeviceToDevice, g->stream));
     DI_CK(cudaStreamSynchronize(g->stream));
@@ -354,7 +447,7 @@ di_status di_history(di_graph h, double *H_out) {
   Graph *g = (Graph *)h;
   if (!g || !H_out) return fail(DI_EINVAL, "di_history: NULL argument");
   if (g->reordered)
-    gather(*g, H_out, g->H, g->new_of);
+    gather(*g, H_out, g->H - g->lo, g->new_of + g->lo);
   else
     DI_CK(cudaMemcpyAsync(H_out, g->H, (size_t)g->n * 8, cudaMemcpyDeviceToDevice, g->stream));
   DI_CK(cudaStreamSynchronize(g->stream));

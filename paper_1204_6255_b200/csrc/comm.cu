@@ -1,0 +1,202 @@
+// comm.cu — NCCL (dlopen'ed) and in-process group backends of the Comm interface (comm.cuh).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "comm.cuh"
+
+namespace di {
+namespace {
+
+// ------------------------------------------------------------------ NCCL entry points
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi &nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    // the copy torch loaded (RTLD_NOLOAD), else whatever the loader finds
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = std::string("cannot dlopen libnccl.so.2: ") + dlerror();
+      return a;
+    }
+#define DI_SYM(f)                                                          \
+  a.f = reinterpret_cast<decltype(a.f)>(dlsym(h, "nccl" #f));              \
+  if (!a.f) {                                                              \
+    a.why = "libnccl.so.2 lacks nccl" #f;                                  \
+    return a;                                                              \
+  }
+    DI_SYM(GetUniqueId)
+    DI_SYM(CommInitRank)
+    DI_SYM(CommDestroy)
+    DI_SYM(AllReduce)
+    DI_SYM(Send)
+    DI_SYM(Recv)
+    DI_SYM(GroupStart)
+    DI_SYM(GroupEnd)
+    DI_SYM(GetErrorString)
+#undef DI_SYM
+    a.ok = true;
+    return a;
+  }();
+  return api;
+}
+
+#define DI_NCK(call)                                                                    \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess) {                                                            \
+      ::di::set_error(std::string(#call) + ": " + nccl().GetErrorString(r_));           \
+      return DI_ENCCL;                                                                  \
+    }                                                                                   \
+  } while (0)
+
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  ~NcclComm() override {
+    if (comm) nccl().CommDestroy(comm);
+  }
+  di_status allreduce_f64(double *dev, int count, cudaStream_t st) override {
+    DI_NCK(nccl().AllReduce(dev, dev, (size_t)count, ncclFloat64, ncclSum, comm, st));
+    return DI_OK;
+  }
+  di_status allreduce_i64(int64_t *dev, int count, cudaStream_t st) override {
+    DI_NCK(nccl().AllReduce(dev, dev, (size_t)count, ncclInt64, ncclSum, comm, st));
+    return DI_OK;
+  }
+  di_status exchange(const void *const *sbuf, const size_t *sbytes, void *const *rbuf,
+                     const size_t *rbytes, cudaStream_t st) override {
+    DI_NCK(nccl().GroupStart());
+    for (int p = 0; p < world; p++) {
+      if (p == rank) continue;
+      if (sbytes[p]) DI_NCK(nccl().Send(sbuf[p], sbytes[p], ncclUint8, p, comm, st));
+      if (rbytes[p]) DI_NCK(nccl().Recv(rbuf[p], rbytes[p], ncclUint8, p, comm, st));
+    }
+    DI_NCK(nccl().GroupEnd());
+    return DI_OK;
+  }
+};
+
+// ------------------------------------------------------------------ in-process group
+struct GroupComm : Comm {
+  Group *g = nullptr;
+  di_status aborted() {
+    set_error("in-process group aborted (another rank failed)");
+    return DI_ESTATE;
+  }
+  template <typename T>
+  di_status allreduce(T *dev, int count, cudaStream_t st, std::vector<std::vector<T>> &stage) {
+    std::vector<T> &mine = stage[rank];
+    mine.assign((size_t)count, T(0));
+    DI_CK(cudaMemcpyAsync(mine.data(), dev, (size_t)count * sizeof(T), cudaMemcpyDeviceToHost, st));
+    DI_CK(cudaStreamSynchronize(st));
+    if (!g->barrier()) return aborted();
+    std::vector<T> sum((size_t)count, T(0));
+    for (int p = 0; p < world; p++)  // rank order: every rank computes the identical sum
+      for (int k = 0; k < count; k++) sum[k] += stage[p][k];
+    if (!g->barrier()) return aborted();  // nobody restages before everyone has summed
+    DI_CK(cudaMemcpyAsync(dev, sum.data(), (size_t)count * sizeof(T), cudaMemcpyHostToDevice, st));
+    DI_CK(cudaStreamSynchronize(st));
+    return DI_OK;
+  }
+  di_status allreduce_f64(double *dev, int count, cudaStream_t st) override {
+    return allreduce(dev, count, st, g->red_f);
+  }
+  di_status allreduce_i64(int64_t *dev, int count, cudaStream_t st) override {
+    return allreduce(dev, count, st, g->red_i);
+  }
+  di_status exchange(const void *const *sbuf, const size_t *sbytes, void *const *rbuf,
+                     const size_t *rbytes, cudaStream_t st) override {
+    DI_CK(cudaStreamSynchronize(st));  // send buffers complete
+    for (int p = 0; p < world; p++) {
+      g->sptr[rank][p] = (p == rank) ? nullptr : sbuf[p];
+      g->sbytes[rank][p] = (p == rank) ? 0 : sbytes[p];
+    }
+    if (!g->barrier()) return aborted();
+    di_status s = DI_OK;
+    for (int p = 0; p < world; p++) {
+      if (p == rank) continue;
+      if (g->sbytes[p][rank] != rbytes[p]) {
+        set_error("group exchange: rank " + std::to_string(p) + " sends " +
+                  std::to_string(g->sbytes[p][rank]) + " bytes to rank " + std::to_string(rank) +
+                  ", which expects " + std::to_string(rbytes[p]));
+        s = DI_ESTATE;
+        continue;
+      }
+      if (rbytes[p] &&
+          cudaMemcpyAsync(rbuf[p], g->sptr[p][rank], rbytes[p], cudaMemcpyDeviceToDevice, st) !=
+              cudaSuccess)
+        s = DI_ECUDA;
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess && s == DI_OK) s = DI_ECUDA;
+    // senders may reuse their buffers only after every receiver copied
+    if (!g->barrier()) return aborted();
+    if (s != DI_OK) g->abort();
+    return s;
+  }
+};
+
+}  // namespace
+
+di_status nccl_unique_id(void *out128) {
+  const NcclApi &a = nccl();
+  if (!a.ok) {
+    set_error(a.why);
+    return DI_ENCCL;
+  }
+  ncclUniqueId id;
+  DI_NCK(a.GetUniqueId(&id));
+  memcpy(out128, &id, sizeof(id));
+  return DI_OK;
+}
+
+di_status make_nccl_comm(const void *unique_id, int rank, int world, Comm **out) {
+  *out = nullptr;
+  const NcclApi &a = nccl();
+  if (!a.ok) {
+    set_error(a.why);
+    return DI_ENCCL;
+  }
+  ncclUniqueId id;
+  memcpy(&id, unique_id, sizeof(id));
+  NcclComm *c = new NcclComm();
+  c->rank = rank;
+  c->world = world;
+  ncclResult_t r = a.CommInitRank(&c->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclCommInitRank: ") + a.GetErrorString(r));
+    c->comm = nullptr;
+    delete c;
+    return DI_ENCCL;
+  }
+  *out = c;
+  return DI_OK;
+}
+
+di_status make_group_comm(Group *grp, int rank, Comm **out) {
+  GroupComm *c = new GroupComm();
+  c->g = grp;
+  c->rank = rank;
+  c->world = grp->world;
+  *out = c;
+  return DI_OK;
+}
+
+}  // namespace di

@@ -48,6 +48,14 @@ struct __align__(16) PullEntry {
 };
 enum SweepMode { MODE_PUSH = 0, MODE_PULL = 1, MODE_AUTO = 2 };
 
+// Multi-GPU: rank g owns the node range [b[g], b[g+1]) (caller's numbering, and
+// internal numbering after the per-range relabelling).
+constexpr int kMaxWorld = 16;
+struct DistBounds {
+  int world;
+  int64_t b[kMaxWorld + 1];
+};
+
 // Device-resident sweep state. Every field is written only by the "last block" of the
 // select kernel (the finaliser) or by the host between solves, so kernels never race on it.
 struct __align__(256) Scalars {
@@ -146,7 +154,20 @@ struct Graph {
   int64_t log_n = 0;
   bool solved = false;
   double last_d = 0.85;
-  void *nccl = nullptr;      // ncclComm_t when world > 1
+  // multi-GPU (dist.cu): partition, communicator and the per-sweep exchange buffers
+  DistBounds bounds{1, {0}};
+  struct Comm *comm = nullptr;
+  struct Group *group = nullptr;
+  double *R = nullptr;            // remote fluid accumulator, fp64[n_global], all-zero between sweeps
+  int32_t *tl = nullptr;          // touched remote ids, segment [b[p], b[p+1]) for owner p
+  double *sval = nullptr;         // packed values of the touched ids (same segmentation)
+  unsigned long long *tcnt = nullptr;  // touched count per owner (one 256-B line each)
+  int64_t *sendcnt = nullptr;     // device: entries for each peer this sweep, then received counts
+  int64_t *sendcnt_h = nullptr;   // pinned: [0, world) sent, [world, 2 world) received
+  double *dsum = nullptr;         // device: q, s, e (local, then global after the allreduce)
+  int64_t *isum = nullptr;        // device: selected, selected non-dangling, links, scanned
+  int32_t *rid = nullptr;         // received ids (global internal), capacity (world-1) * n
+  double *rval = nullptr;         // received values
 };
 
 // ---------------------------------------------------------------- error plumbing
@@ -175,6 +196,12 @@ void launch_push(Graph &g, int64_t *launches);
 void launch_finalize(Graph &g, int64_t *launches);
 void launch_pull(Graph &g, int64_t *launches);
 di_status alloc_pull(Graph &g);
+di_status alloc_dist(Graph &g);
+// dist.cu
+di_status solve_dist(Graph &g, double d, const double *B, double tol, int variant,
+                     int64_t max_sweeps, uint32_t flags, di_stats *st);
+di_status dist_residual(Graph &g, double *l1);
+void free_dist(Graph &g);
 // comparators.cu
 di_status run_comparator(Graph &g, double d, double tol, int variant, int64_t max_sweeps,
                          uint32_t flags, di_stats *st);

@@ -1,0 +1,501 @@
+// dist.cu — D-iteration over a 1-D node partition, one rank per GPU.
+//
+// D-iteration is order-free (any sequence of diffusions keeps F = B + P.H - H), so a
+// sweep splits into local diffusion plus one additive exchange of the fluid sent across the
+// partition. Rank g owns nodes [lo, hi) (F, H, deg, kloop and the CSR rows of its sources with
+// global column ids). One sweep on every rank:
+//   1. k_select    — the single-GPU select/compact kernel on the owned nodes, global r_n.
+//   2. k_push_dist — degree-binned push; a local target gets a RED into F, a remote target j an
+//                    fp64 atomicAdd into the remote accumulator R[j] (global size, all-zero
+//                    between sweeps). The add that finds R[j] == 0.0 is the first touch of j this
+//                    sweep (v > 0 and sums of positives never return to 0), and appends j to
+//                    the touched list of j's owner (warp-aggregated reservation). Its last block
+//                    writes this rank's sweep sums and per-peer counts.
+//   3. k_pack      — for every touched j: value = R[j], R[j] = 0 (R is clean for the next sweep).
+//   4. allreduce of the sweep sums; exchange of the per-peer counts (8 B per peer).
+//   5. exchange of the (id int32, value fp64) lists — 12 B per distinct (remote target, sweep)
+//      pair, the algorithmic exchange of SURVEY §8(d).
+//   6. k_apply_recv — F[j - lo] += value (RED: several peers may send the same j).
+//   7. k_dist_finalize — the single-GPU finaliser on the global sums: every rank takes the same
+//      stop / guard decision.
+// The host reads the counts after step 4 (one synchronisation per sweep: NCCL needs the receive
+// sizes on the host). The collectives are NCCL send/recv + allreduce (comm.cu), or the
+// in-process group backend for emulated ranks on one GPU.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "comm.cuh"
+#include "sweep.cuh"
+
+namespace di {
+namespace {
+
+struct DistArgs {
+  double *R;
+  int32_t *tl;
+  double *sval;
+  unsigned long long *tcnt;  // [world * 32]: touched count per owner, one line each
+  int64_t *sendcnt;          // [world]
+  double *dsum;              // q, s, e
+  int64_t *isum;             // sel, nd, lk, scanned
+  DistBounds bd;
+  int rank;
+};
+
+__device__ __forceinline__ int owner_of(const DistBounds &bd, int64_t j) {
+  int p = 0;
+#pragma unroll 1
+  for (int q = 1; q < bd.world; q++) p += (j >= bd.b[q]) ? 1 : 0;
+  return p;
+}
+
+// One target of one link, executed by all 32 lanes of a warp in convergence (the callers' loops
+// are warp-uniform); `valid` masks the lanes without a target.
+__device__ __forceinline__ void dist_add(const SweepArgs &a, const DistArgs &x, int32_t j, double v,
+                                         bool valid, uint64_t fpol) {
+  const int lane = threadIdx.x & 31;
+  bool first = false;
+  int p = -1;
+  if (valid) {
+    const int64_t jl = (int64_t)j - a.lo;
+    if (jl >= 0 && jl < a.n) {
+      red_add_f64_hint(a.F + jl, v, fpol);
+    } else {
+      const double old = atomicAdd(x.R + j, v);
+      if (old == 0.0) {
+        first = true;
+        p = owner_of(x.bd, j);
+      }
+    }
+  }
+  const unsigned fm = __ballot_sync(0xffffffffu, first);
+  if (fm == 0u) return;
+  const unsigned peers = __match_any_sync(0xffffffffu, p);
+  const int leader = __ffs(peers) - 1;
+  unsigned long long base = 0;
+  if (first && lane == leader)
+    base = atomicAdd(x.tcnt + 32 * p, (unsigned long long)__popc(peers));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (first) {
+    const unsigned lt = peers & ((1u << lane) - 1u);
+    x.tl[x.bd.b[p] + (int64_t)base + __popc(lt)] = j;
+  }
+}
+
+template <bool LOOPS>
+__device__ __forceinline__ void dist_group(const SweepArgs &a, const DistArgs &x, int4 q, int64_t p0,
+                                           int64_t beg, int64_t end, int32_t gi, double v,
+                                           bool valid, uint64_t fpol) {
+  const int32_t jj[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    const int64_t p = p0 + c;
+    const bool ok = valid && p >= beg && p < end && (!LOOPS || jj[c] != gi);
+    dist_add(a, x, jj[c], v, ok, fpol);
+  }
+}
+
+// The bins of k_push (diffusion.cu), with warp-uniform loops so that dist_add can aggregate.
+template <bool LOOPS>
+__global__ void __launch_bounds__(kPushThreads) k_push_dist(const SweepArgs a, const DistArgs x) {
+  __shared__ bool s_last;
+  Scalars *sc = a.sc;
+  if (sc->stop) return;
+  const uint64_t pol = policy_evict_first();
+  const uint64_t fpol = a.red_hint ? policy_evict_last() : policy_evict_normal();
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * (kPushThreads / 32);
+  const int64_t w = (int64_t)blockIdx.x * (kPushThreads / 32) + (threadIdx.x >> 5);
+  const int32_t *__restrict__ col = a.col;
+  int64_t U[kBins];
+#pragma unroll
+  for (int b = 0; b < kBins; b++) U[b] = (int64_t)sc->bin_fill[b][0];
+  // bins C and W: warp per row (chunk)
+  for (int b = BIN_C; b >= BIN_W; b--) {
+    for (int64_t u = w; u < U[b]; u += W) {
+      const Entry en = a.fr.ent[b][u];
+      const int32_t gi = LOOPS ? (int32_t)(a.fr.id[b][u] + a.lo) : -1;
+      const int64_t beg = (int64_t)(en.bl & kBegMask);
+      const int64_t end = beg + (int64_t)(en.bl >> kLenShift);
+      const int64_t a0 = beg & ~3ll;
+      const int nvec = (int)((end - a0 + 3) >> 2);
+      const bool vpos = en.v > 0.0;
+      for (int vb = 0; vb < nvec; vb += 32) {
+        const int v0 = vb + lane;
+        int4 q = make_int4(0, 0, 0, 0);
+        if (v0 < nvec) q = ld_col4(col + a0 + 4 * (int64_t)v0, pol);
+        dist_group<LOOPS>(a, x, q, a0 + 4 * (int64_t)v0, beg, end, gi, en.v, vpos && v0 < nvec, fpol);
+      }
+    }
+  }
+  // bin G: 8-lane group per row, 4 rows per warp step
+  {
+    const int sub = lane & 7;
+    for (int64_t ub = 4 * w; ub < U[BIN_G]; ub += 4 * W) {
+      const int64_t u = ub + (lane >> 3);
+      const bool row = u < U[BIN_G];
+      Entry en{0, 0.0};
+      int32_t gi = -1;
+      if (row) {
+        en = a.fr.ent[BIN_G][u];
+        if (LOOPS) gi = (int32_t)(a.fr.id[BIN_G][u] + a.lo);
+      }
+      const int64_t beg = (int64_t)(en.bl & kBegMask);
+      const int64_t end = beg + (int64_t)(en.bl >> kLenShift);
+      const int64_t a0 = beg & ~3ll;
+      const int nvec = row ? (int)((end - a0 + 3) >> 2) : 0;
+      const bool vpos = en.v > 0.0;
+      int4 q0 = make_int4(0, 0, 0, 0), q1 = make_int4(0, 0, 0, 0);
+      if (sub < nvec) q0 = ld_col4(col + a0 + 4 * sub, pol);
+      if (sub + 8 < nvec) q1 = ld_col4(col + a0 + 4 * (sub + 8), pol);
+      dist_group<LOOPS>(a, x, q0, a0 + 4 * sub, beg, end, gi, en.v, vpos && sub < nvec, fpol);
+      dist_group<LOOPS>(a, x, q1, a0 + 4 * (sub + 8), beg, end, gi, en.v, vpos && sub + 8 < nvec,
+                        fpol);
+    }
+  }
+  // bin T: one thread per row
+  for (int64_t ub = 32 * w; ub < U[BIN_T]; ub += 32 * W) {
+    const int64_t u = ub + lane;
+    const bool row = u < U[BIN_T];
+    Entry en{0, 0.0};
+    int32_t gi = -1;
+    if (row) {
+      en = a.fr.ent[BIN_T][u];
+      if (LOOPS) gi = (int32_t)(a.fr.id[BIN_T][u] + a.lo);
+    }
+    const int64_t beg = (int64_t)(en.bl & kBegMask);
+    const int64_t end = beg + (int64_t)(en.bl >> kLenShift);
+    const int64_t a0 = beg & ~3ll;
+    const int nvec = row ? (int)((end - a0 + 3) >> 2) : 0;
+    const bool vpos = en.v > 0.0;
+    int4 q0 = make_int4(0, 0, 0, 0), q1 = make_int4(0, 0, 0, 0), q2 = make_int4(0, 0, 0, 0);
+    if (nvec > 0) q0 = ld_col4(col + a0, pol);
+    if (nvec > 1) q1 = ld_col4(col + a0 + 4, pol);
+    if (nvec > 2) q2 = ld_col4(col + a0 + 8, pol);
+    dist_group<LOOPS>(a, x, q0, a0, beg, end, gi, en.v, vpos && nvec > 0, fpol);
+    dist_group<LOOPS>(a, x, q1, a0 + 4, beg, end, gi, en.v, vpos && nvec > 1, fpol);
+    dist_group<LOOPS>(a, x, q2, a0 + 8, beg, end, gi, en.v, vpos && nvec > 2, fpol);
+  }
+  // last block: this rank's sweep sums and per-peer counts
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const SweepSums s = reduce_partials(a, kPushThreads);
+  if (threadIdx.x == 0) {
+    x.dsum[0] = s.q;
+    x.dsum[1] = s.s;
+    x.dsum[2] = s.e;
+    x.isum[0] = s.sel;
+    x.isum[1] = s.nd;
+    x.isum[2] = s.lk;
+    x.isum[3] = s.scanned;
+    sc->ticket = 0;
+  }
+  if (threadIdx.x < x.bd.world) {
+    volatile unsigned long long *c = x.tcnt + 32 * threadIdx.x;
+    x.sendcnt[threadIdx.x] = (int64_t)*c;
+    *c = 0ull;
+  }
+}
+
+// value of every touched remote id; R back to all-zero
+__global__ void k_pack(const Scalars *sc, DistArgs x) {
+  if (sc->stop) return;
+  for (int p = 0; p < x.bd.world; p++) {
+    if (p == x.rank) continue;
+    const int64_t m = x.sendcnt[p], off = x.bd.b[p];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)gridDim.x * blockDim.x) {
+      const int32_t j = x.tl[off + k];
+      x.sval[off + k] = x.R[j];
+      x.R[j] = 0.0;
+    }
+  }
+}
+
+__global__ void k_apply_recv(double *__restrict__ F, int64_t lo, const int32_t *__restrict__ rid,
+                             const double *__restrict__ rval, int64_t m) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x)
+    red_add_f64(F + ((int64_t)rid[k] - lo), rval[k]);
+}
+
+// the single-GPU finaliser on the allreduced sums
+__global__ void k_dist_finalize(const SweepArgs a, const double *dsum, const int64_t *isum) {
+  if (threadIdx.x != 0 || a.sc->stop) return;
+  SweepSums s{dsum[0], dsum[1], dsum[2], isum[0], isum[1], isum[2], isum[3]};
+  apply_sweep(a, s);
+}
+
+__global__ void k_set_r(Scalars *sc, const double *sum, int set_r) {
+  sc->resid = *sum;
+  if (set_r) sc->r = *sum;
+}
+
+__global__ void k_copy_resid(const Scalars *sc, double *out) { *out = sc->resid; }
+
+int grid_of(int64_t n, int sms) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+}
+
+DistArgs dist_args(Graph &g) {
+  DistArgs x;
+  x.R = g.R;
+  x.tl = g.tl;
+  x.sval = g.sval;
+  x.tcnt = g.tcnt;
+  x.sendcnt = g.sendcnt;
+  x.dsum = g.dsum;
+  x.isum = g.isum;
+  x.bd = g.bounds;
+  x.rank = g.rank;
+  return x;
+}
+
+// global sum F (exact local tree sum, then the allreduce); set_r: also r = that sum
+di_status global_sum_F(Graph &g, int set_r, int64_t *launches) {
+  launch_reduce_F(g, launches);
+  k_copy_resid<<<1, 1, 0, g.stream>>>(g.sc, g.dsum + 3);
+  di_status s = g.comm->allreduce_f64(g.dsum + 3, 1, g.stream);
+  if (s != DI_OK) return s;
+  k_set_r<<<1, 1, 0, g.stream>>>(g.sc, g.dsum + 3, set_r);
+  *launches += 2;
+  return DI_OK;
+}
+
+}  // namespace
+
+di_status alloc_dist(Graph &g) {
+  const int64_t N = g.n_global;
+  const int G = g.world;
+  DI_CK(cudaMalloc(&g.R, (size_t)N * 8));
+  DI_CK(cudaMemset(g.R, 0, (size_t)N * 8));
+  DI_CK(cudaMalloc(&g.tl, (size_t)N * 4));
+  DI_CK(cudaMalloc(&g.sval, (size_t)N * 8));
+  DI_CK(cudaMalloc(&g.tcnt, (size_t)G * 32 * 8));
+  DI_CK(cudaMemset(g.tcnt, 0, (size_t)G * 32 * 8));
+  DI_CK(cudaMalloc(&g.sendcnt, (size_t)2 * G * 8));
+  DI_CK(cudaMemset(g.sendcnt, 0, (size_t)2 * G * 8));
+  DI_CK(cudaMallocHost(&g.sendcnt_h, (size_t)2 * G * 8 + 8 * 8));
+  DI_CK(cudaMalloc(&g.dsum, 8 * 8));
+  DI_CK(cudaMalloc(&g.isum, 8 * 8));
+  const size_t cap = (size_t)std::max<int64_t>(1, (int64_t)(G - 1) * g.n);
+  DI_CK(cudaMalloc(&g.rid, cap * 4));
+  DI_CK(cudaMalloc(&g.rval, cap * 8));
+  return DI_OK;
+}
+
+void free_dist(Graph &g) {
+  void *p[] = {g.R, g.tl, g.sval, g.tcnt, g.sendcnt, g.dsum, g.isum, g.rid, g.rval};
+  for (void *q : p)
+    if (q) cudaFree(q);
+  if (g.sendcnt_h) cudaFreeHost(g.sendcnt_h);
+  delete g.comm;
+  g.comm = nullptr;
+}
+
+di_status dist_residual(Graph &g, double *l1) {
+  int64_t launches = 0;
+  di_status s = global_sum_F(g, 0, &launches);
+  if (s != DI_OK) return s;
+  DI_CK(cudaMemcpyAsync(l1, g.dsum + 3, 8, cudaMemcpyDeviceToHost, g.stream));
+  DI_CK(cudaStreamSynchronize(g.stream));
+  return DI_OK;
+}
+
+di_status solve_dist(Graph &g, double d, const double *B, double tol, int variant,
+                     int64_t max_sweeps, uint32_t flags, di_stats *st) {
+  const int G = g.world, me = g.rank;
+  const bool resume = flags & DI_RESUME;
+  const int paper = (flags & DI_PAPER_ERROR) ? 1 : 0;
+  int64_t launches = 0;
+  cudaEvent_t t0, t1;
+  DI_CK(cudaEventCreate(&t0));
+  DI_CK(cudaEventCreate(&t1));
+  {
+    Scalars &s = *g.sc_host;
+    const uint32_t epoch = s.epoch ? s.epoch : 1;
+    const double e_prev = s.e;
+    memset(&s, 0, sizeof(Scalars));
+    s.epoch = epoch;
+    s.e = resume ? e_prev : 0.0;
+    s.d = d;
+    s.tol = tol;
+    s.variant = variant;
+    s.paper_err = paper;
+    s.trace = (flags & DI_TRACE) ? 1 : 0;
+    s.mode = MODE_PUSH;
+  }
+  DI_CK(cudaEventRecord(t0, g.stream));
+  DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
+  DI_CK(cudaMemsetAsync(g.R, 0, (size_t)g.n_global * 8, g.stream));
+  DI_CK(cudaMemsetAsync(g.tcnt, 0, (size_t)G * 32 * 8, g.stream));
+  di_status s = DI_OK;
+  if (!resume) {
+    launch_init(g, B, d, &launches);  // F = B (local slice), H = 0; local sum
+  }
+  s = global_sum_F(g, 1, &launches);
+  if (s != DI_OK) return s;
+  DI_CK(cudaMemcpyAsync(g.sc_host, g.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, g.stream));
+  DI_CK(cudaStreamSynchronize(g.stream));
+  auto err_of = [&](double r, double e) { return paper ? r / (1.0 - d - d * e) : r; };
+  bool converged = err_of(g.sc_host->r, g.sc_host->e) <= tol;
+  const SweepArgs a = sweep_args(g, 0);
+  const DistArgs x = dist_args(g);
+  int occ = 0;
+  if (g.has_loops)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push_dist<true>, kPushThreads, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push_dist<false>, kPushThreads, 0);
+  occ = std::max(1, occ);
+  std::vector<const void *> sb(G), sbv(G), cb_s(G);
+  std::vector<void *> rb(G), rbv(G), cb_r(G);
+  std::vector<size_t> s4(G), r4(G), s8(G), r8(G), c8(G, 8);
+  for (int p = 0; p < G; p++) {
+    cb_s[p] = g.sendcnt + p;
+    cb_r[p] = g.sendcnt + G + p;
+  }
+  double xbytes = 0.0;
+  int64_t xentries = 0;
+  int64_t launched = 0;
+  const bool prof = flags & DI_PROFILE;
+  cudaEvent_t pe[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (prof)
+    for (auto &e : pe) DI_CK(cudaEventCreate(&e));
+  double push_ms = 0.0, select_ms = 0.0, xchg_ms = 0.0;
+  int64_t push_launches = 0;
+  while (!converged && launched < max_sweeps) {
+    while (launched < max_sweeps) {
+      if (prof) DI_CK(cudaEventRecord(pe[0], g.stream));
+      launch_select(g, 0, &launches);
+      if (prof) DI_CK(cudaEventRecord(pe[1], g.stream));
+      if (g.has_loops)
+        k_push_dist<true><<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a, x);
+      else
+        k_push_dist<false><<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a, x);
+      if (prof) DI_CK(cudaEventRecord(pe[2], g.stream));
+      k_pack<<<g.num_sms * 4, 256, 0, g.stream>>>(g.sc, x);
+      launches += 2;
+      launched++;
+      if ((s = g.comm->allreduce_f64(g.dsum, 3, g.stream)) != DI_OK) return s;
+      if ((s = g.comm->allreduce_i64(g.isum, 4, g.stream)) != DI_OK) return s;
+      if ((s = g.comm->exchange(cb_s.data(), c8.data(), cb_r.data(), c8.data(), g.stream)) != DI_OK)
+        return s;
+      DI_CK(cudaMemcpyAsync(g.sendcnt_h, g.sendcnt, (size_t)2 * G * 8, cudaMemcpyDeviceToHost,
+                            g.stream));
+      DI_CK(cudaMemcpyAsync(g.sc_host, g.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, g.stream));
+      DI_CK(cudaStreamSynchronize(g.stream));
+      if (g.sc_host->stop) {  // the previous sweep converged: this one was a no-op on every rank
+        launched--;
+        break;
+      }
+      if (prof) {
+        float a01 = 0.f, a12 = 0.f;
+        cudaEventElapsedTime(&a01, pe[0], pe[1]);
+        cudaEventElapsedTime(&a12, pe[1], pe[2]);
+        select_ms += a01;
+        push_ms += a12;
+        push_launches++;
+        DI_CK(cudaEventRecord(pe[3], g.stream));
+      }
+      int64_t off = 0;
+      for (int p = 0; p < G; p++) {
+        const int64_t ns = (p == me) ? 0 : g.sendcnt_h[p];
+        const int64_t nr = (p == me) ? 0 : g.sendcnt_h[G + p];
+        sb[p] = g.tl + g.bounds.b[p];
+        sbv[p] = g.sval + g.bounds.b[p];
+        s4[p] = (size_t)ns * 4;
+        s8[p] = (size_t)ns * 8;
+        rb[p] = g.rid + off;
+        rbv[p] = g.rval + off;
+        r4[p] = (size_t)nr * 4;
+        r8[p] = (size_t)nr * 8;
+        off += nr;
+        xentries += ns;
+      }
+      if ((s = g.comm->exchange(sb.data(), s4.data(), rb.data(), r4.data(), g.stream)) != DI_OK)
+        return s;
+      if ((s = g.comm->exchange(sbv.data(), s8.data(), rbv.data(), r8.data(), g.stream)) != DI_OK)
+        return s;
+      if (off > 0) {
+        k_apply_recv<<<grid_of(off, g.num_sms), 256, 0, g.stream>>>(g.F, g.lo, g.rid, g.rval, off);
+        launches++;
+      }
+      k_dist_finalize<<<1, 32, 0, g.stream>>>(a, g.dsum, g.isum);
+      launches++;
+      if (prof) {  // exchange of the lists + apply (the counts exchange is in the sync above)
+        DI_CK(cudaEventRecord(pe[0], g.stream));
+        DI_CK(cudaEventSynchronize(pe[0]));
+        float a30 = 0.f;
+        cudaEventElapsedTime(&a30, pe[3], pe[0]);
+        xchg_ms += a30;
+      }
+      // the device decided; its stop flag is read back with the next sweep's counts
+    }
+    // exact global residual (deterministic on each rank, summed by the collective)
+    if ((s = global_sum_F(g, 0, &launches)) != DI_OK) return s;
+    DI_CK(cudaMemcpyAsync(g.sc_host, g.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, g.stream));
+    DI_CK(cudaStreamSynchronize(g.stream));
+    converged = err_of(g.sc_host->resid, g.sc_host->e) <= tol;
+    if (converged || !g.sc_host->stop) break;
+    // the q + s prediction said converged but the exact sum disagrees by rounding: continue
+    const int32_t zero = 0;
+    DI_CK(cudaMemcpyAsync(&g.sc->stop, &zero, 4, cudaMemcpyHostToDevice, g.stream));
+    DI_CK(cudaStreamSynchronize(g.stream));
+    g.sc_host->stop = 0;
+  }
+  if (launched == 0 && !converged) {
+    if ((s = global_sum_F(g, 0, &launches)) != DI_OK) return s;
+    DI_CK(cudaMemcpyAsync(g.sc_host, g.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, g.stream));
+    DI_CK(cudaStreamSynchronize(g.stream));
+  }
+  for (auto e : pe)
+    if (e) cudaEventDestroy(e);
+  DI_CK(cudaEventRecord(t1, g.stream));
+  DI_CK(cudaEventSynchronize(t1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  DI_CK(cudaGetLastError());
+  g.solved = true;
+  g.last_d = d;
+  g.log_n = std::min<int64_t>(g.sc_host->sweeps, kLogCap);
+  if (st) {
+    const Scalars &c = *g.sc_host;
+    memset(st, 0, sizeof(*st));
+    st->sweeps = c.sweeps;
+    st->selected_total = c.selected_total;
+    st->link_diffusions = c.links_total;
+    st->starvation_fallbacks = c.guards;
+    st->nodes_scanned = c.scanned_total;
+    st->gpu_launches = launches;
+    st->residual_l1 = c.resid;
+    st->dangling_absorbed = c.e;
+    st->equivalent_iterations = g.l_global > 0 ? (double)c.links_total / (double)g.l_global : 0.0;
+    st->solve_ms = ms;
+    st->counted_bytes = 12.0 * c.scanned_total + 40.0 * c.selected_total + 20.0 * c.links_total;
+    st->push_bytes = 16.0 * c.selected_nd_total + 20.0 * c.links_total;
+    st->error_estimate = c.resid / (1.0 - d - d * c.e);
+    st->converged = converged ? 1 : 0;
+    st->variant = variant;
+    xbytes = 12.0 * (double)xentries;
+    st->exchange_bytes = xbytes;
+    st->exchange_entries = xentries;
+    st->push_ms = push_ms;
+    st->select_ms = select_ms;
+    st->push_launches = push_launches;
+    st->exchange_ms = xchg_ms;
+  }
+  return converged ? DI_OK : DI_NOT_CONVERGED;
+}
+
+}  // namespace di

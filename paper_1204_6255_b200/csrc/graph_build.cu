@@ -28,31 +28,73 @@ __global__ void k_validate(const int32_t *__restrict__ src, const int32_t *__res
   }
 }
 
-// sort key for the relabelling: descending in-degree (ties: ascending id, radix sort is stable)
-__global__ void k_perm_keys(const uint32_t *__restrict__ indeg, int64_t n, uint32_t *__restrict__ key,
-                            int32_t *__restrict__ iota) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    key[i] = 0xFFFFFFFFu - indeg[i];
-    iota[i] = (int32_t)i;
-  }
-}
-
 // rank r (0 = largest in-degree) -> internal id: rank r goes to stripe r % P at position r / P,
 // stripes laid out contiguously. Nodes of similar rank share L2 lines (hot lines are fully hot)
 // while the P hottest nodes sit in P different lines / L2 slices (no single hot slice for the
-// push's REDs).
-__global__ void k_place(const int32_t *__restrict__ sorted_old, int64_t n, int64_t P,
-                        int32_t *__restrict__ new_of, int32_t *__restrict__ old_of) {
-  const int64_t M = n / P, rem = n % P;
+// push's REDs). Multi-GPU: the sorted order is (owner range, rank); every range is striped on its
+// own, so a rank's internal ids stay inside the node range it owns.
+__global__ void k_place(const int32_t *__restrict__ sorted_old, int64_t n, DistBounds bd,
+                        int64_t stripes, int32_t *__restrict__ new_of, int32_t *__restrict__ old_of) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = r % P, idx = r / P;
-    const int64_t k = s * M + (s < rem ? s : rem) + idx;
+    int g = 0;
+    while (g + 1 < bd.world && r >= bd.b[g + 1]) g++;
+    const int64_t lo = bd.b[g], m = bd.b[g + 1] - lo, rr = r - lo;
+    const int64_t P = stripes < m ? stripes : m;
+    const int64_t M = m / P, rem = m % P;
+    const int64_t s = rr % P, idx = rr / P;
+    const int64_t k = lo + s * M + (s < rem ? s : rem) + idx;
     const int32_t o = sorted_old[r];
     new_of[o] = (int32_t)k;
     old_of[k] = o;
   }
+}
+
+// relabelling key: (owner range of i, descending in-degree); ties keep ascending id (stable sort)
+__global__ void k_perm_keys64(const uint32_t *__restrict__ indeg, int64_t n, DistBounds bd,
+                              uint64_t *__restrict__ key, int32_t *__restrict__ iota) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int g = 0;
+    while (g + 1 < bd.world && i >= bd.b[g + 1]) g++;
+    key[i] = ((uint64_t)g << 32) | (uint64_t)(0xFFFFFFFFu - indeg[i]);
+    iota[i] = (int32_t)i;
+  }
+}
+
+// out-degree histogram in the caller's numbering (partition weights)
+__global__ void k_outdeg(const int32_t *__restrict__ src, int64_t L, int64_t *__restrict__ od) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
+       k += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(reinterpret_cast<unsigned long long *>(od + src[k]), 1ull);
+}
+
+// bound g = smallest i with 20*pre[i] + 12*i >= g * W / world (W = 20 L + 12 n): ranges balanced
+// on the counted bytes of a full sweep (20 per link, 12 per scanned node)
+__global__ void k_bounds(const int64_t *__restrict__ pre, int64_t n, int world, int64_t *out) {
+  const int g = threadIdx.x;
+  if (g > world) return;
+  const double W = 20.0 * (double)pre[n] + 12.0 * (double)n;
+  const double target = W * (double)g / (double)world;
+  int64_t a = 0, b = n;  // answer in [0, n]
+  while (a < b) {
+    const int64_t m = (a + b) / 2;
+    if (20.0 * (double)pre[m] + 12.0 * (double)m >= target) b = m; else a = m + 1;
+  }
+  out[g] = (g == 0) ? 0 : (g == world ? n : a);
+}
+
+// first index k in sorted keys with (key >> b) >= node
+__global__ void k_key_bound(const uint64_t *__restrict__ keys, int64_t L, int b, int64_t node0,
+                            int64_t node1, int64_t *out) {
+  if (threadIdx.x > 1) return;
+  const uint64_t target = (uint64_t)(threadIdx.x == 0 ? node0 : node1) << b;
+  int64_t a = 0, c = L;
+  while (a < c) {
+    const int64_t m = (a + c) / 2;
+    if (keys[m] >= target) c = m; else a = m + 1;
+  }
+  out[threadIdx.x] = a;
 }
 
 __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
@@ -84,19 +126,20 @@ __global__ void k_keep_flags(const uint64_t *__restrict__ keys, int64_t L, int b
 }
 
 // row_ptr[i] = first k with major(key_k) >= i; col[k] = minor(key_k); kloop via self entries.
+// keys: the links of rows [lo, lo + n) (majors relative to lo); row ids of the output are local.
 __global__ void k_csr_from_sorted(const uint64_t *__restrict__ keys, int64_t L, int64_t n, int b,
-                                  int64_t *__restrict__ ptr, int32_t *__restrict__ idx,
+                                  int64_t lo, int64_t *__restrict__ ptr, int32_t *__restrict__ idx,
                                   int32_t *__restrict__ kloop) {
   const uint64_t mask = (1ull << b) - 1;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= L;
        k += (int64_t)gridDim.x * blockDim.x) {
-    int64_t cur = (k < L) ? (int64_t)(keys[k] >> b) : n;
-    int64_t prev = (k > 0) ? (int64_t)(keys[k - 1] >> b) : -1;
+    int64_t cur = (k < L) ? (int64_t)(keys[k] >> b) - lo : n;
+    int64_t prev = (k > 0) ? (int64_t)(keys[k - 1] >> b) - lo : -1;
     for (int64_t i = prev + 1; i <= cur; i++) ptr[i] = k;
     if (k < L) {
       int32_t minor = (int32_t)(keys[k] & mask);
       idx[k] = minor;
-      if (kloop && (int64_t)minor == cur) atomicAdd(&kloop[cur], 1);
+      if (kloop && (int64_t)minor == cur + lo) atomicAdd(&kloop[cur], 1);
     }
   }
 }
@@ -141,6 +184,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
                       uint32_t flags) {
   cudaStream_t st = g.stream;
   const int64_t n = g.n_global;
+  const int world = g.world;
   int b = 1;
   while ((1ll << b) < n) b++;
   const int sms = g.num_sms;
@@ -160,12 +204,11 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   const size_t LL = (size_t)(L > 0 ? L : 1);
   DI_CK(cudaMalloc(&keys_a.p, LL * 8));
   DI_CK(cudaMalloc(&keys_b.p, LL * 8));
-  DI_CK(cudaMalloc(&badb.p, 8));
+  DI_CK(cudaMalloc(&badb.p, 16));
   unsigned long long init_bad = ~0ull;
   DI_CK(cudaMemcpyAsync(badb.p, &init_bad, 8, cudaMemcpyHostToDevice, st));
   uint64_t *ka = (uint64_t *)keys_a.p, *kb = (uint64_t *)keys_b.p;
   const bool reorder = !(flags & DI_NO_REORDER);
-  // keys_b doubles as the in-degree scratch (n uint32 <= 8L bytes unless L tiny: separate buf)
   DevBuf indeg_b;
   uint32_t *indeg = nullptr;
   if (reorder) {
@@ -193,29 +236,63 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
               ")");
     return DI_EINVAL;
   }
-  // ---- locality relabelling: node ids sorted by descending in-degree, so the
-  //      hot push targets (and, R-MAT being correlated, the hot pull sources) share L2 lines
+  // ---- multi-GPU: 1-D node ranges in the caller's numbering, balanced on counted sweep bytes
+  //      (SURVEY §8(e)); every rank holds the full link list and computes the same bounds
+  DistBounds &bd = g.bounds;
+  bd.world = world;
+  bd.b[0] = 0;
+  bd.b[1] = n;
+  if (world > 1) {
+    DevBuf od, pre, ctmp, bnd;
+    DI_CK(cudaMalloc(&od.p, (size_t)(n + 1) * 8));
+    DI_CK(cudaMalloc(&pre.p, (size_t)(n + 1) * 8));
+    DI_CK(cudaMalloc(&bnd.p, (size_t)(kMaxWorld + 1) * 8));
+    DI_CK(cudaMemsetAsync(od.p, 0, (size_t)(n + 1) * 8, st));
+    if (L > 0) k_outdeg<<<grid_for(L, sms), 256, 0, st>>>(s_dev, L, (int64_t *)od.p);
+    size_t cb = 0;
+    DI_CK(cub::DeviceScan::ExclusiveSum(nullptr, cb, (int64_t *)od.p, (int64_t *)pre.p, n + 1, st));
+    DI_CK(cudaMalloc(&ctmp.p, cb));
+    DI_CK(cub::DeviceScan::ExclusiveSum(ctmp.p, cb, (int64_t *)od.p, (int64_t *)pre.p, n + 1, st));
+    k_bounds<<<1, 32, 0, st>>>((const int64_t *)pre.p, n, world, (int64_t *)bnd.p);
+    DI_CK(cudaMemcpyAsync(bd.b, bnd.p, (size_t)(world + 1) * 8, cudaMemcpyDeviceToHost, st));
+    DI_CK(cudaStreamSynchronize(st));
+    // every range non-empty (n >= world is checked by the caller)
+    for (int q = 1; q < world; q++) {
+      if (bd.b[q] < bd.b[q - 1] + 1) bd.b[q] = bd.b[q - 1] + 1;
+      if (bd.b[q] > n - (world - q)) bd.b[q] = n - (world - q);
+    }
+    bd.b[world] = n;
+  }
+  g.lo = bd.b[g.rank];
+  g.hi = bd.b[g.rank + 1];
+  g.n = g.hi - g.lo;
+  // ---- locality relabelling: node ids sorted by descending in-degree inside
+  //      each owner range, so the hot push targets share L2 lines; ranges keep their extent
   if (reorder) {
     DevBuf kin, kout, vin;
-    DI_CK(cudaMalloc(&kin.p, (size_t)n * 4));
-    DI_CK(cudaMalloc(&kout.p, (size_t)n * 4));
+    DI_CK(cudaMalloc(&kin.p, (size_t)n * 8));
+    DI_CK(cudaMalloc(&kout.p, (size_t)n * 8));
     DI_CK(cudaMalloc(&vin.p, (size_t)n * 4));
     DevBuf sorted;
     DI_CK(cudaMalloc(&sorted.p, (size_t)n * 4));
     DI_CK(cudaMalloc(&g.old_of, (size_t)n * 4));
     DI_CK(cudaMalloc(&g.new_of, (size_t)n * 4));
-    k_perm_keys<<<grid_for(n, sms), 256, 0, st>>>(indeg, n, (uint32_t *)kin.p, (int32_t *)vin.p);
+    int wb = 0;
+    while ((1 << wb) < world) wb++;
+    k_perm_keys64<<<grid_for(n, sms), 256, 0, st>>>(indeg, n, bd, (uint64_t *)kin.p,
+                                                     (int32_t *)vin.p);
     size_t pb = 0;
-    DI_CK(cub::DeviceRadixSort::SortPairs(nullptr, pb, (uint32_t *)kin.p, (uint32_t *)kout.p,
-                                          (int32_t *)vin.p, (int32_t *)sorted.p, (int64_t)n, 0, 32,
-                                          st));
+    DI_CK(cub::DeviceRadixSort::SortPairs(nullptr, pb, (uint64_t *)kin.p, (uint64_t *)kout.p,
+                                          (int32_t *)vin.p, (int32_t *)sorted.p, (int64_t)n, 0,
+                                          32 + wb, st));
     DevBuf ptmp;
     DI_CK(cudaMalloc(&ptmp.p, pb));
-    DI_CK(cub::DeviceRadixSort::SortPairs(ptmp.p, pb, (uint32_t *)kin.p, (uint32_t *)kout.p,
-                                          (int32_t *)vin.p, (int32_t *)sorted.p, (int64_t)n, 0, 32,
-                                          st));
-    const int64_t P = std::max<int64_t>(1, std::min<int64_t>(g.stripes, n));
-    k_place<<<grid_for(n, sms), 256, 0, st>>>((const int32_t *)sorted.p, n, P, g.new_of, g.old_of);
+    DI_CK(cub::DeviceRadixSort::SortPairs(ptmp.p, pb, (uint64_t *)kin.p, (uint64_t *)kout.p,
+                                          (int32_t *)vin.p, (int32_t *)sorted.p, (int64_t)n, 0,
+                                          32 + wb, st));
+    const int64_t P = std::max<int64_t>(1, (int64_t)g.stripes);
+    k_place<<<grid_for(n, sms), 256, 0, st>>>((const int32_t *)sorted.p, n, bd, P, g.new_of,
+                                               g.old_of);
     g.reordered = true;
   }
   if (L > 0) k_make_keys<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, b, g.new_of, ka);
@@ -254,25 +331,37 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     DI_CK(cudaStreamSynchronize(st));
     std::swap(ka, kb);  // kb = compacted sorted keys
   }
-  g.l = Lk;
   g.l_global = Lk;
-  const size_t LkS = (size_t)(Lk > 0 ? Lk : 1);
-  DI_CK(cudaMalloc(&g.row_ptr, ((size_t)n + 1) * 8));
+  // ---- this rank's rows: the contiguous key range of majors in [lo, hi)
+  int64_t kbeg = 0, kend = Lk;
+  if (world > 1 && Lk > 0) {
+    int64_t hb[2];
+    k_key_bound<<<1, 32, 0, st>>>(kb, Lk, b, g.lo, g.hi, (int64_t *)badb.p);
+    DI_CK(cudaMemcpyAsync(hb, badb.p, 16, cudaMemcpyDeviceToHost, st));
+    DI_CK(cudaStreamSynchronize(st));
+    kbeg = hb[0];
+    kend = hb[1];
+  }
+  const int64_t Ll = kend - kbeg;
+  const int64_t nl = g.n;
+  g.l = Ll;
+  const size_t LlS = (size_t)(Ll > 0 ? Ll : 1);
+  DI_CK(cudaMalloc(&g.row_ptr, ((size_t)nl + 1) * 8));
   // +8 elements of padding: the push reads whole aligned int4 groups around each row
-  DI_CK(cudaMalloc(&g.col, (LkS + 8) * 4));
-  DI_CK(cudaMemsetAsync(g.col + LkS, 0, 8 * 4, st));
-  DI_CK(cudaMalloc(&g.deg, (size_t)n * 4));
-  DI_CK(cudaMalloc(&g.kloop, (size_t)n * 4));
-  DI_CK(cudaMemsetAsync(g.kloop, 0, (size_t)n * 4, st));
-  k_csr_from_sorted<<<grid_for(Lk + 1, sms), 256, 0, st>>>(kb, Lk, n, b, g.row_ptr, g.col,
-                                                          g.kloop);
+  DI_CK(cudaMalloc(&g.col, (LlS + 8) * 4));
+  DI_CK(cudaMemsetAsync(g.col + LlS, 0, 8 * 4, st));
+  DI_CK(cudaMalloc(&g.deg, (size_t)nl * 4));
+  DI_CK(cudaMalloc(&g.kloop, (size_t)nl * 4));
+  DI_CK(cudaMemsetAsync(g.kloop, 0, (size_t)nl * 4, st));
+  k_csr_from_sorted<<<grid_for(Ll + 1, sms), 256, 0, st>>>(kb + kbeg, Ll, nl, b, g.lo, g.row_ptr,
+                                                          g.col, g.kloop);
   int *any_loop = (int *)badb.p;  // reuse 8 bytes
   DI_CK(cudaMemsetAsync(any_loop, 0, 4, st));
-  k_deg<<<grid_for(n, sms), 256, 0, st>>>(g.row_ptr, n, g.deg, g.kloop, any_loop);
+  k_deg<<<grid_for(nl, sms), 256, 0, st>>>(g.row_ptr, nl, g.deg, g.kloop, any_loop);
   int hl = 0;
   DI_CK(cudaMemcpyAsync(&hl, any_loop, 4, cudaMemcpyDeviceToHost, st));
 
-  if (flags & DI_BUILD_CSC) {
+  if (flags & DI_BUILD_CSC) {  // single GPU only (checked by the caller)
     if (Lk > 0) {
       k_swap_keys<<<grid_for(Lk, sms), 256, 0, st>>>(kb, Lk, b, ka);
       size_t sb = 0;
@@ -285,11 +374,12 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
       }
       DI_CK(cub::DeviceRadixSort::SortKeys(tmp.p, sb, ka, kb, (int64_t)Lk, 0, 2 * b, st));
     }
+    const size_t LkS = (size_t)(Lk > 0 ? Lk : 1);
     DI_CK(cudaMalloc(&g.csc_ptr, ((size_t)n + 1) * 8));
     DI_CK(cudaMalloc(&g.csc_row, (LkS + 8) * 4));
     DI_CK(cudaMemsetAsync(g.csc_row + LkS, 0, 8 * 4, st));
-    k_csr_from_sorted<<<grid_for(Lk + 1, sms), 256, 0, st>>>(kb, Lk, n, b, g.csc_ptr, g.csc_row,
-                                                            nullptr);
+    k_csr_from_sorted<<<grid_for(Lk + 1, sms), 256, 0, st>>>(kb, Lk, n, b, 0, g.csc_ptr,
+                                                            g.csc_row, nullptr);
     g.has_csc = true;
   }
   DI_CK(cudaStreamSynchronize(st));

@@ -1,0 +1,234 @@
+"""Partitioned D-iteration on emulated ranks: G host threads share one GPU
+through a LocalGroup (the collectives become host barriers + device copies; no kernel waits for
+another rank). Every kernel of the multi-GPU sweep runs: select on the owned range, the push
+that routes remote targets into R with first-touch lists, pack, the exchange, apply, and the
+finaliser on the allreduced sums. The NCCL backend differs only in how the bytes move."""
+import numpy as np
+import pytest
+
+import digen
+import oracle
+from conftest import load_pins
+from gpu_util import l1, need_gpu
+from oracle import definition as defn
+
+pytestmark = pytest.mark.gpu
+D = 0.85
+torch = pytest.importorskip("torch")
+
+
+def run(src, dst, n, G, solves, reorder=True, B=None, **kw):
+    """Build the partitioned graph on G emulated ranks and run `solves` (list of solve kwargs);
+    returns per solve: (assembled H, assembled F, stats of rank 0, all ranks' stats, ranges)."""
+    import paper_1204_6255_b200 as di
+    from paper_1204_6255_b200.dist import assemble, run_local_group
+
+    def fn(r, grp):
+        torch.cuda.set_device(0)
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            g = di.Graph(src, dst, n, rank=r, world=G, group=grp, stream=stream, reorder=reorder, **kw)
+            out = []
+            for sk in solves:
+                sk = dict(sk)
+                if B is not None:
+                    sk["B"] = B[g.lo:g.hi]
+                st = g.solve(**sk)
+                H = g.history().cpu().numpy()
+                l1f, F = g.residual(return_F=True)
+                out.append((H, F.cpu().numpy(), st, l1f))
+            rng = (g.lo, g.hi)
+            g.free()
+        return rng, out
+
+    res = run_local_group(G, fn)
+    ranges = [r for r, _ in res]
+    outs = []
+    for k in range(len(solves)):
+        H = assemble([o[k][0] for _, o in res], ranges, n)
+        F = assemble([o[k][1] for _, o in res], ranges, n)
+        sts = [o[k][2] for _, o in res]
+        l1s = [o[k][3] for _, o in res]
+        assert len(set(l1s)) == 1            # di_residual is collective: same value everywhere
+        outs.append((H, F, sts[0], sts, ranges))
+    return outs
+
+
+def same_stats(sts):
+    keys = ("sweeps", "selected_total", "link_diffusions", "starvation_fallbacks", "residual_l1",
+            "dangling_absorbed", "converged")
+    for k in keys:
+        assert len({s[k] for s in sts}) == 1, (k, [s[k] for s in sts])
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_pins_partitioned(G):
+    """T1 on partitions: the exact rationals of tests/golden/pins.txt (graphs with >= G nodes)."""
+    need_gpu()
+    for name, n, links, X in load_pins():
+        if n < G:
+            continue
+        src = np.array([s for s, _ in links], dtype=np.int32)
+        dst = np.array([t for _, t in links], dtype=np.int32)
+        for variant in ("sop", "cyc"):
+            H, F, st, sts, _ = run(src, dst, n, G, [dict(d=D, tol=1e-16, variant=variant)])[0]
+            same_stats(sts)
+            assert st["converged"] == 1, (name, st)
+            assert l1(H, [float(x) for x in X]) <= 1e-14, (name, variant, H)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_random_vs_dense_partitioned(G):
+    """T2 on partitions: random graphs with self-loops, duplicates, dangling nodes."""
+    need_gpu()
+    for seed in range(25):
+        src, dst, n = digen.small_random(seed)
+        if n < G:
+            continue
+        X = defn.solve_dense(src, dst, n, D)
+        for H, F, st, sts, ranges in run(src, dst, n, G, [dict(d=D, tol=1e-15, variant="sop"),
+                                                           dict(d=D, tol=1e-15, variant="cyc")]):
+            same_stats(sts)
+            assert st["converged"] == 1
+            assert l1(H, X) <= 1e-13, (seed, G)
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+@pytest.mark.parametrize("variant", ["sop", "cyc"])
+def test_north_star_parity_partitioned(G, variant):
+    """T11 / T10 on partitions: C1 at tol 1e-10 vs the oracle (1e-9, and the G19 bound against
+    the tight 1e-13 oracle run); the partition and the exchange counters are sane."""
+    need_gpu()
+    src, dst, n = digen.make("c1", seed=1)
+    (H, F, st, sts, ranges), = run(src, dst, n, G, [dict(d=D, tol=1e-10, variant=variant)])
+    same_stats(sts)
+    assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
+    Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant=variant)
+    assert l1(H, Ho) <= 1e-9
+    Ht, _, _ = oracle.di(src, dst, n, d=D, tol=1e-13, variant=variant)
+    assert l1(H, Ht) <= 1e-10 / (1 - D) + 1e-13 / (1 - D)
+    # partition: contiguous, non-empty, balanced on 20 B/link + 12 B/node
+    out = np.bincount(src, minlength=n).astype(np.int64)
+    w = 20 * out + 12
+    W = w.sum()
+    for lo, hi in ranges:
+        assert hi > lo
+        assert w[lo:hi].sum() <= W / G + w.max() + 12
+    # the exchange moved something, and never more than one entry per (remote node, sweep)
+    assert all(s["exchange_entries"] > 0 for s in sts)
+    for s, (lo, hi) in zip(sts, ranges):
+        assert s["exchange_entries"] <= (n - (hi - lo)) * s["sweeps"]
+        assert s["exchange_bytes"] == 12 * s["exchange_entries"]
+
+
+def test_cyc_neumann_partitioned():
+    """T7 on partitions: bulk DI-CYC without loops is the Neumann series, F_n = P^n B and
+    H_n = sum_{k<n} P^k B, whatever the partition (the exchange only moves where fluid is added)."""
+    need_gpu()
+    src, dst, n = digen.make("c1")
+    P = defn.sparse_P(src, dst, n, D)
+    B = defn.uniform_B(n, D)
+    solves = [dict(d=D, tol=1e-300, variant="cyc", max_sweeps=k) for k in range(1, 9)]
+    res = run(src, dst, n, 3, solves)
+    Fn, Hn = B.copy(), np.zeros(n)
+    for k, (H, F, st, sts, _) in enumerate(res, start=1):
+        Hn = Hn + Fn
+        Fn = P @ Fn
+        assert st["sweeps"] == k
+        nz = Fn > 0
+        assert np.array_equal(F > 0, nz)
+        assert np.max(np.abs(F[nz] - Fn[nz]) / Fn[nz]) <= 1e-13
+        assert np.max(np.abs(H - Hn) / np.maximum(Hn, 1e-300)) <= 1e-13
+
+
+def test_invariants_and_matches_single_gpu():
+    """T8 mid-solve on partitions (F = B + P.H - H, conservation) and T11's 'same sweep count
+    within 1' against the single-GPU solve, on C1 and a host-block graph; custom B; resume."""
+    need_gpu()
+    from gpu_util import upload
+    src, dst, n = digen.make("c1", seed=2)
+    P = defn.sparse_P(src, dst, n, D)
+    B = defn.uniform_B(n, D)
+    outd = np.bincount(src, minlength=n)
+    for H, F, st, sts, _ in run(src, dst, n, 4, [dict(d=D, tol=1e-300, variant="sop", max_sweeps=k)
+                                                 for k in (1, 4, 9)]):
+        assert np.all(F >= 0)
+        assert np.abs(F - (B + P @ H - H)).max() <= 1e-15
+        cons = F.sum() + (1 - D) * H[outd > 0].sum() + H[outd == 0].sum()
+        assert abs(cons - (1 - D)) <= 1e-14
+    g = upload(src, dst, n)
+    st1 = g.solve(d=D, tol=1e-10, variant="sop")
+    H1 = g.history().cpu().numpy()
+    g.free()
+    H, F, st, sts, _ = run(src, dst, n, 4, [dict(d=D, tol=1e-10, variant="sop")])[0]
+    assert abs(st["sweeps"] - st1["sweeps"]) <= 1
+    assert l1(H, H1) <= 2e-10 / (1 - D)
+    # custom B (each rank passes its slice in the caller's numbering) + resume
+    rng = np.random.default_rng(3)
+    Bc = rng.random(n) * (1 - D) / n * 2
+    X = defn.solve_sparse(src, dst, n, D, B=Bc)
+    res = run(src, dst, n, 3, [dict(d=D, tol=1e-12, variant="sop", max_sweeps=6),
+                               dict(d=D, tol=1e-12, variant="sop", resume=True)], B=Bc)
+    assert res[0][2]["converged"] == 0 and res[0][2]["sweeps"] == 6
+    assert res[1][2]["converged"] == 1
+    assert l1(res[1][0], X) <= 1e-12 / (1 - D)
+
+
+def test_edge_cases_partitioned():
+    """n == G (one node per rank), no links at all, hubs above the chunk size, no relabelling,
+    self-loops kept, dedup; and C2 (10^6 nodes) at G = 2 vs the oracle."""
+    need_gpu()
+    # one node per rank: 0 -> 1 -> 2 -> 3 -> 0 ring plus a self-loop
+    src = np.array([0, 1, 2, 3, 2], np.int32)
+    dst = np.array([1, 2, 3, 0, 2], np.int32)
+    X = defn.solve_dense(src, dst, 4, D)
+    H, *_ = run(src, dst, 4, 4, [dict(d=D, tol=1e-15)])[0]
+    assert l1(H, X) <= 1e-14
+    # no links: every node dangling, X = (1-d)/N
+    H, F, st, _, _ = run(np.zeros(0, np.int32), np.zeros(0, np.int32), 1000, 3, [dict(d=D, tol=1e-12)])[0]
+    assert st["sweeps"] == 1 and np.allclose(H, (1 - D) / 1000, rtol=0, atol=1e-18)
+    # hubs (push bin C) crossing the partition, duplicates, no relabelling
+    n = 20000
+    rng = np.random.default_rng(7)
+    s = rng.integers(0, n, 4 * n).astype(np.int32)
+    t = rng.integers(0, n, 4 * n).astype(np.int32)
+    s = np.concatenate([s, np.zeros(15000, np.int32), s[:100]])
+    t = np.concatenate([t, np.arange(1, 15001, dtype=np.int32), t[:100]])
+    X = defn.solve_sparse(s, t, n, D)
+    for reorder in (True, False):
+        H, *_ = run(s, t, n, 3, [dict(d=D, tol=1e-13)], reorder=reorder)[0]
+        assert l1(H, X) <= 1e-13 / (1 - D) + 1e-14
+    Xd = defn.solve_sparse(*csr_dedup(s, t), n, D)
+    H, *_ = run(s, t, n, 2, [dict(d=D, tol=1e-13)], dedup=True)[0]
+    assert l1(H, Xd) <= 1e-13 / (1 - D) + 1e-14
+
+
+def csr_dedup(s, t):
+    k = np.unique(s.astype(np.int64) * (1 << 32) + t.astype(np.int64))
+    return (k >> 32).astype(np.int32), (k & 0xFFFFFFFF).astype(np.int32)
+
+
+@pytest.mark.slow
+def test_c2_partitioned_vs_oracle():
+    need_gpu()
+    src, dst, n = digen.make("c2", seed=1)
+    H, F, st, sts, _ = run(src, dst, n, 2, [dict(d=D, tol=1e-10, variant="sop")])[0]
+    same_stats(sts)
+    Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
+    assert st["converged"] == 1 and l1(H, Ho) <= 1e-9
+
+
+def test_invalid_partitioned_arguments():
+    need_gpu()
+    import paper_1204_6255_b200 as di
+    src, dst, n = digen.make("c1")
+
+    def bad_csc(r, grp):
+        di.Graph(src, dst, n, rank=r, world=2, group=grp, build_csc=True)
+
+    from paper_1204_6255_b200.dist import run_local_group
+    with pytest.raises(di.DIError):
+        run_local_group(2, bad_csc)
+    with pytest.raises(di.DIError):   # world larger than the group
+        grp = di.LocalGroup(2)
+        di.Graph(src, dst, n, rank=0, world=3, group=grp)

@@ -25,6 +25,19 @@ FLAGS = [
 ]
 
 
+def nccl_include():
+    """The header of the NCCL torch ships (the library libdi.so dlopens at run time)."""
+    try:
+        import nvidia.nccl
+        for base in nvidia.nccl.__path__:
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except Exception:
+        pass
+    return "/usr/include"
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -44,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return SO
     tmp = SO + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *sources()]
+    cmd = [NVCC, *FLAGS, "-I", nccl_include(), "-o", tmp, *sources(), "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
