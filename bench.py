@@ -128,8 +128,11 @@ def run_ours(args):
         from paper_1204_6255_b200.dist import nccl_rendezvous
         _, _, nid = nccl_rendezvous()
         args.mode = "push"                   # the partitioned sweep is push-only
+        args.blocks = 1                      # ... and bulk (block order is single-GPU)
     import paper_1204_6255_b200 as di
-    part = dict(rank=rank, world=world, nccl_id=nid) if world > 1 else dict(build_csc=True)
+    if args.mode != "push":
+        args.blocks = 1
+    part = dict(rank=rank, world=world, nccl_id=nid) if world > 1 else dict(build_csc=args.mode != "push")
 
     src, dst, n, gen_s = make_graph(args.config, args.seed)
     L = len(src)
@@ -153,7 +156,8 @@ def run_ours(args):
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        st = g.solve(d=D, tol=TOL, variant=args.variant, profile=profile, mode=args.mode)
+        st = g.solve(d=D, tol=TOL, variant=args.variant, profile=profile, mode=args.mode,
+                     blocks=args.blocks)
         ev1.record(stream)
         ev1.synchronize()
         assert st["converged"] == 1, st
@@ -191,7 +195,8 @@ def run_ours(args):
     achieved = push_bytes / (push_ms * 1e-3) / 1e9 if push_ms > 0 else 0.0
     tr = ncu_traffic()
     counted = sum(s["counted_bytes"] for s in stats) / world
-    roofline = {"bound": "hbm", "kernel": "k_push + k_pull (a5/a5': diffusion of the frontier's fluid)",
+    roofline = {"bound": "hbm", "kernel": ("k_push (a5: diffusion of the frontier's fluid)" if args.mode == "push"
+                                           else "k_push + k_pull (a5/a5': diffusion of the frontier's fluid)"),
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": tr,
                 "peak_source": peak_src,
@@ -213,7 +218,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         gh = di.Graph(src_p, dst_p, n, stream=stream, **part)  # DI_HOST_PTRS: H2D inside
-        st = gh.solve(d=D, tol=TOL, variant=args.variant, mode=args.mode)
+        st = gh.solve(d=D, tol=TOL, variant=args.variant, mode=args.mode, blocks=args.blocks)
         H = gh.history()
         H_host.copy_(H, non_blocking=True)
         torch.cuda.synchronize()
@@ -241,6 +246,7 @@ def run_ours(args):
         "config": {"workload": f"{args.config}: " + __import__("digen").CONFIGS[args.config].note,
                    "n": n, "links": L, "variant": "DI-" + args.variant.upper(), "d": D,
                    "tol_l1_fluid": TOL, "seed": args.seed, "sweep_mode": args.mode,
+                   "cycle_blocks": args.blocks,
                    "l2": "inputs > 126 MB L2 and 512 MiB L2 flush before each step",
                    "parallelism": f"1-D node range x{world}, NCCL (id, value) exchange" if world > 1
                    else "single GPU",
@@ -312,7 +318,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4")
     ap.add_argument("--variant", default="sop", choices=["sop", "cyc"])
-    ap.add_argument("--mode", default="auto", choices=["push", "pull", "auto"])
+    ap.add_argument("--mode", default="push", choices=["push", "pull", "auto"])
+    ap.add_argument("--blocks", type=int, default=8,
+                    help="block-ordered cycles: K ordered node blocks per cycle (1 = plain bulk sweeps)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)

@@ -70,6 +70,12 @@ typedef enum {
 #define DI_TRACE        0x10u  /* record the per-sweep log read by di_sweep_log                    */
 #define DI_PROFILE      0x20u  /* time every kernel with CUDA events (fills *_ms fields)           */
 #define DI_GRAPH_LOOP   0x40u  /* run the sweep loop as one CUDA graph with a device-side while    */
+/* Block-ordered cycles (F1): each cycle visits K ordered blocks of
+ * internal node ids; block b is selected against the cycle's threshold r (computed once per
+ * cycle) with the live F, i.e. including the fluid pushed by blocks 0..b-1 this
+ * cycle: the paper's cyclic order at block granularity. K in [2, 255]; push sweeps only;
+ * 0 or 1 = the plain bulk sweep. Single GPU. */
+#define DI_BLOCKS(K)    ((((uint32_t)(K)) & 0xFFu) << 16)
 
 typedef struct {
   int64_t sweeps;               /* bulk sweeps executed (incl. starvation fallbacks)            */

@@ -218,12 +218,14 @@ class Graph:
     # -------------------------------------------------------------- solve
     def solve(self, d=0.85, tol=1e-10, variant="sop", max_sweeps=100_000, B=None, resume=False,
               paper_error=False, trace=False, profile=False, mode="push", graph_loop=False,
-              raise_on_not_converged=False):
-        """di_solve. Returns the di_stats dict (status under key 'status')."""
+              blocks=1, raise_on_not_converged=False):
+        """di_solve. Returns the di_stats dict (status under key 'status').
+        blocks=K > 1: block-ordered cycles (K ordered node blocks per cycle, push only)."""
         torch = _torch()
         flags = (RESUME if resume else 0) | (PAPER_ERROR if paper_error else 0) | \
                 (TRACE if trace else 0) | (PROFILE if profile else 0) | \
-                (GRAPH_LOOP if graph_loop else 0) | {"push": PUSH, "pull": PULL, "auto": AUTO}[mode]
+                (GRAPH_LOOP if graph_loop else 0) | {"push": PUSH, "pull": PULL, "auto": AUTO}[mode] | \
+                ((int(blocks) & 0xFF) << 16)
         bp = None
         if B is not None:
             Bt = B if isinstance(B, torch.Tensor) else torch.as_tensor(np.asarray(B))

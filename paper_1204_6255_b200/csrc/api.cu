@@ -253,8 +253,8 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   if (g.world > 1) {
     if (v != DI_SOP && v != DI_CYC)
       return fail(DI_EINVAL, "di_solve: a partitioned graph runs DI_SOP / DI_CYC only");
-    if (flags & (DI_PULL | DI_AUTO | DI_GRAPH_LOOP))
-      return fail(DI_EINVAL, "di_solve: a partitioned graph runs push sweeps only");
+    if ((flags & (DI_PULL | DI_AUTO | DI_GRAPH_LOOP)) || ((flags >> 16) & 0xFFu) > 1)
+      return fail(DI_EINVAL, "di_solve: a partitioned graph runs plain push sweeps only");
     if ((flags & DI_RESUME) && !g.solved) return fail(DI_ESTATE, "di_solve: DI_RESUME before any solve");
     const double *Bint = B;
     if (B && g.reordered) {  // caller's slice [lo, hi) in the caller's numbering
@@ -269,6 +269,12 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   const int mode = (flags & DI_PULL) ? MODE_PULL : ((flags & DI_AUTO) ? MODE_AUTO : MODE_PUSH);
   if (mode != MODE_PUSH && !g.has_csc)
     return fail(DI_EINVAL, "di_solve: DI_PULL / DI_AUTO need the CSC (upload with DI_BUILD_CSC)");
+  // block-ordered cycles (F1): K sub-sweeps over ordered node blocks per cycle
+  int blocks = (int)((flags >> 16) & 0xFFu);
+  if (blocks < 1) blocks = 1;
+  if (blocks > 1 && mode != MODE_PUSH)
+    return fail(DI_EINVAL, "di_solve: block-ordered cycles (DI_BLOCKS) run push sweeps only");
+  blocks = (int)std::min<int64_t>(blocks, std::max<int64_t>(1, select_tiles(g.n)));
   const bool resume = flags & DI_RESUME;
   if (resume && !g.solved) return fail(DI_ESTATE, "di_solve: DI_RESUME before any solve");
   const int paper = (flags & DI_PAPER_ERROR) ? 1 : 0;
@@ -316,20 +322,23 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   bool converged = err_of(g.sc_host->r, g.sc_host->e) <= tol;
   double resid = g.sc_host->r;
   int64_t launched = 0;
-  int64_t K = 4;
+  int64_t batch = 4;
   double push_ms = 0.0, select_ms = 0.0;
   int64_t push_launches = 0;
   double r_prev = g.sc_host->r;
   while (!converged && launched < max_sweeps) {
-    const int64_t k = std::min<int64_t>(K, max_sweeps - launched);
+    const int64_t k = std::min<int64_t>(batch, max_sweeps - launched);
     const int64_t sweeps_before = g.sc_host->sweeps;
+    const int64_t ev_per = 2 * blocks + 1;
     for (int64_t j = 0; j < k; j++) {
-      if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 0), g.stream));
-      launch_select(g, 0, &launches);
-      if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 1), g.stream));
-      if (mode != MODE_PULL) launch_push(g, &launches);
-      if (mode != MODE_PUSH) launch_pull(g, &launches);
-      if (prof) DI_CK(cudaEventRecord(evs.get(4 * j + 2), g.stream));
+      for (int b = 0; b < blocks; b++) {
+        if (prof) DI_CK(cudaEventRecord(evs.get(ev_per * j + 2 * b), g.stream));
+        launch_select(g, 0, &launches, b, blocks);
+        if (prof) DI_CK(cudaEventRecord(evs.get(ev_per * j + 2 * b + 1), g.stream));
+        if (mode != MODE_PULL) launch_push(g, &launches, b, blocks);
+        if (mode != MODE_PUSH) launch_pull(g, &launches);
+      }
+      if (prof) DI_CK(cudaEventRecord(evs.get(ev_per * j + 2 * blocks), g.stream));
     }
     launched += k;
     s = sync_scalars(g);
@@ -338,12 +347,15 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     const int64_t real = g.sc_host->sweeps - sweeps_before;
     if (prof) {
       for (int64_t j = 0; j < real && j < k; j++) {
-        float a = 0.f, b = 0.f;
-        cudaEventElapsedTime(&a, evs.get(4 * j + 0), evs.get(4 * j + 1));
-        cudaEventElapsedTime(&b, evs.get(4 * j + 1), evs.get(4 * j + 2));
-        select_ms += a;
-        push_ms += b;
-        push_launches++;
+        for (int b = 0; b < blocks; b++) {
+          float a = 0.f, c = 0.f;
+          cudaEventElapsedTime(&a, evs.get(ev_per * j + 2 * b), evs.get(ev_per * j + 2 * b + 1));
+          cudaEventElapsedTime(&c, evs.get(ev_per * j + 2 * b + 1),
+                               evs.get(ev_per * j + 2 * b + 2));
+          select_ms += a;
+          push_ms += c;
+          push_launches++;
+        }
       }
     }
     if (g.sc_host->stop) {
@@ -371,7 +383,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
         next = (int64_t)std::ceil(std::max(1.0, left));
       }
     }
-    K = std::max<int64_t>(1, std::min<int64_t>(next, 32));
+    batch = std::max<int64_t>(1, std::min<int64_t>(next, blocks > 1 ? 8 : 32));
     r_prev = r_now;
   }
   if (!converged || launched == 0) {

@@ -28,6 +28,8 @@ constexpr int kChunk = 1024;
 constexpr int kPushThreads = 256;
 constexpr int kRedThreads = 512;
 constexpr int kLogCap = 1 << 16;  // per-sweep trace capacity
+constexpr int kMaxSlices = 4096;   // finaliser slices (= push/pull grid size, <= this)
+constexpr int kMaxBlocks = 256;    // block-ordered sweeps: sub-sweeps per cycle
 
 enum BinId { BIN_T = 0, BIN_G = 1, BIN_W = 2, BIN_C = 3 };
 
@@ -80,6 +82,8 @@ struct __align__(256) Scalars {
   int64_t sweep_sel, sweep_links, sweep_sel_nd;
   int64_t sweeps, selected_total, selected_nd_total, links_total, scanned_total, guards,
       pull_sweeps;
+  double r_run;              // block-ordered sweeps: running sum F inside a cycle
+  int64_t sel_cyc, links_cyc;
 };
 
 // One push work item: a row (or a kChunk-link chunk of a hub row) of a selected node.
@@ -142,7 +146,8 @@ struct Graph {
   double *aux = nullptr;     // comparators: x_new
   Scalars *sc = nullptr;     // device
   Scalars *sc_host = nullptr;  // pinned mirror
-  double *partials = nullptr;  // per-tile q, s, e partials (3 per tile)
+  double *partials = nullptr;  // per-tile q, s, e, taken partials (4 per tile)
+  double *ppartials = nullptr; // per-slice reductions of the tile partials (finaliser level 1)
   int64_t *ipartials = nullptr;  // per-tile selected, selected non-dangling, links
   int64_t ntiles = 0;
   double *red_partials = nullptr;
@@ -191,8 +196,8 @@ di_status alloc_state(Graph &g);
 void launch_init(Graph &g, const double *B, double d, int64_t *launches);
 void launch_reduce_F(Graph &g, int64_t *launches);
 void launch_reduce_F_setr(Graph &g, int64_t *launches);
-void launch_select(Graph &g, int test_mode, int64_t *launches);
-void launch_push(Graph &g, int64_t *launches);
+void launch_select(Graph &g, int test_mode, int64_t *launches, int blk = 0, int blocks = 1);
+void launch_push(Graph &g, int64_t *launches, int blk = 0, int blocks = 1);
 void launch_finalize(Graph &g, int64_t *launches);
 void launch_pull(Graph &g, int64_t *launches);
 di_status alloc_pull(Graph &g);

@@ -90,14 +90,14 @@ template <bool LOOPS>
 __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
   constexpr int NW = kSelThreads / 32;
   __shared__ int s_wcnt[NW][kBins];
-  __shared__ double s_red[NW][3];
+  __shared__ double s_red[NW][4];
   __shared__ int64_t s_links[NW];
   __shared__ int s_sel[NW], s_selnd[NW];
   __shared__ unsigned long long s_res[kBins];
 
   Scalars *sc = a.sc;
   if (!a.test_mode && sc->stop) return;
-  const int64_t tile = blockIdx.x;
+  const int64_t tile = a.t0 + blockIdx.x;   // block-ordered sweeps scan tiles [t0, t1)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double r = sc->r;
   const double d = sc->d;
@@ -156,13 +156,14 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
   // ---- pass 1: the selection test (P:258 / P:298) and the bin counts
   uint32_t selmask = 0, dangmask = 0;
   int cnt[kBins] = {0, 0, 0, 0};
-  double q = 0.0;
+  double q = 0.0, tk = 0.0;   // fluid left unselected / taken from F by the selection
 #pragma unroll
   for (int j = 0; j < kSelItems; j++) {
     const int64_t i = base + j;
     if (i >= a.n) continue;
     const double thr = cyc ? 0.0 : __dmul_rn(t, (double)o[j]);  // (r/L)*out[i]
     if (f[j] > thr) {                                             // strict '>'
+      tk = __dadd_rn(tk, f[j]);
       if (o[j] == 0) {
         dangmask |= 1u << j;
       } else {
@@ -320,6 +321,7 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
   q = warp_sum(q);
   s = warp_sum(s);
   e = warp_sum(e);
+  tk = warp_sum(tk);
   links = warp_sum(links);
   nsel = warp_sum(nsel);
   nsel_nd = warp_sum(nsel_nd);
@@ -327,13 +329,14 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
     s_red[warp][0] = q;
     s_red[warp][1] = s;
     s_red[warp][2] = e;
+    s_red[warp][3] = tk;
     s_links[warp] = links;
     s_sel[warp] = nsel;
     s_selnd[warp] = nsel_nd;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double tq = 0.0, ts = 0.0, te = 0.0;
+    double tq = 0.0, ts = 0.0, te = 0.0, tt = 0.0;
     int64_t tl = 0;
     int tsel = 0, tnd = 0;
 #pragma unroll
@@ -341,13 +344,13 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
       tq += s_red[w][0];
       ts += s_red[w][1];
       te += s_red[w][2];
+      tt += s_red[w][3];
       tl += s_links[w];
       tsel += s_sel[w];
       tnd += s_selnd[w];
     }
-    a.partials[tile * 3 + 0] = tq;
-    a.partials[tile * 3 + 1] = ts;
-    a.partials[tile * 3 + 2] = te;
+    reinterpret_cast<double2 *>(a.partials)[2 * tile] = make_double2(tq, ts);
+    reinterpret_cast<double2 *>(a.partials)[2 * tile + 1] = make_double2(te, tt);
     reinterpret_cast<longlong2 *>(a.ipartials)[2 * tile] = make_longlong2(tsel, tnd);
     if (mode == MODE_AUTO && tl) atomicAdd(&sc->fill_links[0], (unsigned long long)tl);
     reinterpret_cast<longlong2 *>(a.ipartials)[2 * tile + 1] = make_longlong2(tl, 0);
@@ -355,7 +358,10 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
 }
 
 __global__ void __launch_bounds__(kPushThreads) k_finalize(const SweepArgs a) {
-  finalize_sweep(a, kPushThreads);
+  slice_partials(a, 0, 1, kPushThreads);
+  __syncthreads();
+  __threadfence();
+  finalize_sweep(a, 1, kPushThreads);
 }
 
 // Static capacity of every bin (rows, or chunks for C) from the degrees, per select tile.
@@ -475,8 +481,10 @@ __global__ void __launch_bounds__(kPushThreads, MINB) k_push(const SweepArgs a) 
       if (nvec > 2) red_group<LOOPS>(F, x2, a0 + 8, beg, end, gi, en.v, fpol);
     }
   }
-  // ---- the last block to finish finalises the sweep (DI_AUTO: k_pull, launched next, does)
+  // ---- every block reduces its slice of the select partials; the last block to finish
+  //      finalises the sweep (DI_AUTO: k_pull, launched next, does)
   if (mode != MODE_PUSH) return;
+  slice_partials(a, blockIdx.x, gridDim.x, kPushThreads);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -485,7 +493,7 @@ __global__ void __launch_bounds__(kPushThreads, MINB) k_push(const SweepArgs a) 
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  finalize_sweep(a, kPushThreads);
+  finalize_sweep(a, gridDim.x, kPushThreads);
 }
 
 // ------------------------------------------------------------------ pull (a5')
@@ -588,7 +596,8 @@ __global__ void __launch_bounds__(kPushThreads) k_pull(const SweepArgs a) {
       }
     }
   }
-  // ---- the last block to finish finalises the sweep (pull and auto modes)
+  // ---- slices of the select partials; the last block finalises (pull and auto modes)
+  slice_partials(a, blockIdx.x, gridDim.x, kPushThreads);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -597,7 +606,7 @@ __global__ void __launch_bounds__(kPushThreads) k_pull(const SweepArgs a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  finalize_sweep(a, kPushThreads);
+  finalize_sweep(a, gridDim.x, kPushThreads);
 }
 
 template <bool LOOPS, int MINB>
@@ -625,8 +634,9 @@ di_status alloc_state(Graph &g) {
   DI_CK(cudaMemset(g.sc, 0, sizeof(Scalars)));
   DI_CK(cudaMallocHost(&g.sc_host, sizeof(Scalars)));
   memset(g.sc_host, 0, sizeof(Scalars));
-  DI_CK(cudaMalloc(&g.partials, (size_t)nt * 3 * 8));
+  DI_CK(cudaMalloc(&g.partials, (size_t)nt * 4 * 8));
   DI_CK(cudaMalloc(&g.ipartials, (size_t)nt * 4 * 8));
+  DI_CK(cudaMalloc(&g.ppartials, (size_t)kMaxSlices * 8 * 8));
   const int rg = reduce_grid(n, g.num_sms);
   DI_CK(cudaMalloc(&g.red_partials, (size_t)rg * 8));
   // frontier: per-bin capacity = rows (chunks for C) whose static degree falls in the bin
@@ -673,17 +683,18 @@ void launch_reduce_F_setr(Graph &g, int64_t *launches) {
   *launches += 1;
 }
 
-void launch_select(Graph &g, int test_mode, int64_t *launches) {
-  const SweepArgs a = sweep_args(g, test_mode);
+void launch_select(Graph &g, int test_mode, int64_t *launches, int blk, int blocks) {
+  const SweepArgs a = sweep_args(g, test_mode, blk, blocks);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, a.t1 - a.t0);
   if (g.has_loops)
-    k_select<true><<<(unsigned)a.ntiles, kSelThreads, 0, g.stream>>>(a);
+    k_select<true><<<grid, kSelThreads, 0, g.stream>>>(a);
   else
-    k_select<false><<<(unsigned)a.ntiles, kSelThreads, 0, g.stream>>>(a);
+    k_select<false><<<grid, kSelThreads, 0, g.stream>>>(a);
   *launches += 1;
 }
 
-void launch_push(Graph &g, int64_t *launches) {
-  const SweepArgs a = sweep_args(g, 0);
+void launch_push(Graph &g, int64_t *launches, int blk, int blocks) {
+  const SweepArgs a = sweep_args(g, 0, blk, blocks);
   if (g.has_loops)
     launch_push_t<true, 4>(g, a);
   else if (g.push_occ >= 6)

@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(kPushThreads) k_push_dist(const SweepArgs a, c
     dist_group<LOOPS>(a, x, q1, a0 + 4, beg, end, gi, en.v, vpos && nvec > 1, fpol);
     dist_group<LOOPS>(a, x, q2, a0 + 8, beg, end, gi, en.v, vpos && nvec > 2, fpol);
   }
-  // last block: this rank's sweep sums and per-peer counts
+  // slices of the select partials; the last block: this rank's sweep sums and per-peer counts
+  slice_partials(a, blockIdx.x, gridDim.x, kPushThreads);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kPushThreads) k_push_dist(const SweepArgs a, c
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const SweepSums s = reduce_partials(a, kPushThreads);
+  const SweepSums s = reduce_partials(a, gridDim.x, kPushThreads);
   if (threadIdx.x == 0) {
     x.dsum[0] = s.q;
     x.dsum[1] = s.s;
@@ -231,7 +232,7 @@ __global__ void k_apply_recv(double *__restrict__ F, int64_t lo, const int32_t *
 // the single-GPU finaliser on the allreduced sums
 __global__ void k_dist_finalize(const SweepArgs a, const double *dsum, const int64_t *isum) {
   if (threadIdx.x != 0 || a.sc->stop) return;
-  SweepSums s{dsum[0], dsum[1], dsum[2], isum[0], isum[1], isum[2], isum[3]};
+  SweepSums s{dsum[0], dsum[1], dsum[2], 0.0, isum[0], isum[1], isum[2], isum[3]};
   apply_sweep(a, s);
 }
 

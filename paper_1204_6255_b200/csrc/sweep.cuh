@@ -17,7 +17,7 @@ struct SweepArgs {
   double L_total;       // global link count (threshold r/L)
   Scalars *sc;
   Frontier fr;
-  double *partials;     // 3 per select tile
+  double *partials;     // 4 per select tile: q, s, e, taken
   int64_t *ipartials;   // 4 per select tile
   double *log_r;
   int64_t *log_sel, *log_links;
@@ -28,29 +28,40 @@ struct SweepArgs {
   const int32_t *csc_row;
   PullEntry *pe[kPullBins];
   int64_t pe_count[kPullBins];
+  // block-ordered sweeps (F1): this launch scans select tiles [t0, t1), sub-sweep blk
+  // of `blocks` per cycle (blocks = 1: the plain bulk sweep over every tile)
+  int64_t t0, t1;
+  int blk, blocks;
+  double *ppartials;    // 8 per finaliser slice: q, s, e, taken, sel, nd, links, 0
 };
 
 // What one sweep moved: r_{n+1} = q + s (a2), dangling absorption e, counters.
 struct SweepSums {
-  double q, s, e;
+  double q, s, e, taken;
   int64_t sel, nd, lk, scanned;
 };
 
-// Fixed-order reduction of the per-tile partials written by k_select. Called by one whole
-// block after every select tile has finished; the result is valid in thread 0.
-__device__ __forceinline__ SweepSums reduce_partials(const SweepArgs &a, int nthreads) {
-  __shared__ double s_fin[32][3];
-  __shared__ long long s_ifin[32][3];
+// Two-level fixed-order reduction of the per-tile partials written by k_select (a2).
+// Level 1: slice p of P (every block of the push/pull grid reduces a fixed contiguous slice of
+// the tiles [t0, t1) into ppartials[p]). Level 2 (reduce_partials): the last block reduces the
+// P slice results. Both orders are fixed, so the sums are reproducible for a given grid.
+__device__ __forceinline__ void slice_partials(const SweepArgs &a, int p, int P, int nthreads) {
+  __shared__ double s_sl[32][4];
+  __shared__ long long s_isl[32][3];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double aq = 0.0, as = 0.0, ae = 0.0;
+  const int64_t nt = a.t1 - a.t0;
+  const int64_t b0 = a.t0 + nt * p / P, b1 = a.t0 + nt * (p + 1) / P;
+  double aq = 0.0, as = 0.0, ae = 0.0, at = 0.0;
   long long c_sel = 0, c_nd = 0, c_lk = 0;
-#pragma unroll 4
-  for (int64_t tt = threadIdx.x; tt < a.ntiles; tt += nthreads) {
-    aq += __ldcg(a.partials + tt * 3 + 0);
-    as += __ldcg(a.partials + tt * 3 + 1);
-    ae += __ldcg(a.partials + tt * 3 + 2);
+  for (int64_t tt = b0 + threadIdx.x; tt < b1; tt += nthreads) {
+    const double2 x01 = __ldcg(reinterpret_cast<const double2 *>(a.partials) + 2 * tt);
+    const double2 x23 = __ldcg(reinterpret_cast<const double2 *>(a.partials) + 2 * tt + 1);
     const longlong2 c01 = __ldcg(reinterpret_cast<const longlong2 *>(a.ipartials) + 2 * tt);
     const longlong2 c23 = __ldcg(reinterpret_cast<const longlong2 *>(a.ipartials) + 2 * tt + 1);
+    aq += x01.x;
+    as += x01.y;
+    ae += x23.x;
+    at += x23.y;
     c_sel += c01.x;
     c_nd += c01.y;
     c_lk += c23.x;
@@ -58,6 +69,61 @@ __device__ __forceinline__ SweepSums reduce_partials(const SweepArgs &a, int nth
   aq = warp_sum(aq);
   as = warp_sum(as);
   ae = warp_sum(ae);
+  at = warp_sum(at);
+  c_sel = warp_sum(c_sel);
+  c_nd = warp_sum(c_nd);
+  c_lk = warp_sum(c_lk);
+  if (lane == 0) {
+    s_sl[warp][0] = aq;
+    s_sl[warp][1] = as;
+    s_sl[warp][2] = ae;
+    s_sl[warp][3] = at;
+    s_isl[warp][0] = c_sel;
+    s_isl[warp][1] = c_nd;
+    s_isl[warp][2] = c_lk;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r[4] = {0.0, 0.0, 0.0, 0.0};
+    long long c[3] = {0, 0, 0};
+    for (int w = 0; w < nthreads / 32; w++) {
+      for (int k = 0; k < 4; k++) r[k] += s_sl[w][k];
+      for (int k = 0; k < 3; k++) c[k] += s_isl[w][k];
+    }
+    double *o = a.ppartials + 8 * (int64_t)p;
+    reinterpret_cast<double2 *>(o)[0] = make_double2(r[0], r[1]);
+    reinterpret_cast<double2 *>(o)[1] = make_double2(r[2], r[3]);
+    reinterpret_cast<longlong2 *>(o)[2] = make_longlong2(c[0], c[1]);
+    reinterpret_cast<longlong2 *>(o)[3] = make_longlong2(c[2], 0);
+  }
+}
+
+// Level 2: reduce the P slice results (valid in thread 0). Called by one whole block after
+// every slice has been written.
+__device__ __forceinline__ SweepSums reduce_partials(const SweepArgs &a, int P, int nthreads) {
+  __shared__ double s_fin[32][4];
+  __shared__ long long s_ifin[32][3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double aq = 0.0, as = 0.0, ae = 0.0, at = 0.0;
+  long long c_sel = 0, c_nd = 0, c_lk = 0;
+  for (int p = threadIdx.x; p < P; p += nthreads) {
+    const double *o = a.ppartials + 8 * (int64_t)p;
+    const double2 x01 = __ldcg(reinterpret_cast<const double2 *>(o));
+    const double2 x23 = __ldcg(reinterpret_cast<const double2 *>(o) + 1);
+    const longlong2 c01 = __ldcg(reinterpret_cast<const longlong2 *>(o) + 2);
+    const longlong2 c23 = __ldcg(reinterpret_cast<const longlong2 *>(o) + 3);
+    aq += x01.x;
+    as += x01.y;
+    ae += x23.x;
+    at += x23.y;
+    c_sel += c01.x;
+    c_nd += c01.y;
+    c_lk += c23.x;
+  }
+  aq = warp_sum(aq);
+  as = warp_sum(as);
+  ae = warp_sum(ae);
+  at = warp_sum(at);
   c_sel = warp_sum(c_sel);
   c_nd = warp_sum(c_nd);
   c_lk = warp_sum(c_lk);
@@ -65,17 +131,20 @@ __device__ __forceinline__ SweepSums reduce_partials(const SweepArgs &a, int nth
     s_fin[warp][0] = aq;
     s_fin[warp][1] = as;
     s_fin[warp][2] = ae;
+    s_fin[warp][3] = at;
     s_ifin[warp][0] = c_sel;
     s_ifin[warp][1] = c_nd;
     s_ifin[warp][2] = c_lk;
   }
   __syncthreads();
-  SweepSums r{0.0, 0.0, 0.0, 0, 0, 0, a.n};
+  const int64_t n0 = a.t0 * kSelTile, n1 = a.t1 * kSelTile < a.n ? a.t1 * kSelTile : a.n;
+  SweepSums r{0.0, 0.0, 0.0, 0.0, 0, 0, 0, n1 - n0};
   if (threadIdx.x == 0) {
     for (int w = 0; w < nthreads / 32; w++) {
       r.q += s_fin[w][0];
       r.s += s_fin[w][1];
       r.e += s_fin[w][2];
+      r.taken += s_fin[w][3];
       r.sel += s_ifin[w][0];
       r.nd += s_ifin[w][1];
       r.lk += s_ifin[w][2];
@@ -88,6 +157,49 @@ __device__ __forceinline__ SweepSums reduce_partials(const SweepArgs &a, int nth
 // P:278-283), the starvation guard (reading G5), counters, the trace, bin counts.
 __device__ __forceinline__ void apply_sweep(const SweepArgs &a, const SweepSums &x) {
   volatile Scalars *vs = a.sc;
+  if (a.blocks > 1) {  // sub-sweep blk of a block-ordered cycle (F1)
+    const bool first = a.blk == 0, last = a.blk == a.blocks - 1;
+    const double d = vs->d;
+    const int variant = vs->variant;
+    // running sum F: r (cycle start) - fluid taken from F + fluid pushed (every sub-sweep)
+    const double r_run = __dadd_rn(__dsub_rn(first ? vs->r : vs->r_run, x.taken), x.s);
+    const double e_tot = vs->e + x.e;
+    const int64_t sel_c = (first ? 0 : vs->sel_cyc) + x.sel;
+    const int64_t lk_c = (first ? 0 : vs->links_cyc) + x.lk;
+    vs->r_run = r_run;
+    vs->sel_cyc = sel_c;
+    vs->links_cyc = lk_c;
+    vs->e = e_tot;
+    vs->q = x.q;
+    vs->s = x.s;
+    vs->e_sw = x.e;
+    vs->selected_total = vs->selected_total + x.sel;
+    vs->selected_nd_total = vs->selected_nd_total + x.nd;
+    vs->links_total = vs->links_total + x.lk;
+    vs->scanned_total = vs->scanned_total + x.scanned;
+    const double err = vs->paper_err ? r_run / (1.0 - d - d * e_tot) : r_run;
+    const int stop = err <= vs->tol;  // checked after every sub-sweep (r_run is sum F)
+    vs->stop = stop;
+    if (last || stop) {
+      const int64_t sw = vs->sweeps;
+      if (vs->trace && sw < kLogCap) {
+        a.log_r[sw] = vs->r;
+        a.log_sel[sw] = sel_c;
+        a.log_links[sw] = lk_c;
+        a.log_mode[sw] = 0;
+      }
+      if (vs->guard && variant != DI_CYC) vs->guards = vs->guards + 1;
+      vs->sweeps = sw + 1;
+      vs->r = r_run;  // threshold fluid of the next cycle (once per cycle)
+      vs->guard = (sel_c == 0 && !stop && variant == DI_SOP) ? 1 : 0;
+    }
+    for (int b = 0; b < kBins; b++) {
+      vs->bin_count[b] = (int64_t)vs->bin_fill[b][0];
+      vs->bin_fill[b][0] = 0;
+    }
+    vs->ticket = 0;
+    return;
+  }
   const int64_t sw = vs->sweeps;
   const double d = vs->d, r = vs->r;
   const int variant = vs->variant;
@@ -126,8 +238,8 @@ __device__ __forceinline__ void apply_sweep(const SweepArgs &a, const SweepSums 
   vs->ticket = 0;
 }
 
-__device__ __forceinline__ void finalize_sweep(const SweepArgs &a, int nthreads) {
-  const SweepSums x = reduce_partials(a, nthreads);
+__device__ __forceinline__ void finalize_sweep(const SweepArgs &a, int P, int nthreads) {
+  const SweepSums x = reduce_partials(a, P, nthreads);
   if (threadIdx.x == 0) apply_sweep(a, x);
 }
 
@@ -145,8 +257,15 @@ __device__ __forceinline__ void red_group(double *__restrict__ F, int4 x, int64_
   }
 }
 
-inline SweepArgs sweep_args(Graph &g, int test_mode) {
+// blk / blocks: sub-sweep blk of `blocks` block-ordered sub-sweeps (tile range [t0, t1))
+inline SweepArgs sweep_args(Graph &g, int test_mode, int blk = 0, int blocks = 1) {
   SweepArgs a;
+  const int64_t nt = select_tiles(g.n);
+  a.t0 = nt * blk / blocks;
+  a.t1 = nt * (blk + 1) / blocks;
+  a.blk = blk;
+  a.blocks = blocks;
+  a.ppartials = g.ppartials;
   a.F = g.F;
   a.H = g.H;
   a.deg = g.deg;
