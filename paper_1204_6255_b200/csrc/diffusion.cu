@@ -111,23 +111,26 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
   double f[kSelItems];
   int o[kSelItems];
   int kl[kSelItems];
+  int64_t rb[kSelItems];  // row extents row_ptr[i] (the push's first link); o_i = rb_{i+1} - rb_i
+  // One round trip: F and row_ptr stream in together (coalesced); #out_i comes from the row
+  // extent instead of a separate deg read, so no second dependent load is needed for the
+  // selected rows' first link.
   if (full) {
     const double2 *F2 = reinterpret_cast<const double2 *>(a.F + base);
+    const longlong2 *R2 = reinterpret_cast<const longlong2 *>(a.row_ptr + base);
+    int64_t rnext;
 #pragma unroll
     for (int j = 0; j < kSelItems / 2; j++) {
       const double2 x = F2[j];
       f[2 * j] = x.x;
       f[2 * j + 1] = x.y;
+      const longlong2 r = R2[j];
+      rb[2 * j] = r.x;
+      rb[2 * j + 1] = r.y;
     }
-    const int4 *D4 = reinterpret_cast<const int4 *>(a.deg + base);
+    rnext = a.row_ptr[base + kSelItems];
 #pragma unroll
-    for (int j = 0; j < kSelItems / 4; j++) {
-      const int4 x = D4[j];
-      o[4 * j] = x.x;
-      o[4 * j + 1] = x.y;
-      o[4 * j + 2] = x.z;
-      o[4 * j + 3] = x.w;
-    }
+    for (int j = 0; j < kSelItems; j++) o[j] = (int)((j + 1 < kSelItems ? rb[j + 1] : rnext) - rb[j]);
     if (LOOPS) {
       const int4 *K4 = reinterpret_cast<const int4 *>(a.kloop + base);
 #pragma unroll
@@ -144,7 +147,8 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
     for (int j = 0; j < kSelItems; j++) {
       const int64_t i = base + j;
       f[j] = (i < a.n) ? a.F[i] : 0.0;
-      o[j] = (i < a.n) ? a.deg[i] : 0;
+      rb[j] = (i < a.n) ? a.row_ptr[i] : 0;
+      o[j] = (i < a.n) ? (int)(a.row_ptr[i + 1] - rb[j]) : 0;
       if (LOOPS) kl[j] = (i < a.n) ? a.kloop[i] : 0;
     }
   }
@@ -177,52 +181,26 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
       q = __dadd_rn(q, f[j]);
     }
   }
-  // ---- pass 2a: move the fluid of selected nodes into H; independent of the bin
-  //      reservation, so its loads and fp64 divisions overlap the reservation latency
+  // ---- pass 2a: move the fluid of selected nodes into H. H_i += T is a RED: the
+  //      L2 adds in fp64 round-to-nearest exactly as a load/add/store would (H_i is touched by
+  //      this thread only), without a dependent load.
   const uint32_t anysel = selmask | dangmask;
   double v[kSelItems];
-  int64_t rb[kSelItems];
 #pragma unroll
   for (int j = 0; j < kSelItems; j++) v[j] = 0.0;
   double s = 0.0, e = 0.0;
   int64_t links = 0;
   int nsel = 0, nsel_nd = 0;
   if (anysel) {
-    double h[kSelItems];
-    if (full) {
-      const double2 *H2 = reinterpret_cast<const double2 *>(a.H + base);
-      const longlong2 *R2 = reinterpret_cast<const longlong2 *>(a.row_ptr + base);
-#pragma unroll
-      for (int j = 0; j < kSelItems / 2; j++) {
-        const double2 x = H2[j];
-        h[2 * j] = x.x;
-        h[2 * j + 1] = x.y;
-      }
-      if (selmask) {
-#pragma unroll
-        for (int j = 0; j < kSelItems / 2; j++) {
-          const longlong2 x = R2[j];
-          rb[2 * j] = x.x;
-          rb[2 * j + 1] = x.y;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < kSelItems; j++) {
-        h[j] = (anysel >> j & 1u) ? a.H[base + j] : 0.0;
-        rb[j] = (selmask >> j & 1u) ? a.row_ptr[base + j] : 0;
-      }
-    }
 #pragma unroll
     for (int j = 0; j < kSelItems; j++) {
-      v[j] = 0.0;
       if (!(anysel & (1u << j))) continue;
       const int64_t i = base + j;
       const double od = (double)o[j];
       double T = f[j];
       if (LOOPS && kl[j] > 0)                           // P:259-263 with k copies (G6)
         T = __ddiv_rn(__dmul_rn(f[j], od), __dsub_rn(od, __dmul_rn((double)kl[j], d)));
-      a.H[i] = __dadd_rn(h[j], T);
+      red_add_f64(a.H + i, T);
       a.F[i] = 0.0;
       nsel++;
       if (o[j] == 0) {
@@ -699,6 +677,10 @@ void launch_push(Graph &g, int64_t *launches, int blk, int blocks) {
     launch_push_t<true, 4>(g, a);
   else if (g.push_occ >= 6)
     launch_push_t<false, 6>(g, a);
+  else if (g.push_occ == 5)
+    launch_push_t<false, 5>(g, a);
+  else if (g.push_occ == 3)
+    launch_push_t<false, 3>(g, a);
   else
     launch_push_t<false, 4>(g, a);
   *launches += 1;
