@@ -8,7 +8,9 @@ import paper_1204_6255_b200 as di
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
 src, dst, n = digen.make(cfg)
 s_d, t_d = torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda()
-for occ, hint, stripes in [(4, 1, 4096), (3, 1, 4096), (5, 1, 4096), (6, 1, 4096), (4, 0, 4096), (4, 1, 1024), (4, 1, 16384), (4, 1, 65536)]:
+CASES = [(4, 1, 4096, 0), (4, 1, 4096, 1), (4, 1, 16384, 0), (4, 1, 16384, 1), (4, 1, 2048, 1), (4, 1, 8192, 1)]
+for occ, hint, stripes, rot in CASES:
+    os.environ["DI_STRIPE_ROT"] = str(rot)
     os.environ["DI_PUSH_OCC"] = str(occ)
     os.environ["DI_RED_HINT"] = str(hint)
     os.environ["DI_STRIPES"] = str(stripes)
@@ -18,6 +20,6 @@ for occ, hint, stripes in [(4, 1, 4096), (3, 1, 4096), (5, 1, 4096), (6, 1, 4096
         sts = [g.solve(d=0.85, tol=1e-10, blocks=K, profile=p) for p in (False, False, True)]
         st = min(sts[:2], key=lambda s: s["solve_ms"])
         pr = sts[2]
-        print(cfg, "occ", occ, "hint", hint, "stripes", stripes, "K", K, "ms", round(st["solve_ms"], 2),
+        print(cfg, "rot", rot, "occ", occ, "hint", hint, "stripes", stripes, "K", K, "ms", round(st["solve_ms"], 2),
               "eq", round(st["equivalent_iterations"], 2), "push_ms", round(pr["push_ms"], 1), "select_ms", round(pr["select_ms"], 1), flush=True)
     g.free()
