@@ -69,7 +69,10 @@ typedef enum {
 #define DI_PAPER_ERROR  0x8u   /* stop on sum(F)/(1-d-d*e) <= tol instead of sum(F)    */
 #define DI_TRACE        0x10u  /* record the per-sweep log read by di_sweep_log                    */
 #define DI_PROFILE      0x20u  /* time every kernel with CUDA events (fills *_ms fields)           */
-#define DI_GRAPH_LOOP   0x40u  /* run the sweep loop as one CUDA graph with a device-side while    */
+#define DI_GRAPH_LOOP   0x40u  /* run the sweep loop as one CUDA graph: a while node whose body is
+                                  one cycle + a condition kernel (!stop && sweeps < max_sweeps);
+                                  one host launch and one synchronisation per solve (ignored with
+                                  DI_PROFILE; single GPU)                                        */
 /* Block-ordered cycles (F1): each cycle visits K ordered blocks of
  * internal node ids; block b is selected against the cycle's threshold r (computed once per
  * cycle) with the live F, i.e. including the fluid pushed by blocks 0..b-1 this

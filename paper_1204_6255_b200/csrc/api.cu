@@ -80,6 +80,8 @@ void free_graph(Graph *g) {
     if (g->re[b]) cudaFree(g->re[b]);
   }
   if (g->cmp_partials) cudaFree(g->cmp_partials);
+  if (g->loop_exec) cudaGraphExecDestroy(g->loop_exec);
+  if (g->loop_graph) cudaGraphDestroy(g->loop_graph);
   if (g->sc_host) cudaFreeHost(g->sc_host);
   free_dist(*g);
   if (g->group) {
@@ -87,6 +89,69 @@ void free_graph(Graph *g) {
     g->group->handles--;
   }
   delete g;
+}
+
+// The sweep loop as one CUDA graph: a while node whose body is one cycle (blocks x (select,
+// push|pull)) followed by k_loop_cond, which keeps looping while !stop && sweeps < max_sweeps.
+// The host launches it once and synchronises once (plus the exact residual check).
+di_status loop_graph(Graph &g, int blocks, int mode) {
+  const int key = blocks * 4 + mode;
+  if (g.loop_exec && g.loop_key == key) return DI_OK;
+  if (g.loop_exec) cudaGraphExecDestroy(g.loop_exec);
+  if (g.loop_graph) cudaGraphDestroy(g.loop_graph);
+  g.loop_exec = nullptr;
+  g.loop_graph = nullptr;
+  cudaGraph_t gr;
+  DI_CK(cudaGraphCreate(&gr, 0));
+  cudaGraphConditionalHandle h;
+  DI_CK(cudaGraphConditionalHandleCreate(&h, gr, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  DI_CK(cudaGraphAddNode(&node, gr, nullptr, 0, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  // capture on a private stream (the handle's stream may be the legacy default stream, which
+  // cannot capture); the graph is launched on the handle's stream
+  cudaStream_t user = g.stream, cs = nullptr;
+  DI_CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  g.stream = cs;
+  cudaError_t be = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                                 cudaStreamCaptureModeThreadLocal);
+  if (be != cudaSuccess) {
+    g.stream = user;
+    cudaStreamDestroy(cs);
+    cudaGraphDestroy(gr);
+    return fail(DI_ECUDA, std::string("DI_GRAPH_LOOP capture: ") + cudaGetErrorString(be));
+  }
+  int64_t launches = 0;
+  for (int b = 0; b < blocks; b++) {
+    launch_select(g, 0, &launches, b, blocks);
+    if (mode != MODE_PULL) launch_push(g, &launches, b, blocks);
+    if (mode != MODE_PUSH) launch_pull(g, &launches);
+  }
+  launch_loop_cond(g, h);
+  launches++;
+  cudaGraph_t cap = body;
+  cudaError_t ce = cudaStreamEndCapture(cs, &cap);
+  g.stream = user;
+  cudaStreamDestroy(cs);
+  if (ce != cudaSuccess) {
+    cudaGraphDestroy(gr);
+    return fail(DI_ECUDA, std::string("DI_GRAPH_LOOP capture: ") + cudaGetErrorString(ce));
+  }
+  ce = cudaGraphInstantiate(&g.loop_exec, gr, 0);
+  if (ce != cudaSuccess) {
+    cudaGraphDestroy(gr);
+    g.loop_exec = nullptr;
+    return fail(DI_ECUDA, std::string("DI_GRAPH_LOOP instantiate: ") + cudaGetErrorString(ce));
+  }
+  g.loop_graph = gr;
+  g.loop_key = key;
+  g.loop_launches = launches;
+  return DI_OK;
 }
 
 di_status sync_scalars(Graph &g) {
@@ -302,6 +367,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     s.trace = trace;
     s.mode = mode;
     s.pull_thr = (int64_t)(g.auto_ratio * (double)g.l_global);
+    s.max_sweeps = max_sweeps;
   }
   DI_CK(cudaEventRecord(t0, g.stream));
   DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
@@ -326,10 +392,18 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   double push_ms = 0.0, select_ms = 0.0;
   int64_t push_launches = 0;
   double r_prev = g.sc_host->r;
+  const bool graph_loop = (flags & DI_GRAPH_LOOP) && !prof;
+  if (graph_loop) {
+    s = loop_graph(g, blocks, mode);
+    if (s != DI_OK) return s;
+  }
   while (!converged && launched < max_sweeps) {
-    const int64_t k = std::min<int64_t>(batch, max_sweeps - launched);
+    const int64_t k = graph_loop ? 0 : std::min<int64_t>(batch, max_sweeps - launched);
     const int64_t sweeps_before = g.sc_host->sweeps;
     const int64_t ev_per = 2 * blocks + 1;
+    if (graph_loop) {  // the whole remaining loop on the device, one launch
+      DI_CK(cudaGraphLaunch(g.loop_exec, g.stream));
+    }
     for (int64_t j = 0; j < k; j++) {
       for (int b = 0; b < blocks; b++) {
         if (prof) DI_CK(cudaEventRecord(evs.get(ev_per * j + 2 * b), g.stream));
@@ -345,6 +419,10 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     if (s != DI_OK) return s;
     DI_CK(cudaGetLastError());
     const int64_t real = g.sc_host->sweeps - sweeps_before;
+    if (graph_loop) {
+      launched = g.sc_host->sweeps;
+      launches += (real + 1) * g.loop_launches;
+    }
     if (prof) {
       for (int64_t j = 0; j < real && j < k; j++) {
         for (int b = 0; b < blocks; b++) {

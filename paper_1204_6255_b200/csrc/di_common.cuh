@@ -84,6 +84,7 @@ struct __align__(256) Scalars {
       pull_sweeps;
   double r_run;              // block-ordered sweeps: running sum F inside a cycle
   int64_t sel_cyc, links_cyc;
+  int64_t max_sweeps;        // DI_GRAPH_LOOP: the device-side loop stops at this many sweeps
 };
 
 // One push work item: a row (or a kChunk-link chunk of a hub row) of a selected node.
@@ -159,6 +160,12 @@ struct Graph {
   int64_t log_n = 0;
   bool solved = false;
   double last_d = 0.85;
+  // DI_GRAPH_LOOP: the sweep loop as a CUDA graph with a device-side while node (one cycle per
+  // iteration), instantiated once per (blocks, mode) and replayed
+  cudaGraphExec_t loop_exec = nullptr;
+  cudaGraph_t loop_graph = nullptr;
+  int loop_key = -1;
+  int64_t loop_launches = 0;   // kernels per loop iteration
   // multi-GPU (dist.cu): partition, communicator and the per-sweep exchange buffers
   DistBounds bounds{1, {0}};
   struct Comm *comm = nullptr;
@@ -200,6 +207,7 @@ void launch_select(Graph &g, int test_mode, int64_t *launches, int blk = 0, int 
 void launch_push(Graph &g, int64_t *launches, int blk = 0, int blocks = 1);
 void launch_finalize(Graph &g, int64_t *launches);
 void launch_pull(Graph &g, int64_t *launches);
+void launch_loop_cond(Graph &g, cudaGraphConditionalHandle h);
 di_status alloc_pull(Graph &g);
 di_status alloc_dist(Graph &g);
 // dist.cu

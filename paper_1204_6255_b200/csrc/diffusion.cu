@@ -725,6 +725,15 @@ di_status alloc_pull(Graph &g) {
   return DI_OK;
 }
 
+// DI_GRAPH_LOOP: condition of the device-side while node, evaluated after every cycle
+__global__ void k_loop_cond(const Scalars *sc, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, (sc->stop == 0 && sc->sweeps < sc->max_sweeps) ? 1u : 0u);
+}
+
+void launch_loop_cond(Graph &g, cudaGraphConditionalHandle h) {
+  k_loop_cond<<<1, 1, 0, g.stream>>>(g.sc, h);
+}
+
 void launch_finalize(Graph &g, int64_t *launches) {
   const SweepArgs a = sweep_args(g, 1);
   k_finalize<<<1, kPushThreads, 0, g.stream>>>(a);

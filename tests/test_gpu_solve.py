@@ -123,6 +123,38 @@ def test_block_ordered_north_star(name, seed, blocks):
     g.free()
 
 
+@pytest.mark.parametrize("blocks,mode", [(1, "push"), (1, "auto"), (8, "push")])
+def test_graph_loop(blocks, mode):
+    """DI_GRAPH_LOOP (the sweep loop as one CUDA graph with a device-side while node) gives the
+    same iterates as the host-driven loop: same sweeps and link diffusions, H within rounding of
+    the fp64 atomics; max_sweeps stops it exactly; pins and the north_star gate hold."""
+    need_gpu()
+    import paper_1204_6255_b200 as di
+    for name in ("c1", "c2"):
+        src, dst, n = digen.make(name, seed=1)
+        g = upload(src, dst, n, build_csc=True)
+        st0 = g.solve(d=D, tol=1e-10, blocks=blocks, mode=mode)
+        H0 = g.history().cpu().numpy()
+        st1 = g.solve(d=D, tol=1e-10, blocks=blocks, mode=mode, graph_loop=True)
+        H1 = g.history().cpu().numpy()
+        assert st1["converged"] == 1 and st1["residual_l1"] <= 1e-10
+        assert st1["sweeps"] == st0["sweeps"] and st1["link_diffusions"] == st0["link_diffusions"]
+        assert l1(H0, H1) <= 1e-13
+        Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
+        assert l1(H1, Ho) <= 1e-9
+        st2 = g.solve(d=D, tol=1e-10, blocks=blocks, mode=mode, graph_loop=True, max_sweeps=7)
+        assert st2["status"] == di.DI_NOT_CONVERGED and st2["sweeps"] == 7
+        g.free()
+    for pname, n, links, X in PINS:
+        src = np.array([s for s, _ in links], dtype=np.int32)
+        dst = np.array([t for _, t in links], dtype=np.int32)
+        g = upload(src, dst, n, build_csc=True)
+        st = g.solve(d=D, tol=1e-16, blocks=blocks, mode=mode, graph_loop=True)
+        assert st["converged"] == 1
+        assert l1(g.history().cpu().numpy(), [float(x) for x in X]) <= 1e-14, pname
+        g.free()
+
+
 @pytest.mark.parametrize("mode", MODES)
 def test_invariants_mid_solve(mode):
     """T8: at any stopping point F = B + P.H - H, F >= 0, conservation, sum F non-increasing."""
