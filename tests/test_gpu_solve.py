@@ -138,8 +138,11 @@ def test_graph_loop(blocks, mode):
         st1 = g.solve(d=D, tol=1e-10, blocks=blocks, mode=mode, graph_loop=True)
         H1 = g.history().cpu().numpy()
         assert st1["converged"] == 1 and st1["residual_l1"] <= 1e-10
-        assert st1["sweeps"] == st0["sweeps"] and st1["link_diffusions"] == st0["link_diffusions"]
-        assert l1(H0, H1) <= 1e-13
+        # fp64 atomics make the iterates order-nondeterministic in the last bits, which can flip a
+        # threshold test: same sweeps +-1 and link diffusions within 0.1 %
+        assert abs(st1["sweeps"] - st0["sweeps"]) <= 1
+        assert abs(st1["link_diffusions"] - st0["link_diffusions"]) <= 1e-3 * st0["link_diffusions"]
+        assert l1(H0, H1) <= 2e-10 / (1 - D)
         Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
         assert l1(H1, Ho) <= 1e-9
         st2 = g.solve(d=D, tol=1e-10, blocks=blocks, mode=mode, graph_loop=True, max_sweeps=7)
