@@ -73,6 +73,11 @@ typedef enum {
                                   one cycle + a condition kernel (!stop && sweeps < max_sweeps);
                                   one host launch and one synchronisation per solve (ignored with
                                   DI_PROFILE; single GPU)                                        */
+#define DI_ASYNC        0x100u /* asynchronous cycles: one persistent kernel per cycle takes tiles
+                                  of nodes in increasing order, selects against the cycle's r with
+                                  the live F (fluid taken by atomic exchange) and pushes at once:
+                                  the paper's cyclic order up to the concurrency of the
+                                  grid; push only, single GPU; iterates not bit-reproducible    */
 /* Block-ordered cycles (F1): each cycle visits K ordered blocks of
  * internal node ids; block b is selected against the cycle's threshold r (computed once per
  * cycle) with the live F, i.e. including the fluid pushed by blocks 0..b-1 this

@@ -32,6 +32,7 @@ DI_EINVAL, DI_ENOMEM, DI_ECUDA, DI_ENCCL, DI_ESTATE = -1, -2, -3, -4, -5
 VARIANTS = {"sop": 0, "cyc": 1, "pi": 2, "pi_pull": 2, "pi_push": 3, "pi_col": 3, "gs": 4, "gs_block": 4}
 DEDUP, DROP_SELF_LOOPS, BUILD_CSC, HOST_PTRS, LOCAL_LINKS, NO_REORDER = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 PUSH, PULL, AUTO, RESUME, PAPER_ERROR, TRACE, PROFILE, GRAPH_LOOP = 0x0, 0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
+ASYNC = 0x100
 
 
 class Stats(ctypes.Structure):
@@ -218,14 +219,14 @@ class Graph:
     # -------------------------------------------------------------- solve
     def solve(self, d=0.85, tol=1e-10, variant="sop", max_sweeps=100_000, B=None, resume=False,
               paper_error=False, trace=False, profile=False, mode="push", graph_loop=False,
-              blocks=1, raise_on_not_converged=False):
+              blocks=1, asynchronous=False, raise_on_not_converged=False):
         """di_solve. Returns the di_stats dict (status under key 'status').
         blocks=K > 1: block-ordered cycles (K ordered node blocks per cycle, push only)."""
         torch = _torch()
         flags = (RESUME if resume else 0) | (PAPER_ERROR if paper_error else 0) | \
                 (TRACE if trace else 0) | (PROFILE if profile else 0) | \
                 (GRAPH_LOOP if graph_loop else 0) | {"push": PUSH, "pull": PULL, "auto": AUTO}[mode] | \
-                ((int(blocks) & 0xFF) << 16)
+                ((int(blocks) & 0xFF) << 16) | (ASYNC if asynchronous else 0)
         bp = None
         if B is not None:
             Bt = B if isinstance(B, torch.Tensor) else torch.as_tensor(np.asarray(B))

@@ -94,8 +94,8 @@ void free_graph(Graph *g) {
 // The sweep loop as one CUDA graph: a while node whose body is one cycle (blocks x (select,
 // push|pull)) followed by k_loop_cond, which keeps looping while !stop && sweeps < max_sweeps.
 // The host launches it once and synchronises once (plus the exact residual check).
-di_status loop_graph(Graph &g, int blocks, int mode) {
-  const int key = blocks * 4 + mode;
+di_status loop_graph(Graph &g, int blocks, int mode, bool async) {
+  const int key = (blocks * 4 + mode) * 2 + (async ? 1 : 0);
   if (g.loop_exec && g.loop_key == key) return DI_OK;
   if (g.loop_exec) cudaGraphExecDestroy(g.loop_exec);
   if (g.loop_graph) cudaGraphDestroy(g.loop_graph);
@@ -128,6 +128,10 @@ di_status loop_graph(Graph &g, int blocks, int mode) {
   }
   int64_t launches = 0;
   for (int b = 0; b < blocks; b++) {
+    if (async) {
+      launch_cycle(g, &launches);
+      continue;
+    }
     launch_select(g, 0, &launches, b, blocks);
     if (mode != MODE_PULL) launch_push(g, &launches, b, blocks);
     if (mode != MODE_PUSH) launch_pull(g, &launches);
@@ -340,6 +344,9 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   if (blocks > 1 && mode != MODE_PUSH)
     return fail(DI_EINVAL, "di_solve: block-ordered cycles (DI_BLOCKS) run push sweeps only");
   blocks = (int)std::min<int64_t>(blocks, std::max<int64_t>(1, select_tiles(g.n)));
+  const bool async = flags & DI_ASYNC;
+  if (async && (mode != MODE_PUSH || blocks > 1))
+    return fail(DI_EINVAL, "di_solve: DI_ASYNC runs push cycles without DI_BLOCKS");
   const bool resume = flags & DI_RESUME;
   if (resume && !g.solved) return fail(DI_ESTATE, "di_solve: DI_RESUME before any solve");
   const int paper = (flags & DI_PAPER_ERROR) ? 1 : 0;
@@ -394,7 +401,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   double r_prev = g.sc_host->r;
   const bool graph_loop = (flags & DI_GRAPH_LOOP) && !prof;
   if (graph_loop) {
-    s = loop_graph(g, blocks, mode);
+    s = loop_graph(g, blocks, mode, async);
     if (s != DI_OK) return s;
   }
   while (!converged && launched < max_sweeps) {
@@ -407,6 +414,11 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     for (int64_t j = 0; j < k; j++) {
       for (int b = 0; b < blocks; b++) {
         if (prof) DI_CK(cudaEventRecord(evs.get(ev_per * j + 2 * b), g.stream));
+        if (async) {
+          if (prof) DI_CK(cudaEventRecord(evs.get(ev_per * j + 2 * b + 1), g.stream));
+          launch_cycle(g, &launches);
+          continue;
+        }
         launch_select(g, 0, &launches, b, blocks);
         if (prof) DI_CK(cudaEventRecord(evs.get(ev_per * j + 2 * b + 1), g.stream));
         if (mode != MODE_PULL) launch_push(g, &launches, b, blocks);

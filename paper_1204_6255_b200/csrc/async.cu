@@ -1,0 +1,287 @@
+// async.cu — asynchronous D-iteration cycles: one persistent kernel per cycle (DI_ASYNC).
+//
+// The paper's cycle visits the nodes in order and reads the LIVE fluid: fluid that
+// node i pushes to a later node j is diffused by j in the same cycle. Bulk sweeps (R1) lose that
+// (fluid waits for the next sweep); block-ordered cycles (R5) recover part of it at the price of
+// 2K kernel boundaries per cycle. Here one persistent grid runs the whole cycle:
+//   - CTAs take tiles of 1024 consecutive nodes in increasing order from a global counter;
+//   - a node is selected against the cycle's threshold t = r/L (r once per cycle) and
+//     its fluid is TAKEN with an atomic exchange F_i <- 0, so fluid that other CTAs push into
+//     F_i concurrently is never lost: it is either in the exchanged value or stays in F_i for
+//     the next visit (any diffusion order keeps F = B + P.H - H);
+//   - the CTA pushes the tile's rows immediately: rows of <= 32 links by the selecting thread,
+//     longer rows as 1024-link chunks claimed by the CTA's warps from a shared-memory list.
+// The order of diffusions is the dynamic order of the tiles, so iterates are not reproducible
+// bit for bit (like every fp64-atomic push); the fixed point and the tolerance are those of the
+// paper's method. The last CTA reduces the per-CTA sums, applies r_{c+1} = r_c - taken + pushed,
+// the stop test and the starvation guard (reading G5), and rewinds the tile counter.
+#include "sweep.cuh"
+
+namespace di {
+namespace {
+
+constexpr int kAsyncThreads = 256;
+constexpr int kAsyncSmall = 32;     // rows with <= this many links: pushed by the selecting thread
+constexpr int kAsyncChunk = 1024;   // longer rows: chunks of this many links, one warp each
+
+__device__ __forceinline__ double take_fluid(double *p) {
+  return __longlong_as_double(
+      (long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
+}
+
+template <bool LOOPS>
+__global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
+  constexpr int NW = kAsyncThreads / 32;
+  __shared__ int64_t s_rb[kSelTile];   // long rows of the tile: first link
+  __shared__ int32_t s_ro[kSelTile];   // #links
+  __shared__ double s_rv[kSelTile];    // v = T d / o
+  __shared__ int32_t s_ri[kSelTile];   // local node id
+  __shared__ int32_t s_rp[kSelTile + 1];  // exclusive chunk prefix
+  __shared__ int s_nrows, s_nchunks, s_claim;
+  __shared__ int64_t s_tile;
+  __shared__ bool s_last;
+  __shared__ double s_red[NW][4];
+  __shared__ long long s_ired[NW][3];
+
+  Scalars *sc = a.sc;
+  if (sc->stop) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double r = sc->r, d = sc->d;
+  const bool cyc = (sc->variant == DI_CYC) || sc->guard;
+  const double t = (a.L_total > 0.0) ? r / a.L_total : 0.0;  // r/L once per cycle (G3, G4)
+  const uint64_t pol = policy_evict_first();
+  const uint64_t fpol = a.red_hint ? policy_evict_last() : policy_evict_normal();
+  const int32_t *__restrict__ col = a.col;
+  double *__restrict__ F = a.F;
+  double acc_tk = 0.0, acc_s = 0.0, acc_e = 0.0;
+  long long acc_sel = 0, acc_nd = 0, acc_lk = 0;
+
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_tile = (int64_t)atomicAdd(&sc->tile_next, 1u);
+      s_nrows = 0;
+      s_claim = 0;
+    }
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= a.ntiles) break;
+    // ---- select: 4 consecutive nodes per thread, F and row extents
+    const int64_t base = tile * (int64_t)kSelTile + (int64_t)threadIdx.x * kSelItems;
+    double f[kSelItems];
+    int64_t rb[kSelItems + 1];
+    int kl[kSelItems];
+#pragma unroll
+    for (int j = 0; j < kSelItems; j++) {
+      const int64_t i = base + j;
+      f[j] = (i < a.n) ? __ldcg(F + i) : 0.0;
+      rb[j] = (i < a.n) ? a.row_ptr[i] : 0;
+      kl[j] = (LOOPS && i < a.n) ? a.kloop[i] : 0;
+    }
+    rb[kSelItems] = (base + kSelItems <= a.n) ? a.row_ptr[base + kSelItems]
+                                              : (base < a.n ? a.row_ptr[a.n] : 0);
+    double sv[kSelItems];
+    int so[kSelItems];
+#pragma unroll
+    for (int j = 0; j < kSelItems; j++) {
+      so[j] = 0;
+      sv[j] = 0.0;
+      const int64_t i = base + j;
+      if (i >= a.n) continue;
+      const int64_t rend = (i + 1 < a.n) ? (j + 1 < kSelItems ? rb[j + 1] : rb[kSelItems])
+                                         : a.row_ptr[a.n];
+      const int o = (int)(rend - rb[j]);
+      const double thr = cyc ? 0.0 : __dmul_rn(t, (double)o);  // (r/L)*out[i]
+      if (!(f[j] > thr)) continue;                              // strict '>'
+      const double T0 = take_fluid(F + i);                     // >= f[j]: only REDs add meanwhile
+      double T = T0;
+      if (LOOPS && kl[j] > 0) {                                 // P:259-263 with k copies (G6)
+        const double od = (double)o;
+        T = __ddiv_rn(__dmul_rn(T0, od), __dsub_rn(od, __dmul_rn((double)kl[j], d)));
+      }
+      red_add_f64(a.H + i, T);
+      acc_tk += T0;
+      acc_sel++;
+      if (o == 0) {
+        acc_e += T;
+        continue;
+      }
+      const double v = __ddiv_rn(__dmul_rn(T, d), (double)o);
+      acc_s += __dmul_rn(v, (double)(o - kl[j]));
+      acc_lk += o;
+      acc_nd++;
+      if (o <= kAsyncSmall) {
+        so[j] = o;
+        sv[j] = v;
+      } else {
+        const int p = atomicAdd(&s_nrows, 1);
+        s_rb[p] = rb[j];
+        s_ro[p] = o;
+        s_rv[p] = v;
+        s_ri[p] = (int32_t)(base + j - tile * kSelTile);
+      }
+    }
+    // ---- short rows: the selecting thread pushes them, int4 column groups
+#pragma unroll
+    for (int j = 0; j < kSelItems; j++) {
+      if (so[j] == 0) continue;
+      const int64_t beg = rb[j], end = beg + so[j], a0 = beg & ~3ll;
+      const int nvec = (int)((end - a0 + 3) >> 2);
+      const int32_t gi = LOOPS ? (int32_t)(base + j + a.lo) : -1;
+      for (int q = 0; q < nvec; q += 3) {
+        int4 x0 = ld_col4(col + a0 + 4 * q, pol);
+        int4 x1 = make_int4(0, 0, 0, 0), x2 = make_int4(0, 0, 0, 0);
+        if (q + 1 < nvec) x1 = ld_col4(col + a0 + 4 * (q + 1), pol);
+        if (q + 2 < nvec) x2 = ld_col4(col + a0 + 4 * (q + 2), pol);
+        red_group<LOOPS>(F, x0, a0 + 4 * q, beg, end, gi, sv[j], fpol);
+        if (q + 1 < nvec) red_group<LOOPS>(F, x1, a0 + 4 * (q + 1), beg, end, gi, sv[j], fpol);
+        if (q + 2 < nvec) red_group<LOOPS>(F, x2, a0 + 4 * (q + 2), beg, end, gi, sv[j], fpol);
+      }
+    }
+    __syncthreads();
+    // ---- long rows: chunk prefix (warp 0), then the CTA's warps claim chunks
+    const int nrows = s_nrows;
+    if (nrows > 0) {
+      if (warp == 0) {
+        const int per = (nrows + 31) / 32;
+        const int r0 = lane * per, r1 = min(nrows, r0 + per);
+        int sum = 0;
+        for (int k = r0; k < r1; k++) sum += (s_ro[k] + kAsyncChunk - 1) / kAsyncChunk;
+        int incl = sum;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += y;
+        }
+        int run = incl - sum;
+        for (int k = r0; k < r1; k++) {
+          s_rp[k] = run;
+          run += (s_ro[k] + kAsyncChunk - 1) / kAsyncChunk;
+        }
+        if (lane == 31) {
+          s_nchunks = incl;
+          s_rp[nrows] = incl;
+        }
+      }
+      __syncthreads();
+      const int nch = s_nchunks;
+      for (;;) {
+        int c = 0;
+        if (lane == 0) c = atomicAdd(&s_claim, 1);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        if (c >= nch) break;
+        int lo = 0, hi = nrows - 1;  // last row with s_rp[row] <= c
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_rp[mid] <= c) lo = mid; else hi = mid - 1;
+        }
+        const int64_t rbeg = s_rb[lo];
+        const int64_t beg = rbeg + (int64_t)(c - s_rp[lo]) * kAsyncChunk;
+        const int64_t end = min(rbeg + (int64_t)s_ro[lo], beg + kAsyncChunk);
+        const double v = s_rv[lo];
+        const int32_t gi = LOOPS ? (int32_t)(tile * kSelTile + s_ri[lo] + a.lo) : -1;
+        const int64_t a0 = beg & ~3ll;
+        const int nvec = (int)((end - a0 + 3) >> 2);
+        for (int vb = 0; vb < nvec; vb += 128) {
+          int4 x[4];
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const int vi = vb + 32 * k + lane;
+            x[k] = make_int4(0, 0, 0, 0);
+            if (vi < nvec) x[k] = ld_col4(col + a0 + 4 * (int64_t)vi, pol);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const int vi = vb + 32 * k + lane;
+            if (vi < nvec) red_group<LOOPS>(F, x[k], a0 + 4 * (int64_t)vi, beg, end, gi, v, fpol);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // ---- this CTA's sums (fixed order inside the CTA) -> ppartials[blockIdx.x]
+  acc_tk = warp_sum(acc_tk);
+  acc_s = warp_sum(acc_s);
+  acc_e = warp_sum(acc_e);
+  acc_sel = warp_sum(acc_sel);
+  acc_nd = warp_sum(acc_nd);
+  acc_lk = warp_sum(acc_lk);
+  if (lane == 0) {
+    s_red[warp][0] = acc_tk;
+    s_red[warp][1] = acc_s;
+    s_red[warp][2] = acc_e;
+    s_ired[warp][0] = acc_sel;
+    s_ired[warp][1] = acc_nd;
+    s_ired[warp][2] = acc_lk;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x[3] = {0.0, 0.0, 0.0};
+    long long c[3] = {0, 0, 0};
+    for (int w = 0; w < NW; w++) {
+      for (int k = 0; k < 3; k++) x[k] += s_red[w][k];
+      for (int k = 0; k < 3; k++) c[k] += s_ired[w][k];
+    }
+    // slot layout of slice_partials: q, s, e, taken, sel, nd, links, 0 (q unused here)
+    double *o = a.ppartials + 8 * (int64_t)blockIdx.x;
+    reinterpret_cast<double2 *>(o)[0] = make_double2(0.0, x[1]);
+    reinterpret_cast<double2 *>(o)[1] = make_double2(x[2], x[0]);
+    reinterpret_cast<longlong2 *>(o)[2] = make_longlong2(c[0], c[1]);
+    reinterpret_cast<longlong2 *>(o)[3] = make_longlong2(c[2], 0);
+    __threadfence();
+    s_last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const SweepSums x = reduce_partials(a, gridDim.x, kAsyncThreads);
+  if (threadIdx.x != 0) return;
+  // ---- the cycle's effect (P:278-283 stop test, G5 guard)
+  volatile Scalars *vs = a.sc;
+  const int variant = vs->variant;
+  const double r_next = __dadd_rn(__dsub_rn(r, x.taken), x.s);
+  const double e_tot = vs->e + x.e;
+  const int64_t sw = vs->sweeps;
+  if (vs->trace && sw < kLogCap) {
+    a.log_r[sw] = r;
+    a.log_sel[sw] = x.sel;
+    a.log_links[sw] = x.lk;
+    a.log_mode[sw] = 0;
+  }
+  if (vs->guard && variant != DI_CYC) vs->guards = vs->guards + 1;
+  vs->e = e_tot;
+  vs->e_sw = x.e;
+  vs->s = x.s;
+  vs->q = __dsub_rn(r, x.taken);
+  vs->r = r_next;
+  vs->sweeps = sw + 1;
+  vs->selected_total = vs->selected_total + x.sel;
+  vs->selected_nd_total = vs->selected_nd_total + x.nd;
+  vs->links_total = vs->links_total + x.lk;
+  vs->scanned_total = vs->scanned_total + a.n;
+  const double err = vs->paper_err ? r_next / (1.0 - d - d * e_tot) : r_next;
+  const int stop = err <= vs->tol;
+  vs->stop = stop;
+  vs->guard = (x.sel == 0 && !stop && variant == DI_SOP) ? 1 : 0;
+  vs->tile_next = 0;
+  vs->ticket = 0;
+}
+
+}  // namespace
+
+void launch_cycle(Graph &g, int64_t *launches) {
+  SweepArgs a = sweep_args(g, 0);
+  static int occ = 0;
+  if (occ == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cycle<false>, kAsyncThreads, 0);
+    if (occ < 1) occ = 1;
+  }
+  const int grid = std::min(g.num_sms * occ, kMaxSlices);
+  if (g.has_loops)
+    k_cycle<true><<<grid, kAsyncThreads, 0, g.stream>>>(a);
+  else
+    k_cycle<false><<<grid, kAsyncThreads, 0, g.stream>>>(a);
+  *launches += 1;
+}
+
+}  // namespace di

@@ -85,6 +85,7 @@ struct __align__(256) Scalars {
   double r_run;              // block-ordered sweeps: running sum F inside a cycle
   int64_t sel_cyc, links_cyc;
   int64_t max_sweeps;        // DI_GRAPH_LOOP: the device-side loop stops at this many sweeps
+  unsigned int tile_next;    // DI_ASYNC: next tile of the cycle (dynamic, increasing order)
 };
 
 // One push work item: a row (or a kChunk-link chunk of a hub row) of a selected node.
@@ -208,6 +209,8 @@ void launch_push(Graph &g, int64_t *launches, int blk = 0, int blocks = 1);
 void launch_finalize(Graph &g, int64_t *launches);
 void launch_pull(Graph &g, int64_t *launches);
 void launch_loop_cond(Graph &g, cudaGraphConditionalHandle h);
+// async.cu
+void launch_cycle(Graph &g, int64_t *launches);
 di_status alloc_pull(Graph &g);
 di_status alloc_dist(Graph &g);
 // dist.cu

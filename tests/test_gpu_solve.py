@@ -158,6 +158,81 @@ def test_graph_loop(blocks, mode):
         g.free()
 
 
+@pytest.mark.parametrize("graph_loop", [False, True])
+def test_async_cycles(graph_loop):
+    """DI_ASYNC (one persistent kernel per cycle, live F taken by atomic exchange, paper's cyclic
+    order up to the grid's concurrency): exact pins, random graphs with loops/duplicates vs the
+    dense solve, F = B + P.H - H and conservation at arbitrary stops, north_star gate on C1 and
+    C2 for DI-SOP and DI-CYC, ragged sizes around the tile and hub rows above the chunk size."""
+    need_gpu()
+    import paper_1204_6255_b200 as di
+    kw = dict(asynchronous=True, graph_loop=graph_loop)
+    for name, n, links, X in PINS:
+        src = np.array([s for s, _ in links], dtype=np.int32)
+        dst = np.array([t for _, t in links], dtype=np.int32)
+        g = upload(src, dst, n)
+        for variant in ("sop", "cyc"):
+            st = g.solve(d=D, tol=1e-16, variant=variant, **kw)
+            assert st["converged"] == 1, (name, st)
+            assert l1(g.history().cpu().numpy(), [float(x) for x in X]) <= 1e-14, name
+        g.free()
+    for seed in range(40):
+        src, dst, n = digen.small_random(seed, n_max=3000 if seed % 4 == 0 else 64)
+        X = defn.solve_dense(src, dst, n, D) if n <= 64 else defn.solve_sparse(src, dst, n, D)
+        P = defn.sparse_P(src, dst, n, D)
+        B = defn.uniform_B(n, D)
+        out = np.bincount(src, minlength=n)
+        g = upload(src, dst, n)
+        for variant in ("sop", "cyc"):
+            st = g.solve(d=D, tol=1e-15, variant=variant, **kw)
+            assert st["converged"] == 1
+            assert l1(g.history().cpu().numpy(), X) <= 1e-13 * max(1, n / 64), (seed, variant)
+            for k in (1, 3):
+                st = g.solve(d=D, tol=1e-300, variant=variant, max_sweeps=k, **kw)
+                # a cycle in (dynamic) node order can drain a small graph completely (F == 0)
+                assert (st["status"] == di.DI_NOT_CONVERGED and st["sweeps"] == k) or \
+                       (st["status"] == di.DI_OK and st["residual_l1"] == 0.0 and st["sweeps"] <= k)
+                H = g.history().cpu().numpy()
+                _, F = g.residual(return_F=True)
+                F = F.cpu().numpy()
+                assert np.all(F >= 0) and np.abs(F - (B + P @ H - H)).max() <= 1e-15
+                cons = F.sum() + (1 - D) * H[out > 0].sum() + H[out == 0].sum()
+                assert abs(cons - (1 - D)) <= 1e-14
+        g.free()
+    for name, seed in (("c1", 1), ("c1", 2), ("c2", 1)):
+        src, dst, n = digen.make(name, seed=seed)
+        g = upload(src, dst, n)
+        for variant in ("sop", "cyc"):
+            st = g.solve(d=D, tol=1e-10, variant=variant, trace=True, **kw)
+            assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
+            H = g.history().cpu().numpy()
+            Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant=variant)
+            assert l1(H, Ho) <= 1e-9, (name, variant)
+            Ht, _, _ = oracle.di(src, dst, n, d=D, tol=1e-13, variant=variant)
+            assert l1(H, Ht) <= 1e-10 / (1 - D) + 1e-13 / (1 - D)
+            if not graph_loop:
+                log = g.sweep_log()
+                assert len(log["r"]) == st["sweeps"] and log["links"].sum() == st["link_diffusions"]
+        g.free()
+    for n in (1, 1023, 1025, 20000):
+        rng = np.random.default_rng(n)
+        src = rng.integers(0, n, 4 * n).astype(np.int32)
+        dst = rng.integers(0, n, 4 * n).astype(np.int32)
+        if n == 20000:   # hub rows of 15000 and 3000 links (several 1024-link chunks)
+            src = np.concatenate([src, np.zeros(15000, np.int32), np.full(3000, 5, np.int32)])
+            dst = np.concatenate([dst, np.arange(1, 15001, dtype=np.int32), np.arange(6, 3006, dtype=np.int32)])
+        X, _, _ = oracle.di(src, dst, n, d=D, tol=1e-15, variant="sop")
+        g = upload(src, dst, n)
+        st = g.solve(d=D, tol=1e-13, **kw)
+        assert st["converged"] == 1
+        assert l1(g.history().cpu().numpy(), X) <= (1e-13 + 1e-15) / (1 - D) + 1e-14
+        g.free()
+    g = di.Graph(np.zeros(0, np.int32), np.zeros(0, np.int32), 3000)
+    st = g.solve(d=D, tol=1e-12, **kw)
+    assert st["converged"] == 1 and st["sweeps"] == 1
+    g.free()
+
+
 @pytest.mark.parametrize("mode", MODES)
 def test_invariants_mid_solve(mode):
     """T8: at any stopping point F = B + P.H - H, F >= 0, conservation, sum F non-increasing."""
