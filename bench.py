@@ -129,10 +129,13 @@ def run_ours(args):
         from paper_1204_6255_b200.dist import nccl_rendezvous
         _, _, nid = nccl_rendezvous()
         args.mode = "push"                   # the partitioned sweep is push-only
-        args.blocks = 1                      # ... and bulk (block order is single-GPU)
+        args.sched = "bulk"                  # ... and bulk (block / async order are single-GPU)
     import paper_1204_6255_b200 as di
     if args.mode != "push":
+        args.sched = "bulk"
+    if args.sched != "block":
         args.blocks = 1
+    use_async = args.sched == "async"
     part = dict(rank=rank, world=world, nccl_id=nid) if world > 1 else dict(build_csc=args.mode != "push")
 
     src, dst, n, gen_s = make_graph(args.config, args.seed)
@@ -163,7 +166,7 @@ def run_ours(args):
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         st = g.solve(d=D, tol=TOL, variant=args.variant, profile=profile, mode=args.mode,
-                     blocks=args.blocks, graph_loop=graph)
+                     blocks=args.blocks, graph_loop=graph, asynchronous=use_async)
         ev1.record(stream)
         ev1.synchronize()
         assert st["converged"] == 1, st
@@ -195,18 +198,22 @@ def run_ours(args):
     value = links / (tot_ms * 1e-3) / 1e9
     ms_per_step = tot_ms / args.steps
 
-    # ---- roofline of the dominant kernel (push, a5): algorithmic bytes / event time
+    # ---- roofline of the dominant kernel: algorithmic bytes / event time. DI_ASYNC: k_cycle does
+    #      the whole cycle (select + push), so its bytes are the full counted bytes of the cycle;
+    #      otherwise k_push's counted push bytes
     peak, peak_src = peaks()
-    push_bytes = sum(s["push_bytes"] for s in pstats) / world   # per GPU (stats are global)
+    push_bytes = sum(s["counted_bytes" if use_async else "push_bytes"] for s in pstats) / world
     push_ms = sum(s["push_ms"] for s in pstats)
     push_launches = sum(s["push_launches"] for s in pstats)
     sel_ms = sum(s["select_ms"] for s in pstats)
     ptot_ms = sum(ptimes)
     achieved = push_bytes / (push_ms * 1e-3) / 1e9 if push_ms > 0 else 0.0
-    tr = ncu_traffic()
+    tr = ncu_traffic("k_cycle" if use_async else "k_push")
     counted = sum(s["counted_bytes"] for s in stats) / world
-    roofline = {"bound": "hbm", "kernel": ("k_push (a5: diffusion of the frontier's fluid)" if args.mode == "push"
-                                           else "k_push + k_pull (a5/a5': diffusion of the frontier's fluid)"),
+    kname = ("k_cycle (a2-a6 fused: asynchronous select + push of one cycle)" if use_async else
+             "k_push (a5: diffusion of the frontier's fluid)" if args.mode == "push" else
+             "k_push + k_pull (a5/a5': diffusion of the frontier's fluid)")
+    roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": tr,
                 "peak_source": peak_src,
@@ -237,6 +244,7 @@ def run_ours(args):
         t0 = time.perf_counter()
         gh = di.Graph(src_p, dst_p, n, stream=stream, **part)  # DI_HOST_PTRS: H2D inside
         st = gh.solve(d=D, tol=TOL, variant=args.variant, mode=args.mode, blocks=args.blocks,
+                      asynchronous=use_async,
                       graph_loop=use_graph)
         H = gh.history()
         H_host.copy_(H, non_blocking=True)
@@ -265,7 +273,9 @@ def run_ours(args):
         "config": {"workload": f"{args.config}: " + __import__("digen").CONFIGS[args.config].note,
                    "n": n, "links": L, "variant": "DI-" + args.variant.upper(), "d": D,
                    "tol_l1_fluid": TOL, "seed": args.seed, "sweep_mode": args.mode,
-                   "cycle_blocks": args.blocks,
+                   "schedule": {"async": "asynchronous cycles (DI_ASYNC)",
+                                "block": f"block-ordered cycles, K = {args.blocks}",
+                                "bulk": "bulk-synchronous sweeps"}[args.sched],
                    "l2": "inputs > 126 MB L2 and 512 MiB L2 flush before each step",
                    "parallelism": f"1-D node range x{world}, NCCL (id, value) exchange" if world > 1
                    else "single GPU",
@@ -340,8 +350,10 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--variant", default="sop", choices=["sop", "cyc"])
     ap.add_argument("--mode", default="push", choices=["push", "pull", "auto"])
-    ap.add_argument("--blocks", type=int, default=8,
-                    help="block-ordered cycles: K ordered node blocks per cycle (1 = plain bulk sweeps)")
+    ap.add_argument("--sched", default="async", choices=["async", "block", "bulk"],
+                    help="async: one persistent kernel per cycle (DI_ASYNC); block: K ordered blocks "
+                         "per cycle (DI_BLOCKS); bulk: bulk-synchronous sweeps")
+    ap.add_argument("--blocks", type=int, default=8, help="K for --sched block")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)

@@ -19,7 +19,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__grid_size", "launch__block_size", "lts__t_sectors_srcunit_tex_op_red.sum",
         "lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed",
-        "smsp__inst_executed_op_global_red.sum"]
+        "smsp__inst_executed_op_global_red.sum", "smsp__inst_executed.sum",
+        "lts__t_tag_requests.max.pct_of_peak_sustained_elapsed",
+        "l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed"]
 
 
 def launches(path):
@@ -96,6 +98,10 @@ if __name__ == "__main__":
                         f.write(f"- {k}: {v}\n")
                 f.write("\n")
         tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        try:
+            old = json.load(open(tr_path))
+        except Exception:
+            old = {}
         tr = {}
         for e in c:
             name = e["kernel"].split("::")[-1].split("<")[0].strip()
@@ -103,7 +109,9 @@ if __name__ == "__main__":
             tr.setdefault(name + "_samples", []).append(b)
         for k in list(tr):
             if k.endswith("_samples"):
-                tr[k[:-8]] = max(tr[k])  # the largest captured launch (full-frontier sweep)
-        tr["source"] = f"profiles/{a.tag}_ncu.md"
-        json.dump(tr, open(tr_path, "w"), indent=1)
+                tr[k[:-8]] = sum(tr[k]) / len(tr[k])  # mean over the captured launches
+                old[k[:-8] + "_source"] = f"profiles/{a.tag}_ncu.md"
+        old.update(tr)
+        old.pop("source", None)
+        json.dump(old, open(tr_path, "w"), indent=1)
     print("ok")

@@ -19,11 +19,13 @@ ap.add_argument("--solves", type=int, default=2)
 ap.add_argument("--mode", default="push")
 ap.add_argument("--no-reorder", action="store_true")
 ap.add_argument("--blocks", type=int, default=1)
+ap.add_argument("--asynchronous", action="store_true")
 args = ap.parse_args()
 src, dst, n = digen.make(args.config)
 g = di.Graph(torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda(), n, build_csc=args.mode != "push",
              reorder=not args.no_reorder)
 for k in range(args.solves):
-    st = g.solve(d=0.85, tol=1e-10, variant=args.variant, mode=args.mode, blocks=args.blocks)
+    st = g.solve(d=0.85, tol=1e-10, variant=args.variant, mode=args.mode, blocks=args.blocks,
+                 asynchronous=args.asynchronous)
     print(k, st["sweeps"], st["solve_ms"], st["equivalent_iterations"], flush=True)
 torch.cuda.synchronize()
