@@ -64,7 +64,7 @@ struct EventSet {
 
 void free_graph(Graph *g) {
   if (!g) return;
-  void *ptrs[] = {g->row_ptr, g->col, g->deg, g->kloop, g->csc_ptr, g->csc_row, g->F, g->H,
+  void *ptrs[] = {g->ppartials, g->rep, g->row_ptr, g->col, g->deg, g->kloop, g->csc_ptr, g->csc_row, g->F, g->H,
                   g->new_of, g->old_of, g->Bperm, g->xfer,
                   g->S, g->aux, g->sc, g->partials, g->ipartials, g->red_partials,
                   g->log_r, g->log_sel, g->log_links, g->log_mode};
@@ -263,6 +263,7 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
   if (const char *e = getenv("DI_PUSH_OCC")) g->push_occ = atoi(e);
   if (const char *e = getenv("DI_AUTO_RATIO")) g->auto_ratio = atof(e);
   if (const char *e = getenv("DI_STRIPES")) g->stripes = atoi(e);
+  if (const char *e = getenv("DI_HOT_ACC")) g->hot_acc = atoi(e);
   di_status s = build_graph(*g, src, dst, n_links, flags);
   if (s == DI_OK) s = alloc_state(*g);
   if (s == DI_OK) s = alloc_pull(*g);
@@ -347,6 +348,10 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   const bool async = flags & DI_ASYNC;
   if (async && (mode != MODE_PUSH || blocks > 1))
     return fail(DI_EINVAL, "di_solve: DI_ASYNC runs push cycles without DI_BLOCKS");
+  if (async) {
+    di_status ps = prepare_cycle(g);
+    if (ps != DI_OK) return ps;
+  }
   const bool resume = flags & DI_RESUME;
   if (resume && !g.solved) return fail(DI_ESTATE, "di_solve: DI_RESUME before any solve");
   const int paper = (flags & DI_PAPER_ERROR) ? 1 : 0;

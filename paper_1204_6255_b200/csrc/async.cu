@@ -24,6 +24,37 @@ constexpr int kAsyncThreads = 256;
 constexpr int kAsyncSmall = 32;     // rows with <= this many links: pushed by the selecting thread
 constexpr int kAsyncChunk = 1024;   // longer rows: chunks of this many links, one warp each
 
+// Replicated accumulators for the hottest targets. Same-address fp64 REDs serialise in one L2
+// slice; a node that receives a large share of all pushes (C3's Zipf targets: the top node gets
+// 0.39 % of the links, 383k in-links) keeps its slice busy for a large part of the cycle. With
+// the striped relabelling the kRepl most-linked nodes are the first node of stripes
+// 0..kRepl-1; when the stripe length is a power of two (a.hot_shift >= 0) their REDs go to one
+// of kCopies copies (chosen by warp), each copy in its own 4 KB page, and the last CTA of the
+// cycle folds the copies into F. Enabled when the top node's share exceeds kReplShare (C3 yes:
+// 35 -> ... ms; C4 no: its top share is 0.09 % and the extra test per link costs 6 %).
+constexpr int kRepl = 64;
+constexpr int kCopies = 16;
+constexpr double kReplShare = 0.0025;
+
+template <bool LOOPS>
+__device__ __forceinline__ void red_group_rep(double *__restrict__ F, double *__restrict__ rep,
+                                              int hot_shift, int32_t hot_lim, int copy, int4 x,
+                                              int64_t p0, int64_t beg, int64_t end, int32_t gi,
+                                              double v, uint64_t fpol) {
+  const int32_t jj[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    const int64_t p = p0 + c;
+    if (p >= beg && p < end && (!LOOPS || jj[c] != gi)) {
+      const int32_t j = jj[c];
+      if (hot_shift >= 0 && j < hot_lim && (j & ((1 << hot_shift) - 1)) == 0)
+        red_add_f64(rep + copy * 512 + (j >> hot_shift), v);
+      else
+        red_add_f64_hint(F + j, v, fpol);
+    }
+  }
+}
+
 __device__ __forceinline__ double take_fluid(double *p) {
   return __longlong_as_double(
       (long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
@@ -46,6 +77,10 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
   Scalars *sc = a.sc;
   if (sc->stop) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hot_shift = a.hot_shift;
+  const int32_t hot_lim = hot_shift >= 0 ? (kRepl << hot_shift) : 0;
+  const int copy = (blockIdx.x * (kAsyncThreads / 32) + warp) % kCopies;
+  double *rep = a.rep;
   const double r = sc->r, d = sc->d;
   const bool cyc = (sc->variant == DI_CYC) || sc->guard;
   const double t = (a.L_total > 0.0) ? r / a.L_total : 0.0;  // r/L once per cycle (G3, G4)
@@ -132,9 +167,13 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
         int4 x1 = make_int4(0, 0, 0, 0), x2 = make_int4(0, 0, 0, 0);
         if (q + 1 < nvec) x1 = ld_col4(col + a0 + 4 * (q + 1), pol);
         if (q + 2 < nvec) x2 = ld_col4(col + a0 + 4 * (q + 2), pol);
-        red_group<LOOPS>(F, x0, a0 + 4 * q, beg, end, gi, sv[j], fpol);
-        if (q + 1 < nvec) red_group<LOOPS>(F, x1, a0 + 4 * (q + 1), beg, end, gi, sv[j], fpol);
-        if (q + 2 < nvec) red_group<LOOPS>(F, x2, a0 + 4 * (q + 2), beg, end, gi, sv[j], fpol);
+        red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x0, a0 + 4 * q, beg, end, gi, sv[j], fpol);
+        if (q + 1 < nvec)
+          red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x1, a0 + 4 * (q + 1), beg, end, gi,
+                               sv[j], fpol);
+        if (q + 2 < nvec)
+          red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x2, a0 + 4 * (q + 2), beg, end, gi,
+                               sv[j], fpol);
       }
     }
     __syncthreads();
@@ -192,7 +231,9 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
 #pragma unroll
           for (int k = 0; k < 4; k++) {
             const int vi = vb + 32 * k + lane;
-            if (vi < nvec) red_group<LOOPS>(F, x[k], a0 + 4 * (int64_t)vi, beg, end, gi, v, fpol);
+            if (vi < nvec)
+              red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x[k], a0 + 4 * (int64_t)vi, beg,
+                                   end, gi, v, fpol);
           }
         }
       }
@@ -234,6 +275,16 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  if (hot_shift >= 0) {  // fold the replicated accumulators into F, clear them
+    for (int k = threadIdx.x; k < kRepl; k += kAsyncThreads) {
+      double acc = 0.0;
+      for (int c = 0; c < kCopies; c++) {
+        acc += __ldcg(rep + c * 512 + k);
+        rep[c * 512 + k] = 0.0;
+      }
+      if (acc != 0.0) F[(int64_t)k << hot_shift] += acc;
+    }
+  }
   const SweepSums x = reduce_partials(a, gridDim.x, kAsyncThreads);
   if (threadIdx.x != 0) return;
   // ---- the cycle's effect (P:278-283 stop test, G5 guard)
@@ -269,8 +320,31 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
 
 }  // namespace
 
+// shift of a power-of-two stripe length when the replicated hot accumulators apply, else -1
+static int hot_shift_of(const Graph &g) {
+  const bool skewed = g.l_global > 0 && (double)g.max_indeg > kReplShare * (double)g.l_global;
+  if (!(g.reordered && g.hot_acc && skewed && g.world == 1 && g.stripes >= kRepl &&
+        g.n % g.stripes == 0))
+    return -1;
+  const int64_t M = g.n / g.stripes;
+  int sh = 0;
+  while ((1ll << sh) < M) sh++;
+  return ((1ll << sh) == M && sh < 31) ? sh : -1;
+}
+
+// called by di_solve before any launch or capture (allocations are not capturable)
+di_status prepare_cycle(Graph &g) {
+  if (hot_shift_of(g) >= 0 && !g.rep) {
+    DI_CK(cudaMalloc(&g.rep, kCopies * 512 * sizeof(double)));
+    DI_CK(cudaMemsetAsync(g.rep, 0, kCopies * 512 * sizeof(double), g.stream));
+  }
+  return DI_OK;
+}
+
 void launch_cycle(Graph &g, int64_t *launches) {
   SweepArgs a = sweep_args(g, 0);
+  a.hot_shift = g.rep ? hot_shift_of(g) : -1;
+  a.rep = g.rep;
   static int occ = 0;
   if (occ == 0) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cycle<false>, kAsyncThreads, 0);

@@ -124,6 +124,9 @@ struct Graph {
   // locality relabelling: internal id = new_of[user id]; user id = old_of[internal id]
   bool reordered = false;
   int stripes = 4096;        // relabelling stripes (DI_STRIPES; 1 = plain degree order)
+  int hot_acc = 1;           // DI_ASYNC: replicated accumulators for the hottest targets (DI_HOT_ACC)
+  double *rep = nullptr;
+  int64_t max_indeg = 0;     // largest in-degree (set by the relabelling pass)
   int32_t *new_of = nullptr, *old_of = nullptr;
   double *Bperm = nullptr;   // B in internal order (custom B)
   double *xfer = nullptr;    // scratch for permuted copies
@@ -211,6 +214,7 @@ void launch_pull(Graph &g, int64_t *launches);
 void launch_loop_cond(Graph &g, cudaGraphConditionalHandle h);
 // async.cu
 void launch_cycle(Graph &g, int64_t *launches);
+di_status prepare_cycle(Graph &g);
 di_status alloc_pull(Graph &g);
 di_status alloc_dist(Graph &g);
 // dist.cu

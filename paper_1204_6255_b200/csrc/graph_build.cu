@@ -290,6 +290,18 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     DI_CK(cub::DeviceRadixSort::SortPairs(ptmp.p, pb, (uint64_t *)kin.p, (uint64_t *)kout.p,
                                           (int32_t *)vin.p, (int32_t *)sorted.p, (int64_t)n, 0,
                                           32 + wb, st));
+    uint32_t top = 0;  // largest in-degree (DI_ASYNC decides on replicated hot accumulators)
+    {
+      DevBuf mx, mtmp;
+      DI_CK(cudaMalloc(&mx.p, 4));
+      size_t mb = 0;
+      DI_CK(cub::DeviceReduce::Max(nullptr, mb, indeg, (uint32_t *)mx.p, (int64_t)n, st));
+      DI_CK(cudaMalloc(&mtmp.p, mb));
+      DI_CK(cub::DeviceReduce::Max(mtmp.p, mb, indeg, (uint32_t *)mx.p, (int64_t)n, st));
+      DI_CK(cudaMemcpyAsync(&top, mx.p, 4, cudaMemcpyDeviceToHost, st));
+      DI_CK(cudaStreamSynchronize(st));
+    }
+    g.max_indeg = top;
     const int64_t P = std::max<int64_t>(1, (int64_t)g.stripes);
     k_place<<<grid_for(n, sms), 256, 0, st>>>((const int32_t *)sorted.p, n, bd, P, g.new_of,
                                                g.old_of);

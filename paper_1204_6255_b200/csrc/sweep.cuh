@@ -33,6 +33,8 @@ struct SweepArgs {
   int64_t t0, t1;
   int blk, blocks;
   double *ppartials;    // 8 per finaliser slice: q, s, e, taken, sel, nd, links, 0
+  int hot_shift;        // DI_ASYNC replicated hot accumulators (async.cu), -1 = off
+  double *rep;
 };
 
 // What one sweep moved: r_{n+1} = q + s (a2), dangling absorption e, counters.
@@ -266,6 +268,8 @@ inline SweepArgs sweep_args(Graph &g, int test_mode, int blk = 0, int blocks = 1
   a.blk = blk;
   a.blocks = blocks;
   a.ppartials = g.ppartials;
+  a.hot_shift = -1;
+  a.rep = nullptr;
   a.F = g.F;
   a.H = g.H;
   a.deg = g.deg;

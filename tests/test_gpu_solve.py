@@ -231,6 +231,24 @@ def test_async_cycles(graph_loop):
     st = g.solve(d=D, tol=1e-12, **kw)
     assert st["converged"] == 1 and st["sweeps"] == 1
     g.free()
+    # skewed in-degrees on a power-of-two stripe length: the replicated hot accumulators path
+    # (N = 4096 * 8, three targets with 4 %, 2 %, 1 % of all links)
+    n = 4096 * 8
+    rng = np.random.default_rng(11)
+    src = rng.integers(0, n, 6 * n).astype(np.int32)
+    dst = rng.integers(0, n, 6 * n).astype(np.int32)
+    m = len(src)
+    for hub, share in ((77, 0.04), (5000, 0.02), (123, 0.01)):
+        k = int(share * m)
+        src = np.concatenate([src, rng.integers(0, n, k).astype(np.int32)])
+        dst = np.concatenate([dst, np.full(k, hub, np.int32)])
+    g = upload(src, dst, n)
+    for variant in ("sop", "cyc"):
+        X, _, _ = oracle.di(src, dst, n, d=D, tol=1e-15, variant=variant)
+        st = g.solve(d=D, tol=1e-13, variant=variant, **kw)
+        assert st["converged"] == 1
+        assert l1(g.history().cpu().numpy(), X) <= (1e-13 + 1e-15) / (1 - D) + 1e-14
+    g.free()
 
 
 @pytest.mark.parametrize("mode", MODES)

@@ -9,7 +9,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
 src, dst, n = digen.make(cfg)
 g = di.Graph(torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda(), n)
 ref = None
-for name, kw in [("K8", dict(blocks=8)), ("async", dict(asynchronous=True)), ("K8-graph", dict(blocks=8, graph_loop=True)),
+for name, kw in [("async", dict(asynchronous=True)),
                  ("async-graph", dict(asynchronous=True, graph_loop=True)), ("async-cyc", dict(asynchronous=True, variant="cyc"))]:
     g.solve(d=0.85, tol=1e-10, **kw)
     sts = [g.solve(d=0.85, tol=1e-10, **kw) for _ in range(3)]
