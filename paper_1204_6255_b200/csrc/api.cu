@@ -19,6 +19,37 @@ namespace di {
 static thread_local std::string g_err;
 void set_error(const std::string &msg) { g_err = msg; }
 
+cudaStream_t &alloc_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+
+cudaError_t dmalloc_bytes(void **p, size_t bytes) {
+  static thread_local int prepared = -1;  // device whose pool was configured by this thread
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (prepared != dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;  // keep freed memory in the pool for the next upload / solve
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    prepared = dev;
+  }
+  cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 1, alloc_stream());
+  // the buffer is then usable on any stream (some host paths touch it with synchronous copies)
+  if (e == cudaSuccess) e = cudaStreamSynchronize(alloc_stream());
+  return e;
+}
+
+void dfree(void *p) {
+  if (p) cudaFreeAsync(p, alloc_stream());
+}
+
+cudaError_t dmemset(void *p, int v, size_t bytes) {
+  return cudaMemsetAsync(p, v, bytes, alloc_stream());
+}
+
 namespace {
 
 __global__ void k_check_B(const double *B, int64_t n, int *bad) {
@@ -69,17 +100,17 @@ void free_graph(Graph *g) {
                   g->S, g->aux, g->sc, g->partials, g->ipartials, g->red_partials,
                   g->log_r, g->log_sel, g->log_links, g->log_mode};
   for (void *p : ptrs)
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   for (int b = 0; b < kBins; b++) {
     void *q[] = {g->fr.ent[b], g->fr.id[b]};
     for (void *p : q)
-      if (p) cudaFree(p);
+      if (p) dfree(p);
   }
   for (int b = 0; b < kPullBins; b++) {
-    if (g->pe[b]) cudaFree(g->pe[b]);
-    if (g->re[b]) cudaFree(g->re[b]);
+    if (g->pe[b]) dfree(g->pe[b]);
+    if (g->re[b]) dfree(g->re[b]);
   }
-  if (g->cmp_partials) cudaFree(g->cmp_partials);
+  if (g->cmp_partials) dfree(g->cmp_partials);
   if (g->loop_exec) cudaGraphExecDestroy(g->loop_exec);
   if (g->loop_graph) cudaGraphDestroy(g->loop_graph);
   if (g->sc_host) cudaFreeHost(g->sc_host);
@@ -235,6 +266,7 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return fail(DI_ECUDA, "di_graph_upload: no CUDA device");
   DI_CK(cudaGetDevice(&dev));
+  AllocScope as((cudaStream_t)stream);
   Graph *g = new Graph();
   g->device = dev;
   g->stream = (cudaStream_t)stream;
@@ -294,8 +326,11 @@ di_status di_graph_links(di_graph h, int64_t *n_links) {
 di_status di_graph_free(di_graph h) {
   Graph *g = (Graph *)h;
   if (!g) return DI_OK;
+  AllocScope as(g->stream);
   cudaStreamSynchronize(g->stream);
+  cudaStream_t st = g->stream;
   free_graph(g);
+  cudaStreamSynchronize(st);
   return DI_OK;
 }
 
@@ -304,20 +339,21 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   Graph *gp = (Graph *)h;
   if (!gp) return fail(DI_EINVAL, "di_solve: NULL handle");
   Graph &g = *gp;
+  AllocScope as(g.stream);
   if (!(d > 0.0 && d < 1.0)) return fail(DI_EINVAL, "di_solve: d must be in (0, 1)");
   if (!(tol > 0.0) || !std::isfinite(tol)) return fail(DI_EINVAL, "di_solve: tol must be > 0");
   if (max_sweeps < 0) return fail(DI_EINVAL, "di_solve: max_sweeps < 0");
   if ((int)v < 0 || (int)v > DI_GS_BLOCK) return fail(DI_EINVAL, "di_solve: bad variant");
   if (B) {
     int *bad = nullptr;
-    DI_CK(cudaMalloc(&bad, 4));
+    DI_CK(dmalloc(&bad, 4));
     DI_CK(cudaMemsetAsync(bad, 0, 4, g.stream));
     k_check_B<<<std::max<int64_t>(1, std::min<int64_t>((g.n + 255) / 256, 4096)), 256, 0,
                 g.stream>>>(B, g.n, bad);
     int hb = 0;
     DI_CK(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, g.stream));
     DI_CK(cudaStreamSynchronize(g.stream));
-    cudaFree(bad);
+    dfree(bad);
     if (hb) return fail(DI_EINVAL, "di_solve: B has a negative or non-finite entry");
   }
   if (g.world > 1) {
@@ -328,7 +364,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     if ((flags & DI_RESUME) && !g.solved) return fail(DI_ESTATE, "di_solve: DI_RESUME before any solve");
     const double *Bint = B;
     if (B && g.reordered) {  // caller's slice [lo, hi) in the caller's numbering
-      if (!g.Bperm) DI_CK(cudaMalloc(&g.Bperm, (size_t)g.n * 8));
+      if (!g.Bperm) DI_CK(dmalloc(&g.Bperm, (size_t)g.n * 8));
       gather(g, g.Bperm, B - g.lo, g.old_of + g.lo);
       Bint = g.Bperm;
     }
@@ -385,7 +421,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
   const double *Bint = B;
   if (B && g.reordered) {   // B arrives in the caller's numbering
-    if (!g.Bperm) DI_CK(cudaMalloc(&g.Bperm, (size_t)g.n * 8));
+    if (!g.Bperm) DI_CK(dmalloc(&g.Bperm, (size_t)g.n * 8));
     gather(g, g.Bperm, B, g.old_of);
     launches++;
     Bint = g.Bperm;

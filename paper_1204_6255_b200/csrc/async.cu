@@ -335,7 +335,7 @@ static int hot_shift_of(const Graph &g) {
 // called by di_solve before any launch or capture (allocations are not capturable)
 di_status prepare_cycle(Graph &g) {
   if (hot_shift_of(g) >= 0 && !g.rep) {
-    DI_CK(cudaMalloc(&g.rep, kCopies * 512 * sizeof(double)));
+    DI_CK(dmalloc(&g.rep, kCopies * 512 * sizeof(double)));
     DI_CK(cudaMemsetAsync(g.rep, 0, kCopies * 512 * sizeof(double), g.stream));
   }
   return DI_OK;

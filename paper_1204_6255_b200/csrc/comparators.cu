@@ -285,14 +285,14 @@ di_status run_comparator(Graph &g, double d, double tol, int variant, int64_t ma
     for (int b = 0; b < kPullBins; b++) {
       std::vector<PullEntry> e = row_entries(rp, n, b);
       g.re_count[b] = (int64_t)e.size();
-      DI_CK(cudaMalloc(&g.re[b], std::max<size_t>(e.size(), 1) * sizeof(PullEntry)));
+      DI_CK(dmalloc(&g.re[b], std::max<size_t>(e.size(), 1) * sizeof(PullEntry)));
       if (!e.empty())
         DI_CK(cudaMemcpy(g.re[b], e.data(), e.size() * sizeof(PullEntry), cudaMemcpyHostToDevice));
     }
   }
-  if (!g.aux) DI_CK(cudaMalloc(&g.aux, (size_t)n * 8));
-  if (!g.S) DI_CK(cudaMalloc(&g.S, (size_t)n * 8));
-  if (!g.cmp_partials) DI_CK(cudaMalloc(&g.cmp_partials, (size_t)grid * 8));
+  if (!g.aux) DI_CK(dmalloc(&g.aux, (size_t)n * 8));
+  if (!g.S) DI_CK(dmalloc(&g.S, (size_t)n * 8));
+  if (!g.cmp_partials) DI_CK(dmalloc(&g.cmp_partials, (size_t)grid * 8));
   CmpArgs a;
   a.deg = g.deg;
   a.kloop = g.kloop;
@@ -344,7 +344,7 @@ di_status run_comparator(Graph &g, double d, double tol, int variant, int64_t ma
     launches += 2;
     std::vector<double> part(kGsBlocks);
     double *dacc = nullptr;
-    DI_CK(cudaMalloc(&dacc, kGsBlocks * 8));
+    DI_CK(dmalloc(&dacc, kGsBlocks * 8));
     while (err > tol && iters < max_sweeps) {
       for (int k = 0; k < kGsBlocks; k++) {
         const int64_t lo = n * k / kGsBlocks, hi = n * (k + 1) / kGsBlocks;
@@ -367,7 +367,7 @@ di_status run_comparator(Graph &g, double d, double tol, int variant, int64_t ma
       err = tot * d / (1.0 - d - d * e);
       iters++;
     }
-    cudaFree(dacc);
+    dfree(dacc);
   }
   if (x != g.H) DI_CK(cudaMemcpyAsync(g.H, x, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
   DI_CK(cudaEventRecord(t1, s));

@@ -186,6 +186,26 @@ struct Graph {
   double *rval = nullptr;         // received values
 };
 
+// ---------------------------------------------------------------- device memory
+// Every device buffer of the library comes from the device's default stream-ordered pool
+// (cudaMallocAsync) on the calling handle's stream, with the pool's release threshold raised so
+// that memory freed by one upload / solve is reused by the next without cudaMalloc/cudaFree
+// (which synchronise the device and cost ms per GB). API entry points set the stream with
+// AllocScope; dmemset is the stream-ordered memset on the same stream.
+cudaStream_t &alloc_stream();
+struct AllocScope {
+  cudaStream_t prev;
+  explicit AllocScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+  ~AllocScope() { alloc_stream() = prev; }
+};
+cudaError_t dmalloc_bytes(void **p, size_t bytes);
+template <typename T>
+inline cudaError_t dmalloc(T **p, size_t bytes) {
+  return dmalloc_bytes(reinterpret_cast<void **>(p), bytes);
+}
+void dfree(void *p);
+cudaError_t dmemset(void *p, int v, size_t bytes);
+
 // ---------------------------------------------------------------- error plumbing
 void set_error(const std::string &msg);
 #define DI_CK(call)                                                                     \

@@ -604,39 +604,40 @@ int64_t select_tiles(int64_t n) { return (n + kSelTile - 1) / kSelTile; }
 di_status alloc_state(Graph &g) {
   const int64_t n = g.n;
   const int64_t nt = select_tiles(n);
-  DI_CK(cudaMalloc(&g.F, (size_t)n * 8));
-  DI_CK(cudaMalloc(&g.H, (size_t)n * 8));
-  DI_CK(cudaMemset(g.H, 0, (size_t)n * 8));
-  DI_CK(cudaMemset(g.F, 0, (size_t)n * 8));
-  DI_CK(cudaMalloc(&g.sc, sizeof(Scalars)));
-  DI_CK(cudaMemset(g.sc, 0, sizeof(Scalars)));
+  DI_CK(dmalloc(&g.F, (size_t)n * 8));
+  DI_CK(dmalloc(&g.H, (size_t)n * 8));
+  DI_CK(dmemset(g.H, 0, (size_t)n * 8));
+  DI_CK(dmemset(g.F, 0, (size_t)n * 8));
+  DI_CK(dmalloc(&g.sc, sizeof(Scalars)));
+  DI_CK(dmemset(g.sc, 0, sizeof(Scalars)));
   DI_CK(cudaMallocHost(&g.sc_host, sizeof(Scalars)));
   memset(g.sc_host, 0, sizeof(Scalars));
-  DI_CK(cudaMalloc(&g.partials, (size_t)nt * 4 * 8));
-  DI_CK(cudaMalloc(&g.ipartials, (size_t)nt * 4 * 8));
-  DI_CK(cudaMalloc(&g.ppartials, (size_t)kMaxSlices * 8 * 8));
+  DI_CK(dmalloc(&g.partials, (size_t)nt * 4 * 8));
+  DI_CK(dmalloc(&g.ipartials, (size_t)nt * 4 * 8));
+  DI_CK(dmalloc(&g.ppartials, (size_t)kMaxSlices * 8 * 8));
   const int rg = reduce_grid(n, g.num_sms);
-  DI_CK(cudaMalloc(&g.red_partials, (size_t)rg * 8));
+  DI_CK(dmalloc(&g.red_partials, (size_t)rg * 8));
   // frontier: per-bin capacity = rows (chunks for C) whose static degree falls in the bin
   g.ntiles = nt;
   int32_t *cap = nullptr;
-  DI_CK(cudaMalloc(&cap, (size_t)nt * kBins * 4));
-  k_tile_caps<<<(unsigned)nt, kSelThreads>>>(g.deg, n, cap, nt);
+  DI_CK(dmalloc(&cap, (size_t)nt * kBins * 4));
+  k_tile_caps<<<(unsigned)nt, kSelThreads, 0, g.stream>>>(g.deg, n, cap, nt);
   std::vector<int32_t> hcap((size_t)nt * kBins);
-  DI_CK(cudaMemcpy(hcap.data(), cap, (size_t)nt * kBins * 4, cudaMemcpyDeviceToHost));
-  cudaFree(cap);
+  DI_CK(cudaMemcpyAsync(hcap.data(), cap, (size_t)nt * kBins * 4, cudaMemcpyDeviceToHost, g.stream));
+  DI_CK(cudaStreamSynchronize(g.stream));
+  dfree(cap);
   for (int b = 0; b < kBins; b++) {
     int64_t acc = 0;
     for (int64_t t = 0; t < nt; t++) acc += hcap[(size_t)b * nt + t];
     g.fr.cap[b] = acc;
     const size_t cap_b = (size_t)std::max<int64_t>(acc, 1);
-    DI_CK(cudaMalloc(&g.fr.ent[b], cap_b * sizeof(Entry)));
-    DI_CK(cudaMalloc(&g.fr.id[b], cap_b * 4));
+    DI_CK(dmalloc(&g.fr.ent[b], cap_b * sizeof(Entry)));
+    DI_CK(dmalloc(&g.fr.id[b], cap_b * 4));
   }
-  DI_CK(cudaMalloc(&g.log_r, (size_t)kLogCap * 8));
-  DI_CK(cudaMalloc(&g.log_sel, (size_t)kLogCap * 8));
-  DI_CK(cudaMalloc(&g.log_links, (size_t)kLogCap * 8));
-  DI_CK(cudaMalloc(&g.log_mode, (size_t)kLogCap));
+  DI_CK(dmalloc(&g.log_r, (size_t)kLogCap * 8));
+  DI_CK(dmalloc(&g.log_sel, (size_t)kLogCap * 8));
+  DI_CK(dmalloc(&g.log_links, (size_t)kLogCap * 8));
+  DI_CK(dmalloc(&g.log_mode, (size_t)kLogCap));
   return DI_OK;
 }
 
@@ -717,11 +718,11 @@ di_status alloc_pull(Graph &g) {
   }
   for (int b = 0; b < kPullBins; b++) {
     g.pe_count[b] = (int64_t)e[b].size();
-    DI_CK(cudaMalloc(&g.pe[b], std::max<size_t>(e[b].size(), 1) * sizeof(PullEntry)));
+    DI_CK(dmalloc(&g.pe[b], std::max<size_t>(e[b].size(), 1) * sizeof(PullEntry)));
     if (!e[b].empty())
       DI_CK(cudaMemcpy(g.pe[b], e[b].data(), e[b].size() * sizeof(PullEntry), cudaMemcpyHostToDevice));
   }
-  DI_CK(cudaMalloc(&g.S, (size_t)std::max<int64_t>(n, 1) * 8));
+  DI_CK(dmalloc(&g.S, (size_t)std::max<int64_t>(n, 1) * 8));
   return DI_OK;
 }
 

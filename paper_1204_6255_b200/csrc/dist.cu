@@ -277,27 +277,27 @@ di_status global_sum_F(Graph &g, int set_r, int64_t *launches) {
 di_status alloc_dist(Graph &g) {
   const int64_t N = g.n_global;
   const int G = g.world;
-  DI_CK(cudaMalloc(&g.R, (size_t)N * 8));
-  DI_CK(cudaMemset(g.R, 0, (size_t)N * 8));
-  DI_CK(cudaMalloc(&g.tl, (size_t)N * 4));
-  DI_CK(cudaMalloc(&g.sval, (size_t)N * 8));
-  DI_CK(cudaMalloc(&g.tcnt, (size_t)G * 32 * 8));
-  DI_CK(cudaMemset(g.tcnt, 0, (size_t)G * 32 * 8));
-  DI_CK(cudaMalloc(&g.sendcnt, (size_t)2 * G * 8));
-  DI_CK(cudaMemset(g.sendcnt, 0, (size_t)2 * G * 8));
+  DI_CK(dmalloc(&g.R, (size_t)N * 8));
+  DI_CK(dmemset(g.R, 0, (size_t)N * 8));
+  DI_CK(dmalloc(&g.tl, (size_t)N * 4));
+  DI_CK(dmalloc(&g.sval, (size_t)N * 8));
+  DI_CK(dmalloc(&g.tcnt, (size_t)G * 32 * 8));
+  DI_CK(dmemset(g.tcnt, 0, (size_t)G * 32 * 8));
+  DI_CK(dmalloc(&g.sendcnt, (size_t)2 * G * 8));
+  DI_CK(dmemset(g.sendcnt, 0, (size_t)2 * G * 8));
   DI_CK(cudaMallocHost(&g.sendcnt_h, (size_t)2 * G * 8 + 8 * 8));
-  DI_CK(cudaMalloc(&g.dsum, 8 * 8));
-  DI_CK(cudaMalloc(&g.isum, 8 * 8));
+  DI_CK(dmalloc(&g.dsum, 8 * 8));
+  DI_CK(dmalloc(&g.isum, 8 * 8));
   const size_t cap = (size_t)std::max<int64_t>(1, (int64_t)(G - 1) * g.n);
-  DI_CK(cudaMalloc(&g.rid, cap * 4));
-  DI_CK(cudaMalloc(&g.rval, cap * 8));
+  DI_CK(dmalloc(&g.rid, cap * 4));
+  DI_CK(dmalloc(&g.rval, cap * 8));
   return DI_OK;
 }
 
 void free_dist(Graph &g) {
   void *p[] = {g.R, g.tl, g.sval, g.tcnt, g.sendcnt, g.dsum, g.isum, g.rid, g.rval};
   for (void *q : p)
-    if (q) cudaFree(q);
+    if (q) dfree(q);
   if (g.sendcnt_h) cudaFreeHost(g.sendcnt_h);
   delete g.comm;
   g.comm = nullptr;

@@ -174,7 +174,7 @@ int grid_for(int64_t n, int sms) {
 struct DevBuf {
   void *p = nullptr;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   }
 };
 
@@ -192,8 +192,8 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   DevBuf dsrc, ddst, keys_a, keys_b, keep, tmp, nsel, badb;
   const int32_t *s_dev = src, *d_dev = dst;
   if (flags & DI_HOST_PTRS) {
-    DI_CK(cudaMalloc(&dsrc.p, (size_t)(L > 0 ? L : 1) * 4));
-    DI_CK(cudaMalloc(&ddst.p, (size_t)(L > 0 ? L : 1) * 4));
+    DI_CK(dmalloc(&dsrc.p, (size_t)(L > 0 ? L : 1) * 4));
+    DI_CK(dmalloc(&ddst.p, (size_t)(L > 0 ? L : 1) * 4));
     if (L > 0) {
       DI_CK(cudaMemcpyAsync(dsrc.p, src, (size_t)L * 4, cudaMemcpyHostToDevice, st));
       DI_CK(cudaMemcpyAsync(ddst.p, dst, (size_t)L * 4, cudaMemcpyHostToDevice, st));
@@ -202,9 +202,9 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     d_dev = (const int32_t *)ddst.p;
   }
   const size_t LL = (size_t)(L > 0 ? L : 1);
-  DI_CK(cudaMalloc(&keys_a.p, LL * 8));
-  DI_CK(cudaMalloc(&keys_b.p, LL * 8));
-  DI_CK(cudaMalloc(&badb.p, 16));
+  DI_CK(dmalloc(&keys_a.p, LL * 8));
+  DI_CK(dmalloc(&keys_b.p, LL * 8));
+  DI_CK(dmalloc(&badb.p, 16));
   unsigned long long init_bad = ~0ull;
   DI_CK(cudaMemcpyAsync(badb.p, &init_bad, 8, cudaMemcpyHostToDevice, st));
   uint64_t *ka = (uint64_t *)keys_a.p, *kb = (uint64_t *)keys_b.p;
@@ -212,7 +212,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   DevBuf indeg_b;
   uint32_t *indeg = nullptr;
   if (reorder) {
-    DI_CK(cudaMalloc(&indeg_b.p, (size_t)n * 4));
+    DI_CK(dmalloc(&indeg_b.p, (size_t)n * 4));
     DI_CK(cudaMemsetAsync(indeg_b.p, 0, (size_t)n * 4, st));
     indeg = (uint32_t *)indeg_b.p;
   }
@@ -244,14 +244,14 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   bd.b[1] = n;
   if (world > 1) {
     DevBuf od, pre, ctmp, bnd;
-    DI_CK(cudaMalloc(&od.p, (size_t)(n + 1) * 8));
-    DI_CK(cudaMalloc(&pre.p, (size_t)(n + 1) * 8));
-    DI_CK(cudaMalloc(&bnd.p, (size_t)(kMaxWorld + 1) * 8));
+    DI_CK(dmalloc(&od.p, (size_t)(n + 1) * 8));
+    DI_CK(dmalloc(&pre.p, (size_t)(n + 1) * 8));
+    DI_CK(dmalloc(&bnd.p, (size_t)(kMaxWorld + 1) * 8));
     DI_CK(cudaMemsetAsync(od.p, 0, (size_t)(n + 1) * 8, st));
     if (L > 0) k_outdeg<<<grid_for(L, sms), 256, 0, st>>>(s_dev, L, (int64_t *)od.p);
     size_t cb = 0;
     DI_CK(cub::DeviceScan::ExclusiveSum(nullptr, cb, (int64_t *)od.p, (int64_t *)pre.p, n + 1, st));
-    DI_CK(cudaMalloc(&ctmp.p, cb));
+    DI_CK(dmalloc(&ctmp.p, cb));
     DI_CK(cub::DeviceScan::ExclusiveSum(ctmp.p, cb, (int64_t *)od.p, (int64_t *)pre.p, n + 1, st));
     k_bounds<<<1, 32, 0, st>>>((const int64_t *)pre.p, n, world, (int64_t *)bnd.p);
     DI_CK(cudaMemcpyAsync(bd.b, bnd.p, (size_t)(world + 1) * 8, cudaMemcpyDeviceToHost, st));
@@ -270,13 +270,13 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   //      each owner range, so the hot push targets share L2 lines; ranges keep their extent
   if (reorder) {
     DevBuf kin, kout, vin;
-    DI_CK(cudaMalloc(&kin.p, (size_t)n * 8));
-    DI_CK(cudaMalloc(&kout.p, (size_t)n * 8));
-    DI_CK(cudaMalloc(&vin.p, (size_t)n * 4));
+    DI_CK(dmalloc(&kin.p, (size_t)n * 8));
+    DI_CK(dmalloc(&kout.p, (size_t)n * 8));
+    DI_CK(dmalloc(&vin.p, (size_t)n * 4));
     DevBuf sorted;
-    DI_CK(cudaMalloc(&sorted.p, (size_t)n * 4));
-    DI_CK(cudaMalloc(&g.old_of, (size_t)n * 4));
-    DI_CK(cudaMalloc(&g.new_of, (size_t)n * 4));
+    DI_CK(dmalloc(&sorted.p, (size_t)n * 4));
+    DI_CK(dmalloc(&g.old_of, (size_t)n * 4));
+    DI_CK(dmalloc(&g.new_of, (size_t)n * 4));
     int wb = 0;
     while ((1 << wb) < world) wb++;
     k_perm_keys64<<<grid_for(n, sms), 256, 0, st>>>(indeg, n, bd, (uint64_t *)kin.p,
@@ -286,17 +286,17 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
                                           (int32_t *)vin.p, (int32_t *)sorted.p, (int64_t)n, 0,
                                           32 + wb, st));
     DevBuf ptmp;
-    DI_CK(cudaMalloc(&ptmp.p, pb));
+    DI_CK(dmalloc(&ptmp.p, pb));
     DI_CK(cub::DeviceRadixSort::SortPairs(ptmp.p, pb, (uint64_t *)kin.p, (uint64_t *)kout.p,
                                           (int32_t *)vin.p, (int32_t *)sorted.p, (int64_t)n, 0,
                                           32 + wb, st));
     uint32_t top = 0;  // largest in-degree (DI_ASYNC decides on replicated hot accumulators)
     {
       DevBuf mx, mtmp;
-      DI_CK(cudaMalloc(&mx.p, 4));
+      DI_CK(dmalloc(&mx.p, 4));
       size_t mb = 0;
       DI_CK(cub::DeviceReduce::Max(nullptr, mb, indeg, (uint32_t *)mx.p, (int64_t)n, st));
-      DI_CK(cudaMalloc(&mtmp.p, mb));
+      DI_CK(dmalloc(&mtmp.p, mb));
       DI_CK(cub::DeviceReduce::Max(mtmp.p, mb, indeg, (uint32_t *)mx.p, (int64_t)n, st));
       DI_CK(cudaMemcpyAsync(&top, mx.p, 4, cudaMemcpyDeviceToHost, st));
       DI_CK(cudaStreamSynchronize(st));
@@ -318,15 +318,15 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   size_t tbytes = 0;
   if (L > 0) {
     DI_CK(cub::DeviceRadixSort::SortKeys(nullptr, tbytes, ka, kb, (int64_t)L, 0, 2 * b, st));
-    DI_CK(cudaMalloc(&tmp.p, tbytes));
+    DI_CK(dmalloc(&tmp.p, tbytes));
     DI_CK(cub::DeviceRadixSort::SortKeys(tmp.p, tbytes, ka, kb, (int64_t)L, 0, 2 * b, st));
   }
   // kb: sorted keys. Optional compaction.
   int64_t Lk = L;
   const int dedup = (flags & DI_DEDUP) ? 1 : 0, drop_self = (flags & DI_DROP_SELF_LOOPS) ? 1 : 0;
   if (L > 0 && (dedup || drop_self)) {
-    DI_CK(cudaMalloc(&keep.p, LL));
-    DI_CK(cudaMalloc(&nsel.p, 8));
+    DI_CK(dmalloc(&keep.p, LL));
+    DI_CK(dmalloc(&nsel.p, 8));
     k_keep_flags<<<grid_for(L, sms), 256, 0, st>>>(kb, L, b, dedup, drop_self, (uint8_t *)keep.p);
     size_t sb = 0;
     DI_CK(cub::DeviceSelect::Flagged(nullptr, sb, kb, (uint8_t *)keep.p, ka, (int64_t *)nsel.p,
@@ -334,7 +334,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     if (sb > tbytes) {
       tmp.~DevBuf();
       tmp.p = nullptr;
-      DI_CK(cudaMalloc(&tmp.p, sb));
+      DI_CK(dmalloc(&tmp.p, sb));
       tbytes = sb;
     }
     DI_CK(cub::DeviceSelect::Flagged(tmp.p, sb, kb, (uint8_t *)keep.p, ka, (int64_t *)nsel.p,
@@ -358,12 +358,12 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   const int64_t nl = g.n;
   g.l = Ll;
   const size_t LlS = (size_t)(Ll > 0 ? Ll : 1);
-  DI_CK(cudaMalloc(&g.row_ptr, ((size_t)nl + 1) * 8));
+  DI_CK(dmalloc(&g.row_ptr, ((size_t)nl + 1) * 8));
   // +8 elements of padding: the push reads whole aligned int4 groups around each row
-  DI_CK(cudaMalloc(&g.col, (LlS + 8) * 4));
+  DI_CK(dmalloc(&g.col, (LlS + 8) * 4));
   DI_CK(cudaMemsetAsync(g.col + LlS, 0, 8 * 4, st));
-  DI_CK(cudaMalloc(&g.deg, (size_t)nl * 4));
-  DI_CK(cudaMalloc(&g.kloop, (size_t)nl * 4));
+  DI_CK(dmalloc(&g.deg, (size_t)nl * 4));
+  DI_CK(dmalloc(&g.kloop, (size_t)nl * 4));
   DI_CK(cudaMemsetAsync(g.kloop, 0, (size_t)nl * 4, st));
   k_csr_from_sorted<<<grid_for(Ll + 1, sms), 256, 0, st>>>(kb + kbeg, Ll, nl, b, g.lo, g.row_ptr,
                                                           g.col, g.kloop);
@@ -381,14 +381,14 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
       if (sb > tbytes) {
         tmp.~DevBuf();
         tmp.p = nullptr;
-        DI_CK(cudaMalloc(&tmp.p, sb));
+        DI_CK(dmalloc(&tmp.p, sb));
         tbytes = sb;
       }
       DI_CK(cub::DeviceRadixSort::SortKeys(tmp.p, sb, ka, kb, (int64_t)Lk, 0, 2 * b, st));
     }
     const size_t LkS = (size_t)(Lk > 0 ? Lk : 1);
-    DI_CK(cudaMalloc(&g.csc_ptr, ((size_t)n + 1) * 8));
-    DI_CK(cudaMalloc(&g.csc_row, (LkS + 8) * 4));
+    DI_CK(dmalloc(&g.csc_ptr, ((size_t)n + 1) * 8));
+    DI_CK(dmalloc(&g.csc_row, (LkS + 8) * 4));
     DI_CK(cudaMemsetAsync(g.csc_row + LkS, 0, 8 * 4, st));
     k_csr_from_sorted<<<grid_for(Lk + 1, sms), 256, 0, st>>>(kb, Lk, n, b, 0, g.csc_ptr,
                                                             g.csc_row, nullptr);
