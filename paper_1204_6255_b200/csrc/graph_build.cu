@@ -7,6 +7,11 @@
 // Everything is integer work and bit-exact (tests/test_gpu_build.py compares byte for byte
 // with a numpy lexsort). The radix sort is CUB's (a library sort, like cuBLAS for a plain
 // GEMM); every other step is a kernel below.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
 #include <cub/cub.cuh>
 
 #include "di_common.cuh"
@@ -163,6 +168,17 @@ __global__ void k_swap_keys(const uint64_t *__restrict__ in, int64_t L, int b,
   }
 }
 
+// DI_BUILD_TRACE=1: host timestamps of the build phases on stderr (diagnostics)
+void btrace(const char *what) {
+  static const bool on = getenv("DI_BUILD_TRACE") && atoi(getenv("DI_BUILD_TRACE"));
+  if (!on) return;
+  static thread_local std::chrono::steady_clock::time_point t0;
+  const auto now = std::chrono::steady_clock::now();
+  if (std::string(what) == "start") t0 = now;
+  fprintf(stderr, "[di build] %-8s %8.2f ms\n", what,
+          std::chrono::duration<double, std::milli>(now - t0).count());
+}
+
 int grid_for(int64_t n, int sms) {
   int64_t g = (n + 255) / 256;
   int64_t cap = (int64_t)sms * 16;
@@ -189,6 +205,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   while ((1ll << b) < n) b++;
   const int sms = g.num_sms;
 
+  btrace("start");
   DevBuf dsrc, ddst, keys_a, keys_b, keep, tmp, nsel, badb;
   const int32_t *s_dev = src, *d_dev = dst;
   if (flags & DI_HOST_PTRS) {
@@ -222,6 +239,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   unsigned long long bad = 0;
   DI_CK(cudaMemcpyAsync(&bad, badb.p, 8, cudaMemcpyDeviceToHost, st));
   DI_CK(cudaStreamSynchronize(st));
+  btrace("sync1");
   if (bad != ~0ull) {
     int32_t sv = 0, dv = 0;
     if (flags & DI_HOST_PTRS) {
@@ -256,6 +274,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     k_bounds<<<1, 32, 0, st>>>((const int64_t *)pre.p, n, world, (int64_t *)bnd.p);
     DI_CK(cudaMemcpyAsync(bd.b, bnd.p, (size_t)(world + 1) * 8, cudaMemcpyDeviceToHost, st));
     DI_CK(cudaStreamSynchronize(st));
+    btrace("sync2");
     // every range non-empty (n >= world is checked by the caller)
     for (int q = 1; q < world; q++) {
       if (bd.b[q] < bd.b[q - 1] + 1) bd.b[q] = bd.b[q - 1] + 1;
@@ -300,6 +319,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
       DI_CK(cub::DeviceReduce::Max(mtmp.p, mb, indeg, (uint32_t *)mx.p, (int64_t)n, st));
       DI_CK(cudaMemcpyAsync(&top, mx.p, 4, cudaMemcpyDeviceToHost, st));
       DI_CK(cudaStreamSynchronize(st));
+      btrace("sync3");
     }
     g.max_indeg = top;
     const int64_t P = std::max<int64_t>(1, (int64_t)g.stripes);
@@ -309,6 +329,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   }
   if (L > 0) k_make_keys<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, b, g.new_of, ka);
   DI_CK(cudaStreamSynchronize(st));
+  btrace("sync4");
   dsrc.~DevBuf();
   dsrc.p = nullptr;
   ddst.~DevBuf();
@@ -341,6 +362,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
                                      (int64_t)L, st));
     DI_CK(cudaMemcpyAsync(&Lk, nsel.p, 8, cudaMemcpyDeviceToHost, st));
     DI_CK(cudaStreamSynchronize(st));
+    btrace("sync5");
     std::swap(ka, kb);  // kb = compacted sorted keys
   }
   g.l_global = Lk;
@@ -351,6 +373,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     k_key_bound<<<1, 32, 0, st>>>(kb, Lk, b, g.lo, g.hi, (int64_t *)badb.p);
     DI_CK(cudaMemcpyAsync(hb, badb.p, 16, cudaMemcpyDeviceToHost, st));
     DI_CK(cudaStreamSynchronize(st));
+    btrace("sync6");
     kbeg = hb[0];
     kend = hb[1];
   }
@@ -395,6 +418,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     g.has_csc = true;
   }
   DI_CK(cudaStreamSynchronize(st));
+  btrace("sync7");
   DI_CK(cudaGetLastError());
   g.has_loops = hl != 0;
   return DI_OK;
