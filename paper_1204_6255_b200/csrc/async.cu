@@ -9,8 +9,9 @@
 //     its fluid is TAKEN with an atomic exchange F_i <- 0, so fluid that other CTAs push into
 //     F_i concurrently is never lost: it is either in the exchanged value or stays in F_i for
 //     the next visit (any diffusion order keeps F = B + P.H - H);
-//   - the CTA pushes the tile's rows immediately: rows of <= 32 links by the selecting thread,
-//     longer rows as 1024-link chunks claimed by the CTA's warps from a shared-memory list.
+//   - the CTA pushes the tile's rows immediately: rows of <= 8 links by the selecting thread,
+//     rows of 9-128 links by 8-lane groups, longer rows as 1024-link chunks, claimed by the CTA's
+//     warps from one shared-memory row list (mid rows from its front, long rows from its back).
 // The order of diffusions is the dynamic order of the tiles, so iterates are not reproducible
 // bit for bit (like every fp64-atomic push); the fixed point and the tolerance are those of the
 // paper's method. The last CTA reduces the per-CTA sums, applies r_{c+1} = r_c - taken + pushed,
@@ -21,7 +22,8 @@ namespace di {
 namespace {
 
 constexpr int kAsyncThreads = 256;
-constexpr int kAsyncSmall = 32;     // rows with <= this many links: pushed by the selecting thread
+constexpr int kAsyncSmall = 16;      // rows with <= this many links: pushed by the selecting thread
+constexpr int kAsyncMid = 256;      // rows up to this: one 8-lane group each (list front)
 constexpr int kAsyncChunk = 1024;   // longer rows: chunks of this many links, one warp each
 
 // Replicated accumulators for the hottest targets. Same-address fp64 REDs serialise in one L2
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
   __shared__ double s_rv[kSelTile];    // v = T d / o
   __shared__ int32_t s_ri[kSelTile];   // local node id
   __shared__ int32_t s_rp[kSelTile + 1];  // exclusive chunk prefix
-  __shared__ int s_nrows, s_nchunks, s_claim;
+  __shared__ int s_nrows, s_nmid, s_nchunks, s_claim, s_mclaim;
   __shared__ int64_t s_tile;
   __shared__ bool s_last;
   __shared__ double s_red[NW][4];
@@ -95,7 +97,9 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
     if (threadIdx.x == 0) {
       s_tile = (int64_t)atomicAdd(&sc->tile_next, 1u);
       s_nrows = 0;
+      s_nmid = 0;
       s_claim = 0;
+      s_mclaim = 0;
     }
     __syncthreads();
     const int64_t tile = s_tile;
@@ -147,8 +151,8 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
       if (o <= kAsyncSmall) {
         so[j] = o;
         sv[j] = v;
-      } else {
-        const int p = atomicAdd(&s_nrows, 1);
+      } else {  // mid rows at the front of the list, long rows at its back
+        const int p = (o <= kAsyncMid) ? atomicAdd(&s_nmid, 1) : kSelTile - 1 - atomicAdd(&s_nrows, 1);
         s_rb[p] = rb[j];
         s_ro[p] = o;
         s_rv[p] = v;
@@ -177,14 +181,15 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
       }
     }
     __syncthreads();
-    // ---- long rows: chunk prefix (warp 0), then the CTA's warps claim chunks
+    // ---- long rows (list back: row k at kSelTile-1-k): chunk prefix (warp 0), then the CTA's
+    //      warps claim chunks; then mid rows (list front), four per warp step
     const int nrows = s_nrows;
     if (nrows > 0) {
       if (warp == 0) {
         const int per = (nrows + 31) / 32;
         const int r0 = lane * per, r1 = min(nrows, r0 + per);
         int sum = 0;
-        for (int k = r0; k < r1; k++) sum += (s_ro[k] + kAsyncChunk - 1) / kAsyncChunk;
+        for (int k = r0; k < r1; k++) sum += (s_ro[kSelTile - 1 - k] + kAsyncChunk - 1) / kAsyncChunk;
         int incl = sum;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
         int run = incl - sum;
         for (int k = r0; k < r1; k++) {
           s_rp[k] = run;
-          run += (s_ro[k] + kAsyncChunk - 1) / kAsyncChunk;
+          run += (s_ro[kSelTile - 1 - k] + kAsyncChunk - 1) / kAsyncChunk;
         }
         if (lane == 31) {
           s_nchunks = incl;
@@ -213,11 +218,12 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
           const int mid = (lo + hi + 1) >> 1;
           if (s_rp[mid] <= c) lo = mid; else hi = mid - 1;
         }
-        const int64_t rbeg = s_rb[lo];
+        const int slot = kSelTile - 1 - lo;
+        const int64_t rbeg = s_rb[slot];
         const int64_t beg = rbeg + (int64_t)(c - s_rp[lo]) * kAsyncChunk;
-        const int64_t end = min(rbeg + (int64_t)s_ro[lo], beg + kAsyncChunk);
-        const double v = s_rv[lo];
-        const int32_t gi = LOOPS ? (int32_t)(tile * kSelTile + s_ri[lo] + a.lo) : -1;
+        const int64_t end = min(rbeg + (int64_t)s_ro[slot], beg + kAsyncChunk);
+        const double v = s_rv[slot];
+        const int32_t gi = LOOPS ? (int32_t)(tile * kSelTile + s_ri[slot] + a.lo) : -1;
         const int64_t a0 = beg & ~3ll;
         const int nvec = (int)((end - a0 + 3) >> 2);
         for (int vb = 0; vb < nvec; vb += 128) {
@@ -234,6 +240,33 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
             if (vi < nvec)
               red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x[k], a0 + 4 * (int64_t)vi, beg,
                                    end, gi, v, fpol);
+          }
+        }
+      }
+    }
+    const int nmid = s_nmid;
+    if (nmid > 0) {
+      const int sub = lane & 7;
+      for (;;) {
+        int q = 0;
+        if (lane == 0) q = atomicAdd(&s_mclaim, 4);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (q >= nmid) break;
+        const int k = q + (lane >> 3);
+        if (k < nmid) {
+          const int64_t beg = s_rb[k], end = beg + s_ro[k], a0 = beg & ~3ll;
+          const int nvec = (int)((end - a0 + 3) >> 2);   // <= 33
+          const double v = s_rv[k];
+          const int32_t gi = LOOPS ? (int32_t)(tile * kSelTile + s_ri[k] + a.lo) : -1;
+          for (int vb = sub; vb < nvec; vb += 16) {
+            const int4 x0 = ld_col4(col + a0 + 4 * (int64_t)vb, pol);
+            int4 x1 = make_int4(0, 0, 0, 0);
+            if (vb + 8 < nvec) x1 = ld_col4(col + a0 + 4 * (int64_t)(vb + 8), pol);
+            red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x0, a0 + 4 * (int64_t)vb, beg, end,
+                                 gi, v, fpol);
+            if (vb + 8 < nvec)
+              red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x1, a0 + 4 * (int64_t)(vb + 8),
+                                   beg, end, gi, v, fpol);
           }
         }
       }
