@@ -63,7 +63,7 @@ __device__ __forceinline__ double take_fluid(double *p) {
 }
 
 template <bool LOOPS>
-__global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
+__global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a) {
   constexpr int NW = kAsyncThreads / 32;
   __shared__ int64_t s_rb[kSelTile];   // long rows of the tile: first link
   __shared__ int32_t s_ro[kSelTile];   // #links
@@ -109,15 +109,27 @@ __global__ void __launch_bounds__(kAsyncThreads, 3) k_cycle(const SweepArgs a) {
     double f[kSelItems];
     int64_t rb[kSelItems + 1];
     int kl[kSelItems];
+    if (base + kSelItems <= a.n) {  // vectorised: 2 x double2 (F, L2 only: REDs land there) and
+                                    // 2 x longlong2 (row extents) + the next row's start
+      const double2 f01 = __ldcg(reinterpret_cast<const double2 *>(F + base));
+      const double2 f23 = __ldcg(reinterpret_cast<const double2 *>(F + base) + 1);
+      const longlong2 r01 = reinterpret_cast<const longlong2 *>(a.row_ptr + base)[0];
+      const longlong2 r23 = reinterpret_cast<const longlong2 *>(a.row_ptr + base)[1];
+      f[0] = f01.x; f[1] = f01.y; f[2] = f23.x; f[3] = f23.y;
+      rb[0] = r01.x; rb[1] = r01.y; rb[2] = r23.x; rb[3] = r23.y;
+      rb[kSelItems] = a.row_ptr[base + kSelItems];
 #pragma unroll
-    for (int j = 0; j < kSelItems; j++) {
-      const int64_t i = base + j;
-      f[j] = (i < a.n) ? __ldcg(F + i) : 0.0;
-      rb[j] = (i < a.n) ? a.row_ptr[i] : 0;
-      kl[j] = (LOOPS && i < a.n) ? a.kloop[i] : 0;
+      for (int j = 0; j < kSelItems; j++) kl[j] = LOOPS ? a.kloop[base + j] : 0;
+    } else {
+#pragma unroll
+      for (int j = 0; j < kSelItems; j++) {
+        const int64_t i = base + j;
+        f[j] = (i < a.n) ? __ldcg(F + i) : 0.0;
+        rb[j] = (i < a.n) ? a.row_ptr[i] : 0;
+        kl[j] = (LOOPS && i < a.n) ? a.kloop[i] : 0;
+      }
+      rb[kSelItems] = base < a.n ? a.row_ptr[a.n] : 0;
     }
-    rb[kSelItems] = (base + kSelItems <= a.n) ? a.row_ptr[base + kSelItems]
-                                              : (base < a.n ? a.row_ptr[a.n] : 0);
     double sv[kSelItems];
     int so[kSelItems];
 #pragma unroll
