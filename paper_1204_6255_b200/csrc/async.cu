@@ -368,10 +368,10 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a) {
 // shift of a power-of-two stripe length when the replicated hot accumulators apply, else -1
 static int hot_shift_of(const Graph &g) {
   const bool skewed = g.l_global > 0 && (double)g.max_indeg > kReplShare * (double)g.l_global;
-  if (!(g.reordered && g.hot_acc && skewed && g.world == 1 && g.stripes >= kRepl &&
-        g.n % g.stripes == 0))
+  if (!(g.reordered && g.hot_acc && skewed && g.world == 1 && g.stripes_eff >= kRepl &&
+        g.n % g.stripes_eff == 0))
     return -1;
-  const int64_t M = g.n / g.stripes;
+  const int64_t M = g.n / g.stripes_eff;
   int sh = 0;
   while ((1ll << sh) < M) sh++;
   return ((1ll << sh) == M && sh < 31) ? sh : -1;

@@ -123,7 +123,9 @@ struct Graph {
   int rank = 0, world = 1;
   // locality relabelling: internal id = new_of[user id]; user id = old_of[internal id]
   bool reordered = false;
-  int stripes = 4096;        // relabelling stripes (DI_STRIPES; 1 = plain degree order)
+  int stripes = 0;           // relabelling stripes (DI_STRIPES; 0 = auto: stripes of ~1024 nodes,
+                             // 1 = plain degree order)
+  int64_t stripes_eff = 1;   // the stripe count used for this rank's range
   int hot_acc = 1;           // DI_ASYNC: replicated accumulators for the hottest targets (DI_HOT_ACC)
   double *rep = nullptr;
   int64_t max_indeg = 0;     // largest in-degree (set by the relabelling pass)

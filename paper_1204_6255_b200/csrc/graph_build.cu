@@ -45,7 +45,9 @@ __global__ void k_place(const int32_t *__restrict__ sorted_old, int64_t n, DistB
     int g = 0;
     while (g + 1 < bd.world && r >= bd.b[g + 1]) g++;
     const int64_t lo = bd.b[g], m = bd.b[g + 1] - lo, rr = r - lo;
-    const int64_t P = stripes < m ? stripes : m;
+    int64_t P = stripes > 0 ? stripes : (m >> 10);  // 0: stripes of ~1024 nodes
+    if (P < 1) P = 1;
+    if (P > m) P = m;
     const int64_t M = m / P, rem = m % P;
     const int64_t s = rr % P, idx = rr / P;
     const int64_t k = lo + s * M + (s < rem ? s : rem) + idx;
@@ -322,7 +324,9 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
       btrace("sync3");
     }
     g.max_indeg = top;
-    const int64_t P = std::max<int64_t>(1, (int64_t)g.stripes);
+    const int64_t P = g.stripes > 0 ? (int64_t)g.stripes : 0;   // 0 = auto (per range)
+    g.stripes_eff = g.stripes > 0 ? std::min<int64_t>(g.stripes, g.n)
+                                  : std::max<int64_t>(1, g.n >> 10);
     k_place<<<grid_for(n, sms), 256, 0, st>>>((const int32_t *)sorted.p, n, bd, P, g.new_of,
                                                g.old_of);
     g.reordered = true;

@@ -65,7 +65,7 @@ def test_reorder_relabelling(name):
     old_of = g.test_perm()
     indeg = np.bincount(dst, minlength=n)
     ranked = np.argsort(-indeg, kind="stable")           # rank r -> caller id
-    P = min(4096, n)                                     # stripes: rank r -> stripe r % P, slot r // P
+    P = max(1, n >> 10)          # auto stripes of ~1024 nodes: rank r -> stripe r % P, slot r // P
     r = np.arange(n)
     M, rem = n // P, n % P
     s_ = r % P
