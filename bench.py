@@ -239,18 +239,24 @@ def run_ours(args):
     e2e_ms, e2e_links = [], 0
     g.free()
     torch.cuda.empty_cache()
-    E2E_WARM = 2                                         # pool growth on the first host-pointer builds
+    E2E_WARM = 3                                         # pool growth on the first host-pointer builds
     for k in range(args.e2e_steps + E2E_WARM):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         gh = di.Graph(src_p, dst_p, n, stream=stream, **part)  # DI_HOST_PTRS: H2D inside
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
         st = gh.solve(d=D, tol=TOL, variant=args.variant, mode=args.mode, blocks=args.blocks,
                       asynchronous=use_async,
                       graph_loop=use_graph)
+        t2 = time.perf_counter()
         H = gh.history()
         H_host.copy_(H, non_blocking=True)
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) * 1e3
+        print(f"[bench] e2e step {k}: upload {(t1 - t0) * 1e3:.1f} ms, solve {(t2 - t1) * 1e3:.1f} ms "
+              f"(device {st['solve_ms']:.1f}), H to host {(time.perf_counter() - t2) * 1e3:.1f} ms",
+              file=sys.stderr, flush=True)
         gh.free()
         del H
         if k >= E2E_WARM:

@@ -3,6 +3,8 @@
 // back in between; the device finaliser decides convergence and later
 // kernels no-op, so the host only synchronises once per batch.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -36,9 +38,14 @@ cudaError_t dmalloc_bytes(void **p, size_t bytes) {
     }
     prepared = dev;
   }
+  static const bool trace = getenv("DI_BUILD_TRACE") && atoi(getenv("DI_BUILD_TRACE"));
+  const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 1, alloc_stream());
   // the buffer is then usable on any stream (some host paths touch it with synchronous copies)
   if (e == cudaSuccess) e = cudaStreamSynchronize(alloc_stream());
+  if (trace && bytes >= (64u << 20))
+    fprintf(stderr, "[di alloc] %8.1f MB %8.2f ms\n", bytes / 1e6,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   return e;
 }
 
