@@ -129,7 +129,8 @@ def run_ours(args):
         from paper_1204_6255_b200.dist import nccl_rendezvous
         _, _, nid = nccl_rendezvous()
         args.mode = "push"                   # the partitioned sweep is push-only
-        args.sched = "bulk"                  # ... and bulk (block / async order are single-GPU)
+        if args.sched == "block":            # block order is single-GPU; async and bulk shard
+            args.sched = "bulk"
     import paper_1204_6255_b200 as di
     if args.mode != "push":
         args.sched = "bulk"

@@ -77,7 +77,9 @@ typedef enum {
                                   of nodes in increasing order, selects against the cycle's r with
                                   the live F (fluid taken by atomic exchange) and pushes at once:
                                   the paper's cyclic order up to the concurrency of the
-                                  grid; push only, single GPU; iterates not bit-reproducible    */
+                                  grid; push only; on a partitioned graph every rank runs its
+                                  range's cycle and the remote fluid is exchanged once per cycle;
+                                  iterates not bit-reproducible                                 */
 /* Block-ordered cycles (F1): each cycle visits K ordered blocks of
  * internal node ids; block b is selected against the cycle's threshold r (computed once per
  * cycle) with the live F, i.e. including the fluid pushed by blocks 0..b-1 this
@@ -169,7 +171,7 @@ di_status di_graph_links(di_graph g, int64_t *n_links);
  *       for those tol bounds the scheme's own error estimate, P:176-180 / P:237-245, and
  *       di_history returns their x: normalised for PI, raw for GS).
  *  st : host pointer, filled on return (may be NULL).
- * Partitioned graph: collective; DI_SOP / DI_CYC with push sweeps only; B is this rank's slice
+ * Partitioned graph: collective; DI_SOP / DI_CYC with bulk push sweeps or DI_ASYNC cycles; B is this rank's slice
  * [lo, hi) in the caller's numbering; the stats are global (identical on every rank).
  * Returns DI_OK, DI_NOT_CONVERGED (state kept; DI_RESUME continues), or an error. */
 di_status di_solve(di_graph g, double d, const double *B, double tol, di_variant v,

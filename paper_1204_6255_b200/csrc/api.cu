@@ -367,7 +367,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     if (v != DI_SOP && v != DI_CYC)
       return fail(DI_EINVAL, "di_solve: a partitioned graph runs DI_SOP / DI_CYC only");
     if ((flags & (DI_PULL | DI_AUTO | DI_GRAPH_LOOP)) || ((flags >> 16) & 0xFFu) > 1)
-      return fail(DI_EINVAL, "di_solve: a partitioned graph runs plain push sweeps only");
+      return fail(DI_EINVAL, "di_solve: a partitioned graph runs push sweeps (bulk or DI_ASYNC)");
     if ((flags & DI_RESUME) && !g.solved) return fail(DI_ESTATE, "di_solve: DI_RESUME before any solve");
     const double *Bint = B;
     if (B && g.reordered) {  // caller's slice [lo, hi) in the caller's numbering

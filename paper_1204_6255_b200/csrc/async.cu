@@ -57,13 +57,38 @@ __device__ __forceinline__ void red_group_rep(double *__restrict__ F, double *__
   }
 }
 
+// DIST: targets are global internal ids; a target outside this rank's range goes through the
+// remote accumulator and first-touch lists (push_remote, sweep.cuh).
+template <bool LOOPS, bool DIST>
+__device__ __forceinline__ void push_group(const SweepArgs &a, const DistArgs &x, double *rep,
+                                           int hot_shift, int32_t hot_lim, int copy, int4 q,
+                                           int64_t p0, int64_t beg, int64_t end, int32_t gi,
+                                           double v, uint64_t fpol) {
+  if (!DIST) {
+    red_group_rep<LOOPS>(a.F, rep, hot_shift, hot_lim, copy, q, p0, beg, end, gi, v, fpol);
+    return;
+  }
+  const int32_t jj[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    const int64_t p = p0 + c;
+    if (p >= beg && p < end && (!LOOPS || jj[c] != gi)) {
+      const int64_t jl = (int64_t)jj[c] - a.lo;
+      if (jl >= 0 && jl < a.n)
+        red_add_f64_hint(a.F + jl, v, fpol);
+      else
+        push_remote(x, jj[c], v);
+    }
+  }
+}
+
 __device__ __forceinline__ double take_fluid(double *p) {
   return __longlong_as_double(
       (long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
 }
 
-template <bool LOOPS>
-__global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a) {
+template <bool LOOPS, bool DIST>
+__global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, const DistArgs x) {
   constexpr int NW = kAsyncThreads / 32;
   __shared__ int64_t s_rb[kSelTile];   // long rows of the tile: first link
   __shared__ int32_t s_ro[kSelTile];   // #links
@@ -183,12 +208,12 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a) {
         int4 x1 = make_int4(0, 0, 0, 0), x2 = make_int4(0, 0, 0, 0);
         if (q + 1 < nvec) x1 = ld_col4(col + a0 + 4 * (q + 1), pol);
         if (q + 2 < nvec) x2 = ld_col4(col + a0 + 4 * (q + 2), pol);
-        red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x0, a0 + 4 * q, beg, end, gi, sv[j], fpol);
+        push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, x0, a0 + 4 * q, beg, end, gi, sv[j], fpol);
         if (q + 1 < nvec)
-          red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x1, a0 + 4 * (q + 1), beg, end, gi,
+          push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, x1, a0 + 4 * (q + 1), beg, end, gi,
                                sv[j], fpol);
         if (q + 2 < nvec)
-          red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x2, a0 + 4 * (q + 2), beg, end, gi,
+          push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, x2, a0 + 4 * (q + 2), beg, end, gi,
                                sv[j], fpol);
       }
     }
@@ -239,19 +264,19 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a) {
         const int64_t a0 = beg & ~3ll;
         const int nvec = (int)((end - a0 + 3) >> 2);
         for (int vb = 0; vb < nvec; vb += 128) {
-          int4 x[4];
+          int4 xq[4];
 #pragma unroll
           for (int k = 0; k < 4; k++) {
             const int vi = vb + 32 * k + lane;
-            x[k] = make_int4(0, 0, 0, 0);
-            if (vi < nvec) x[k] = ld_col4(col + a0 + 4 * (int64_t)vi, pol);
+            xq[k] = make_int4(0, 0, 0, 0);
+            if (vi < nvec) xq[k] = ld_col4(col + a0 + 4 * (int64_t)vi, pol);
           }
 #pragma unroll
           for (int k = 0; k < 4; k++) {
             const int vi = vb + 32 * k + lane;
             if (vi < nvec)
-              red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x[k], a0 + 4 * (int64_t)vi, beg,
-                                   end, gi, v, fpol);
+              push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, xq[k], a0 + 4 * (int64_t)vi,
+                                      beg, end, gi, v, fpol);
           }
         }
       }
@@ -274,10 +299,10 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a) {
             const int4 x0 = ld_col4(col + a0 + 4 * (int64_t)vb, pol);
             int4 x1 = make_int4(0, 0, 0, 0);
             if (vb + 8 < nvec) x1 = ld_col4(col + a0 + 4 * (int64_t)(vb + 8), pol);
-            red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x0, a0 + 4 * (int64_t)vb, beg, end,
+            push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, x0, a0 + 4 * (int64_t)vb, beg, end,
                                  gi, v, fpol);
             if (vb + 8 < nvec)
-              red_group_rep<LOOPS>(F, rep, hot_shift, hot_lim, copy, x1, a0 + 4 * (int64_t)(vb + 8),
+              push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, x1, a0 + 4 * (int64_t)(vb + 8),
                                    beg, end, gi, v, fpol);
           }
         }
@@ -330,35 +355,55 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a) {
       if (acc != 0.0) F[(int64_t)k << hot_shift] += acc;
     }
   }
-  const SweepSums x = reduce_partials(a, gridDim.x, kAsyncThreads);
+  const SweepSums sm = reduce_partials(a, gridDim.x, kAsyncThreads);
+  if (DIST) {  // this rank's sums and per-peer counts; the host exchanges, k_dist_finalize applies
+    if (threadIdx.x < x.bd.world) {
+      volatile unsigned long long *cnt = x.tcnt + 32 * threadIdx.x;
+      x.sendcnt[threadIdx.x] = (int64_t)*cnt;
+      *cnt = 0ull;
+    }
+    if (threadIdx.x == 0) {
+      x.dsum[0] = 0.0;
+      x.dsum[1] = sm.s;
+      x.dsum[2] = sm.e;
+      x.dsum[3] = sm.taken;
+      x.isum[0] = sm.sel;
+      x.isum[1] = sm.nd;
+      x.isum[2] = sm.lk;
+      x.isum[3] = a.n;
+      sc->tile_next = 0;
+      sc->ticket = 0;
+    }
+    return;
+  }
   if (threadIdx.x != 0) return;
   // ---- the cycle's effect (P:278-283 stop test, G5 guard)
   volatile Scalars *vs = a.sc;
   const int variant = vs->variant;
-  const double r_next = __dadd_rn(__dsub_rn(r, x.taken), x.s);
-  const double e_tot = vs->e + x.e;
+  const double r_next = __dadd_rn(__dsub_rn(r, sm.taken), sm.s);
+  const double e_tot = vs->e + sm.e;
   const int64_t sw = vs->sweeps;
   if (vs->trace && sw < kLogCap) {
     a.log_r[sw] = r;
-    a.log_sel[sw] = x.sel;
-    a.log_links[sw] = x.lk;
+    a.log_sel[sw] = sm.sel;
+    a.log_links[sw] = sm.lk;
     a.log_mode[sw] = 0;
   }
   if (vs->guard && variant != DI_CYC) vs->guards = vs->guards + 1;
   vs->e = e_tot;
-  vs->e_sw = x.e;
-  vs->s = x.s;
-  vs->q = __dsub_rn(r, x.taken);
+  vs->e_sw = sm.e;
+  vs->s = sm.s;
+  vs->q = __dsub_rn(r, sm.taken);
   vs->r = r_next;
   vs->sweeps = sw + 1;
-  vs->selected_total = vs->selected_total + x.sel;
-  vs->selected_nd_total = vs->selected_nd_total + x.nd;
-  vs->links_total = vs->links_total + x.lk;
+  vs->selected_total = vs->selected_total + sm.sel;
+  vs->selected_nd_total = vs->selected_nd_total + sm.nd;
+  vs->links_total = vs->links_total + sm.lk;
   vs->scanned_total = vs->scanned_total + a.n;
   const double err = vs->paper_err ? r_next / (1.0 - d - d * e_tot) : r_next;
   const int stop = err <= vs->tol;
   vs->stop = stop;
-  vs->guard = (x.sel == 0 && !stop && variant == DI_SOP) ? 1 : 0;
+  vs->guard = (sm.sel == 0 && !stop && variant == DI_SOP) ? 1 : 0;
   vs->tile_next = 0;
   vs->ticket = 0;
 }
@@ -388,18 +433,28 @@ di_status prepare_cycle(Graph &g) {
 
 void launch_cycle(Graph &g, int64_t *launches) {
   SweepArgs a = sweep_args(g, 0);
+  const bool dist = g.world > 1;
+  DistArgs x{};
+  if (dist) x = dist_args(g);
   a.hot_shift = g.rep ? hot_shift_of(g) : -1;
   a.rep = g.rep;
   static int occ = 0;
   if (occ == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cycle<false>, kAsyncThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cycle<false, false>, kAsyncThreads, 0);
     if (occ < 1) occ = 1;
   }
   const int grid = std::min(g.num_sms * occ, kMaxSlices);
-  if (g.has_loops)
-    k_cycle<true><<<grid, kAsyncThreads, 0, g.stream>>>(a);
-  else
-    k_cycle<false><<<grid, kAsyncThreads, 0, g.stream>>>(a);
+  if (dist) {
+    if (g.has_loops)
+      k_cycle<true, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+    else
+      k_cycle<false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+  } else {
+    if (g.has_loops)
+      k_cycle<true, false><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+    else
+      k_cycle<false, false><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+  }
   *launches += 1;
 }
 

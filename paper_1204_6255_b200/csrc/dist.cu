@@ -33,17 +33,6 @@
 namespace di {
 namespace {
 
-struct DistArgs {
-  double *R;
-  int32_t *tl;
-  double *sval;
-  unsigned long long *tcnt;  // [world * 32]: touched count per owner, one line each
-  int64_t *sendcnt;          // [world]
-  double *dsum;              // q, s, e
-  int64_t *isum;             // sel, nd, lk, scanned
-  DistBounds bd;
-  int rank;
-};
 
 __device__ __forceinline__ int owner_of(const DistBounds &bd, int64_t j) {
   int p = 0;
@@ -194,6 +183,7 @@ __global__ void __launch_bounds__(kPushThreads) k_push_dist(const SweepArgs a, c
     x.dsum[0] = s.q;
     x.dsum[1] = s.s;
     x.dsum[2] = s.e;
+    x.dsum[3] = 0.0;
     x.isum[0] = s.sel;
     x.isum[1] = s.nd;
     x.isum[2] = s.lk;
@@ -230,9 +220,13 @@ __global__ void k_apply_recv(double *__restrict__ F, int64_t lo, const int32_t *
 }
 
 // the single-GPU finaliser on the allreduced sums
-__global__ void k_dist_finalize(const SweepArgs a, const double *dsum, const int64_t *isum) {
+__global__ void k_dist_finalize(const SweepArgs a, const double *dsum, const int64_t *isum,
+                                int async) {
   if (threadIdx.x != 0 || a.sc->stop) return;
-  SweepSums s{dsum[0], dsum[1], dsum[2], 0.0, isum[0], isum[1], isum[2], isum[3]};
+  // the asynchronous cycle reports the fluid it took from F (dsum[3]) instead of the fluid it
+  // left: r_{c+1} = r_c - taken + pushed, i.e. q = r_c - taken for apply_sweep's q + s
+  const double q = async ? __dsub_rn(a.sc->r, dsum[3]) : dsum[0];
+  SweepSums s{q, dsum[1], dsum[2], 0.0, isum[0], isum[1], isum[2], isum[3]};
   apply_sweep(a, s);
 }
 
@@ -247,19 +241,6 @@ int grid_of(int64_t n, int sms) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
 }
 
-DistArgs dist_args(Graph &g) {
-  DistArgs x;
-  x.R = g.R;
-  x.tl = g.tl;
-  x.sval = g.sval;
-  x.tcnt = g.tcnt;
-  x.sendcnt = g.sendcnt;
-  x.dsum = g.dsum;
-  x.isum = g.isum;
-  x.bd = g.bounds;
-  x.rank = g.rank;
-  return x;
-}
 
 // global sum F (exact local tree sum, then the allreduce); set_r: also r = that sum
 di_status global_sum_F(Graph &g, int set_r, int64_t *launches) {
@@ -316,6 +297,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
                      int64_t max_sweeps, uint32_t flags, di_stats *st) {
   const int G = g.world, me = g.rank;
   const bool resume = flags & DI_RESUME;
+  const bool async = flags & DI_ASYNC;
   const int paper = (flags & DI_PAPER_ERROR) ? 1 : 0;
   int64_t launches = 0;
   cudaEvent_t t0, t1;
@@ -376,9 +358,11 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   while (!converged && launched < max_sweeps) {
     while (launched < max_sweeps) {
       if (prof) DI_CK(cudaEventRecord(pe[0], g.stream));
-      launch_select(g, 0, &launches);
+      if (!async) launch_select(g, 0, &launches);
       if (prof) DI_CK(cudaEventRecord(pe[1], g.stream));
-      if (g.has_loops)
+      if (async)
+        launch_cycle(g, &launches);   // the asynchronous cycle on this rank's range (R7)
+      else if (g.has_loops)
         k_push_dist<true><<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a, x);
       else
         k_push_dist<false><<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a, x);
@@ -386,7 +370,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       k_pack<<<g.num_sms * 4, 256, 0, g.stream>>>(g.sc, x);
       launches += 2;
       launched++;
-      if ((s = g.comm->allreduce_f64(g.dsum, 3, g.stream)) != DI_OK) return s;
+      if ((s = g.comm->allreduce_f64(g.dsum, 4, g.stream)) != DI_OK) return s;
       if ((s = g.comm->allreduce_i64(g.isum, 4, g.stream)) != DI_OK) return s;
       if ((s = g.comm->exchange(cb_s.data(), c8.data(), cb_r.data(), c8.data(), g.stream)) != DI_OK)
         return s;
@@ -430,7 +414,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
         k_apply_recv<<<grid_of(off, g.num_sms), 256, 0, g.stream>>>(g.F, g.lo, g.rid, g.rval, off);
         launches++;
       }
-      k_dist_finalize<<<1, 32, 0, g.stream>>>(a, g.dsum, g.isum);
+      k_dist_finalize<<<1, 32, 0, g.stream>>>(a, g.dsum, g.isum, async ? 1 : 0);
       launches++;
       if (prof) {  // exchange of the lists + apply (the counts exchange is in the sync above)
         DI_CK(cudaEventRecord(pe[0], g.stream));

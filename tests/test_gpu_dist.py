@@ -61,9 +61,11 @@ def same_stats(sts):
         assert len({s[k] for s in sts}) == 1, (k, [s[k] for s in sts])
 
 
+@pytest.mark.parametrize("asynchronous", [False, True])
 @pytest.mark.parametrize("G", [2, 3, 4])
-def test_pins_partitioned(G):
-    """T1 on partitions: the exact rationals of tests/golden/pins.txt (graphs with >= G nodes)."""
+def test_pins_partitioned(G, asynchronous):
+    """T1 on partitions: the exact rationals of tests/golden/pins.txt (graphs with >= G nodes),
+    bulk sweeps and asynchronous cycles (R7 on every rank, one exchange per cycle)."""
     need_gpu()
     for name, n, links, X in load_pins():
         if n < G:
@@ -71,14 +73,16 @@ def test_pins_partitioned(G):
         src = np.array([s for s, _ in links], dtype=np.int32)
         dst = np.array([t for _, t in links], dtype=np.int32)
         for variant in ("sop", "cyc"):
-            H, F, st, sts, _ = run(src, dst, n, G, [dict(d=D, tol=1e-16, variant=variant)])[0]
+            H, F, st, sts, _ = run(src, dst, n, G, [dict(d=D, tol=1e-16, variant=variant,
+                                                         asynchronous=asynchronous)])[0]
             same_stats(sts)
             assert st["converged"] == 1, (name, st)
             assert l1(H, [float(x) for x in X]) <= 1e-14, (name, variant, H)
 
 
+@pytest.mark.parametrize("asynchronous", [False, True])
 @pytest.mark.parametrize("G", [2, 4])
-def test_random_vs_dense_partitioned(G):
+def test_random_vs_dense_partitioned(G, asynchronous):
     """T2 on partitions: random graphs with self-loops, duplicates, dangling nodes."""
     need_gpu()
     for seed in range(25):
@@ -86,21 +90,24 @@ def test_random_vs_dense_partitioned(G):
         if n < G:
             continue
         X = defn.solve_dense(src, dst, n, D)
-        for H, F, st, sts, ranges in run(src, dst, n, G, [dict(d=D, tol=1e-15, variant="sop"),
-                                                           dict(d=D, tol=1e-15, variant="cyc")]):
+        kw = dict(d=D, tol=1e-15, asynchronous=asynchronous)
+        for H, F, st, sts, ranges in run(src, dst, n, G, [dict(variant="sop", **kw),
+                                                           dict(variant="cyc", **kw)]):
             same_stats(sts)
             assert st["converged"] == 1
             assert l1(H, X) <= 1e-13, (seed, G)
 
 
+@pytest.mark.parametrize("asynchronous", [False, True])
 @pytest.mark.parametrize("G", [2, 3, 4, 8])
 @pytest.mark.parametrize("variant", ["sop", "cyc"])
-def test_north_star_parity_partitioned(G, variant):
+def test_north_star_parity_partitioned(G, variant, asynchronous):
     """T11 / T10 on partitions: C1 at tol 1e-10 vs the oracle (1e-9, and the G19 bound against
     the tight 1e-13 oracle run); the partition and the exchange counters are sane."""
     need_gpu()
     src, dst, n = digen.make("c1", seed=1)
-    (H, F, st, sts, ranges), = run(src, dst, n, G, [dict(d=D, tol=1e-10, variant=variant)])
+    (H, F, st, sts, ranges), = run(src, dst, n, G, [dict(d=D, tol=1e-10, variant=variant,
+                                                         asynchronous=asynchronous)])
     same_stats(sts)
     assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
     Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant=variant)
@@ -210,13 +217,41 @@ def csr_dedup(s, t):
 
 
 @pytest.mark.slow
-def test_c2_partitioned_vs_oracle():
+@pytest.mark.parametrize("asynchronous", [False, True])
+def test_c2_partitioned_vs_oracle(asynchronous):
     need_gpu()
     src, dst, n = digen.make("c2", seed=1)
-    H, F, st, sts, _ = run(src, dst, n, 2, [dict(d=D, tol=1e-10, variant="sop")])[0]
+    H, F, st, sts, _ = run(src, dst, n, 2, [dict(d=D, tol=1e-10, variant="sop",
+                                                 asynchronous=asynchronous)])[0]
     same_stats(sts)
     Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
     assert st["converged"] == 1 and l1(H, Ho) <= 1e-9
+
+
+def test_async_partitioned_invariants():
+    """Asynchronous cycles on 3 ranks: F = B + P.H - H and conservation after 1, 2, 5 cycles
+    (every fluid move is atomic, across the exchange as well), and the hub / ragged graph."""
+    need_gpu()
+    src, dst, n = digen.make("c1", seed=3)
+    P = defn.sparse_P(src, dst, n, D)
+    B = defn.uniform_B(n, D)
+    outd = np.bincount(src, minlength=n)
+    for H, F, st, sts, _ in run(src, dst, n, 3, [dict(d=D, tol=1e-300, variant="sop", max_sweeps=k,
+                                                      asynchronous=True) for k in (1, 2, 5)]):
+        same_stats(sts)
+        assert np.all(F >= 0)
+        assert np.abs(F - (B + P @ H - H)).max() <= 1e-15
+        cons = F.sum() + (1 - D) * H[outd > 0].sum() + H[outd == 0].sum()
+        assert abs(cons - (1 - D)) <= 1e-14
+    n = 20000
+    rng = np.random.default_rng(7)
+    s = rng.integers(0, n, 4 * n).astype(np.int32)
+    t = rng.integers(0, n, 4 * n).astype(np.int32)
+    s = np.concatenate([s, np.zeros(15000, np.int32)])
+    t = np.concatenate([t, np.arange(1, 15001, dtype=np.int32)])
+    X, _, _ = oracle.di(s, t, n, d=D, tol=1e-15, variant="sop")
+    H, *_ = run(s, t, n, 4, [dict(d=D, tol=1e-13, asynchronous=True)])[0]
+    assert l1(H, X) <= (1e-13 + 1e-15) / (1 - D) + 1e-14
 
 
 def test_invalid_partitioned_arguments():
