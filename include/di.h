@@ -157,6 +157,12 @@ di_status di_group_abort(di_group grp);
 di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_links, int64_t n_nodes,
                           uint32_t flags, void *stream, const di_dist *dist, di_graph *out);
 
+/* DI-SOP threshold scale: later solves select F_i > alpha * (r/L) * #out_i.
+ * alpha = 1 (the default) is the paper's rule and computes bit for bit the same
+ * threshold; alpha > 1 diffuses fewer, larger amounts. alpha must be finite and > 0 (DI_EINVAL).
+ * On a partitioned graph every rank must set the same value. */
+di_status di_set_threshold_scale(di_graph g, double alpha);
+
 /* Node slice [lo, hi) owned by this rank ([0, n) on one GPU). */
 di_status di_graph_range(di_graph g, int64_t *lo, int64_t *hi);
 

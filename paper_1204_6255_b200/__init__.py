@@ -79,6 +79,8 @@ _lib.di_graph_free.restype = _ci
 _lib.di_graph_free.argtypes = [_vp]
 _lib.di_last_error.restype = ctypes.c_char_p
 _lib.di_last_error.argtypes = []
+_lib.di_set_threshold_scale.restype = _ci
+_lib.di_set_threshold_scale.argtypes = [_vp, _dbl]
 _lib.di_nccl_unique_id.restype = _ci
 _lib.di_nccl_unique_id.argtypes = [_vp]
 _lib.di_group_create.restype = _ci
@@ -99,6 +101,7 @@ _lib.di_test_bins.argtypes = [_vp]
 EXPORTED = ["di_graph_upload", "di_graph_range", "di_graph_links", "di_solve", "di_residual",
             "di_history", "di_sweep_log", "di_graph_free", "di_last_error",
             "di_nccl_unique_id", "di_group_create", "di_group_free", "di_group_abort",
+            "di_set_threshold_scale",
             "di_test_select", "di_test_csr", "di_test_bins", "di_test_perm"]
 
 
@@ -264,6 +267,10 @@ class Graph:
                                  cap, ctypes.byref(n)))
         k = n.value
         return dict(r=r[:k].copy(), selected=sel[:k].copy(), links=lk[:k].copy(), mode=mode[:k].copy())
+
+    def set_threshold_scale(self, alpha):
+        """DI-SOP threshold scale alpha (F_i > alpha * r/L * #out_i; 1 = the paper's rule)."""
+        _check(_lib.di_set_threshold_scale(self._h, float(alpha)))
 
     def range(self):
         lo, hi = _i64(), _i64()

@@ -315,6 +315,15 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
   return DI_OK;
 }
 
+di_status di_set_threshold_scale(di_graph h, double alpha) {
+  Graph *g = (Graph *)h;
+  if (!g) return fail(DI_EINVAL, "di_set_threshold_scale: NULL handle");
+  if (!(alpha > 0.0) || !std::isfinite(alpha))
+    return fail(DI_EINVAL, "di_set_threshold_scale: alpha must be finite and > 0");
+  g->alpha = alpha;
+  return DI_OK;
+}
+
 di_status di_graph_range(di_graph h, int64_t *lo, int64_t *hi) {
   Graph *g = (Graph *)h;
   if (!g) return fail(DI_EINVAL, "NULL handle");
@@ -419,6 +428,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     s.tol = tol;
     s.variant = (int32_t)v;
     s.paper_err = paper;
+    s.alpha = g.alpha;
     s.trace = trace;
     s.mode = mode;
     s.pull_thr = (int64_t)(g.auto_ratio * (double)g.l_global);
@@ -688,6 +698,7 @@ di_status di_test_select(di_graph h, const double *F_in, const double *H_in, dou
     s.epoch = epoch;
     s.r = r;
     s.d = d;
+    s.alpha = g.alpha;
     s.tol = 1e300;
     s.variant = (int32_t)v;
   }

@@ -110,7 +110,8 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
   double *rep = a.rep;
   const double r = sc->r, d = sc->d;
   const bool cyc = (sc->variant == DI_CYC) || sc->guard;
-  const double t = (a.L_total > 0.0) ? r / a.L_total : 0.0;  // r/L once per cycle (G3, G4)
+  double t = (a.L_total > 0.0) ? r / a.L_total : 0.0;  // r/L once per cycle (G3, G4)
+  if (sc->alpha != 1.0) t = __dmul_rn(t, sc->alpha);  // F4 threshold scale (1 = the paper's rule)
   const uint64_t pol = policy_evict_first();
   const uint64_t fpol = a.red_hint ? policy_evict_last() : policy_evict_normal();
   const int32_t *__restrict__ col = a.col;

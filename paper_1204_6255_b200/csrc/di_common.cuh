@@ -86,6 +86,7 @@ struct __align__(256) Scalars {
   int64_t sel_cyc, links_cyc;
   int64_t max_sweeps;        // DI_GRAPH_LOOP: the device-side loop stops at this many sweeps
   unsigned int tile_next;    // DI_ASYNC: next tile of the cycle (dynamic, increasing order)
+  double alpha;              // DI-SOP threshold scale (di_set_threshold_scale; 1 = P:298)
 };
 
 // One push work item: a row (or a kChunk-link chunk of a hub row) of a selected node.
@@ -126,6 +127,7 @@ struct Graph {
   int stripes = 0;           // relabelling stripes (DI_STRIPES; 0 = auto: stripes of ~1024 nodes,
                              // 1 = plain degree order)
   int64_t stripes_eff = 1;   // the stripe count used for this rank's range
+  double alpha = 1.0;        // DI-SOP threshold scale
   int hot_acc = 1;           // DI_ASYNC: replicated accumulators for the hottest targets (DI_HOT_ACC)
   double *rep = nullptr;
   int64_t max_indeg = 0;     // largest in-degree (set by the relabelling pass)

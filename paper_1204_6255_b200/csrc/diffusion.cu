@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(kSelThreads, 3) k_select(const SweepArgs a) {
   const bool cyc = (sc->variant == DI_CYC) || sc->guard;
   const int mode = sc->mode;
   const bool emit = mode != MODE_PULL, dense = mode != MODE_PUSH;
-  const double t = (a.L_total > 0.0) ? r / a.L_total : 0.0;  // r/L once (G3, G4)
+  double t = (a.L_total > 0.0) ? r / a.L_total : 0.0;  // r/L once (G3, G4)
+  if (sc->alpha != 1.0) t = __dmul_rn(t, sc->alpha);  // F4 threshold scale (1 = the paper's rule)
   const int64_t base = tile * (int64_t)kSelTile + (int64_t)threadIdx.x * kSelItems;
   const bool full = base + kSelItems <= a.n;
 

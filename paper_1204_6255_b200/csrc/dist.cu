@@ -314,6 +314,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
     s.tol = tol;
     s.variant = variant;
     s.paper_err = paper;
+    s.alpha = g.alpha;
     s.trace = (flags & DI_TRACE) ? 1 : 0;
     s.mode = MODE_PUSH;
   }

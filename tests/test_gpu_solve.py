@@ -251,6 +251,28 @@ def test_async_cycles(graph_loop):
     g.free()
 
 
+def test_threshold_scale():
+    """F4: di_set_threshold_scale. alpha = 1 is the paper's rule (same solve as the default);
+    other alphas reach the same fixed point within the north_star gate; alpha <= 0 is refused."""
+    need_gpu()
+    import paper_1204_6255_b200 as di
+    src, dst, n = digen.make("c1", seed=1)
+    Ht, _, _ = oracle.di(src, dst, n, d=D, tol=1e-13, variant="sop")
+    g = upload(src, dst, n)
+    st0 = g.solve(d=D, tol=1e-10, variant="sop")
+    for alpha in (1.0, 0.5, 2.0, 4.0):
+        g.set_threshold_scale(alpha)
+        for kw in (dict(), dict(asynchronous=True), dict(blocks=4)):
+            st = g.solve(d=D, tol=1e-10, variant="sop", **kw)
+            assert st["converged"] == 1
+            assert l1(g.history().cpu().numpy(), Ht) <= 1e-10 / (1 - D) + 1e-13 / (1 - D)
+            if alpha == 1.0 and not kw:
+                assert abs(st["sweeps"] - st0["sweeps"]) <= 1
+    with pytest.raises(di.DIError):
+        g.set_threshold_scale(0.0)
+    g.free()
+
+
 @pytest.mark.parametrize("mode", MODES)
 def test_invariants_mid_solve(mode):
     """T8: at any stopping point F = B + P.H - H, F >= 0, conservation, sum F non-increasing."""
