@@ -132,6 +132,24 @@ def make(name: str, seed: int = 1, n: int | None = None, threads: int = 0):
     return src, dst, nn
 
 
+def transpose(src: np.ndarray, dst: np.ndarray):
+    """P^T workload of the paper's tables: every link reversed (input plumbing)."""
+    return np.ascontiguousarray(dst, dtype=np.int32), np.ascontiguousarray(src, dtype=np.int32)
+
+
+def add_self_loops(src: np.ndarray, dst: np.ndarray, n: int, frac: float = 0.2, seed: int = 1):
+    """Loop-heavy stand-in (O/N ~ frac, as the uk-2007 prefixes' 11-24 %): one self-loop
+    on a hash-chosen fraction of the nodes that already have out-links. Returns (src, dst) sorted."""
+    outd = np.bincount(src, minlength=n)
+    rng = np.random.default_rng(seed * 7919 + 17)
+    cand = np.nonzero(outd > 0)[0]
+    pick = cand[rng.random(cand.size) < frac * n / max(cand.size, 1)]
+    s = np.concatenate([np.asarray(src, np.int64), pick])
+    t = np.concatenate([np.asarray(dst, np.int64), pick])
+    order = np.lexsort((t, s))
+    return s[order].astype(np.int32), t[order].astype(np.int32)
+
+
 def stats(src: np.ndarray, dst: np.ndarray, n: int) -> dict:
     """Table-1 style shape statistics (§2.4): L, D, zero-in, O, max_in, max_out.
     E (the recursive closure) is computed by closure_size()."""

@@ -43,3 +43,17 @@ def test_raw_keeps_duplicates():
     s, d = digen.rmat(256, 20000, raw=True, repair=False)
     key = s.astype(np.int64) * 256 + d
     assert np.all(np.diff(key) >= 0) and len(np.unique(key)) < len(key)
+
+
+def test_paper_axes_workloads():
+    """F3 input plumbing: P^T reverses every link; the loop-heavy stand-in adds one self-loop on
+    ~20 % of the nodes (only nodes that already have out-links, so no new dangling change)."""
+    import digen
+    src, dst, n = digen.make("c1", seed=1)
+    ts, tt = digen.transpose(src, dst)
+    assert np.array_equal(ts, dst) and np.array_equal(tt, src)
+    ls, lt = digen.add_self_loops(src, dst, n, frac=0.2)
+    st = digen.stats(ls, lt, n)
+    assert 0.17 <= st["o_over_n"] <= 0.23
+    assert np.array_equal(np.bincount(ls, minlength=n) > 0, np.bincount(src, minlength=n) > 0)
+    assert len(ls) - len(src) == int(np.sum(ls == lt))
