@@ -95,7 +95,9 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
   __shared__ double s_rv[kSelTile];    // v = T d / o
   __shared__ int32_t s_ri[kSelTile];   // local node id
   __shared__ int32_t s_rp[kSelTile + 1];  // exclusive chunk prefix
-  __shared__ int s_nrows, s_nmid, s_nchunks, s_claim, s_mclaim;
+  __shared__ int16_t s_si[kSelTile];   // short rows of the tile: local node id
+  __shared__ double s_sv[kSelTile];    //   and v
+  __shared__ int s_nrows, s_nmid, s_nsmall, s_nchunks, s_claim, s_mclaim, s_sclaim;
   __shared__ int64_t s_tile;
   __shared__ bool s_last;
   __shared__ double s_red[NW][4];
@@ -124,8 +126,10 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
       s_tile = (int64_t)atomicAdd(&sc->tile_next, 1u);
       s_nrows = 0;
       s_nmid = 0;
+      s_nsmall = 0;
       s_claim = 0;
       s_mclaim = 0;
+      s_sclaim = 0;
     }
     __syncthreads();
     const int64_t tile = s_tile;
@@ -156,12 +160,8 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
       }
       rb[kSelItems] = base < a.n ? a.row_ptr[a.n] : 0;
     }
-    double sv[kSelItems];
-    int so[kSelItems];
 #pragma unroll
     for (int j = 0; j < kSelItems; j++) {
-      so[j] = 0;
-      sv[j] = 0.0;
       const int64_t i = base + j;
       if (i >= a.n) continue;
       const int64_t rend = (i + 1 < a.n) ? (j + 1 < kSelItems ? rb[j + 1] : rb[kSelItems])
@@ -186,36 +186,16 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
       acc_s += __dmul_rn(v, (double)(o - kl[j]));
       acc_lk += o;
       acc_nd++;
-      if (o <= kAsyncSmall) {
-        so[j] = o;
-        sv[j] = v;
+      if (o <= kAsyncSmall) {   // short rows: their own list, a lane each (balanced below)
+        const int p = atomicAdd(&s_nsmall, 1);
+        s_si[p] = (int16_t)(base + j - tile * kSelTile);
+        s_sv[p] = v;
       } else {  // mid rows at the front of the list, long rows at its back
         const int p = (o <= kAsyncMid) ? atomicAdd(&s_nmid, 1) : kSelTile - 1 - atomicAdd(&s_nrows, 1);
         s_rb[p] = rb[j];
         s_ro[p] = o;
         s_rv[p] = v;
         s_ri[p] = (int32_t)(base + j - tile * kSelTile);
-      }
-    }
-    // ---- short rows: the selecting thread pushes them, int4 column groups
-#pragma unroll
-    for (int j = 0; j < kSelItems; j++) {
-      if (so[j] == 0) continue;
-      const int64_t beg = rb[j], end = beg + so[j], a0 = beg & ~3ll;
-      const int nvec = (int)((end - a0 + 3) >> 2);
-      const int32_t gi = LOOPS ? (int32_t)(base + j + a.lo) : -1;
-      for (int q = 0; q < nvec; q += 3) {
-        int4 x0 = ld_col4(col + a0 + 4 * q, pol);
-        int4 x1 = make_int4(0, 0, 0, 0), x2 = make_int4(0, 0, 0, 0);
-        if (q + 1 < nvec) x1 = ld_col4(col + a0 + 4 * (q + 1), pol);
-        if (q + 2 < nvec) x2 = ld_col4(col + a0 + 4 * (q + 2), pol);
-        push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, x0, a0 + 4 * q, beg, end, gi, sv[j], fpol);
-        if (q + 1 < nvec)
-          push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, x1, a0 + 4 * (q + 1), beg, end, gi,
-                               sv[j], fpol);
-        if (q + 2 < nvec)
-          push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, x2, a0 + 4 * (q + 2), beg, end, gi,
-                               sv[j], fpol);
       }
     }
     __syncthreads();
@@ -279,6 +259,36 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
               push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, xq[k], a0 + 4 * (int64_t)vi,
                                       beg, end, gi, v, fpol);
           }
+        }
+      }
+    }
+    // short rows (<= kAsyncSmall links, <= 5 int4 groups): 32 per warp claim, one per lane
+    const int nsmall = s_nsmall;
+    if (nsmall > 0) {
+      const int64_t tb = tile * (int64_t)kSelTile;
+      for (;;) {
+        int q = 0;
+        if (lane == 0) q = atomicAdd(&s_sclaim, 32);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (q >= nsmall) break;
+        const int k = q + lane;
+        if (k < nsmall) {
+          const int li = s_si[k];
+          const double v = s_sv[k];
+          const int64_t beg = a.row_ptr[tb + li], end = a.row_ptr[tb + li + 1], a0 = beg & ~3ll;
+          const int nvec = (int)((end - a0 + 3) >> 2);
+          const int32_t gi = LOOPS ? (int32_t)(tb + li + a.lo) : -1;
+          int4 xs[5];
+#pragma unroll
+          for (int u = 0; u < 5; u++) {
+            xs[u] = make_int4(0, 0, 0, 0);
+            if (u < nvec) xs[u] = ld_col4(col + a0 + 4 * u, pol);
+          }
+#pragma unroll
+          for (int u = 0; u < 5; u++)
+            if (u < nvec)
+              push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, xs[u], a0 + 4 * u, beg,
+                                      end, gi, v, fpol);
         }
       }
     }
