@@ -28,15 +28,13 @@ constexpr int kAsyncChunk = 1024;   // longer rows: chunks of this many links, o
 
 // Replicated accumulators for the hottest targets. Same-address fp64 REDs serialise in one L2
 // slice; a node that receives a large share of all pushes (C3's Zipf targets: the top node gets
-// 0.39 % of the links, 383k in-links) keeps its slice busy for a large part of the cycle. With
-// the striped relabelling the kRepl most-linked nodes are the first node of stripes
-// 0..kRepl-1; when the stripe length is a power of two (a.hot_shift >= 0) their REDs go to one
-// of kCopies copies (chosen by warp), each copy in its own 4 KB page, and the last CTA of the
-// cycle folds the copies into F. Enabled when the top node's share exceeds kReplShare (C3 yes:
-// 35 -> ... ms; C4 no: its top share is 0.09 % and the extra test per link costs 6 %).
-constexpr int kRepl = 64;
+// 0.39 % of the links, 383k in-links) keeps its slice busy for a large part of the cycle. On such
+// a graph (top share > kReplShare) the upload places the kHotRanks hottest nodes at internal
+// ids 0..kHotRanks-1 (graph_build.cu, k_place); their REDs go to one of kCopies copies (chosen
+// by warp), each copy in its own 4 KB page, and the last CTA of the cycle folds the copies into
+// F (C3: 44.5 -> 33.6 ms). C4's top share is 0.09 %: no hot ids, no extra test per link.
+constexpr int kRepl = kHotRanks;
 constexpr int kCopies = 16;
-constexpr double kReplShare = 0.0025;
 
 template <bool LOOPS>
 __device__ __forceinline__ void red_group_rep(double *__restrict__ F, double *__restrict__ rep,
@@ -49,8 +47,8 @@ __device__ __forceinline__ void red_group_rep(double *__restrict__ F, double *__
     const int64_t p = p0 + c;
     if (p >= beg && p < end && (!LOOPS || jj[c] != gi)) {
       const int32_t j = jj[c];
-      if (hot_shift >= 0 && j < hot_lim && (j & ((1 << hot_shift) - 1)) == 0)
-        red_add_f64(rep + copy * 512 + (j >> hot_shift), v);
+      if (j < hot_lim)   // one of the hot ids 0..hot_lim-1 (0 when off)
+        red_add_f64(rep + copy * 512 + j, v);
       else
         red_add_f64_hint(F + j, v, fpol);
     }
@@ -107,7 +105,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
   if (sc->stop) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hot_shift = a.hot_shift;
-  const int32_t hot_lim = hot_shift >= 0 ? (kRepl << hot_shift) : 0;
+  const int32_t hot_lim = hot_shift >= 0 ? hot_shift : 0;   // a.hot_shift = hot-id count here
   const int copy = (blockIdx.x * (kAsyncThreads / 32) + warp) % kCopies;
   double *rep = a.rep;
   const double r = sc->r, d = sc->d;
@@ -357,13 +355,13 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
   if (!s_last) return;
   __threadfence();
   if (hot_shift >= 0) {  // fold the replicated accumulators into F, clear them
-    for (int k = threadIdx.x; k < kRepl; k += kAsyncThreads) {
+    for (int k = threadIdx.x; k < hot_lim; k += kAsyncThreads) {
       double acc = 0.0;
       for (int c = 0; c < kCopies; c++) {
         acc += __ldcg(rep + c * 512 + k);
         rep[c * 512 + k] = 0.0;
       }
-      if (acc != 0.0) F[(int64_t)k << hot_shift] += acc;
+      if (acc != 0.0) F[k] += acc;
     }
   }
   const SweepSums sm = reduce_partials(a, gridDim.x, kAsyncThreads);
@@ -421,16 +419,9 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
 
 }  // namespace
 
-// shift of a power-of-two stripe length when the replicated hot accumulators apply, else -1
+// number of hot ids (replicated accumulators) for this graph, or -1 when off
 static int hot_shift_of(const Graph &g) {
-  const bool skewed = g.l_global > 0 && (double)g.max_indeg > kReplShare * (double)g.l_global;
-  if (!(g.reordered && g.hot_acc && skewed && g.world == 1 && g.stripes_eff >= kRepl &&
-        g.n % g.stripes_eff == 0))
-    return -1;
-  const int64_t M = g.n / g.stripes_eff;
-  int sh = 0;
-  while ((1ll << sh) < M) sh++;
-  return ((1ll << sh) == M && sh < 31) ? sh : -1;
+  return (g.reordered && g.hot_acc && g.world == 1 && g.hot_count > 0) ? (int)g.hot_count : -1;
 }
 
 // called by di_solve before any launch or capture (allocations are not capturable)

@@ -30,6 +30,10 @@ constexpr int kRedThreads = 512;
 constexpr int kLogCap = 1 << 16;  // per-sweep trace capacity
 constexpr int kMaxSlices = 4096;   // finaliser slices (= push/pull grid size, <= this)
 constexpr int kMaxBlocks = 256;    // block-ordered sweeps: sub-sweeps per cycle
+// Skewed in-degrees (async.cu): when the top node takes more than kReplShare of the links, the
+// kHotRanks hottest nodes are placed first and their REDs spread over replicated accumulators.
+constexpr int kHotRanks = 64;
+constexpr double kReplShare = 0.0025;
 
 enum BinId { BIN_T = 0, BIN_G = 1, BIN_W = 2, BIN_C = 3 };
 
@@ -126,7 +130,7 @@ struct Graph {
   bool reordered = false;
   int stripes = 0;           // relabelling stripes (DI_STRIPES; 0 = auto: stripes of ~1024 nodes,
                              // 1 = plain degree order)
-  int64_t stripes_eff = 1;   // the stripe count used for this rank's range
+  int64_t hot_count = 0;     // skewed graphs: the hot_count hottest nodes are internal ids 0..
   double alpha = 1.0;        // DI-SOP threshold scale
   int hot_acc = 1;           // DI_ASYNC: replicated accumulators for the hottest targets (DI_HOT_ACC)
   double *rep = nullptr;

@@ -33,28 +33,57 @@ __global__ void k_validate(const int32_t *__restrict__ src, const int32_t *__res
   }
 }
 
-// rank r (0 = largest in-degree) -> internal id: rank r goes to stripe r % P at position r / P,
-// stripes laid out contiguously. Nodes of similar rank share L2 lines (hot lines are fully hot)
-// while the P hottest nodes sit in P different lines / L2 slices (no single hot slice for the
-// push's REDs). Multi-GPU: the sorted order is (owner range, rank); every range is striped on its
-// own, so a rank's internal ids stay inside the node range it owns.
+// rank r (0 = largest in-degree) -> internal id. The first hot[g] ranks of range g are placed
+// contiguously at the range start (the replicated-accumulator targets of a skewed graph, async.cu);
+// the others go to stripe r' % P at position r' / P (r' = r - hot), stripes laid out contiguously.
+// Nodes of similar rank share L2 lines (hot lines are fully hot) while the P hottest sit in P
+// different lines. P is a prime near (#nodes)/1024: a power-of-two stripe length would put all
+// stripe heads (the hottest lines) at one power-of-two address stride, which the L2 slice hash
+// maps onto fewer slices (C4: 16384 stripes 65.7 ms, 16411 63.1 ms). Multi-GPU: the sorted order
+// is (owner range, rank) and every range is placed on its own, so a rank's internal ids stay in
+// the node range it owns.
+struct PlaceParams {
+  int64_t hot[kMaxWorld];
+  int64_t stripes[kMaxWorld];
+};
+
 __global__ void k_place(const int32_t *__restrict__ sorted_old, int64_t n, DistBounds bd,
-                        int64_t stripes, int32_t *__restrict__ new_of, int32_t *__restrict__ old_of) {
+                        PlaceParams pp, int32_t *__restrict__ new_of, int32_t *__restrict__ old_of) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
     int g = 0;
     while (g + 1 < bd.world && r >= bd.b[g + 1]) g++;
-    const int64_t lo = bd.b[g], m = bd.b[g + 1] - lo, rr = r - lo;
-    int64_t P = stripes > 0 ? stripes : (m >> 10);  // 0: stripes of ~1024 nodes
-    if (P < 1) P = 1;
-    if (P > m) P = m;
-    const int64_t M = m / P, rem = m % P;
-    const int64_t s = rr % P, idx = rr / P;
-    const int64_t k = lo + s * M + (s < rem ? s : rem) + idx;
+    const int64_t lo = bd.b[g], rr = r - lo, hot = pp.hot[g];
+    int64_t k;
+    if (rr < hot) {
+      k = lo + rr;
+    } else {
+      const int64_t m = bd.b[g + 1] - lo - hot, q = rr - hot;
+      int64_t P = pp.stripes[g];
+      if (P < 1) P = 1;
+      if (P > m) P = m;
+      const int64_t M = m / P, rem = m % P;
+      const int64_t s = q % P, idx = q / P;
+      k = lo + hot + s * M + (s < rem ? s : rem) + idx;
+    }
     const int32_t o = sorted_old[r];
     new_of[o] = (int32_t)k;
     old_of[k] = o;
   }
+}
+
+int64_t prime_at_most(int64_t x) {
+  if (x < 2) return 1;
+  for (int64_t p = x; p >= 2; p--) {
+    bool prime = true;
+    for (int64_t d = 2; d * d <= p; d++)
+      if (p % d == 0) {
+        prime = false;
+        break;
+      }
+    if (prime) return p;
+  }
+  return 1;
 }
 
 // relabelling key: (owner range of i, descending in-degree); ties keep ascending id (stable sort)
@@ -324,10 +353,18 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
       btrace("sync3");
     }
     g.max_indeg = top;
-    const int64_t P = g.stripes > 0 ? (int64_t)g.stripes : 0;   // 0 = auto (per range)
-    g.stripes_eff = g.stripes > 0 ? std::min<int64_t>(g.stripes, g.n)
-                                  : std::max<int64_t>(1, g.n >> 10);
-    k_place<<<grid_for(n, sms), 256, 0, st>>>((const int32_t *)sorted.p, n, bd, P, g.new_of,
+    // skewed in-degrees (single GPU): the kHotRanks hottest nodes first (replicated accumulators)
+    const bool skewed = world == 1 && g.hot_acc && L > 0 &&
+                        (double)top > kReplShare * (double)L && n > 4 * kHotRanks;
+    g.hot_count = skewed ? kHotRanks : 0;
+    PlaceParams pp;
+    for (int q = 0; q < world; q++) {
+      const int64_t m = bd.b[q + 1] - bd.b[q];
+      pp.hot[q] = (q == 0) ? g.hot_count : 0;
+      pp.stripes[q] = g.stripes > 0 ? (int64_t)g.stripes
+                                     : prime_at_most(std::max<int64_t>(1, (m - pp.hot[q]) >> 10));
+    }
+    k_place<<<grid_for(n, sms), 256, 0, st>>>((const int32_t *)sorted.p, n, bd, pp, g.new_of,
                                                g.old_of);
     g.reordered = true;
   }

@@ -65,11 +65,24 @@ def test_reorder_relabelling(name):
     old_of = g.test_perm()
     indeg = np.bincount(dst, minlength=n)
     ranked = np.argsort(-indeg, kind="stable")           # rank r -> caller id
-    P = max(1, n >> 10)          # auto stripes of ~1024 nodes: rank r -> stripe r % P, slot r // P
-    r = np.arange(n)
-    M, rem = n // P, n % P
+    # placement (graph_build.cu k_place): on a skewed graph (top in-degree > 0.25 % of the links)
+    # the 64 hottest ranks come first; the rest in P stripes, P = largest prime <= (n - hot)/1024
+    hot = 64 if (indeg.max() > 0.0025 * len(src) and n > 256) else 0
+
+    def prime_at_most(x):
+        if x < 2:
+            return 1
+        for p in range(x, 1, -1):
+            if all(p % d for d in range(2, int(p ** 0.5) + 1)):
+                return p
+        return 1
+
+    P = prime_at_most(max(1, (n - hot) >> 10))
+    m = n - hot
+    r = np.arange(m)
+    M, rem = m // P, m % P
     s_ = r % P
-    k = s_ * M + np.minimum(s_, rem) + r // P
+    k = np.concatenate([np.arange(hot), hot + s_ * M + np.minimum(s_, rem) + r // P])
     expect = np.empty(n, np.int64)
     expect[k] = ranked
     assert np.array_equal(old_of, expect.astype(np.int32))
