@@ -218,10 +218,22 @@ int grid_for(int64_t n, int sms) {
   return (int)g;
 }
 
-struct DevBuf {
-  void *p = nullptr;
-  ~DevBuf() {
-    if (p) dfree(p);
+// All temporaries of one build come from ONE pool allocation carved here (sizes known up front,
+// CUB temp sizes queried with null pointers). One block of the same size per upload is reused by
+// the stream-ordered pool without growing it; separate allocations of mixed sizes fragmented the
+// pool and made some uploads map fresh memory (0.5 s on C4).
+struct Arena {
+  char *base = nullptr;
+  size_t cap = 0, off = 0;
+  ~Arena() {
+    if (base) dfree(base);
+  }
+  static size_t up(size_t x) { return (x + 255) & ~(size_t)255; }
+  template <typename T>
+  T *take(size_t bytes) {
+    T *p = reinterpret_cast<T *>(base + off);
+    off += up(bytes ? bytes : 1);
+    return p;
   }
 };
 
@@ -235,45 +247,101 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   int b = 1;
   while ((1ll << b) < n) b++;
   const int sms = g.num_sms;
+  const bool host = flags & DI_HOST_PTRS;
+  const bool reorder = !(flags & DI_NO_REORDER);
+  const int dedup = (flags & DI_DEDUP) ? 1 : 0, drop_self = (flags & DI_DROP_SELF_LOOPS) ? 1 : 0;
+  const size_t LL = (size_t)(L > 0 ? L : 1);
+  int wb = 0;
+  while ((1 << wb) < world) wb++;
 
   btrace("start");
-  DevBuf dsrc, ddst, keys_a, keys_b, keep, tmp, nsel, badb;
-  const int32_t *s_dev = src, *d_dev = dst;
-  if (flags & DI_HOST_PTRS) {
-    DI_CK(dmalloc(&dsrc.p, (size_t)(L > 0 ? L : 1) * 4));
-    DI_CK(dmalloc(&ddst.p, (size_t)(L > 0 ? L : 1) * 4));
-    if (L > 0) {
-      DI_CK(cudaMemcpyAsync(dsrc.p, src, (size_t)L * 4, cudaMemcpyHostToDevice, st));
-      DI_CK(cudaMemcpyAsync(ddst.p, dst, (size_t)L * 4, cudaMemcpyHostToDevice, st));
-    }
-    s_dev = (const int32_t *)dsrc.p;
-    d_dev = (const int32_t *)ddst.p;
+  // ---- one arena for every temporary: CUB temp sizes first (null pointers: size queries only)
+  size_t cub_tmp = 0, q = 0;
+  DI_CK(cub::DeviceRadixSort::SortKeys(nullptr, q, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                       (int64_t)LL, 0, 2 * b, st));
+  cub_tmp = std::max(cub_tmp, q);
+  if (dedup || drop_self) {
+    DI_CK(cub::DeviceSelect::Flagged(nullptr, q, (uint64_t *)nullptr, (uint8_t *)nullptr,
+                                     (uint64_t *)nullptr, (int64_t *)nullptr, (int64_t)LL, st));
+    cub_tmp = std::max(cub_tmp, q);
   }
-  const size_t LL = (size_t)(L > 0 ? L : 1);
-  DI_CK(dmalloc(&keys_a.p, LL * 8));
-  DI_CK(dmalloc(&keys_b.p, LL * 8));
-  DI_CK(dmalloc(&badb.p, 16));
+  if (reorder) {
+    DI_CK(cub::DeviceRadixSort::SortPairs(nullptr, q, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                          (int32_t *)nullptr, (int32_t *)nullptr, (int64_t)n, 0,
+                                          32 + wb, st));
+    cub_tmp = std::max(cub_tmp, q);
+    DI_CK(cub::DeviceReduce::Max(nullptr, q, (uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)n,
+                                 st));
+    cub_tmp = std::max(cub_tmp, q);
+  }
+  if (world > 1) {
+    DI_CK(cub::DeviceScan::ExclusiveSum(nullptr, q, (int64_t *)nullptr, (int64_t *)nullptr, n + 1,
+                                        st));
+    cub_tmp = std::max(cub_tmp, q);
+  }
+  const size_t nn = (size_t)n;
+  size_t total = 0;
+  auto add = [&](size_t x) { total += Arena::up(x ? x : 1); };
+  if (host) {
+    add(LL * 4);
+    add(LL * 4);
+  }
+  add(LL * 8);                        // keys_a
+  add(LL * 8);                        // keys_b
+  add(cub_tmp);
+  if (dedup || drop_self) add(LL);    // keep flags
+  add(64);                            // bad index / counts / max / key bounds
+  add((kMaxWorld + 1) * 8);           // partition bounds
+  if (reorder) {
+    add(nn * 4);                      // indeg
+    add(nn * 8);                      // relabel keys in/out
+    add(nn * 8);
+    add(nn * 4);                      // iota
+    add(nn * 4);                      // sorted ranks
+  }
+  if (world > 1) {
+    add((nn + 1) * 8);                // out-degrees
+    add((nn + 1) * 8);                // prefix
+  }
+  Arena ar;
+  DI_CK(dmalloc(&ar.base, total));
+  ar.cap = total;
+
+  const int32_t *s_dev = src, *d_dev = dst;
+  if (host) {
+    int32_t *hs = ar.take<int32_t>(LL * 4), *hd = ar.take<int32_t>(LL * 4);
+    if (L > 0) {
+      DI_CK(cudaMemcpyAsync(hs, src, (size_t)L * 4, cudaMemcpyHostToDevice, st));
+      DI_CK(cudaMemcpyAsync(hd, dst, (size_t)L * 4, cudaMemcpyHostToDevice, st));
+    }
+    s_dev = hs;
+    d_dev = hd;
+  }
+  uint64_t *ka = ar.take<uint64_t>(LL * 8), *kb = ar.take<uint64_t>(LL * 8);
+  void *tmp = ar.take<char>(cub_tmp);
+  uint8_t *keep = (dedup || drop_self) ? ar.take<uint8_t>(LL) : nullptr;
+  char *small = ar.take<char>(64);
+  unsigned long long *badb = reinterpret_cast<unsigned long long *>(small);
+  int64_t *nsel = reinterpret_cast<int64_t *>(small + 16);
+  uint32_t *mx = reinterpret_cast<uint32_t *>(small + 24);
+  int64_t *kbnd = reinterpret_cast<int64_t *>(small + 32);
+  int64_t *bnd = ar.take<int64_t>((kMaxWorld + 1) * 8);
   unsigned long long init_bad = ~0ull;
-  DI_CK(cudaMemcpyAsync(badb.p, &init_bad, 8, cudaMemcpyHostToDevice, st));
-  uint64_t *ka = (uint64_t *)keys_a.p, *kb = (uint64_t *)keys_b.p;
-  const bool reorder = !(flags & DI_NO_REORDER);
-  DevBuf indeg_b;
+  DI_CK(cudaMemcpyAsync(badb, &init_bad, 8, cudaMemcpyHostToDevice, st));
   uint32_t *indeg = nullptr;
   if (reorder) {
-    DI_CK(dmalloc(&indeg_b.p, (size_t)n * 4));
-    DI_CK(cudaMemsetAsync(indeg_b.p, 0, (size_t)n * 4, st));
-    indeg = (uint32_t *)indeg_b.p;
+    indeg = ar.take<uint32_t>(nn * 4);
+    DI_CK(cudaMemsetAsync(indeg, 0, nn * 4, st));
   }
   if (L > 0)
-    k_validate<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, n, (unsigned long long *)badb.p,
-                                                 indeg);
+    k_validate<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, n, badb, indeg);
   unsigned long long bad = 0;
-  DI_CK(cudaMemcpyAsync(&bad, badb.p, 8, cudaMemcpyDeviceToHost, st));
+  DI_CK(cudaMemcpyAsync(&bad, badb, 8, cudaMemcpyDeviceToHost, st));
   DI_CK(cudaStreamSynchronize(st));
   btrace("sync1");
   if (bad != ~0ull) {
     int32_t sv = 0, dv = 0;
-    if (flags & DI_HOST_PTRS) {
+    if (host) {
       sv = src[bad];
       dv = dst[bad];
     } else {
@@ -292,116 +360,72 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   bd.b[0] = 0;
   bd.b[1] = n;
   if (world > 1) {
-    DevBuf od, pre, ctmp, bnd;
-    DI_CK(dmalloc(&od.p, (size_t)(n + 1) * 8));
-    DI_CK(dmalloc(&pre.p, (size_t)(n + 1) * 8));
-    DI_CK(dmalloc(&bnd.p, (size_t)(kMaxWorld + 1) * 8));
-    DI_CK(cudaMemsetAsync(od.p, 0, (size_t)(n + 1) * 8, st));
-    if (L > 0) k_outdeg<<<grid_for(L, sms), 256, 0, st>>>(s_dev, L, (int64_t *)od.p);
-    size_t cb = 0;
-    DI_CK(cub::DeviceScan::ExclusiveSum(nullptr, cb, (int64_t *)od.p, (int64_t *)pre.p, n + 1, st));
-    DI_CK(dmalloc(&ctmp.p, cb));
-    DI_CK(cub::DeviceScan::ExclusiveSum(ctmp.p, cb, (int64_t *)od.p, (int64_t *)pre.p, n + 1, st));
-    k_bounds<<<1, 32, 0, st>>>((const int64_t *)pre.p, n, world, (int64_t *)bnd.p);
-    DI_CK(cudaMemcpyAsync(bd.b, bnd.p, (size_t)(world + 1) * 8, cudaMemcpyDeviceToHost, st));
+    int64_t *od = ar.take<int64_t>((nn + 1) * 8), *pre = ar.take<int64_t>((nn + 1) * 8);
+    DI_CK(cudaMemsetAsync(od, 0, (nn + 1) * 8, st));
+    if (L > 0) k_outdeg<<<grid_for(L, sms), 256, 0, st>>>(s_dev, L, od);
+    size_t cb = cub_tmp;
+    DI_CK(cub::DeviceScan::ExclusiveSum(tmp, cb, od, pre, n + 1, st));
+    k_bounds<<<1, 32, 0, st>>>(pre, n, world, bnd);
+    DI_CK(cudaMemcpyAsync(bd.b, bnd, (size_t)(world + 1) * 8, cudaMemcpyDeviceToHost, st));
     DI_CK(cudaStreamSynchronize(st));
     btrace("sync2");
     // every range non-empty (n >= world is checked by the caller)
-    for (int q = 1; q < world; q++) {
-      if (bd.b[q] < bd.b[q - 1] + 1) bd.b[q] = bd.b[q - 1] + 1;
-      if (bd.b[q] > n - (world - q)) bd.b[q] = n - (world - q);
+    for (int r = 1; r < world; r++) {
+      if (bd.b[r] < bd.b[r - 1] + 1) bd.b[r] = bd.b[r - 1] + 1;
+      if (bd.b[r] > n - (world - r)) bd.b[r] = n - (world - r);
     }
     bd.b[world] = n;
   }
   g.lo = bd.b[g.rank];
   g.hi = bd.b[g.rank + 1];
   g.n = g.hi - g.lo;
-  // ---- locality relabelling (DESIGN.md §Layout): node ids sorted by descending in-degree inside
+  // ---- locality relabelling (DESIGN.md §6): node ids sorted by descending in-degree inside
   //      each owner range, so the hot push targets share L2 lines; ranges keep their extent
   if (reorder) {
-    DevBuf kin, kout, vin;
-    DI_CK(dmalloc(&kin.p, (size_t)n * 8));
-    DI_CK(dmalloc(&kout.p, (size_t)n * 8));
-    DI_CK(dmalloc(&vin.p, (size_t)n * 4));
-    DevBuf sorted;
-    DI_CK(dmalloc(&sorted.p, (size_t)n * 4));
-    DI_CK(dmalloc(&g.old_of, (size_t)n * 4));
-    DI_CK(dmalloc(&g.new_of, (size_t)n * 4));
-    int wb = 0;
-    while ((1 << wb) < world) wb++;
-    k_perm_keys64<<<grid_for(n, sms), 256, 0, st>>>(indeg, n, bd, (uint64_t *)kin.p,
-                                                     (int32_t *)vin.p);
-    size_t pb = 0;
-    DI_CK(cub::DeviceRadixSort::SortPairs(nullptr, pb, (uint64_t *)kin.p, (uint64_t *)kout.p,
-                                          (int32_t *)vin.p, (int32_t *)sorted.p, (int64_t)n, 0,
-                                          32 + wb, st));
-    DevBuf ptmp;
-    DI_CK(dmalloc(&ptmp.p, pb));
-    DI_CK(cub::DeviceRadixSort::SortPairs(ptmp.p, pb, (uint64_t *)kin.p, (uint64_t *)kout.p,
-                                          (int32_t *)vin.p, (int32_t *)sorted.p, (int64_t)n, 0,
-                                          32 + wb, st));
+    uint64_t *kin = ar.take<uint64_t>(nn * 8), *kout = ar.take<uint64_t>(nn * 8);
+    int32_t *vin = ar.take<int32_t>(nn * 4), *sorted = ar.take<int32_t>(nn * 4);
+    DI_CK(dmalloc(&g.old_of, nn * 4));
+    DI_CK(dmalloc(&g.new_of, nn * 4));
+    k_perm_keys64<<<grid_for(n, sms), 256, 0, st>>>(indeg, n, bd, kin, vin);
+    size_t pb = cub_tmp;
+    DI_CK(cub::DeviceRadixSort::SortPairs(tmp, pb, kin, kout, vin, sorted, (int64_t)n, 0, 32 + wb,
+                                          st));
     uint32_t top = 0;  // largest in-degree (DI_ASYNC decides on replicated hot accumulators)
-    {
-      DevBuf mx, mtmp;
-      DI_CK(dmalloc(&mx.p, 4));
-      size_t mb = 0;
-      DI_CK(cub::DeviceReduce::Max(nullptr, mb, indeg, (uint32_t *)mx.p, (int64_t)n, st));
-      DI_CK(dmalloc(&mtmp.p, mb));
-      DI_CK(cub::DeviceReduce::Max(mtmp.p, mb, indeg, (uint32_t *)mx.p, (int64_t)n, st));
-      DI_CK(cudaMemcpyAsync(&top, mx.p, 4, cudaMemcpyDeviceToHost, st));
-      DI_CK(cudaStreamSynchronize(st));
-      btrace("sync3");
-    }
+    size_t mb = cub_tmp;
+    DI_CK(cub::DeviceReduce::Max(tmp, mb, indeg, mx, (int64_t)n, st));
+    DI_CK(cudaMemcpyAsync(&top, mx, 4, cudaMemcpyDeviceToHost, st));
+    DI_CK(cudaStreamSynchronize(st));
+    btrace("sync3");
     g.max_indeg = top;
     // skewed in-degrees (single GPU): the kHotRanks hottest nodes first (replicated accumulators)
     const bool skewed = world == 1 && g.hot_acc && L > 0 &&
                         (double)top > kReplShare * (double)L && n > 4 * kHotRanks;
     g.hot_count = skewed ? kHotRanks : 0;
     PlaceParams pp;
-    for (int q = 0; q < world; q++) {
-      const int64_t m = bd.b[q + 1] - bd.b[q];
-      pp.hot[q] = (q == 0) ? g.hot_count : 0;
-      pp.stripes[q] = g.stripes > 0 ? (int64_t)g.stripes
-                                     : prime_at_most(std::max<int64_t>(1, (m - pp.hot[q]) >> 10));
+    for (int r = 0; r < world; r++) {
+      const int64_t m = bd.b[r + 1] - bd.b[r];
+      pp.hot[r] = (r == 0) ? g.hot_count : 0;
+      pp.stripes[r] = g.stripes > 0 ? (int64_t)g.stripes
+                                     : prime_at_most(std::max<int64_t>(1, (m - pp.hot[r]) >> 10));
     }
-    k_place<<<grid_for(n, sms), 256, 0, st>>>((const int32_t *)sorted.p, n, bd, pp, g.new_of,
-                                               g.old_of);
+    k_place<<<grid_for(n, sms), 256, 0, st>>>(sorted, n, bd, pp, g.new_of, g.old_of);
     g.reordered = true;
   }
   if (L > 0) k_make_keys<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, b, g.new_of, ka);
-  DI_CK(cudaStreamSynchronize(st));
   btrace("sync4");
-  dsrc.~DevBuf();
-  dsrc.p = nullptr;
-  ddst.~DevBuf();
-  ddst.p = nullptr;
 
   // ---- sort by (src, dst)
-  size_t tbytes = 0;
   if (L > 0) {
-    DI_CK(cub::DeviceRadixSort::SortKeys(nullptr, tbytes, ka, kb, (int64_t)L, 0, 2 * b, st));
-    DI_CK(dmalloc(&tmp.p, tbytes));
-    DI_CK(cub::DeviceRadixSort::SortKeys(tmp.p, tbytes, ka, kb, (int64_t)L, 0, 2 * b, st));
+    size_t tb = cub_tmp;
+    DI_CK(cub::DeviceRadixSort::SortKeys(tmp, tb, ka, kb, (int64_t)L, 0, 2 * b, st));
   }
   // kb: sorted keys. Optional compaction.
   int64_t Lk = L;
-  const int dedup = (flags & DI_DEDUP) ? 1 : 0, drop_self = (flags & DI_DROP_SELF_LOOPS) ? 1 : 0;
   if (L > 0 && (dedup || drop_self)) {
-    DI_CK(dmalloc(&keep.p, LL));
-    DI_CK(dmalloc(&nsel.p, 8));
-    k_keep_flags<<<grid_for(L, sms), 256, 0, st>>>(kb, L, b, dedup, drop_self, (uint8_t *)keep.p);
-    size_t sb = 0;
-    DI_CK(cub::DeviceSelect::Flagged(nullptr, sb, kb, (uint8_t *)keep.p, ka, (int64_t *)nsel.p,
-                                     (int64_t)L, st));
-    if (sb > tbytes) {
-      tmp.~DevBuf();
-      tmp.p = nullptr;
-      DI_CK(dmalloc(&tmp.p, sb));
-      tbytes = sb;
-    }
-    DI_CK(cub::DeviceSelect::Flagged(tmp.p, sb, kb, (uint8_t *)keep.p, ka, (int64_t *)nsel.p,
-                                     (int64_t)L, st));
-    DI_CK(cudaMemcpyAsync(&Lk, nsel.p, 8, cudaMemcpyDeviceToHost, st));
+    k_keep_flags<<<grid_for(L, sms), 256, 0, st>>>(kb, L, b, dedup, drop_self, keep);
+    size_t sb = cub_tmp;
+    DI_CK(cub::DeviceSelect::Flagged(tmp, sb, kb, keep, ka, nsel, (int64_t)L, st));
+    DI_CK(cudaMemcpyAsync(&Lk, nsel, 8, cudaMemcpyDeviceToHost, st));
     DI_CK(cudaStreamSynchronize(st));
     btrace("sync5");
     std::swap(ka, kb);  // kb = compacted sorted keys
@@ -411,8 +435,8 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   int64_t kbeg = 0, kend = Lk;
   if (world > 1 && Lk > 0) {
     int64_t hb[2];
-    k_key_bound<<<1, 32, 0, st>>>(kb, Lk, b, g.lo, g.hi, (int64_t *)badb.p);
-    DI_CK(cudaMemcpyAsync(hb, badb.p, 16, cudaMemcpyDeviceToHost, st));
+    k_key_bound<<<1, 32, 0, st>>>(kb, Lk, b, g.lo, g.hi, kbnd);
+    DI_CK(cudaMemcpyAsync(hb, kbnd, 16, cudaMemcpyDeviceToHost, st));
     DI_CK(cudaStreamSynchronize(st));
     btrace("sync6");
     kbeg = hb[0];
@@ -431,7 +455,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   DI_CK(cudaMemsetAsync(g.kloop, 0, (size_t)nl * 4, st));
   k_csr_from_sorted<<<grid_for(Ll + 1, sms), 256, 0, st>>>(kb + kbeg, Ll, nl, b, g.lo, g.row_ptr,
                                                           g.col, g.kloop);
-  int *any_loop = (int *)badb.p;  // reuse 8 bytes
+  int *any_loop = reinterpret_cast<int *>(small);  // reuse (bad index no longer needed)
   DI_CK(cudaMemsetAsync(any_loop, 0, 4, st));
   k_deg<<<grid_for(nl, sms), 256, 0, st>>>(g.row_ptr, nl, g.deg, g.kloop, any_loop);
   int hl = 0;
@@ -440,15 +464,8 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   if (flags & DI_BUILD_CSC) {  // single GPU only (checked by the caller)
     if (Lk > 0) {
       k_swap_keys<<<grid_for(Lk, sms), 256, 0, st>>>(kb, Lk, b, ka);
-      size_t sb = 0;
-      DI_CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, ka, kb, (int64_t)Lk, 0, 2 * b, st));
-      if (sb > tbytes) {
-        tmp.~DevBuf();
-        tmp.p = nullptr;
-        DI_CK(dmalloc(&tmp.p, sb));
-        tbytes = sb;
-      }
-      DI_CK(cub::DeviceRadixSort::SortKeys(tmp.p, sb, ka, kb, (int64_t)Lk, 0, 2 * b, st));
+      size_t sb = cub_tmp;
+      DI_CK(cub::DeviceRadixSort::SortKeys(tmp, sb, ka, kb, (int64_t)Lk, 0, 2 * b, st));
     }
     const size_t LkS = (size_t)(Lk > 0 ? Lk : 1);
     DI_CK(dmalloc(&g.csc_ptr, ((size_t)n + 1) * 8));
