@@ -204,7 +204,7 @@ class Graph:
         h = _vp()
         dist = None
         self._group = group
-        if int(world) > 1:
+        if int(world) > 1 or nccl_id is not None or group is not None:
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
             dist = Dist(int(rank), int(world),
                         ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None,

@@ -258,7 +258,10 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
     return fail(DI_EINVAL, "di_graph_upload: dist->world must be in [1, " +
                                std::to_string(kMaxWorld) + "]");
   if (rank < 0 || rank >= world) return fail(DI_EINVAL, "di_graph_upload: dist->rank out of range");
-  if (world > 1) {
+  // partitioned: any rank of a communicator, including a communicator of one rank (which runs
+  // the whole multi-GPU protocol with nothing to exchange: tests the NCCL backend on one GPU)
+  const bool partitioned = dist && (world > 1 || grp || dist->nccl_unique_id);
+  if (partitioned) {
     if (n_nodes < world) return fail(DI_EINVAL, "di_graph_upload: fewer nodes than ranks");
     if (flags & (DI_BUILD_CSC | DI_LOCAL_LINKS))
       return fail(DI_EINVAL, "di_graph_upload: DI_BUILD_CSC and DI_LOCAL_LINKS are single-GPU / "
@@ -283,7 +286,8 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
   g->hi = n_nodes;
   g->rank = rank;
   g->world = world;
-  if (world > 1) {  // the communicator first: ncclCommInitRank is collective
+  g->partitioned = partitioned;
+  if (partitioned) {  // the communicator first: ncclCommInitRank is collective
     Comm *c = nullptr;
     di_status cs = grp ? make_group_comm(grp, rank, &c)
                        : make_nccl_comm(dist->nccl_unique_id, rank, world, &c);
@@ -306,7 +310,7 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
   di_status s = build_graph(*g, src, dst, n_links, flags);
   if (s == DI_OK) s = alloc_state(*g);
   if (s == DI_OK) s = alloc_pull(*g);
-  if (s == DI_OK && world > 1) s = alloc_dist(*g);
+  if (s == DI_OK && partitioned) s = alloc_dist(*g);
   if (s != DI_OK) {
     free_graph(g);
     return s;
@@ -372,7 +376,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     dfree(bad);
     if (hb) return fail(DI_EINVAL, "di_solve: B has a negative or non-finite entry");
   }
-  if (g.world > 1) {
+  if (g.partitioned) {
     if (v != DI_SOP && v != DI_CYC)
       return fail(DI_EINVAL, "di_solve: a partitioned graph runs DI_SOP / DI_CYC only");
     if ((flags & (DI_PULL | DI_AUTO | DI_GRAPH_LOOP)) || ((flags >> 16) & 0xFFu) > 1)
@@ -581,7 +585,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
 di_status di_residual(di_graph h, double *l1_out, double *F_out) {
   Graph *g = (Graph *)h;
   if (!g) return fail(DI_EINVAL, "di_residual: NULL handle");
-  if (g->world > 1) {  // collective: the global sum
+  if (g->partitioned) {  // collective: the global sum
     double l1 = 0.0;
     di_status s = dist_residual(*g, &l1);
     if (s != DI_OK) return s;

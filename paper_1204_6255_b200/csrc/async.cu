@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
 
 // number of hot ids (replicated accumulators) for this graph, or -1 when off
 static int hot_shift_of(const Graph &g) {
-  return (g.reordered && g.hot_acc && g.world == 1 && g.hot_count > 0) ? (int)g.hot_count : -1;
+  return (g.reordered && g.hot_acc && !g.partitioned && g.hot_count > 0) ? (int)g.hot_count : -1;
 }
 
 // called by di_solve before any launch or capture (allocations are not capturable)
@@ -435,7 +435,7 @@ di_status prepare_cycle(Graph &g) {
 
 void launch_cycle(Graph &g, int64_t *launches) {
   SweepArgs a = sweep_args(g, 0);
-  const bool dist = g.world > 1;
+  const bool dist = g.partitioned;
   DistArgs x{};
   if (dist) x = dist_args(g);
   a.hot_shift = g.rep ? hot_shift_of(g) : -1;

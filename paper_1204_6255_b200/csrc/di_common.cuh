@@ -126,6 +126,7 @@ struct Graph {
   int push_occ = 4;         // k_push min blocks per SM (DI_PUSH_OCC)
   int red_hint = 1;         // L2 evict_last hint on the push's REDs into F (DI_RED_HINT=0 disables)
   int rank = 0, world = 1;
+  bool partitioned = false;  // built with a communicator (dist.cu path), even of one rank
   // locality relabelling: internal id = new_of[user id]; user id = old_of[internal id]
   bool reordered = false;
   int stripes = 0;           // relabelling stripes (DI_STRIPES; 0 = auto: stripes of ~1024 nodes,

@@ -398,7 +398,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     btrace("sync3");
     g.max_indeg = top;
     // skewed in-degrees (single GPU): the kHotRanks hottest nodes first (replicated accumulators)
-    const bool skewed = world == 1 && g.hot_acc && L > 0 &&
+    const bool skewed = !g.partitioned && g.hot_acc && L > 0 &&
                         (double)top > kReplShare * (double)L && n > 4 * kHotRanks;
     g.hot_count = skewed ? kHotRanks : 0;
     PlaceParams pp;

@@ -268,3 +268,29 @@ def test_invalid_partitioned_arguments():
     with pytest.raises(di.DIError):   # world larger than the group
         grp = di.LocalGroup(2)
         di.Graph(src, dst, n, rank=0, world=3, group=grp)
+
+
+@pytest.mark.parametrize("asynchronous", [False, True])
+def test_nccl_backend_single_rank(asynchronous):
+    """The NCCL backend for real on one GPU: a communicator of one rank (ncclCommInitRank,
+    ncclAllReduce, grouped send/recv with no peers) runs the whole partitioned protocol with
+    nothing to exchange; C1 to the north_star gate, and the same through a group of one."""
+    need_gpu()
+    import paper_1204_6255_b200 as di
+    src, dst, n = digen.make("c1", seed=2)
+    Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
+    nid = di.nccl_unique_id()
+    g = di.Graph(src, dst, n, rank=0, world=1, nccl_id=nid)
+    assert g.range() == (0, n)
+    st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous)
+    assert st["converged"] == 1 and st["exchange_entries"] == 0
+    assert l1(g.history().cpu().numpy(), Ho) <= 1e-9
+    assert g.residual() <= 1e-10
+    g.free()
+    grp = di.LocalGroup(1)
+    g = di.Graph(src, dst, n, rank=0, world=1, group=grp)
+    st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous)
+    assert st["converged"] == 1
+    assert l1(g.history().cpu().numpy(), Ho) <= 1e-9
+    g.free()
+    grp.free()
