@@ -56,7 +56,8 @@ typedef enum {
 #define DI_DROP_SELF_LOOPS  0x2u  /* drop i -> i links (default folds them)            */
 #define DI_BUILD_CSC        0x4u  /* also build the in-link (CSC) index: pull variant, PI, GS     */
 #define DI_HOST_PTRS        0x8u  /* src/dst are host pointers (copied inside the call)           */
-#define DI_LOCAL_LINKS      0x10u /* multi-GPU: each rank passes only links whose src it owns     */
+#define DI_LOCAL_LINKS      0x10u /* reserved (multi-GPU, each rank passing only its own links):
+                                     not available in this build, DI_EINVAL                       */
 #define DI_NO_REORDER       0x20u /* keep the caller's node numbering internally (default relabels
                                      by descending in-degree for L2 locality; results are always
                                      returned in the caller's numbering)                          */
@@ -88,7 +89,8 @@ typedef enum {
 #define DI_BLOCKS(K)    ((((uint32_t)(K)) & 0xFFu) << 16)
 
 typedef struct {
-  int64_t sweeps;               /* bulk sweeps executed (incl. starvation fallbacks)            */
+  int64_t sweeps;               /* sweeps (bulk) or cycles (DI_BLOCKS, DI_ASYNC) executed, incl.
+                                   starvation fallbacks                                           */
   int64_t selected_total;       /* sum over sweeps of |S_n| (diffused nodes, dangling included)  */
   int64_t link_diffusions;      /* sum over sweeps of sum_{i in S_n} #out_i         */
   int64_t starvation_fallbacks; /* sweeps that selected nothing and forced one DI-CYC sweep (G5) */
