@@ -19,6 +19,8 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
@@ -47,6 +49,7 @@ const NcclApi &nccl() {
     DI_SYM(CommInitRank)
     DI_SYM(CommDestroy)
     DI_SYM(AllReduce)
+    DI_SYM(AllGather)
     DI_SYM(Send)
     DI_SYM(Recv)
     DI_SYM(GroupStart)
@@ -79,6 +82,10 @@ struct NcclComm : Comm {
   }
   di_status allreduce_i64(int64_t *dev, int count, cudaStream_t st) override {
     DI_NCK(nccl().AllReduce(dev, dev, (size_t)count, ncclInt64, ncclSum, comm, st));
+    return DI_OK;
+  }
+  di_status allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
+    DI_NCK(nccl().AllGather(send, recv, bytes, ncclUint8, comm, st));
     return DI_OK;
   }
   di_status exchange(const void *const *sbuf, const size_t *sbytes, void *const *rbuf,
@@ -121,6 +128,19 @@ struct GroupComm : Comm {
   }
   di_status allreduce_i64(int64_t *dev, int count, cudaStream_t st) override {
     return allreduce(dev, count, st, g->red_i);
+  }
+  di_status allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
+    std::vector<char> &mine = g->gat[rank];
+    mine.resize(bytes);
+    DI_CK(cudaMemcpyAsync(mine.data(), send, bytes, cudaMemcpyDeviceToHost, st));
+    DI_CK(cudaStreamSynchronize(st));
+    if (!g->barrier()) return aborted();
+    for (int p = 0; p < world; p++)
+      DI_CK(cudaMemcpyAsync((char *)recv + (size_t)p * bytes, g->gat[p].data(), bytes,
+                            cudaMemcpyHostToDevice, st));
+    DI_CK(cudaStreamSynchronize(st));
+    if (!g->barrier()) return aborted();  // nobody restages before everyone has copied
+    return DI_OK;
   }
   di_status exchange(const void *const *sbuf, const size_t *sbytes, void *const *rbuf,
                      const size_t *rbytes, cudaStream_t st) override {

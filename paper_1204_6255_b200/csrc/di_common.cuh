@@ -187,10 +187,16 @@ struct Graph {
   int32_t *tl = nullptr;          // touched remote ids, segment [b[p], b[p+1]) for owner p
   double *sval = nullptr;         // packed values of the touched ids (same segmentation)
   unsigned long long *tcnt = nullptr;  // touched count per owner (one 256-B line each)
-  int64_t *sendcnt = nullptr;     // device: entries for each peer this sweep, then received counts
-  int64_t *sendcnt_h = nullptr;   // pinned: [0, world) sent, [world, 2 world) received
-  double *dsum = nullptr;         // device: q, s, e (local, then global after the allreduce)
-  int64_t *isum = nullptr;        // device: selected, selected non-dangling, links, scanned
+  // per-sweep header of this rank, 8 + world int64 words: dsum (q, s, e, taken as fp64), isum
+  // (selected, non-dangling, links, scanned), sendcnt (entries for each peer); one allgather per
+  // sweep gives every rank all headers (global sums in rank order, its receive counts)
+  int64_t *hdr = nullptr;
+  int64_t *ghdr = nullptr;        // device: world headers after the allgather
+  int64_t *ghdr_h = nullptr;      // pinned copy of ghdr
+  int64_t *sendcnt = nullptr;     // views into hdr
+  double *dsum = nullptr;
+  int64_t *isum = nullptr;
+  int64_t *sendcnt_h = nullptr;   // unused (kept null)
   int32_t *rid = nullptr;         // received ids (global internal), capacity (world-1) * n
   double *rval = nullptr;         // received values
 };

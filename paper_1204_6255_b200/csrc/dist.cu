@@ -220,13 +220,22 @@ __global__ void k_apply_recv(double *__restrict__ F, int64_t lo, const int32_t *
 }
 
 // the single-GPU finaliser on the allreduced sums
-__global__ void k_dist_finalize(const SweepArgs a, const double *dsum, const int64_t *isum,
-                                int async) {
+// the single-GPU finaliser on the sums of the gathered headers (rank order: every rank computes
+// the same values bit for bit)
+__global__ void k_dist_finalize(const SweepArgs a, const int64_t *ghdr, int world, int async) {
   if (threadIdx.x != 0 || a.sc->stop) return;
-  // the asynchronous cycle reports the fluid it took from F (dsum[3]) instead of the fluid it
+  const int hw = 8 + world;
+  double d[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t c[4] = {0, 0, 0, 0};
+  for (int p = 0; p < world; p++) {
+    const int64_t *h = ghdr + (int64_t)p * hw;
+    for (int k = 0; k < 4; k++) d[k] += __longlong_as_double(h[k]);
+    for (int k = 0; k < 4; k++) c[k] += h[4 + k];
+  }
+  // the asynchronous cycle reports the fluid it took from F (d[3]) instead of the fluid it
   // left: r_{c+1} = r_c - taken + pushed, i.e. q = r_c - taken for apply_sweep's q + s
-  const double q = async ? __dsub_rn(a.sc->r, dsum[3]) : dsum[0];
-  SweepSums s{q, dsum[1], dsum[2], 0.0, isum[0], isum[1], isum[2], isum[3]};
+  const double q = async ? __dsub_rn(a.sc->r, d[3]) : d[0];
+  SweepSums s{q, d[1], d[2], 0.0, c[0], c[1], c[2], c[3]};
   apply_sweep(a, s);
 }
 
@@ -245,10 +254,11 @@ int grid_of(int64_t n, int sms) {
 // global sum F (exact local tree sum, then the allreduce); set_r: also r = that sum
 di_status global_sum_F(Graph &g, int set_r, int64_t *launches) {
   launch_reduce_F(g, launches);
-  k_copy_resid<<<1, 1, 0, g.stream>>>(g.sc, g.dsum + 3);
-  di_status s = g.comm->allreduce_f64(g.dsum + 3, 1, g.stream);
+  double *scratch = reinterpret_cast<double *>(g.hdr + 8 + g.world);
+  k_copy_resid<<<1, 1, 0, g.stream>>>(g.sc, scratch);
+  di_status s = g.comm->allreduce_f64(scratch, 1, g.stream);
   if (s != DI_OK) return s;
-  k_set_r<<<1, 1, 0, g.stream>>>(g.sc, g.dsum + 3, set_r);
+  k_set_r<<<1, 1, 0, g.stream>>>(g.sc, scratch, set_r);
   *launches += 2;
   return DI_OK;
 }
@@ -264,11 +274,14 @@ di_status alloc_dist(Graph &g) {
   DI_CK(dmalloc(&g.sval, (size_t)N * 8));
   DI_CK(dmalloc(&g.tcnt, (size_t)G * 32 * 8));
   DI_CK(dmemset(g.tcnt, 0, (size_t)G * 32 * 8));
-  DI_CK(dmalloc(&g.sendcnt, (size_t)2 * G * 8));
-  DI_CK(dmemset(g.sendcnt, 0, (size_t)2 * G * 8));
-  DI_CK(cudaMallocHost(&g.sendcnt_h, (size_t)2 * G * 8 + 8 * 8));
-  DI_CK(dmalloc(&g.dsum, 8 * 8));
-  DI_CK(dmalloc(&g.isum, 8 * 8));
+  const size_t hw = (size_t)(8 + G);
+  DI_CK(dmalloc(&g.hdr, 8 * 8 + hw * 8));   // +8 words: global_sum_F's scratch at dsum[3..]
+  DI_CK(dmemset(g.hdr, 0, 8 * 8 + hw * 8));
+  DI_CK(dmalloc(&g.ghdr, (size_t)G * hw * 8));
+  DI_CK(cudaMallocHost(&g.ghdr_h, (size_t)G * hw * 8));
+  g.dsum = reinterpret_cast<double *>(g.hdr);
+  g.isum = g.hdr + 4;
+  g.sendcnt = g.hdr + 8;
   const size_t cap = (size_t)std::max<int64_t>(1, (int64_t)(G - 1) * g.n);
   DI_CK(dmalloc(&g.rid, cap * 4));
   DI_CK(dmalloc(&g.rval, cap * 8));
@@ -276,10 +289,10 @@ di_status alloc_dist(Graph &g) {
 }
 
 void free_dist(Graph &g) {
-  void *p[] = {g.R, g.tl, g.sval, g.tcnt, g.sendcnt, g.dsum, g.isum, g.rid, g.rval};
+  void *p[] = {g.R, g.tl, g.sval, g.tcnt, g.hdr, g.ghdr, g.rid, g.rval};
   for (void *q : p)
     if (q) dfree(q);
-  if (g.sendcnt_h) cudaFreeHost(g.sendcnt_h);
+  if (g.ghdr_h) cudaFreeHost(g.ghdr_h);
   delete g.comm;
   g.comm = nullptr;
 }
@@ -288,7 +301,7 @@ di_status dist_residual(Graph &g, double *l1) {
   int64_t launches = 0;
   di_status s = global_sum_F(g, 0, &launches);
   if (s != DI_OK) return s;
-  DI_CK(cudaMemcpyAsync(l1, g.dsum + 3, 8, cudaMemcpyDeviceToHost, g.stream));
+  DI_CK(cudaMemcpyAsync(l1, g.hdr + 8 + g.world, 8, cudaMemcpyDeviceToHost, g.stream));
   DI_CK(cudaStreamSynchronize(g.stream));
   return DI_OK;
 }
@@ -340,13 +353,10 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   else
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push_dist<false>, kPushThreads, 0);
   occ = std::max(1, occ);
-  std::vector<const void *> sb(G), sbv(G), cb_s(G);
-  std::vector<void *> rb(G), rbv(G), cb_r(G);
-  std::vector<size_t> s4(G), r4(G), s8(G), r8(G), c8(G, 8);
-  for (int p = 0; p < G; p++) {
-    cb_s[p] = g.sendcnt + p;
-    cb_r[p] = g.sendcnt + G + p;
-  }
+  std::vector<const void *> sb(G), sbv(G);
+  std::vector<void *> rb(G), rbv(G);
+  std::vector<size_t> s4(G), r4(G), s8(G), r8(G);
+  const size_t hw = (size_t)(8 + G);
   double xbytes = 0.0;
   int64_t xentries = 0;
   int64_t launched = 0;
@@ -371,11 +381,9 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       k_pack<<<g.num_sms * 4, 256, 0, g.stream>>>(g.sc, x);
       launches += 2;
       launched++;
-      if ((s = g.comm->allreduce_f64(g.dsum, 4, g.stream)) != DI_OK) return s;
-      if ((s = g.comm->allreduce_i64(g.isum, 4, g.stream)) != DI_OK) return s;
-      if ((s = g.comm->exchange(cb_s.data(), c8.data(), cb_r.data(), c8.data(), g.stream)) != DI_OK)
-        return s;
-      DI_CK(cudaMemcpyAsync(g.sendcnt_h, g.sendcnt, (size_t)2 * G * 8, cudaMemcpyDeviceToHost,
+      // one collective for the sums and the per-peer counts of every rank
+      if ((s = g.comm->allgather(g.hdr, g.ghdr, (size_t)hw * 8, g.stream)) != DI_OK) return s;
+      DI_CK(cudaMemcpyAsync(g.ghdr_h, g.ghdr, (size_t)G * hw * 8, cudaMemcpyDeviceToHost,
                             g.stream));
       DI_CK(cudaMemcpyAsync(g.sc_host, g.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, g.stream));
       DI_CK(cudaStreamSynchronize(g.stream));
@@ -394,8 +402,8 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       }
       int64_t off = 0;
       for (int p = 0; p < G; p++) {
-        const int64_t ns = (p == me) ? 0 : g.sendcnt_h[p];
-        const int64_t nr = (p == me) ? 0 : g.sendcnt_h[G + p];
+        const int64_t ns = (p == me) ? 0 : g.ghdr_h[(size_t)me * hw + 8 + p];
+        const int64_t nr = (p == me) ? 0 : g.ghdr_h[(size_t)p * hw + 8 + me];
         sb[p] = g.tl + g.bounds.b[p];
         sbv[p] = g.sval + g.bounds.b[p];
         s4[p] = (size_t)ns * 4;
@@ -415,7 +423,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
         k_apply_recv<<<grid_of(off, g.num_sms), 256, 0, g.stream>>>(g.F, g.lo, g.rid, g.rval, off);
         launches++;
       }
-      k_dist_finalize<<<1, 32, 0, g.stream>>>(a, g.dsum, g.isum, async ? 1 : 0);
+      k_dist_finalize<<<1, 32, 0, g.stream>>>(a, g.ghdr, G, async ? 1 : 0);
       launches++;
       if (prof) {  // exchange of the lists + apply (the counts exchange is in the sync above)
         DI_CK(cudaEventRecord(pe[0], g.stream));
