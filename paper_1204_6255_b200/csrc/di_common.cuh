@@ -185,7 +185,7 @@ struct Graph {
   struct Group *group = nullptr;
   double *R = nullptr;            // remote fluid accumulator, fp64[n_global], all-zero between sweeps
   int32_t *tl = nullptr;          // touched remote ids, segment [b[p], b[p+1]) for owner p
-  double *sval = nullptr;         // packed values of the touched ids (same segmentation)
+  double *sval = nullptr;         // packed 12-byte (id, value) records of the touched ids
   unsigned long long *tcnt = nullptr;  // touched count per owner (one 256-B line each)
   // per-sweep header of this rank, 8 + world int64 words: dsum (q, s, e, taken as fp64), isum
   // (selected, non-dangling, links, scanned), sendcnt (entries for each peer); one allgather per
@@ -197,8 +197,7 @@ struct Graph {
   double *dsum = nullptr;
   int64_t *isum = nullptr;
   int64_t *sendcnt_h = nullptr;   // unused (kept null)
-  int32_t *rid = nullptr;         // received ids (global internal), capacity (world-1) * n
-  double *rval = nullptr;         // received values
+  int32_t *rid = nullptr;         // received 12-byte records, capacity (world-1) * n
 };
 
 // ---------------------------------------------------------------- device memory

@@ -13,8 +13,8 @@
 //                    writes this rank's sweep sums and per-peer counts.
 //   3. k_pack      — for every touched j: value = R[j], R[j] = 0 (R is clean for the next sweep).
 //   4. allreduce of the sweep sums; exchange of the per-peer counts (8 B per peer).
-//   5. exchange of the (id int32, value fp64) lists — 12 B per distinct (remote target, sweep)
-//      pair, the algorithmic exchange of SURVEY §8(d).
+//   5. exchange of the (id int32, value fp64) records — 12 B per distinct (remote target, sweep)
+//      pair, the algorithmic exchange of SURVEY §8(d), one send per peer.
 //   6. k_apply_recv — F[j - lo] += value (RED: several peers may send the same j).
 //   7. k_dist_finalize — the single-GPU finaliser on the global sums: every rank takes the same
 //      stop / guard decision.
@@ -205,18 +205,27 @@ __global__ void k_pack(const Scalars *sc, DistArgs x) {
     const int64_t m = x.sendcnt[p], off = x.bd.b[p];
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
          k += (int64_t)gridDim.x * blockDim.x) {
+      // 12-byte record (id, value) in 3 int32 words: the algorithmic exchange, one send per peer
       const int32_t j = x.tl[off + k];
-      x.sval[off + k] = x.R[j];
+      const double v = x.R[j];
       x.R[j] = 0.0;
+      int32_t *rec = reinterpret_cast<int32_t *>(x.sval) + 3 * (off + k);
+      const long long bits = __double_as_longlong(v);
+      rec[0] = j;
+      rec[1] = (int32_t)(bits & 0xffffffffll);
+      rec[2] = (int32_t)(bits >> 32);
     }
   }
 }
 
-__global__ void k_apply_recv(double *__restrict__ F, int64_t lo, const int32_t *__restrict__ rid,
-                             const double *__restrict__ rval, int64_t m) {
+__global__ void k_apply_recv(double *__restrict__ F, int64_t lo, const int32_t *__restrict__ rec,
+                             int64_t m) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
-       k += (int64_t)gridDim.x * blockDim.x)
-    red_add_f64(F + ((int64_t)rid[k] - lo), rval[k]);
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t *r = rec + 3 * k;
+    const double v = __longlong_as_double(((long long)(uint32_t)r[1]) | ((long long)r[2] << 32));
+    red_add_f64(F + ((int64_t)r[0] - lo), v);
+  }
 }
 
 // the single-GPU finaliser on the allreduced sums
@@ -271,7 +280,7 @@ di_status alloc_dist(Graph &g) {
   DI_CK(dmalloc(&g.R, (size_t)N * 8));
   DI_CK(dmemset(g.R, 0, (size_t)N * 8));
   DI_CK(dmalloc(&g.tl, (size_t)N * 4));
-  DI_CK(dmalloc(&g.sval, (size_t)N * 8));
+  DI_CK(dmalloc(&g.sval, (size_t)N * 12));   // send records, segment p at record b[p]
   DI_CK(dmalloc(&g.tcnt, (size_t)G * 32 * 8));
   DI_CK(dmemset(g.tcnt, 0, (size_t)G * 32 * 8));
   const size_t hw = (size_t)(8 + G);
@@ -283,13 +292,12 @@ di_status alloc_dist(Graph &g) {
   g.isum = g.hdr + 4;
   g.sendcnt = g.hdr + 8;
   const size_t cap = (size_t)std::max<int64_t>(1, (int64_t)(G - 1) * g.n);
-  DI_CK(dmalloc(&g.rid, cap * 4));
-  DI_CK(dmalloc(&g.rval, cap * 8));
+  DI_CK(dmalloc(&g.rid, cap * 12));          // received records
   return DI_OK;
 }
 
 void free_dist(Graph &g) {
-  void *p[] = {g.R, g.tl, g.sval, g.tcnt, g.hdr, g.ghdr, g.rid, g.rval};
+  void *p[] = {g.R, g.tl, g.sval, g.tcnt, g.hdr, g.ghdr, g.rid};
   for (void *q : p)
     if (q) dfree(q);
   if (g.ghdr_h) cudaFreeHost(g.ghdr_h);
@@ -353,9 +361,9 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   else
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push_dist<false>, kPushThreads, 0);
   occ = std::max(1, occ);
-  std::vector<const void *> sb(G), sbv(G);
-  std::vector<void *> rb(G), rbv(G);
-  std::vector<size_t> s4(G), r4(G), s8(G), r8(G);
+  std::vector<const void *> sb(G);
+  std::vector<void *> rb(G);
+  std::vector<size_t> s12(G), r12(G);
   const size_t hw = (size_t)(8 + G);
   double xbytes = 0.0;
   int64_t xentries = 0;
@@ -404,23 +412,17 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       for (int p = 0; p < G; p++) {
         const int64_t ns = (p == me) ? 0 : g.ghdr_h[(size_t)me * hw + 8 + p];
         const int64_t nr = (p == me) ? 0 : g.ghdr_h[(size_t)p * hw + 8 + me];
-        sb[p] = g.tl + g.bounds.b[p];
-        sbv[p] = g.sval + g.bounds.b[p];
-        s4[p] = (size_t)ns * 4;
-        s8[p] = (size_t)ns * 8;
-        rb[p] = g.rid + off;
-        rbv[p] = g.rval + off;
-        r4[p] = (size_t)nr * 4;
-        r8[p] = (size_t)nr * 8;
+        sb[p] = reinterpret_cast<const char *>(g.sval) + (size_t)12 * g.bounds.b[p];
+        s12[p] = (size_t)ns * 12;
+        rb[p] = reinterpret_cast<char *>(g.rid) + (size_t)12 * off;
+        r12[p] = (size_t)nr * 12;
         off += nr;
         xentries += ns;
       }
-      if ((s = g.comm->exchange(sb.data(), s4.data(), rb.data(), r4.data(), g.stream)) != DI_OK)
-        return s;
-      if ((s = g.comm->exchange(sbv.data(), s8.data(), rbv.data(), r8.data(), g.stream)) != DI_OK)
+      if ((s = g.comm->exchange(sb.data(), s12.data(), rb.data(), r12.data(), g.stream)) != DI_OK)
         return s;
       if (off > 0) {
-        k_apply_recv<<<grid_of(off, g.num_sms), 256, 0, g.stream>>>(g.F, g.lo, g.rid, g.rval, off);
+        k_apply_recv<<<grid_of(off, g.num_sms), 256, 0, g.stream>>>(g.F, g.lo, g.rid, off);
         launches++;
       }
       k_dist_finalize<<<1, 32, 0, g.stream>>>(a, g.ghdr, G, async ? 1 : 0);
