@@ -217,6 +217,7 @@ def run_ours(args):
     roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": tr,
+                "frac_vs_8TBps_spec": round(achieved / 8000.0, 4),
                 "peak_source": peak_src,
                 "bytes_per_launch": push_bytes / max(push_launches, 1),
                 "avg_launch_ms": push_ms / max(push_launches, 1),
@@ -231,6 +232,18 @@ def run_ours(args):
                            "peak_G_per_s": RED_PEAK, "unit": "G fp64 RED/s"}}
 
     gl_ms = round(statistics.median(ptimes), 3)       # the profiled host-loop solve, for reference
+    # warm number (report cold and warm): the same solve without the L2 flush
+    warm = []
+    for _ in range(3):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.solve(d=D, tol=TOL, variant=args.variant, mode=args.mode, blocks=args.blocks,
+                graph_loop=use_graph, asynchronous=use_async)
+        e1.record(stream)
+        e1.synchronize()
+        warm.append(e0.elapsed_time(e1))
+    warm_ms = round(statistics.median(warm), 3)
 
     # ---- e2e through the C ABI with host buffers (H2D of the link list, build, solve, D2H of H)
     src_p = torch.from_numpy(src).pin_memory()
@@ -289,6 +302,7 @@ def run_ours(args):
                    else "single GPU",
                    "init_build_ms": round(init_ms, 1), "generator_s": round(gen_s, 1)},
         "time_to_tol_ms": round(ms_per_step, 3),
+        "warm_ms_per_step": warm_ms,
         "sweeps": stats[-1]["sweeps"], "equivalent_iterations": round(stats[-1]["equivalent_iterations"], 2),
         "residual_l1": stats[-1]["residual_l1"],
         "hbm_frac_counted_whole_solve": round(counted / (tot_ms * 1e-3) / 1e9 / peak, 4),
