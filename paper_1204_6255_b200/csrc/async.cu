@@ -55,8 +55,8 @@ __device__ __forceinline__ void red_group_rep(double *__restrict__ F, double *__
   }
 }
 
-// DIST: targets are global internal ids; a target outside this rank's range goes through the
-// remote accumulator and first-touch lists (push_remote, sweep.cuh).
+// DIST: targets are global internal ids; a target outside this rank's range gets a RED into the
+// remote accumulator (push_remote, sweep.cuh).
 template <bool LOOPS, bool DIST>
 __device__ __forceinline__ void push_group(const SweepArgs &a, const DistArgs &x, double *rep,
                                            int hot_shift, int32_t hot_lim, int copy, int4 q,
@@ -365,12 +365,7 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
     }
   }
   const SweepSums sm = reduce_partials(a, gridDim.x, kAsyncThreads);
-  if (DIST) {  // this rank's sums and per-peer counts; the host exchanges, k_dist_finalize applies
-    if (threadIdx.x < x.bd.world) {
-      volatile unsigned long long *cnt = x.tcnt + 32 * threadIdx.x;
-      x.sendcnt[threadIdx.x] = (int64_t)*cnt;
-      *cnt = 0ull;
-    }
+  if (DIST) {  // this rank's sums; k_compact_remote counts, the host exchanges, finalize applies
     if (threadIdx.x == 0) {
       x.dsum[0] = 0.0;
       x.dsum[1] = sm.s;

@@ -184,9 +184,8 @@ struct Graph {
   struct Comm *comm = nullptr;
   struct Group *group = nullptr;
   double *R = nullptr;            // remote fluid accumulator, fp64[n_global], all-zero between sweeps
-  int32_t *tl = nullptr;          // touched remote ids, segment [b[p], b[p+1]) for owner p
   double *sval = nullptr;         // packed 12-byte (id, value) records of the touched ids
-  unsigned long long *tcnt = nullptr;  // touched count per owner (one 256-B line each)
+  unsigned long long *tcnt = nullptr;  // records per owner (one 256-B line each) + a ticket
   // per-sweep header of this rank, 8 + world int64 words: dsum (q, s, e, taken as fp64), isum
   // (selected, non-dangling, links, scanned), sendcnt (entries for each peer); one allgather per
   // sweep gives every rank all headers (global sums in rank order, its receive counts)

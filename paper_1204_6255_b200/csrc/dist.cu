@@ -5,13 +5,11 @@
 // partition. Rank g owns nodes [lo, hi) (F, H, deg, kloop and the CSR rows of its sources with
 // global column ids). One sweep on every rank:
 //   1. k_select    — the single-GPU select/compact kernel on the owned nodes, global r_n.
-//   2. k_push_dist — degree-binned push; a local target gets a RED into F, a remote target j an
-//                    fp64 atomicAdd into the remote accumulator R[j] (global size, all-zero
-//                    between sweeps). The add that finds R[j] == 0.0 is the first touch of j this
-//                    sweep (v > 0 and sums of positives never return to 0), and appends j to
-//                    the touched list of j's owner (warp-aggregated reservation). Its last block
-//                    writes this rank's sweep sums and per-peer counts.
-//   3. k_pack      — for every touched j: value = R[j], R[j] = 0 (R is clean for the next sweep).
+//   2. k_push_dist — degree-binned push; a local target gets a RED into F, a remote target j a
+//                    RED into the remote accumulator R[j] (global size, all-zero between
+//                    sweeps). Its last block writes this rank's sweep sums.
+//   3. k_compact_remote — one scan over R's remote segments: nonzero entries become (id, value)
+//                    records in their owner's send segment, R back to zero, per-peer counts.
 //   4. allreduce of the sweep sums; exchange of the per-peer counts (8 B per peer).
 //   5. exchange of the (id int32, value fp64) records — 12 B per distinct (remote target, sweep)
 //      pair, the algorithmic exchange of SURVEY §8(d), one send per peer.
@@ -34,44 +32,16 @@ namespace di {
 namespace {
 
 
-__device__ __forceinline__ int owner_of(const DistBounds &bd, int64_t j) {
-  int p = 0;
-#pragma unroll 1
-  for (int q = 1; q < bd.world; q++) p += (j >= bd.b[q]) ? 1 : 0;
-  return p;
-}
 
-// One target of one link, executed by all 32 lanes of a warp in convergence (the callers' loops
-// are warp-uniform); `valid` masks the lanes without a target.
+// One target of one link: a RED into F (local) or into the remote accumulator R.
 __device__ __forceinline__ void dist_add(const SweepArgs &a, const DistArgs &x, int32_t j, double v,
                                          bool valid, uint64_t fpol) {
-  const int lane = threadIdx.x & 31;
-  bool first = false;
-  int p = -1;
-  if (valid) {
-    const int64_t jl = (int64_t)j - a.lo;
-    if (jl >= 0 && jl < a.n) {
-      red_add_f64_hint(a.F + jl, v, fpol);
-    } else {
-      const double old = atomicAdd(x.R + j, v);
-      if (old == 0.0) {
-        first = true;
-        p = owner_of(x.bd, j);
-      }
-    }
-  }
-  const unsigned fm = __ballot_sync(0xffffffffu, first);
-  if (fm == 0u) return;
-  const unsigned peers = __match_any_sync(0xffffffffu, p);
-  const int leader = __ffs(peers) - 1;
-  unsigned long long base = 0;
-  if (first && lane == leader)
-    base = atomicAdd(x.tcnt + 32 * p, (unsigned long long)__popc(peers));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  if (first) {
-    const unsigned lt = peers & ((1u << lane) - 1u);
-    x.tl[x.bd.b[p] + (int64_t)base + __popc(lt)] = j;
-  }
+  if (!valid) return;
+  const int64_t jl = (int64_t)j - a.lo;
+  if (jl >= 0 && jl < a.n)
+    red_add_f64_hint(a.F + jl, v, fpol);
+  else
+    push_remote(x, j, v);
 }
 
 template <bool LOOPS>
@@ -87,7 +57,7 @@ __device__ __forceinline__ void dist_group(const SweepArgs &a, const DistArgs &x
   }
 }
 
-// The bins of k_push (diffusion.cu), with warp-uniform loops so that dist_add can aggregate.
+// The bins of k_push (diffusion.cu) with the local / remote routing of dist_add.
 template <bool LOOPS>
 __global__ void __launch_bounds__(kPushThreads) k_push_dist(const SweepArgs a, const DistArgs x) {
   __shared__ bool s_last;
@@ -190,32 +160,93 @@ __global__ void __launch_bounds__(kPushThreads) k_push_dist(const SweepArgs a, c
     x.isum[3] = s.scanned;
     sc->ticket = 0;
   }
-  if (threadIdx.x < x.bd.world) {
-    volatile unsigned long long *c = x.tcnt + 32 * threadIdx.x;
-    x.sendcnt[threadIdx.x] = (int64_t)*c;
-    *c = 0ull;
-  }
 }
 
-// value of every touched remote id; R back to all-zero
-__global__ void k_pack(const Scalars *sc, DistArgs x) {
+// Compaction of the remote accumulator (after the push, before the exchange): for every owner
+// p != rank, the nonzero entries of R[b[p], b[p+1]) become 12-byte (id, value) records in p's
+// send segment, and R returns to all-zero. Chunks of kCompChunk consecutive ids; each block
+// reserves its chunk's records with one atomic (block scan for the positions), so the counter
+// atomics are per chunk, not per entry. The last block publishes the per-peer counts into the
+// sweep header and rewinds the counters. Record order inside a segment is the (free) reservation
+// order; the receiver adds every record with a RED.
+constexpr int kCompThreads = 256, kCompPer = 16, kCompChunk = kCompThreads * kCompPer;
+
+__global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *sc, DistArgs x) {
+  __shared__ int s_w[kCompThreads / 32];
+  __shared__ unsigned long long s_base;
+  __shared__ bool s_last;
   if (sc->stop) return;
-  for (int p = 0; p < x.bd.world; p++) {
-    if (p == x.rank) continue;
-    const int64_t m = x.sendcnt[p], off = x.bd.b[p];
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
-         k += (int64_t)gridDim.x * blockDim.x) {
-      // 12-byte record (id, value) in 3 int32 words: the algorithmic exchange, one send per peer
-      const int32_t j = x.tl[off + k];
-      const double v = x.R[j];
-      x.R[j] = 0.0;
-      int32_t *rec = reinterpret_cast<int32_t *>(x.sval) + 3 * (off + k);
-      const long long bits = __double_as_longlong(v);
-      rec[0] = j;
-      rec[1] = (int32_t)(bits & 0xffffffffll);
-      rec[2] = (int32_t)(bits >> 32);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // chunk index space: owners in order, chunks of kCompChunk ids inside each (own range skipped)
+  int64_t nchunks = 0;
+  for (int p = 0; p < x.bd.world; p++)
+    if (p != x.rank) nchunks += (x.bd.b[p + 1] - x.bd.b[p] + kCompChunk - 1) / kCompChunk;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    int p = 0;
+    int64_t cc = c;
+    for (; p < x.bd.world; p++) {
+      if (p == x.rank) continue;
+      const int64_t k = (x.bd.b[p + 1] - x.bd.b[p] + kCompChunk - 1) / kCompChunk;
+      if (cc < k) break;
+      cc -= k;
     }
+    const int64_t j0 = x.bd.b[p] + cc * kCompChunk + (int64_t)threadIdx.x * kCompPer;
+    const int64_t jend = x.bd.b[p + 1];
+    double v[kCompPer];
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kCompPer; k++) {
+      v[k] = (j0 + k < jend) ? __ldcg(x.R + j0 + k) : 0.0;
+      cnt += (v[k] != 0.0) ? 1 : 0;
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kCompThreads / 32; w++) {
+      before += (w < warp) ? s_w[w] : 0;
+      total += s_w[w];
+    }
+    if (threadIdx.x == 0)
+      s_base = total ? atomicAdd(x.tcnt + 32 * p, (unsigned long long)total) : 0ull;
+    __syncthreads();
+    int64_t pos = x.bd.b[p] + (int64_t)s_base + before + incl - cnt;
+    int32_t *recs = reinterpret_cast<int32_t *>(x.sval);
+#pragma unroll
+    for (int k = 0; k < kCompPer; k++) {
+      if (v[k] == 0.0) continue;
+      const long long bits = __double_as_longlong(v[k]);
+      int32_t *r = recs + 3 * pos;
+      r[0] = (int32_t)(j0 + k);
+      r[1] = (int32_t)(bits & 0xffffffffll);
+      r[2] = (int32_t)(bits >> 32);
+      x.R[j0 + k] = 0.0;
+      pos++;
+    }
+    __syncthreads();  // s_w / s_base reused by the next chunk
   }
+  // the last block: per-peer counts into the header, counters rewound
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(reinterpret_cast<unsigned int *>(x.tcnt + 32 * x.bd.world), 1u) ==
+             gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < x.bd.world) {
+    volatile unsigned long long *cn = x.tcnt + 32 * threadIdx.x;
+    x.sendcnt[threadIdx.x] = (threadIdx.x == x.rank) ? 0 : (int64_t)*cn;
+    *cn = 0ull;
+  }
+  if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned int *>(x.tcnt + 32 * x.bd.world) = 0u;
 }
 
 __global__ void k_apply_recv(double *__restrict__ F, int64_t lo, const int32_t *__restrict__ rec,
@@ -279,10 +310,9 @@ di_status alloc_dist(Graph &g) {
   const int G = g.world;
   DI_CK(dmalloc(&g.R, (size_t)N * 8));
   DI_CK(dmemset(g.R, 0, (size_t)N * 8));
-  DI_CK(dmalloc(&g.tl, (size_t)N * 4));
   DI_CK(dmalloc(&g.sval, (size_t)N * 12));   // send records, segment p at record b[p]
-  DI_CK(dmalloc(&g.tcnt, (size_t)G * 32 * 8));
-  DI_CK(dmemset(g.tcnt, 0, (size_t)G * 32 * 8));
+  DI_CK(dmalloc(&g.tcnt, (size_t)(G + 1) * 32 * 8));   // + the compaction's block ticket
+  DI_CK(dmemset(g.tcnt, 0, (size_t)(G + 1) * 32 * 8));
   const size_t hw = (size_t)(8 + G);
   DI_CK(dmalloc(&g.hdr, 8 * 8 + hw * 8));   // +8 words: global_sum_F's scratch at dsum[3..]
   DI_CK(dmemset(g.hdr, 0, 8 * 8 + hw * 8));
@@ -297,7 +327,7 @@ di_status alloc_dist(Graph &g) {
 }
 
 void free_dist(Graph &g) {
-  void *p[] = {g.R, g.tl, g.sval, g.tcnt, g.hdr, g.ghdr, g.rid};
+  void *p[] = {g.R, g.sval, g.tcnt, g.hdr, g.ghdr, g.rid};
   for (void *q : p)
     if (q) dfree(q);
   if (g.ghdr_h) cudaFreeHost(g.ghdr_h);
@@ -342,7 +372,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   DI_CK(cudaEventRecord(t0, g.stream));
   DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
   DI_CK(cudaMemsetAsync(g.R, 0, (size_t)g.n_global * 8, g.stream));
-  DI_CK(cudaMemsetAsync(g.tcnt, 0, (size_t)G * 32 * 8, g.stream));
+  DI_CK(cudaMemsetAsync(g.tcnt, 0, (size_t)(G + 1) * 32 * 8, g.stream));
   di_status s = DI_OK;
   if (!resume) {
     launch_init(g, B, d, &launches);  // F = B (local slice), H = 0; local sum
@@ -386,7 +416,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       else
         k_push_dist<false><<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a, x);
       if (prof) DI_CK(cudaEventRecord(pe[2], g.stream));
-      k_pack<<<g.num_sms * 4, 256, 0, g.stream>>>(g.sc, x);
+      k_compact_remote<<<g.num_sms * 4, kCompThreads, 0, g.stream>>>(g.sc, x);
       launches += 2;
       launched++;
       // one collective for the sums and the per-peer counts of every rank
