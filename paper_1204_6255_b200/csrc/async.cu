@@ -158,16 +158,30 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
       }
       rb[kSelItems] = base < a.n ? a.row_ptr[a.n] : 0;
     }
+    // the selection test for the 4 nodes first, then all their exchanges in flight together
+    // (one round trip per tile instead of one per selected node)
+    int o4[kSelItems];
+    double T04[kSelItems];
 #pragma unroll
     for (int j = 0; j < kSelItems; j++) {
       const int64_t i = base + j;
+      o4[j] = -1;  // not selected
       if (i >= a.n) continue;
       const int64_t rend = (i + 1 < a.n) ? (j + 1 < kSelItems ? rb[j + 1] : rb[kSelItems])
                                          : a.row_ptr[a.n];
       const int o = (int)(rend - rb[j]);
       const double thr = cyc ? 0.0 : __dmul_rn(t, (double)o);  // (r/L)*out[i]
-      if (!(f[j] > thr)) continue;                              // strict '>'
-      const double T0 = take_fluid(F + i);                     // >= f[j]: only REDs add meanwhile
+      if (f[j] > thr) o4[j] = o;                                // strict '>'
+    }
+#pragma unroll
+    for (int j = 0; j < kSelItems; j++)
+      T04[j] = (o4[j] >= 0) ? take_fluid(F + base + j) : 0.0;  // >= f[j]: only REDs add meanwhile
+#pragma unroll
+    for (int j = 0; j < kSelItems; j++) {
+      if (o4[j] < 0) continue;
+      const int64_t i = base + j;
+      const int o = o4[j];
+      const double T0 = T04[j];
       double T = T0;
       if (LOOPS && kl[j] > 0) {                                 // P:259-263 with k copies (G6)
         const double od = (double)o;
