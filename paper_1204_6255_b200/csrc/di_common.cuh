@@ -184,7 +184,7 @@ struct Graph {
   struct Comm *comm = nullptr;
   struct Group *group = nullptr;
   double *R = nullptr;            // remote fluid accumulator, fp64[n_global], all-zero between sweeps
-  double *sval = nullptr;         // packed 12-byte (id, value) records of the touched ids
+  double *sval = nullptr;         // send records: 12-byte (id, value), owner p's segment at b[p]
   unsigned long long *tcnt = nullptr;  // records per owner (one 256-B line each) + a ticket
   // per-sweep header of this rank, 8 + world int64 words: dsum (q, s, e, taken as fp64), isum
   // (selected, non-dangling, links, scanned), sendcnt (entries for each peer); one allgather per
@@ -195,7 +195,6 @@ struct Graph {
   int64_t *sendcnt = nullptr;     // views into hdr
   double *dsum = nullptr;
   int64_t *isum = nullptr;
-  int64_t *sendcnt_h = nullptr;   // unused (kept null)
   int32_t *rid = nullptr;         // received 12-byte records, capacity (world-1) * n
 };
 

@@ -260,12 +260,12 @@ __device__ __forceinline__ void red_group(double *__restrict__ F, int4 x, int64_
 }
 
 // blk / blocks: sub-sweep blk of `blocks` block-ordered sub-sweeps (tile range [t0, t1))
-// Multi-GPU sweep state (dist.cu, async.cu): remote accumulator, first-touch lists, exchanges.
+// Multi-GPU sweep state (dist.cu, async.cu): remote accumulator, send records, sweep header.
 struct DistArgs {
   double *R;
   double *sval;
-  unsigned long long *tcnt;  // [world * 32]: touched count per owner, one line each
-  int64_t *sendcnt;          // [world]
+  unsigned long long *tcnt;  // [(world + 1) * 32]: records per owner, one line each; a ticket
+  int64_t *sendcnt;          // [world] (view into the sweep header)
   double *dsum;              // q, s, e, taken
   int64_t *isum;             // sel, nd, lk, scanned
   DistBounds bd;
