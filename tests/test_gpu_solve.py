@@ -231,6 +231,19 @@ def test_async_cycles(graph_loop):
     st = g.solve(d=D, tol=1e-12, **kw)
     assert st["converged"] == 1 and st["sweeps"] == 1
     g.free()
+    # resume after max_sweeps, custom B, the paper's stop
+    src, dst, n = digen.make("c1", seed=3)
+    g = upload(src, dst, n)
+    rng = np.random.default_rng(9)
+    Bc = rng.random(n) * (1 - D) / n * 2
+    st = g.solve(d=D, tol=1e-12, B=Bc, max_sweeps=4, **kw)
+    assert st["status"] == di.DI_NOT_CONVERGED and st["sweeps"] == 4
+    st = g.solve(d=D, tol=1e-12, B=Bc, resume=True, **kw)
+    assert st["converged"] == 1
+    assert l1(g.history().cpu().numpy(), defn.solve_sparse(src, dst, n, D, B=Bc)) <= 1e-12 / (1 - D)
+    st = g.solve(d=D, tol=1.0 / n, paper_error=True, **kw)
+    assert st["converged"] == 1 and st["error_estimate"] <= 1.0 / n
+    g.free()
     # skewed in-degrees on a power-of-two stripe length: the replicated hot accumulators path
     # (N = 4096 * 8, three targets with 4 %, 2 %, 1 % of all links)
     n = 4096 * 8
