@@ -22,9 +22,21 @@ namespace di {
 namespace {
 
 constexpr int kAsyncThreads = 256;
-constexpr int kAsyncSmall = 16;      // rows with <= this many links: pushed by the selecting thread
-constexpr int kAsyncMid = 256;      // rows up to this: one 8-lane group each (list front)
-constexpr int kAsyncChunk = 1024;   // longer rows: chunks of this many links, one warp each
+#ifndef DI_ASYNC_SMALL
+#define DI_ASYNC_SMALL 16
+#endif
+#ifndef DI_ASYNC_MID
+#define DI_ASYNC_MID 256
+#endif
+#ifndef DI_ASYNC_CHUNK
+#define DI_ASYNC_CHUNK 1024
+#endif
+#ifndef DI_ASYNC_MINB   // CTAs per SM: 3 (vs 4) narrows the window of tiles in flight, a more
+#define DI_ASYNC_MINB 3  // sequential order: C4 43 -> 42 cycles (58.7 ms), C2 3.6 -> 3.2 ms, same rate
+#endif
+constexpr int kAsyncSmall = DI_ASYNC_SMALL;  // rows with <= this many links: a lane each
+constexpr int kAsyncMid = DI_ASYNC_MID;      // rows up to this: one 8-lane group each (list front)
+constexpr int kAsyncChunk = DI_ASYNC_CHUNK;  // longer rows: chunks of this many links, one warp each
 
 // Replicated accumulators for the hottest targets. Same-address fp64 REDs serialise in one L2
 // slice; a node that receives a large share of all pushes (C3's Zipf targets: the top node gets
@@ -86,7 +98,7 @@ __device__ __forceinline__ double take_fluid(double *p) {
 }
 
 template <bool LOOPS, bool DIST>
-__global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, const DistArgs x) {
+__global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const SweepArgs a, const DistArgs x) {
   constexpr int NW = kAsyncThreads / 32;
   __shared__ int64_t s_rb[kSelTile];   // long rows of the tile: first link
   __shared__ int32_t s_ro[kSelTile];   // #links
@@ -290,14 +302,15 @@ __global__ void __launch_bounds__(kAsyncThreads, 4) k_cycle(const SweepArgs a, c
           const int64_t beg = a.row_ptr[tb + li], end = a.row_ptr[tb + li + 1], a0 = beg & ~3ll;
           const int nvec = (int)((end - a0 + 3) >> 2);
           const int32_t gi = LOOPS ? (int32_t)(tb + li + a.lo) : -1;
-          int4 xs[5];
+          constexpr int NG = (kAsyncSmall + 6) / 4;   // aligned int4 groups of a short row
+          int4 xs[NG];
 #pragma unroll
-          for (int u = 0; u < 5; u++) {
+          for (int u = 0; u < NG; u++) {
             xs[u] = make_int4(0, 0, 0, 0);
             if (u < nvec) xs[u] = ld_col4(col + a0 + 4 * u, pol);
           }
 #pragma unroll
-          for (int u = 0; u < 5; u++)
+          for (int u = 0; u < NG; u++)
             if (u < nvec)
               push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, xs[u], a0 + 4 * u, beg,
                                       end, gi, v, fpol);
