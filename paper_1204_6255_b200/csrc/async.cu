@@ -22,6 +22,11 @@ namespace di {
 namespace {
 
 constexpr int kAsyncThreads = 256;
+#ifndef DI_CYC_ITEMS
+#define DI_CYC_ITEMS 2
+#endif
+constexpr int kCycItems = DI_CYC_ITEMS;               // consecutive nodes per thread (even)
+constexpr int kCycTile = kAsyncThreads * kCycItems;   // nodes per tile
 #ifndef DI_ASYNC_SMALL
 #define DI_ASYNC_SMALL 16
 #endif
@@ -31,8 +36,12 @@ constexpr int kAsyncThreads = 256;
 #ifndef DI_ASYNC_CHUNK
 #define DI_ASYNC_CHUNK 1024
 #endif
-#ifndef DI_ASYNC_MINB   // CTAs per SM: 3 (vs 4) narrows the window of tiles in flight, a more
-#define DI_ASYNC_MINB 3  // sequential order: C4 43 -> 42 cycles (58.7 ms), C2 3.6 -> 3.2 ms, same rate
+// The window of nodes in flight (CTAs x tile) sets how close the order is to the paper's
+// sequential cycle: 1024-node tiles x 4 CTAs/SM: C4 43 cycles / 60.2 ms, C2 3.6 ms; 3 CTAs/SM:
+// 42 / 58.7 ms, C2 3.2 ms; 512-node tiles (2 nodes per thread) x 4 CTAs/SM: C4 42 / 58.2 ms,
+// C3 25.8 -> 24.2 ms, C2 3.0 ms at the same per-link rate (tools/exp/async.py)
+#ifndef DI_ASYNC_MINB
+#define DI_ASYNC_MINB 4
 #endif
 constexpr int kAsyncSmall = DI_ASYNC_SMALL;  // rows with <= this many links: a lane each
 constexpr int kAsyncMid = DI_ASYNC_MID;      // rows up to this: one 8-lane group each (list front)
@@ -100,13 +109,13 @@ __device__ __forceinline__ double take_fluid(double *p) {
 template <bool LOOPS, bool DIST>
 __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const SweepArgs a, const DistArgs x) {
   constexpr int NW = kAsyncThreads / 32;
-  __shared__ int64_t s_rb[kSelTile];   // long rows of the tile: first link
-  __shared__ int32_t s_ro[kSelTile];   // #links
-  __shared__ double s_rv[kSelTile];    // v = T d / o
-  __shared__ int32_t s_ri[kSelTile];   // local node id
-  __shared__ int32_t s_rp[kSelTile + 1];  // exclusive chunk prefix
-  __shared__ int16_t s_si[kSelTile];   // short rows of the tile: local node id
-  __shared__ double s_sv[kSelTile];    //   and v
+  __shared__ int64_t s_rb[kCycTile];   // long rows of the tile: first link
+  __shared__ int32_t s_ro[kCycTile];   // #links
+  __shared__ double s_rv[kCycTile];    // v = T d / o
+  __shared__ int32_t s_ri[kCycTile];   // local node id
+  __shared__ int32_t s_rp[kCycTile + 1];  // exclusive chunk prefix
+  __shared__ int16_t s_si[kCycTile];   // short rows of the tile: local node id
+  __shared__ double s_sv[kCycTile];    //   and v
   __shared__ int s_nrows, s_nmid, s_nsmall, s_nchunks, s_claim, s_mclaim, s_sclaim;
   __shared__ int64_t s_tile;
   __shared__ bool s_last;
@@ -145,51 +154,54 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
     const int64_t tile = s_tile;
     if (tile >= a.ntiles) break;
     // ---- select: 4 consecutive nodes per thread, F and row extents
-    const int64_t base = tile * (int64_t)kSelTile + (int64_t)threadIdx.x * kSelItems;
-    double f[kSelItems];
-    int64_t rb[kSelItems + 1];
-    int kl[kSelItems];
-    if (base + kSelItems <= a.n) {  // vectorised: 2 x double2 (F, L2 only: REDs land there) and
+    const int64_t base = tile * (int64_t)kCycTile + (int64_t)threadIdx.x * kCycItems;
+    double f[kCycItems];
+    int64_t rb[kCycItems + 1];
+    int kl[kCycItems];
+    if (base + kCycItems <= a.n) {  // vectorised: 2 x double2 (F, L2 only: REDs land there) and
                                     // 2 x longlong2 (row extents) + the next row's start
-      const double2 f01 = __ldcg(reinterpret_cast<const double2 *>(F + base));
-      const double2 f23 = __ldcg(reinterpret_cast<const double2 *>(F + base) + 1);
-      const longlong2 r01 = reinterpret_cast<const longlong2 *>(a.row_ptr + base)[0];
-      const longlong2 r23 = reinterpret_cast<const longlong2 *>(a.row_ptr + base)[1];
-      f[0] = f01.x; f[1] = f01.y; f[2] = f23.x; f[3] = f23.y;
-      rb[0] = r01.x; rb[1] = r01.y; rb[2] = r23.x; rb[3] = r23.y;
-      rb[kSelItems] = a.row_ptr[base + kSelItems];
 #pragma unroll
-      for (int j = 0; j < kSelItems; j++) kl[j] = LOOPS ? a.kloop[base + j] : 0;
+      for (int h = 0; h < kCycItems / 2; h++) {
+        const double2 fp = __ldcg(reinterpret_cast<const double2 *>(F + base) + h);
+        const longlong2 rp = reinterpret_cast<const longlong2 *>(a.row_ptr + base)[h];
+        f[2 * h] = fp.x;
+        f[2 * h + 1] = fp.y;
+        rb[2 * h] = rp.x;
+        rb[2 * h + 1] = rp.y;
+      }
+      rb[kCycItems] = a.row_ptr[base + kCycItems];
+#pragma unroll
+      for (int j = 0; j < kCycItems; j++) kl[j] = LOOPS ? a.kloop[base + j] : 0;
     } else {
 #pragma unroll
-      for (int j = 0; j < kSelItems; j++) {
+      for (int j = 0; j < kCycItems; j++) {
         const int64_t i = base + j;
         f[j] = (i < a.n) ? __ldcg(F + i) : 0.0;
         rb[j] = (i < a.n) ? a.row_ptr[i] : 0;
         kl[j] = (LOOPS && i < a.n) ? a.kloop[i] : 0;
       }
-      rb[kSelItems] = base < a.n ? a.row_ptr[a.n] : 0;
+      rb[kCycItems] = base < a.n ? a.row_ptr[a.n] : 0;
     }
     // the selection test for the 4 nodes first, then all their exchanges in flight together
     // (one round trip per tile instead of one per selected node)
-    int o4[kSelItems];
-    double T04[kSelItems];
+    int o4[kCycItems];
+    double T04[kCycItems];
 #pragma unroll
-    for (int j = 0; j < kSelItems; j++) {
+    for (int j = 0; j < kCycItems; j++) {
       const int64_t i = base + j;
       o4[j] = -1;  // not selected
       if (i >= a.n) continue;
-      const int64_t rend = (i + 1 < a.n) ? (j + 1 < kSelItems ? rb[j + 1] : rb[kSelItems])
+      const int64_t rend = (i + 1 < a.n) ? (j + 1 < kCycItems ? rb[j + 1] : rb[kCycItems])
                                          : a.row_ptr[a.n];
       const int o = (int)(rend - rb[j]);
       const double thr = cyc ? 0.0 : __dmul_rn(t, (double)o);  // (r/L)*out[i]
       if (f[j] > thr) o4[j] = o;                                // strict '>'
     }
 #pragma unroll
-    for (int j = 0; j < kSelItems; j++)
+    for (int j = 0; j < kCycItems; j++)
       T04[j] = (o4[j] >= 0) ? take_fluid(F + base + j) : 0.0;  // >= f[j]: only REDs add meanwhile
 #pragma unroll
-    for (int j = 0; j < kSelItems; j++) {
+    for (int j = 0; j < kCycItems; j++) {
       if (o4[j] < 0) continue;
       const int64_t i = base + j;
       const int o = o4[j];
@@ -212,18 +224,18 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       acc_nd++;
       if (o <= kAsyncSmall) {   // short rows: their own list, a lane each (balanced below)
         const int p = atomicAdd(&s_nsmall, 1);
-        s_si[p] = (int16_t)(base + j - tile * kSelTile);
+        s_si[p] = (int16_t)(base + j - tile * kCycTile);
         s_sv[p] = v;
       } else {  // mid rows at the front of the list, long rows at its back
-        const int p = (o <= kAsyncMid) ? atomicAdd(&s_nmid, 1) : kSelTile - 1 - atomicAdd(&s_nrows, 1);
+        const int p = (o <= kAsyncMid) ? atomicAdd(&s_nmid, 1) : kCycTile - 1 - atomicAdd(&s_nrows, 1);
         s_rb[p] = rb[j];
         s_ro[p] = o;
         s_rv[p] = v;
-        s_ri[p] = (int32_t)(base + j - tile * kSelTile);
+        s_ri[p] = (int32_t)(base + j - tile * kCycTile);
       }
     }
     __syncthreads();
-    // ---- long rows (list back: row k at kSelTile-1-k): chunk prefix (warp 0), then the CTA's
+    // ---- long rows (list back: row k at kCycTile-1-k): chunk prefix (warp 0), then the CTA's
     //      warps claim chunks; then mid rows (list front), four per warp step
     const int nrows = s_nrows;
     if (nrows > 0) {
@@ -231,7 +243,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         const int per = (nrows + 31) / 32;
         const int r0 = lane * per, r1 = min(nrows, r0 + per);
         int sum = 0;
-        for (int k = r0; k < r1; k++) sum += (s_ro[kSelTile - 1 - k] + kAsyncChunk - 1) / kAsyncChunk;
+        for (int k = r0; k < r1; k++) sum += (s_ro[kCycTile - 1 - k] + kAsyncChunk - 1) / kAsyncChunk;
         int incl = sum;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -241,7 +253,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         int run = incl - sum;
         for (int k = r0; k < r1; k++) {
           s_rp[k] = run;
-          run += (s_ro[kSelTile - 1 - k] + kAsyncChunk - 1) / kAsyncChunk;
+          run += (s_ro[kCycTile - 1 - k] + kAsyncChunk - 1) / kAsyncChunk;
         }
         if (lane == 31) {
           s_nchunks = incl;
@@ -260,12 +272,12 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           const int mid = (lo + hi + 1) >> 1;
           if (s_rp[mid] <= c) lo = mid; else hi = mid - 1;
         }
-        const int slot = kSelTile - 1 - lo;
+        const int slot = kCycTile - 1 - lo;
         const int64_t rbeg = s_rb[slot];
         const int64_t beg = rbeg + (int64_t)(c - s_rp[lo]) * kAsyncChunk;
         const int64_t end = min(rbeg + (int64_t)s_ro[slot], beg + kAsyncChunk);
         const double v = s_rv[slot];
-        const int32_t gi = LOOPS ? (int32_t)(tile * kSelTile + s_ri[slot] + a.lo) : -1;
+        const int32_t gi = LOOPS ? (int32_t)(tile * kCycTile + s_ri[slot] + a.lo) : -1;
         const int64_t a0 = beg & ~3ll;
         const int nvec = (int)((end - a0 + 3) >> 2);
         for (int vb = 0; vb < nvec; vb += 128) {
@@ -289,7 +301,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
     // short rows (<= kAsyncSmall links, <= 5 int4 groups): 32 per warp claim, one per lane
     const int nsmall = s_nsmall;
     if (nsmall > 0) {
-      const int64_t tb = tile * (int64_t)kSelTile;
+      const int64_t tb = tile * (int64_t)kCycTile;
       for (;;) {
         int q = 0;
         if (lane == 0) q = atomicAdd(&s_sclaim, 32);
@@ -330,7 +342,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           const int64_t beg = s_rb[k], end = beg + s_ro[k], a0 = beg & ~3ll;
           const int nvec = (int)((end - a0 + 3) >> 2);   // <= 33
           const double v = s_rv[k];
-          const int32_t gi = LOOPS ? (int32_t)(tile * kSelTile + s_ri[k] + a.lo) : -1;
+          const int32_t gi = LOOPS ? (int32_t)(tile * kCycTile + s_ri[k] + a.lo) : -1;
           for (int vb = sub; vb < nvec; vb += 16) {
             const int4 x0 = ld_col4(col + a0 + 4 * (int64_t)vb, pol);
             int4 x1 = make_int4(0, 0, 0, 0);
@@ -457,6 +469,7 @@ di_status prepare_cycle(Graph &g) {
 
 void launch_cycle(Graph &g, int64_t *launches) {
   SweepArgs a = sweep_args(g, 0);
+  a.ntiles = (g.n + kCycTile - 1) / kCycTile;
   const bool dist = g.partitioned;
   DistArgs x{};
   if (dist) x = dist_args(g);
