@@ -102,7 +102,7 @@ struct EventSet {
 
 void free_graph(Graph *g) {
   if (!g) return;
-  void *ptrs[] = {g->ppartials, g->rep, g->row_ptr, g->col, g->deg, g->kloop, g->csc_ptr, g->csc_row, g->F, g->H,
+  void *ptrs[] = {g->ppartials, g->rep, g->hub_items, g->row_ptr, g->col, g->deg, g->kloop, g->csc_ptr, g->csc_row, g->F, g->H,
                   g->new_of, g->old_of, g->Bperm, g->xfer,
                   g->S, g->aux, g->sc, g->partials, g->ipartials, g->red_partials,
                   g->log_r, g->log_sel, g->log_links, g->log_mode};
@@ -307,6 +307,7 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
   if (const char *e = getenv("DI_AUTO_RATIO")) g->auto_ratio = atof(e);
   if (const char *e = getenv("DI_STRIPES")) g->stripes = atoi(e);
   if (const char *e = getenv("DI_HOT_ACC")) g->hot_acc = atoi(e);
+  if (const char *e = getenv("DI_REPL_SHARE")) g->repl_share = atof(e);
   di_status s = build_graph(*g, src, dst, n_links, flags);
   if (s == DI_OK) s = alloc_state(*g);
   if (s == DI_OK) s = alloc_pull(*g);

@@ -16,6 +16,9 @@
 // bit for bit (like every fp64-atomic push); the fixed point and the tolerance are those of the
 // paper's method. The last CTA reduces the per-CTA sums, applies r_{c+1} = r_c - taken + pushed,
 // the stop test and the starvation guard (reading G5), and rewinds the tile counter.
+#include <algorithm>
+#include <vector>
+
 #include "sweep.cuh"
 
 namespace di {
@@ -44,18 +47,30 @@ constexpr int kCycTile = kAsyncThreads * kCycItems;   // nodes per tile
 #define DI_ASYNC_MINB 4
 #endif
 constexpr int kAsyncSmall = DI_ASYNC_SMALL;  // rows with <= this many links: a lane each
+static_assert(kAsyncSmall < 256, "short-row length is packed in 8 bits");
 constexpr int kAsyncMid = DI_ASYNC_MID;      // rows up to this: one 8-lane group each (list front)
 constexpr int kAsyncChunk = DI_ASYNC_CHUNK;  // longer rows: chunks of this many links, one warp each
 
 // Replicated accumulators for the hottest targets. Same-address fp64 REDs serialise in one L2
 // slice; a node that receives a large share of all pushes (C3's Zipf targets: the top node gets
-// 0.39 % of the links, 383k in-links) keeps its slice busy for a large part of the cycle. On such
-// a graph (top share > kReplShare) the upload places the kHotRanks hottest nodes at internal
-// ids 0..kHotRanks-1 (graph_build.cu, k_place); their REDs go to one of kCopies copies (chosen
-// by warp), each copy in its own 4 KB page, and the last CTA of the cycle folds the copies into
-// F (C3: 44.5 -> 33.6 ms). C4's top share is 0.09 %: no hot ids, no extra test per link.
+// 0.39 % of the links; C4's R-MAT top node 0.09 %) keeps its slice busy for a large part of the
+// cycle and throttles every SM that has a RED queued behind it. On such a graph (top share >
+// kReplShare) the upload places the kHotRanks hottest nodes at internal ids 0..kHotRanks-1
+// (graph_build.cu, k_place); their REDs go to one of kCopies copies (chosen by warp), every copy
+// in its own 128-B line (copies sharing a line serialise like one address: tools/micro/hot.cu,
+// profiles/micro_hot.txt), and the last CTA of the cycle folds the copies into F.
 constexpr int kRepl = kHotRanks;
 constexpr int kCopies = 16;
+constexpr int kRepStride = 16;  // doubles between accumulators: one 128-B line each
+
+// Hub items. On R-MAT graphs the hottest targets are also the largest rows (node 0 of C4 has
+// ~240k out-links): pushed by the CTA that takes tile 0 they would make it the straggler of
+// every cycle. Hot rows longer than kHubMin are therefore split into items of kHubItem links
+// (built once by prepare_cycle): the CTA of tile 0 (claim 0) takes their fluid, publishes
+// v = T d / o per hub row in hv[] and raises hub_flag; claims 1..n_hub are the items, pushed
+// by whichever CTAs draw them once the flag is up; claims > n_hub are tiles 1, 2, ...
+constexpr int64_t kHubMin = 8192;
+constexpr int64_t kHubItem = 16384;
 
 template <bool LOOPS>
 __device__ __forceinline__ void red_group_rep(double *__restrict__ F, double *__restrict__ rep,
@@ -69,7 +84,7 @@ __device__ __forceinline__ void red_group_rep(double *__restrict__ F, double *__
     if (p >= beg && p < end && (!LOOPS || jj[c] != gi)) {
       const int32_t j = jj[c];
       if (j < hot_lim)   // one of the hot ids 0..hot_lim-1 (0 when off)
-        red_add_f64(rep + copy * 512 + j, v);
+        red_add_f64(rep + (int64_t)(copy * kRepl + j) * kRepStride, v);
       else
         red_add_f64_hint(F + j, v, fpol);
     }
@@ -116,8 +131,10 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   __shared__ int32_t s_rp[kCycTile + 1];  // exclusive chunk prefix
   __shared__ int16_t s_si[kCycTile];   // short rows of the tile: local node id
   __shared__ double s_sv[kCycTile];    //   and v
+  __shared__ int64_t s_sb[kCycTile];   //   and first link << 8 | #links
   __shared__ int s_nrows, s_nmid, s_nsmall, s_nchunks, s_claim, s_mclaim, s_sclaim;
   __shared__ int64_t s_tile;
+  __shared__ int s_item;
   __shared__ bool s_last;
   __shared__ double s_red[NW][4];
   __shared__ long long s_ired[NW][3];
@@ -129,6 +146,8 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   const int32_t hot_lim = hot_shift >= 0 ? hot_shift : 0;   // a.hot_shift = hot-id count here
   const int copy = (blockIdx.x * (kAsyncThreads / 32) + warp) % kCopies;
   double *rep = a.rep;
+  double *hv = rep + kCopies * kRepl * kRepStride;  // hub rows' v (valid when a.n_hub > 0)
+  const unsigned hub_tag = sc->hub_want + 1u;       // hub_flag value of this cycle
   const double r = sc->r, d = sc->d;
   const bool cyc = (sc->variant == DI_CYC) || sc->guard;
   double t = (a.L_total > 0.0) ? r / a.L_total : 0.0;  // r/L once per cycle (G3, G4)
@@ -142,7 +161,19 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
 
   for (;;) {
     if (threadIdx.x == 0) {
-      s_tile = (int64_t)atomicAdd(&sc->tile_next, 1u);
+      const int64_t c = (int64_t)atomicAdd(&sc->tile_next, 1u);
+      int64_t tl = c;
+      int it = -1;
+      if (c > 0 && a.n_hub > 0) {  // claims 1..n_hub: hub items; then tiles 1, 2, ...
+        if (c <= a.n_hub) {
+          it = (int)(c - 1);
+          tl = 0;
+        } else {
+          tl = c - a.n_hub;
+        }
+      }
+      s_tile = tl;
+      s_item = it;
       s_nrows = 0;
       s_nmid = 0;
       s_nsmall = 0;
@@ -153,6 +184,21 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile >= a.ntiles) break;
+    if (s_item >= 0) {  // ---- a hub item: links [beg, end) of hot row `row`, v from tile 0
+      if (threadIdx.x == 0) {
+        const int64_t *h = a.hub + 3 * (int64_t)s_item;
+        const int64_t row = h[0], beg = h[1], end = h[2];
+        while (ld_acquire_u32(&sc->hub_flag) != hub_tag) __nanosleep(64);
+        const double v = __ldcg(hv + row);
+        if (v != 0.0) {
+          s_rb[kCycTile - 1] = beg;
+          s_ro[kCycTile - 1] = (int32_t)(end - beg);
+          s_rv[kCycTile - 1] = v;
+          s_ri[kCycTile - 1] = (int32_t)row;
+          s_nrows = 1;
+        }
+      }
+    } else {
     // ---- select: 4 consecutive nodes per thread, F and row extents
     const int64_t base = tile * (int64_t)kCycTile + (int64_t)threadIdx.x * kCycItems;
     double f[kCycItems];
@@ -163,13 +209,13 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
 #pragma unroll
       for (int h = 0; h < kCycItems / 2; h++) {
         const double2 fp = __ldcg(reinterpret_cast<const double2 *>(F + base) + h);
-        const longlong2 rp = reinterpret_cast<const longlong2 *>(a.row_ptr + base)[h];
+        const longlong2 rp = ld_i64x2_stream(a.row_ptr + base + 2 * h, pol);
         f[2 * h] = fp.x;
         f[2 * h + 1] = fp.y;
         rb[2 * h] = rp.x;
         rb[2 * h + 1] = rp.y;
       }
-      rb[kCycItems] = a.row_ptr[base + kCycItems];
+      rb[kCycItems] = ld_i64_stream(a.row_ptr + base + kCycItems, pol);
 #pragma unroll
       for (int j = 0; j < kCycItems; j++) kl[j] = LOOPS ? a.kloop[base + j] : 0;
     } else {
@@ -185,15 +231,18 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
     // the selection test for the 4 nodes first, then all their exchanges in flight together
     // (one round trip per tile instead of one per selected node)
     int o4[kCycItems];
+    bool hub4[kCycItems];
     double T04[kCycItems];
 #pragma unroll
     for (int j = 0; j < kCycItems; j++) {
       const int64_t i = base + j;
       o4[j] = -1;  // not selected
+      hub4[j] = false;
       if (i >= a.n) continue;
       const int64_t rend = (i + 1 < a.n) ? (j + 1 < kCycItems ? rb[j + 1] : rb[kCycItems])
                                          : a.row_ptr[a.n];
       const int o = (int)(rend - rb[j]);
+      hub4[j] = i < hot_lim && o > kHubMin && a.n_hub > 0;      // pushed as hub items
       const double thr = cyc ? 0.0 : __dmul_rn(t, (double)o);  // (r/L)*out[i]
       if (f[j] > thr) o4[j] = o;                                // strict '>'
     }
@@ -202,7 +251,13 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       T04[j] = (o4[j] >= 0) ? take_fluid(F + base + j) : 0.0;  // >= f[j]: only REDs add meanwhile
 #pragma unroll
     for (int j = 0; j < kCycItems; j++) {
-      if (o4[j] < 0) continue;
+      if (o4[j] < 0) {
+        if (hub4[j]) {  // not selected: its items push nothing this cycle
+          hv[base + j] = 0.0;
+          __threadfence();
+        }
+        continue;
+      }
       const int64_t i = base + j;
       const int o = o4[j];
       const double T0 = T04[j];
@@ -211,7 +266,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         const double od = (double)o;
         T = __ddiv_rn(__dmul_rn(T0, od), __dsub_rn(od, __dmul_rn((double)kl[j], d)));
       }
-      red_add_f64(a.H + i, T);
+      red_add_f64_hint(a.H + i, T, pol);                        // P:264 (streamed: evict_first)
       acc_tk += T0;
       acc_sel++;
       if (o == 0) {
@@ -222,10 +277,14 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       acc_s += __dmul_rn(v, (double)(o - kl[j]));
       acc_lk += o;
       acc_nd++;
-      if (o <= kAsyncSmall) {   // short rows: their own list, a lane each (balanced below)
+      if (hub4[j]) {
+        hv[i] = v;
+        __threadfence();
+      } else if (o <= kAsyncSmall) {   // short rows: their own list, a lane each (balanced below)
         const int p = atomicAdd(&s_nsmall, 1);
         s_si[p] = (int16_t)(base + j - tile * kCycTile);
         s_sv[p] = v;
+        s_sb[p] = (rb[j] << 8) | (int64_t)o;
       } else {  // mid rows at the front of the list, long rows at its back
         const int p = (o <= kAsyncMid) ? atomicAdd(&s_nmid, 1) : kCycTile - 1 - atomicAdd(&s_nrows, 1);
         s_rb[p] = rb[j];
@@ -234,7 +293,12 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         s_ri[p] = (int32_t)(base + j - tile * kCycTile);
       }
     }
+    }
     __syncthreads();
+    if (tile == 0 && s_item < 0 && a.n_hub > 0 && threadIdx.x == 0) {  // hv[] complete: release
+      __threadfence();
+      st_release_u32(&sc->hub_flag, hub_tag);
+    }
     // ---- long rows (list back: row k at kCycTile-1-k): chunk prefix (warp 0), then the CTA's
     //      warps claim chunks; then mid rows (list front), four per warp step
     const int nrows = s_nrows;
@@ -311,7 +375,8 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         if (k < nsmall) {
           const int li = s_si[k];
           const double v = s_sv[k];
-          const int64_t beg = a.row_ptr[tb + li], end = a.row_ptr[tb + li + 1], a0 = beg & ~3ll;
+          const int64_t sb = s_sb[k];
+          const int64_t beg = sb >> 8, end = beg + (sb & 255), a0 = beg & ~3ll;
           const int nvec = (int)((end - a0 + 3) >> 2);
           const int32_t gi = LOOPS ? (int32_t)(tb + li + a.lo) : -1;
           constexpr int NG = (kAsyncSmall + 6) / 4;   // aligned int4 groups of a short row
@@ -397,8 +462,9 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
     for (int k = threadIdx.x; k < hot_lim; k += kAsyncThreads) {
       double acc = 0.0;
       for (int c = 0; c < kCopies; c++) {
-        acc += __ldcg(rep + c * 512 + k);
-        rep[c * 512 + k] = 0.0;
+        double *p = rep + (int64_t)(c * kRepl + k) * kRepStride;
+        acc += __ldcg(p);
+        *p = 0.0;
       }
       if (acc != 0.0) F[k] += acc;
     }
@@ -416,6 +482,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       x.isum[3] = a.n;
       sc->tile_next = 0;
       sc->ticket = 0;
+      sc->hub_want = hub_tag;
     }
     return;
   }
@@ -448,6 +515,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   vs->stop = stop;
   vs->guard = (sm.sel == 0 && !stop && variant == DI_SOP) ? 1 : 0;
   vs->tile_next = 0;
+  vs->hub_want = hub_tag;
   vs->ticket = 0;
 }
 
@@ -460,9 +528,31 @@ static int hot_shift_of(const Graph &g) {
 
 // called by di_solve before any launch or capture (allocations are not capturable)
 di_status prepare_cycle(Graph &g) {
-  if (hot_shift_of(g) >= 0 && !g.rep) {
-    DI_CK(dmalloc(&g.rep, kCopies * 512 * sizeof(double)));
-    DI_CK(cudaMemsetAsync(g.rep, 0, kCopies * 512 * sizeof(double), g.stream));
+  const int hot = hot_shift_of(g);
+  if (hot >= 0 && !g.rep) {
+    const size_t rep_bytes = ((size_t)kCopies * kRepl * kRepStride + kRepl) * sizeof(double);
+    DI_CK(dmalloc(&g.rep, rep_bytes));
+    DI_CK(cudaMemsetAsync(g.rep, 0, rep_bytes, g.stream));
+    // hub items: hot rows longer than kHubMin, in kHubItem-link pieces (static: the CSR is)
+    std::vector<int64_t> rp(hot + 1);
+    DI_CK(cudaMemcpyAsync(rp.data(), g.row_ptr, (hot + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                          g.stream));
+    DI_CK(cudaStreamSynchronize(g.stream));
+    std::vector<int64_t> items;
+    for (int k = 0; k < hot; k++)
+      if (rp[k + 1] - rp[k] > kHubMin)
+        for (int64_t b = rp[k]; b < rp[k + 1]; b += kHubItem) {
+          items.push_back(k);
+          items.push_back(b);
+          items.push_back(std::min(b + kHubItem, rp[k + 1]));
+        }
+    g.n_hub = (int)(items.size() / 3);
+    if (g.n_hub > 0) {
+      DI_CK(dmalloc(&g.hub_items, items.size() * sizeof(int64_t)));
+      DI_CK(cudaMemcpyAsync(g.hub_items, items.data(), items.size() * sizeof(int64_t),
+                            cudaMemcpyHostToDevice, g.stream));
+      DI_CK(cudaStreamSynchronize(g.stream));
+    }
   }
   return DI_OK;
 }
@@ -475,6 +565,10 @@ void launch_cycle(Graph &g, int64_t *launches) {
   if (dist) x = dist_args(g);
   a.hot_shift = g.rep ? hot_shift_of(g) : -1;
   a.rep = g.rep;
+  if (a.hot_shift >= 0) {
+    a.hub = g.hub_items;
+    a.n_hub = g.n_hub;
+  }
   static int occ = 0;
   if (occ == 0) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cycle<false, false>, kAsyncThreads, 0);

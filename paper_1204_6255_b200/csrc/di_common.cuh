@@ -33,7 +33,7 @@ constexpr int kMaxBlocks = 256;    // block-ordered sweeps: sub-sweeps per cycle
 // Skewed in-degrees (async.cu): when the top node takes more than kReplShare of the links, the
 // kHotRanks hottest nodes are placed first and their REDs spread over replicated accumulators.
 constexpr int kHotRanks = 64;
-constexpr double kReplShare = 0.0025;
+constexpr double kReplShare = 0.0005;
 
 enum BinId { BIN_T = 0, BIN_G = 1, BIN_W = 2, BIN_C = 3 };
 
@@ -90,6 +90,8 @@ struct __align__(256) Scalars {
   int64_t sel_cyc, links_cyc;
   int64_t max_sweeps;        // DI_GRAPH_LOOP: the device-side loop stops at this many sweeps
   unsigned int tile_next;    // DI_ASYNC: next tile of the cycle (dynamic, increasing order)
+  unsigned int hub_flag;     // DI_ASYNC hub items: tile 0 published hv[] for cycle hub_want + 1
+  unsigned int hub_want;     //   (advanced by the last CTA of every cycle)
   double alpha;              // DI-SOP threshold scale (di_set_threshold_scale; 1 = P:298)
 };
 
@@ -133,8 +135,11 @@ struct Graph {
                              // 1 = plain degree order)
   int64_t hot_count = 0;     // skewed graphs: the hot_count hottest nodes are internal ids 0..
   double alpha = 1.0;        // DI-SOP threshold scale
+  double repl_share = kReplShare;  // top in-degree share that turns hot placement on (DI_REPL_SHARE)
   int hot_acc = 1;           // DI_ASYNC: replicated accumulators for the hottest targets (DI_HOT_ACC)
-  double *rep = nullptr;
+  double *rep = nullptr;     // replicated accumulators, then hv[kHotRanks] (async.cu)
+  int64_t *hub_items = nullptr;  // DI_ASYNC hub items: (row, first link, end link) triples
+  int n_hub = 0;
   int64_t max_indeg = 0;     // largest in-degree (set by the relabelling pass)
   int32_t *new_of = nullptr, *old_of = nullptr;
   double *Bperm = nullptr;   // B in internal order (custom B)

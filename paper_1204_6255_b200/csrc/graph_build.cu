@@ -72,15 +72,6 @@ __global__ void k_place(const int32_t *__restrict__ sorted_old, int64_t n, DistB
   }
 }
 
-// total out-degree of the k highest-ranked nodes (hot-node placement guard)
-__global__ void k_hot_outdeg(const int32_t *__restrict__ sorted, const int64_t *__restrict__ od,
-                             int k, int64_t *out) {
-  int64_t s = 0;
-  for (int r = threadIdx.x; r < k; r += 32) s += od[sorted[r]];
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (threadIdx.x == 0) *out = s;
-}
-
 int64_t prime_at_most(int64_t x) {
   if (x < 2) return 1;
   for (int64_t p = x; p >= 2; p--) {
@@ -308,7 +299,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     add(nn * 4);                      // iota
     add(nn * 4);                      // sorted ranks
   }
-  if (world > 1 || reorder) add((nn + 1) * 8);   // out-degrees (partition / hot-node guard)
+  if (world > 1) add((nn + 1) * 8);   // out-degrees (partition bounds)
   if (world > 1) add((nn + 1) * 8);              // prefix
   Arena ar;
   DI_CK(dmalloc(&ar.base, total));
@@ -366,7 +357,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   bd.world = world;
   bd.b[0] = 0;
   bd.b[1] = n;
-  int64_t *od = (world > 1 || reorder) ? ar.take<int64_t>((nn + 1) * 8) : nullptr;
+  int64_t *od = (world > 1) ? ar.take<int64_t>((nn + 1) * 8) : nullptr;
   if (world > 1) {
     int64_t *pre = ar.take<int64_t>((nn + 1) * 8);
     DI_CK(cudaMemsetAsync(od, 0, (nn + 1) * 8, st));
@@ -405,20 +396,10 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     DI_CK(cudaStreamSynchronize(st));
     btrace("sync3");
     g.max_indeg = top;
-    // skewed in-degrees (single GPU): the kHotRanks hottest nodes first (replicated accumulators)
+    // skewed in-degrees (single GPU): the kHotRanks hottest nodes first (replicated accumulators;
+    // hot rows that are also hubs are pushed as hub items, async.cu)
     bool skewed = !g.partitioned && g.hot_acc && L > 0 &&
-                  (double)top > kReplShare * (double)L && n > 4 * kHotRanks;
-    if (skewed) {  // ... unless they are also hubs: one tile (one CTA of k_cycle) would hold all
-      if (world == 1) {  //     their rows and become the straggler of every cycle
-        DI_CK(cudaMemsetAsync(od, 0, (nn + 1) * 8, st));
-        k_outdeg<<<grid_for(L, sms), 256, 0, st>>>(s_dev, L, od);
-      }
-      k_hot_outdeg<<<1, 32, 0, st>>>(sorted, od, kHotRanks, reinterpret_cast<int64_t *>(small + 48));
-      int64_t hot_links = 0;
-      DI_CK(cudaMemcpyAsync(&hot_links, small + 48, 8, cudaMemcpyDeviceToHost, st));
-      DI_CK(cudaStreamSynchronize(st));
-      skewed = hot_links <= (int64_t)kHotRanks * 1024;
-    }
+                  (double)top > g.repl_share * (double)L && n > 4 * kHotRanks;
     g.hot_count = skewed ? kHotRanks : 0;
     PlaceParams pp;
     for (int r = 0; r < world; r++) {

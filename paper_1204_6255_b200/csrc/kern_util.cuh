@@ -20,6 +20,21 @@ __device__ __forceinline__ int4 ld_col4(const int32_t *p, uint64_t pol) {
                : "l"(p), "l"(pol));
   return v;
 }
+// streaming read of two row extents (read once per cycle: do not displace F in L2)
+__device__ __forceinline__ longlong2 ld_i64x2_stream(const int64_t *p, uint64_t pol) {
+  longlong2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s64 {%0, %1}, [%2], %3;"
+               : "=l"(v.x), "=l"(v.y)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int64_t ld_i64_stream(const int64_t *p, uint64_t pol) {
+  int64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;"
+               : "=l"(v)
+               : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -41,6 +56,15 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 }
 __device__ __forceinline__ void red_add_f64(double *p, double v) {
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 template <typename T>

@@ -35,6 +35,8 @@ struct SweepArgs {
   double *ppartials;    // 8 per finaliser slice: q, s, e, taken, sel, nd, links, 0
   int hot_shift;        // DI_ASYNC replicated hot accumulators (async.cu), -1 = off
   double *rep;
+  const int64_t *hub;   // DI_ASYNC hub items (async.cu), n_hub of them
+  int n_hub;
 };
 
 // What one sweep moved: r_{n+1} = q + s (a2), dangling absorption e, counters.
@@ -304,6 +306,8 @@ inline SweepArgs sweep_args(Graph &g, int test_mode, int blk = 0, int blocks = 1
   a.ppartials = g.ppartials;
   a.hot_shift = -1;
   a.rep = nullptr;
+  a.hub = nullptr;
+  a.n_hub = 0;
   a.F = g.F;
   a.H = g.H;
   a.deg = g.deg;

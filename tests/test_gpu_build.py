@@ -67,10 +67,7 @@ def test_reorder_relabelling(name):
     ranked = np.argsort(-indeg, kind="stable")           # rank r -> caller id
     # placement (graph_build.cu k_place): on a skewed graph (top in-degree > 0.25 % of the links)
     # the 64 hottest ranks come first; the rest in P stripes, P = largest prime <= (n - hot)/1024
-    hot = 64 if (indeg.max() > 0.0025 * len(src) and n > 256) else 0
-    outd = np.bincount(src, minlength=n)
-    if hot and outd[ranked[:64]].sum() > 64 * 1024:   # ... unless the hot nodes are also hubs
-        hot = 0
+    hot = 64 if (indeg.max() > 0.0005 * len(src) and n > 256) else 0
 
     def prime_at_most(x):
         if x < 2:

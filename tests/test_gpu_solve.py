@@ -262,6 +262,27 @@ def test_async_cycles(graph_loop):
         assert st["converged"] == 1
         assert l1(g.history().cpu().numpy(), X) <= (1e-13 + 1e-15) / (1 - D) + 1e-14
     g.free()
+    # hot targets that are also hubs (R-MAT-like): rows of 30000 / 9000 links (> kHubMin) are
+    # pushed as hub items (async.cu); one hub row carries a self-loop (LOOPS path)
+    rng = np.random.default_rng(12)
+    src = rng.integers(0, n, 6 * n).astype(np.int32)
+    dst = rng.integers(0, n, 6 * n).astype(np.int32)
+    m = len(src)
+    for hub, share, out in ((77, 0.04, 30000), (5000, 0.02, 9000), (123, 0.01, 100)):
+        k = int(share * m)
+        tgt = rng.choice(n, out, replace=False).astype(np.int32)
+        src = np.concatenate([src, rng.integers(0, n, k).astype(np.int32), np.full(out, hub, np.int32)])
+        dst = np.concatenate([dst, np.full(k, hub, np.int32), tgt])
+    src = np.concatenate([src, np.array([77], np.int32)])
+    dst = np.concatenate([dst, np.array([77], np.int32)])
+    g = upload(src, dst, n)
+    for variant in ("sop", "cyc"):
+        X, _, _ = oracle.di(src, dst, n, d=D, tol=1e-15, variant=variant)
+        for rep in range(2):   # a second solve on the same graph: hub flags carry over
+            st = g.solve(d=D, tol=1e-13, variant=variant, **kw)
+            assert st["converged"] == 1
+            assert l1(g.history().cpu().numpy(), X) <= (1e-13 + 1e-15) / (1 - D) + 1e-14
+    g.free()
 
 
 def test_threshold_scale():
