@@ -555,6 +555,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   DI_CK(cudaGetLastError());
   g.solved = true;
   g.last_d = d;
+  if (async) report_cycle_times(g, g.sc_host->sweeps);
   g.log_n = std::min<int64_t>(g.sc_host->sweeps, kLogCap);
   if (st) {
     const Scalars &c = *g.sc_host;

@@ -141,6 +141,8 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
 
   Scalars *sc = a.sc;
   if (sc->stop) return;
+  unsigned long long t_begin = 0;
+  if (a.times && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int hot_shift = a.hot_shift;
   const int32_t hot_lim = hot_shift >= 0 ? hot_shift : 0;   // a.hot_shift = hot-id count here
@@ -452,6 +454,13 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
     reinterpret_cast<double2 *>(o)[1] = make_double2(x[2], x[0]);
     reinterpret_cast<longlong2 *>(o)[2] = make_longlong2(c[0], c[1]);
     reinterpret_cast<longlong2 *>(o)[3] = make_longlong2(c[2], 0);
+    if (a.times) {
+      unsigned long long t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      unsigned long long *tp = a.times + 2 * ((int64_t)(sc->sweeps & 63) * gridDim.x + blockIdx.x);
+      tp[0] = t_begin;
+      tp[1] = t_end;
+    }
     __threadfence();
     s_last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
   }
@@ -547,6 +556,8 @@ di_status prepare_cycle(Graph &g) {
           items.push_back(std::min(b + kHubItem, rp[k + 1]));
         }
     g.n_hub = (int)(items.size() / 3);
+    if (getenv("DI_CYC_TIMES") && !g.cyc_times)
+      DI_CK(dmalloc(&g.cyc_times, (size_t)64 * kMaxSlices * 2 * sizeof(unsigned long long)));
     if (g.n_hub > 0) {
       DI_CK(dmalloc(&g.hub_items, items.size() * sizeof(int64_t)));
       DI_CK(cudaMemcpyAsync(g.hub_items, items.data(), items.size() * sizeof(int64_t),
@@ -557,6 +568,44 @@ di_status prepare_cycle(Graph &g) {
   return DI_OK;
 }
 
+static int cycle_grid(const Graph &g) {
+  static int occ = 0;
+  if (occ == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cycle<false, false>, kAsyncThreads, 0);
+    if (occ < 1) occ = 1;
+  }
+  return std::min(g.num_sms * occ, kMaxSlices);
+}
+
+// DI_CYC_TIMES diagnostic: per cycle, the spread of CTA start and end times (stderr)
+void report_cycle_times(Graph &g, int64_t cycles) {
+  if (!g.cyc_times || cycles <= 0) return;
+  const int grid = cycle_grid(g);
+  const int64_t nc = std::min<int64_t>(cycles, 64);
+  std::vector<unsigned long long> t((size_t)nc * grid * 2);
+  if (cudaMemcpy(t.data(), g.cyc_times, t.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  double span = 0, skew = 0, tail = 0, busy = 0;
+  for (int64_t c = 0; c < nc; c++) {
+    std::vector<double> st(grid), en(grid);
+    for (int b = 0; b < grid; b++) {
+      st[b] = (double)t[2 * (c * grid + b)];
+      en[b] = (double)t[2 * (c * grid + b) + 1];
+    }
+    const double s0 = *std::min_element(st.begin(), st.end()), s1 = *std::max_element(st.begin(), st.end());
+    std::vector<double> e2(en);
+    std::sort(e2.begin(), e2.end());
+    const double e1 = e2.back(), emed = e2[grid / 2];
+    double b = 0;
+    for (int k = 0; k < grid; k++) b += en[k] - st[k];
+    span += e1 - s0;
+    skew += s1 - s0;
+    tail += e1 - emed;
+    busy += b / grid;
+  }
+  fprintf(stderr, "[DI_CYC_TIMES] %lld cycles, grid %d: span %.1f us, start skew %.1f us, tail (max - median end) %.1f us, mean CTA busy %.1f us\n",
+          (long long)nc, grid, span / nc / 1e3, skew / nc / 1e3, tail / nc / 1e3, busy / nc / 1e3);
+}
+
 void launch_cycle(Graph &g, int64_t *launches) {
   SweepArgs a = sweep_args(g, 0);
   a.ntiles = (g.n + kCycTile - 1) / kCycTile;
@@ -565,16 +614,12 @@ void launch_cycle(Graph &g, int64_t *launches) {
   if (dist) x = dist_args(g);
   a.hot_shift = g.rep ? hot_shift_of(g) : -1;
   a.rep = g.rep;
+  a.times = g.cyc_times;
   if (a.hot_shift >= 0) {
     a.hub = g.hub_items;
     a.n_hub = g.n_hub;
   }
-  static int occ = 0;
-  if (occ == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cycle<false, false>, kAsyncThreads, 0);
-    if (occ < 1) occ = 1;
-  }
-  const int grid = std::min(g.num_sms * occ, kMaxSlices);
+  const int grid = cycle_grid(g);
   if (dist) {
     if (g.has_loops)
       k_cycle<true, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);

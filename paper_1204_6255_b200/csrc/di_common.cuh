@@ -138,6 +138,7 @@ struct Graph {
   double repl_share = kReplShare;  // top in-degree share that turns hot placement on (DI_REPL_SHARE)
   int hot_acc = 1;           // DI_ASYNC: replicated accumulators for the hottest targets (DI_HOT_ACC)
   double *rep = nullptr;     // replicated accumulators, then hv[kHotRanks] (async.cu)
+  unsigned long long *cyc_times = nullptr;  // DI_CYC_TIMES diagnostic: per-CTA start/end per cycle
   int64_t *hub_items = nullptr;  // DI_ASYNC hub items: (row, first link, end link) triples
   int n_hub = 0;
   int64_t max_indeg = 0;     // largest in-degree (set by the relabelling pass)
@@ -250,6 +251,7 @@ void launch_finalize(Graph &g, int64_t *launches);
 void launch_pull(Graph &g, int64_t *launches);
 void launch_loop_cond(Graph &g, cudaGraphConditionalHandle h);
 // async.cu
+void report_cycle_times(Graph &g, int64_t cycles);
 void launch_cycle(Graph &g, int64_t *launches);
 di_status prepare_cycle(Graph &g);
 di_status alloc_pull(Graph &g);

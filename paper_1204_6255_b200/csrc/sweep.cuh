@@ -37,6 +37,7 @@ struct SweepArgs {
   double *rep;
   const int64_t *hub;   // DI_ASYNC hub items (async.cu), n_hub of them
   int n_hub;
+  unsigned long long *times;  // DI_CYC_TIMES diagnostic (async.cu), nullptr = off
 };
 
 // What one sweep moved: r_{n+1} = q + s (a2), dangling absorption e, counters.
@@ -308,6 +309,7 @@ inline SweepArgs sweep_args(Graph &g, int test_mode, int blk = 0, int blocks = 1
   a.rep = nullptr;
   a.hub = nullptr;
   a.n_hub = 0;
+  a.times = nullptr;
   a.F = g.F;
   a.H = g.H;
   a.deg = g.deg;

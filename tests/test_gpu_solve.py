@@ -455,25 +455,30 @@ def test_trace_log():
 
 @pytest.mark.slow
 def test_c4_full_size_properties():
-    """C4 at full size in the bench's launch configuration: converged residual, sampled invariant
-    F_i = B_i + (P.H)_i - H_i on 2000 nodes, and ||X - H||_1 <= ||F||_1/(1-d) by construction."""
+    """C4 at full size, first in the bench's launch configuration (asynchronous cycles in the
+    device-side graph loop), then bulk sweeps with the push/pull choice: converged residual,
+    sampled invariant F_i = B_i + (P.H)_i - H_i on 2000 nodes, conservation, and
+    ||X - H||_1 <= ||F||_1/(1-d) by construction."""
     need_gpu()
     src, dst, n = digen.make("c4")
     g = upload(src, dst, n, build_csc=True)
-    st = g.solve(d=D, tol=1e-10, variant="sop", mode="auto")
-    assert st["converged"] == 1 and st["residual_l1"] <= 1e-10 and 0 < st["pull_sweeps"] < st["sweeps"]
-    H = g.history().cpu().numpy()
-    _, F = g.residual(return_F=True)
-    F = F.cpu().numpy()
-    assert np.all(F >= 0) and np.all(H >= 0)
     rng = np.random.default_rng(0)
     sample = rng.choice(n, 2000, replace=False)
     out = np.bincount(src, minlength=n).astype(np.float64)
     insample = np.isin(dst, sample)
-    ph = np.zeros(n)
-    np.add.at(ph, dst[insample], D * H[src[insample]] / out[src[insample]])
-    resid = (1 - D) / n + ph[sample] - H[sample]
-    assert np.max(np.abs(resid - F[sample])) <= 1e-15
-    cons = F.sum() + (1 - D) * H[out > 0].sum() + H[out == 0].sum()
-    assert abs(cons - (1 - D)) <= 1e-12
+    for kw in (dict(asynchronous=True, graph_loop=True), dict(mode="auto")):
+        st = g.solve(d=D, tol=1e-10, variant="sop", **kw)
+        assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
+        if "mode" in kw:
+            assert 0 < st["pull_sweeps"] < st["sweeps"]
+        H = g.history().cpu().numpy()
+        _, F = g.residual(return_F=True)
+        F = F.cpu().numpy()
+        assert np.all(F >= 0) and np.all(H >= 0)
+        ph = np.zeros(n)
+        np.add.at(ph, dst[insample], D * H[src[insample]] / out[src[insample]])
+        resid = (1 - D) / n + ph[sample] - H[sample]
+        assert np.max(np.abs(resid - F[sample])) <= 1e-15, kw
+        cons = F.sum() + (1 - D) * H[out > 0].sum() + H[out == 0].sum()
+        assert abs(cons - (1 - D)) <= 1e-12, kw
     g.free()
