@@ -81,6 +81,13 @@ typedef enum {
                                   grid; push only; on a partitioned graph every rank runs its
                                   range's cycle and the remote fluid is exchanged once per cycle;
                                   iterates not bit-reproducible                                 */
+/* Exchange of remote fluid on a partitioned graph: by default each sweep
+ * chooses by predicted bytes between the sparse (id, value) lists (12 B per touched remote
+ * target) and the dense fallback, a per-owner reduction of the remote accumulator (8 B per remote
+ * node: (G-1)/G * 8N per rank), taking the dense one when the last sparse sweep's lists were
+ * larger; these flags force one of them. Ignored on one GPU. */
+#define DI_XCHG_SPARSE  0x200u
+#define DI_XCHG_DENSE   0x400u
 /* Block-ordered cycles (F1): each cycle visits K ordered blocks of
  * internal node ids; block b is selected against the cycle's threshold r (computed once per
  * cycle) with the live F, i.e. including the fluid pushed by blocks 0..b-1 this
@@ -109,9 +116,11 @@ typedef struct {
   int64_t push_launches;        /* DI_PROFILE: push/pull launches that did work                  */
   int32_t converged;            /* 1 if the stop test passed                                     */
   int32_t variant;
-  double exchange_bytes;        /* multi-GPU: bytes this rank sent (12 per (remote id, sweep))    */
+  double exchange_bytes;        /* multi-GPU: bytes this rank sent (12 per (remote id, sweep); dense
+                                   sweeps: 8 per remote node)                                     */
   int64_t exchange_entries;     /* multi-GPU: (remote id, value) entries this rank sent           */
   double exchange_ms;           /* multi-GPU, DI_PROFILE: event time of list exchange + apply     */
+  int64_t dense_exchanges;      /* multi-GPU: sweeps whose exchange took the dense fallback       */
 } di_stats;
 
 /* In-process rank group: `world` emulated ranks, one host thread each, sharing one GPU. The

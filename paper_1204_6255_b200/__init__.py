@@ -33,6 +33,7 @@ VARIANTS = {"sop": 0, "cyc": 1, "pi": 2, "pi_pull": 2, "pi_push": 3, "pi_col": 3
 DEDUP, DROP_SELF_LOOPS, BUILD_CSC, HOST_PTRS, LOCAL_LINKS, NO_REORDER = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 PUSH, PULL, AUTO, RESUME, PAPER_ERROR, TRACE, PROFILE, GRAPH_LOOP = 0x0, 0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
 ASYNC = 0x100
+XCHG_SPARSE, XCHG_DENSE = 0x200, 0x400
 
 
 class Stats(ctypes.Structure):
@@ -48,7 +49,7 @@ class Stats(ctypes.Structure):
         ("error_estimate", ctypes.c_double), ("push_launches", ctypes.c_int64),
         ("converged", ctypes.c_int32), ("variant", ctypes.c_int32),
         ("exchange_bytes", ctypes.c_double), ("exchange_entries", ctypes.c_int64),
-        ("exchange_ms", ctypes.c_double),
+        ("exchange_ms", ctypes.c_double), ("dense_exchanges", ctypes.c_int64),
     ]
 
     def as_dict(self):
@@ -222,14 +223,16 @@ class Graph:
     # -------------------------------------------------------------- solve
     def solve(self, d=0.85, tol=1e-10, variant="sop", max_sweeps=100_000, B=None, resume=False,
               paper_error=False, trace=False, profile=False, mode="push", graph_loop=False,
-              blocks=1, asynchronous=False, raise_on_not_converged=False):
+              blocks=1, asynchronous=False, exchange="auto", raise_on_not_converged=False):
         """di_solve. Returns the di_stats dict (status under key 'status').
-        blocks=K > 1: block-ordered cycles (K ordered node blocks per cycle, push only)."""
+        blocks=K > 1: block-ordered cycles (K ordered node blocks per cycle, push only).
+        exchange ("auto" | "sparse" | "dense"): remote-fluid exchange of a partitioned graph."""
         torch = _torch()
         flags = (RESUME if resume else 0) | (PAPER_ERROR if paper_error else 0) | \
                 (TRACE if trace else 0) | (PROFILE if profile else 0) | \
                 (GRAPH_LOOP if graph_loop else 0) | {"push": PUSH, "pull": PULL, "auto": AUTO}[mode] | \
-                ((int(blocks) & 0xFF) << 16) | (ASYNC if asynchronous else 0)
+                ((int(blocks) & 0xFF) << 16) | (ASYNC if asynchronous else 0) | \
+                {"auto": 0, "sparse": XCHG_SPARSE, "dense": XCHG_DENSE}[exchange]
         bp = None
         if B is not None:
             Bt = B if isinstance(B, torch.Tensor) else torch.as_tensor(np.asarray(B))

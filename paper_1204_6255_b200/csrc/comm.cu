@@ -2,6 +2,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -21,6 +22,8 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
@@ -50,6 +53,7 @@ const NcclApi &nccl() {
     DI_SYM(CommDestroy)
     DI_SYM(AllReduce)
     DI_SYM(AllGather)
+    DI_SYM(Reduce)
     DI_SYM(Send)
     DI_SYM(Recv)
     DI_SYM(GroupStart)
@@ -99,7 +103,30 @@ struct NcclComm : Comm {
     DI_NCK(nccl().GroupEnd());
     return DI_OK;
   }
+  di_status reduce_segments(const double *send, double *recv, const int64_t *b,
+                            cudaStream_t st) override {
+    DI_NCK(nccl().GroupStart());   // one reduction per owner (ranges differ in size)
+    for (int p = 0; p < world; p++)
+      DI_NCK(nccl().Reduce(send + b[p], recv, (size_t)(b[p + 1] - b[p]), ncclFloat64, ncclSum, p,
+                           comm, st));
+    DI_NCK(nccl().GroupEnd());
+    return DI_OK;
+  }
 };
+
+// group backend's dense reduction: this rank's slice summed over every rank's accumulator, in
+// rank order (the values are the same on every run)
+struct SendPtrs {
+  const double *p[kMaxWorld];
+};
+__global__ void k_sum_segments(SendPtrs sp, int world, int64_t off, int64_t n, double *recv) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < world; q++) s += sp.p[q][off + k];
+    recv[k] = s;
+  }
+}
 
 // ------------------------------------------------------------------ in-process group
 struct GroupComm : Comm {
@@ -167,6 +194,24 @@ struct GroupComm : Comm {
     }
     if (cudaStreamSynchronize(st) != cudaSuccess && s == DI_OK) s = DI_ECUDA;
     // senders may reuse their buffers only after every receiver copied
+    if (!g->barrier()) return aborted();
+    if (s != DI_OK) g->abort();
+    return s;
+  }
+  di_status reduce_segments(const double *send, double *recv, const int64_t *b,
+                            cudaStream_t st) override {
+    DI_CK(cudaStreamSynchronize(st));  // this rank's accumulator complete
+    g->dsend[rank] = send;
+    if (!g->barrier()) return aborted();
+    SendPtrs sp{};
+    for (int q = 0; q < world; q++) sp.p[q] = g->dsend[q];
+    const int64_t n = b[rank + 1] - b[rank];
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1184));
+    k_sum_segments<<<grid, 256, 0, st>>>(sp, world, b[rank], n, recv);
+    di_status s = (cudaGetLastError() == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess)
+                      ? DI_OK
+                      : DI_ECUDA;
+    // owners may clear their accumulators only after every rank has read them
     if (!g->barrier()) return aborted();
     if (s != DI_OK) g->abort();
     return s;

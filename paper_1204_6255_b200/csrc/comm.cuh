@@ -34,6 +34,11 @@ struct Comm {
   // rbytes[p] bytes into rbuf[p] (sizes agreed beforehand; 0 = nothing). Enqueued on st.
   virtual di_status exchange(const void *const *sbuf, const size_t *sbytes, void *const *rbuf,
                              const size_t *rbytes, cudaStream_t st) = 0;
+  // dense fallback of the exchange: owner p receives recv[k] = sum over ranks of
+  // send[b[p] + k], k < b[p+1] - b[p] (send: every rank's global-size accumulator; recv: this
+  // rank's slice). Enqueued on st; send may be modified once the call returns (stream order).
+  virtual di_status reduce_segments(const double *send, double *recv, const int64_t *b,
+                                    cudaStream_t st) = 0;
 };
 
 // In-process rank group (di_group): a generation barrier plus per-rank mailboxes.
@@ -48,11 +53,12 @@ struct Group {
   std::vector<std::vector<char>> gat;        // allgather staging
   std::vector<std::vector<const void *>> sptr;  // sptr[src][dst]
   std::vector<std::vector<size_t>> sbytes;
+  std::vector<const double *> dsend;         // reduce_segments: every rank's accumulator
   int handles = 0;                           // graphs built on this group (for di_group_free)
   bool aborted = false;                      // di_group_abort: every barrier fails from now on
   explicit Group(int w)
       : world(w), red_f(w), red_i(w), gat(w), sptr(w, std::vector<const void *>(w, nullptr)),
-        sbytes(w, std::vector<size_t>(w, 0)) {}
+        sbytes(w, std::vector<size_t>(w, 0)), dsend(w, nullptr) {}
   // false once the group is aborted (a rank failed: the others must not wait for it forever)
   bool barrier() {
     std::unique_lock<std::mutex> lk(m);

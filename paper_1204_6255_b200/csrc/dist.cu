@@ -259,7 +259,15 @@ __global__ void k_apply_recv(double *__restrict__ F, int64_t lo, const int32_t *
   }
 }
 
-// the single-GPU finaliser on the allreduced sums
+// dense fallback: this rank's slice of the reduced accumulators into F
+__global__ void k_apply_dense(double *__restrict__ F, const double *__restrict__ recv, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double v = recv[k];
+    if (v != 0.0) F[k] += v;
+  }
+}
+
 // the single-GPU finaliser on the sums of the gathered headers (rank order: every rank computes
 // the same values bit for bit)
 __global__ void k_dist_finalize(const SweepArgs a, const int64_t *ghdr, int world, int async) {
@@ -395,8 +403,16 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   std::vector<void *> rb(G);
   std::vector<size_t> s12(G), r12(G);
   const size_t hw = (size_t)(8 + G);
-  double xbytes = 0.0;
-  int64_t xentries = 0;
+  double xbytes = 0.0, xdense = 0.0;
+  int64_t xentries = 0, ndense = 0;
+  // exchange choice: sparse lists unless the last sparse sweep's lists
+  // (12 B per entry, all ranks) outweighed the dense reduction (8 B per remote node per rank);
+  // after kDenseRun dense sweeps one sparse sweep measures the lists again
+  constexpr int kDenseRun = 4;
+  const bool force_dense = (flags & DI_XCHG_DENSE) && G > 1;
+  const bool force_sparse = (flags & DI_XCHG_SPARSE) || G == 1;
+  int64_t last_lists = -1;
+  int dense_run = 0;
   int64_t launched = 0;
   const bool prof = flags & DI_PROFILE;
   cudaEvent_t pe[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -416,7 +432,14 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       else
         k_push_dist<false><<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a, x);
       if (prof) DI_CK(cudaEventRecord(pe[2], g.stream));
-      k_compact_remote<<<g.num_sms * 4, kCompThreads, 0, g.stream>>>(g.sc, x);
+      const bool dense =
+          force_dense ||
+          (!force_sparse && dense_run < kDenseRun && last_lists >= 0 &&
+           12.0 * (double)last_lists > 8.0 * (double)(G - 1) * (double)g.n_global);
+      if (dense)  // no lists: the header's per-peer counts are zero
+        DI_CK(cudaMemsetAsync(g.sendcnt, 0, (size_t)G * 8, g.stream));
+      else
+        k_compact_remote<<<g.num_sms * 4, kCompThreads, 0, g.stream>>>(g.sc, x);
       launches += 2;
       launched++;
       // one collective for the sums and the per-peer counts of every rank
@@ -439,7 +462,25 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
         DI_CK(cudaEventRecord(pe[3], g.stream));
       }
       int64_t off = 0;
-      for (int p = 0; p < G; p++) {
+      if (dense) {  // per-owner reduction of R, then R's remote segments back to zero
+        double *recv = reinterpret_cast<double *>(g.rid);
+        if ((s = g.comm->reduce_segments(g.R, recv, g.bounds.b, g.stream)) != DI_OK) return s;
+        k_apply_dense<<<grid_of(g.n, g.num_sms), 256, 0, g.stream>>>(g.F, recv, g.n);
+        const int64_t b0 = g.bounds.b[me], b1 = g.bounds.b[me + 1];
+        if (b0 > 0) DI_CK(cudaMemsetAsync(g.R, 0, (size_t)b0 * 8, g.stream));
+        if (b1 < g.n_global)
+          DI_CK(cudaMemsetAsync(g.R + b1, 0, (size_t)(g.n_global - b1) * 8, g.stream));
+        launches++;
+        xdense += 8.0 * (double)(g.n_global - g.n);
+        ndense++;
+        dense_run++;
+      } else {
+        last_lists = 0;
+        for (int p = 0; p < G; p++)
+          for (int q = 0; q < G; q++) last_lists += (p == q) ? 0 : g.ghdr_h[(size_t)p * hw + 8 + q];
+        dense_run = 0;
+      }
+      for (int p = 0; p < G && !dense; p++) {
         const int64_t ns = (p == me) ? 0 : g.ghdr_h[(size_t)me * hw + 8 + p];
         const int64_t nr = (p == me) ? 0 : g.ghdr_h[(size_t)p * hw + 8 + me];
         sb[p] = reinterpret_cast<const char *>(g.sval) + (size_t)12 * g.bounds.b[p];
@@ -449,7 +490,8 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
         off += nr;
         xentries += ns;
       }
-      if ((s = g.comm->exchange(sb.data(), s12.data(), rb.data(), r12.data(), g.stream)) != DI_OK)
+      if (!dense &&
+          (s = g.comm->exchange(sb.data(), s12.data(), rb.data(), r12.data(), g.stream)) != DI_OK)
         return s;
       if (off > 0) {
         k_apply_recv<<<grid_of(off, g.num_sms), 256, 0, g.stream>>>(g.F, g.lo, g.rid, off);
@@ -513,8 +555,9 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
     st->error_estimate = c.resid / (1.0 - d - d * c.e);
     st->converged = converged ? 1 : 0;
     st->variant = variant;
-    xbytes = 12.0 * (double)xentries;
+    xbytes = 12.0 * (double)xentries + xdense;
     st->exchange_bytes = xbytes;
+    st->dense_exchanges = ndense;
     st->exchange_entries = xentries;
     st->push_ms = push_ms;
     st->select_ms = select_ms;

@@ -107,7 +107,8 @@ def test_north_star_parity_partitioned(G, variant, asynchronous):
     need_gpu()
     src, dst, n = digen.make("c1", seed=1)
     (H, F, st, sts, ranges), = run(src, dst, n, G, [dict(d=D, tol=1e-10, variant=variant,
-                                                         asynchronous=asynchronous)])
+                                                         asynchronous=asynchronous,
+                                                         exchange="sparse")])
     same_stats(sts)
     assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
     Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant=variant)
@@ -126,6 +127,59 @@ def test_north_star_parity_partitioned(G, variant, asynchronous):
     for s, (lo, hi) in zip(sts, ranges):
         assert s["exchange_entries"] <= (n - (hi - lo)) * s["sweeps"]
         assert s["exchange_bytes"] == 12 * s["exchange_entries"]
+
+
+@pytest.mark.parametrize("asynchronous", [False, True])
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_dense_exchange_partitioned(G, asynchronous):
+    """The dense fallback of the exchange (a per-owner reduction of the
+    remote accumulator): exact pins, C1 at the north_star gate, F = B + P.H - H mid-solve, its
+    byte count (8 B per remote node per sweep); and the automatic choice, which must take it on
+    a graph whose every sweep touches every remote node, and still reach the same fixed point."""
+    need_gpu()
+    for name, n, links, X in load_pins():
+        if n < G:
+            continue
+        src = np.array([s for s, _ in links], dtype=np.int32)
+        dst = np.array([t for _, t in links], dtype=np.int32)
+        H, F, st, sts, _ = run(src, dst, n, G, [dict(d=D, tol=1e-16, asynchronous=asynchronous,
+                                                     exchange="dense")])[0]
+        same_stats(sts)
+        assert st["converged"] == 1 and l1(H, [float(x) for x in X]) <= 1e-14, name
+    src, dst, n = digen.make("c1", seed=1)
+    P = defn.sparse_P(src, dst, n, D)
+    B = defn.uniform_B(n, D)
+    Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
+    kw = dict(d=D, variant="sop", asynchronous=asynchronous)
+    res = run(src, dst, n, G, [dict(tol=1e-10, exchange="dense", **kw),
+                               dict(tol=1e-300, max_sweeps=3, exchange="dense", **kw),
+                               dict(tol=1e-10, exchange="auto", **kw)])
+    for H, F, st, sts, ranges in (res[0], res[2]):
+        same_stats(sts)
+        assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
+        assert l1(H, Ho) <= 1e-9
+    H, F, st, sts, ranges = res[0]
+    for s_, (lo, hi) in zip(sts, ranges):
+        assert s_["dense_exchanges"] == s_["sweeps"] and s_["exchange_entries"] == 0
+        assert s_["exchange_bytes"] == 8 * (n - (hi - lo)) * s_["sweeps"]
+    H, F, st, sts, ranges = res[1]
+    assert st["sweeps"] == 3 and np.all(F >= 0)
+    assert np.abs(F - (B + P @ H - H)).max() <= 1e-15
+    # 40 random out-links per node: every bulk DI-CYC sweep touches ~every remote node, so the
+    # lists (12 B per entry) outweigh the reduction (8 B per remote node) and auto goes dense,
+    # with a sparse sweep every 5th to measure again
+    rng = np.random.default_rng(G)
+    n = 3000
+    s2 = np.repeat(np.arange(n, dtype=np.int32), 40)
+    t2 = rng.integers(0, n, 40 * n).astype(np.int32)
+    X, _, _ = oracle.di(s2, t2, n, d=D, tol=1e-15, variant="cyc")
+    H, F, st, sts, _ = run(s2, t2, n, G, [dict(d=D, tol=1e-13, variant="cyc", exchange="auto",
+                                               asynchronous=asynchronous)])[0]
+    same_stats(sts)
+    assert len({s_["dense_exchanges"] for s_ in sts}) == 1     # every rank takes the same choice
+    assert st["converged"] == 1 and l1(H, X) <= (1e-13 + 1e-15) / (1 - D) + 1e-14
+    if not asynchronous:
+        assert 0 < st["dense_exchanges"] < st["sweeps"]
 
 
 def test_cyc_neumann_partitioned():
@@ -285,6 +339,8 @@ def test_nccl_backend_single_rank(asynchronous):
     st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous)
     assert st["converged"] == 1 and st["exchange_entries"] == 0
     assert l1(g.history().cpu().numpy(), Ho) <= 1e-9
+    st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous, exchange="dense")  # one rank: no-op
+    assert st["converged"] == 1 and st["dense_exchanges"] == 0
     assert g.residual() <= 1e-10
     g.free()
     grp = di.LocalGroup(1)
