@@ -88,6 +88,11 @@ typedef enum {
  * larger; these flags force one of them. Ignored on one GPU. */
 #define DI_XCHG_SPARSE  0x200u
 #define DI_XCHG_DENSE   0x400u
+/* The sparse lists are written by the compaction kernel straight into the owner's inbox through
+ * peer memory (fused pack + transfer: NVLink stores into an NCCL symmetric window, or device
+ * pointers of one GPU for an in-process group) when the upload could create the inboxes; this
+ * flag moves them with the backend's send/recv instead. */
+#define DI_XCHG_NOP2P   0x800u
 /* Block-ordered cycles (F1): each cycle visits K ordered blocks of
  * internal node ids; block b is selected against the cycle's threshold r (computed once per
  * cycle) with the live F, i.e. including the fluid pushed by blocks 0..b-1 this
@@ -121,6 +126,7 @@ typedef struct {
   int64_t exchange_entries;     /* multi-GPU: (remote id, value) entries this rank sent           */
   double exchange_ms;           /* multi-GPU, DI_PROFILE: event time of list exchange + apply     */
   int64_t dense_exchanges;      /* multi-GPU: sweeps whose exchange took the dense fallback       */
+  int64_t p2p_exchanges;        /* multi-GPU: sweeps whose lists went through peer memory (fused) */
 } di_stats;
 
 /* In-process rank group: `world` emulated ranks, one host thread each, sharing one GPU. The

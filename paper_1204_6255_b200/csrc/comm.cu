@@ -1,6 +1,7 @@
 // comm.cu — NCCL (dlopen'ed) and in-process group backends of the Comm interface (comm.cuh).
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <algorithm>
 #include <cstring>
@@ -29,6 +30,11 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  // symmetric memory (optional: the peer-memory inbox)
+  ncclResult_t (*MemAlloc)(void **, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void *) = nullptr;
+  ncclResult_t (*CommWindowRegister)(ncclComm_t, void *, size_t, ncclWindow_t *, int) = nullptr;
+  ncclResult_t (*CommWindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
 };
 
 const NcclApi &nccl() {
@@ -60,6 +66,12 @@ const NcclApi &nccl() {
     DI_SYM(GroupEnd)
     DI_SYM(GetErrorString)
 #undef DI_SYM
+    a.MemAlloc = reinterpret_cast<decltype(a.MemAlloc)>(dlsym(h, "ncclMemAlloc"));
+    a.MemFree = reinterpret_cast<decltype(a.MemFree)>(dlsym(h, "ncclMemFree"));
+    a.CommWindowRegister =
+        reinterpret_cast<decltype(a.CommWindowRegister)>(dlsym(h, "ncclCommWindowRegister"));
+    a.CommWindowDeregister =
+        reinterpret_cast<decltype(a.CommWindowDeregister)>(dlsym(h, "ncclCommWindowDeregister"));
     a.ok = true;
     return a;
   }();
@@ -75,10 +87,52 @@ const NcclApi &nccl() {
     }                                                                                   \
   } while (0)
 
+// the LSA (NVLink load/store) pointers of every rank's window, read on the device
+__global__ void k_window_peers(ncclWindow_t w, int world, char **out) {
+  for (int p = threadIdx.x; p < world; p += blockDim.x)
+    out[p] = static_cast<char *>(ncclGetPeerPointer(w, 0, p));
+}
+
 struct NcclComm : Comm {
   ncclComm_t comm = nullptr;
+  void *ibuf = nullptr;
+  ncclWindow_t iwin = nullptr;
   ~NcclComm() override {
+    free_inbox();
     if (comm) nccl().CommDestroy(comm);
+  }
+  di_status make_inbox(size_t bytes, std::vector<char *> *peers) override {
+    const NcclApi &a = nccl();
+    if (!a.MemAlloc || !a.MemFree || !a.CommWindowRegister || !a.CommWindowDeregister) {
+      set_error("libnccl.so.2 lacks the symmetric-memory API (ncclMemAlloc / ncclCommWindowRegister)");
+      return DI_ENCCL;
+    }
+    free_inbox();
+    bytes = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT *
+            NCCL_WIN_REQUIRED_ALIGNMENT;
+    DI_NCK(a.MemAlloc(&ibuf, bytes));
+    ncclResult_t r = a.CommWindowRegister(comm, ibuf, bytes, &iwin, NCCL_WIN_COLL_SYMMETRIC);
+    if (r != ncclSuccess) {
+      set_error(std::string("ncclCommWindowRegister: ") + a.GetErrorString(r));
+      a.MemFree(ibuf);
+      ibuf = nullptr;
+      iwin = nullptr;
+      return DI_ENCCL;
+    }
+    char **dp = nullptr;
+    DI_CK(cudaMalloc(&dp, sizeof(char *) * world));
+    k_window_peers<<<1, 32>>>(iwin, world, dp);
+    peers->assign(world, nullptr);
+    cudaError_t e = cudaMemcpy(peers->data(), dp, sizeof(char *) * world, cudaMemcpyDeviceToHost);
+    cudaFree(dp);
+    DI_CK(e);
+    return DI_OK;
+  }
+  void free_inbox() override {
+    if (iwin) nccl().CommWindowDeregister(comm, iwin);
+    if (ibuf) nccl().MemFree(ibuf);
+    iwin = nullptr;
+    ibuf = nullptr;
   }
   di_status allreduce_f64(double *dev, int count, cudaStream_t st) override {
     DI_NCK(nccl().AllReduce(dev, dev, (size_t)count, ncclFloat64, ncclSum, comm, st));
@@ -197,6 +251,21 @@ struct GroupComm : Comm {
     if (!g->barrier()) return aborted();
     if (s != DI_OK) g->abort();
     return s;
+  }
+  char *ibuf = nullptr;
+  ~GroupComm() override { free_inbox(); }
+  di_status make_inbox(size_t bytes, std::vector<char *> *peers) override {
+    free_inbox();
+    DI_CK(cudaMalloc(&ibuf, bytes));
+    g->inbox[rank] = ibuf;
+    if (!g->barrier()) return aborted();
+    peers->assign(g->inbox.begin(), g->inbox.end());
+    if (!g->barrier()) return aborted();
+    return DI_OK;
+  }
+  void free_inbox() override {
+    if (ibuf) cudaFree(ibuf);
+    ibuf = nullptr;
   }
   di_status reduce_segments(const double *send, double *recv, const int64_t *b,
                             cudaStream_t st) override {

@@ -39,6 +39,14 @@ struct Comm {
   // rank's slice). Enqueued on st; send may be modified once the call returns (stream order).
   virtual di_status reduce_segments(const double *send, double *recv, const int64_t *b,
                                     cudaStream_t st) = 0;
+  // Peer-memory inbox (collective; the same `bytes` on every rank): allocates this rank's
+  // inbox and returns, for every rank p, a pointer to p's inbox that THIS rank's kernels can
+  // store to (peers[rank] = the local inbox). NCCL: ncclMemAlloc + a symmetric window
+  // (ncclCommWindowRegister) and its LSA peer pointers (NVLink P2P mappings); group: plain
+  // device pointers of one GPU. DI_ENCCL when the window cannot be created (the caller then
+  // moves the lists with exchange()).
+  virtual di_status make_inbox(size_t bytes, std::vector<char *> *peers) = 0;
+  virtual void free_inbox() = 0;
 };
 
 // In-process rank group (di_group): a generation barrier plus per-rank mailboxes.
@@ -54,11 +62,13 @@ struct Group {
   std::vector<std::vector<const void *>> sptr;  // sptr[src][dst]
   std::vector<std::vector<size_t>> sbytes;
   std::vector<const double *> dsend;         // reduce_segments: every rank's accumulator
+  std::vector<char *> inbox;                 // make_inbox: every rank's inbox
   int handles = 0;                           // graphs built on this group (for di_group_free)
   bool aborted = false;                      // di_group_abort: every barrier fails from now on
   explicit Group(int w)
       : world(w), red_f(w), red_i(w), gat(w), sptr(w, std::vector<const void *>(w, nullptr)),
-        sbytes(w, std::vector<size_t>(w, 0)), dsend(w, nullptr) {}
+        sbytes(w, std::vector<size_t>(w, 0)), dsend(w, nullptr),
+        inbox(w, nullptr) {}
   // false once the group is aborted (a rank failed: the others must not wait for it forever)
   bool barrier() {
     std::unique_lock<std::mutex> lk(m);

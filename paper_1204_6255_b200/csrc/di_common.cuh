@@ -1,6 +1,7 @@
 // di_common.cuh — internal types shared by the libdi.so translation units.
 // Product code: nothing here is shared with oracle/ (which is independent C).
 #pragma once
+#include <vector>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -129,6 +130,9 @@ struct Graph {
   int red_hint = 1;         // L2 evict_last hint on the push's REDs into F (DI_RED_HINT=0 disables)
   int rank = 0, world = 1;
   bool partitioned = false;  // built with a communicator (dist.cu path), even of one rank
+  std::vector<char *> inbox;  // fused exchange: every rank's inbox as mapped here (dist.cu)
+  int64_t icap = 0;          // records per inbox segment (largest owned range)
+  bool p2p = false;          // the inbox exists: k_compact_remote writes through peer memory
   // locality relabelling: internal id = new_of[user id]; user id = old_of[internal id]
   bool reordered = false;
   int stripes = 0;           // relabelling stripes (DI_STRIPES; 0 = auto: stripes of ~1024 nodes,

@@ -216,8 +216,12 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *
     if (threadIdx.x == 0)
       s_base = total ? atomicAdd(x.tcnt + 32 * p, (unsigned long long)total) : 0ull;
     __syncthreads();
-    int64_t pos = x.bd.b[p] + (int64_t)s_base + before + incl - cnt;
-    int32_t *recs = reinterpret_cast<int32_t *>(x.sval);
+    int64_t pos = (int64_t)s_base + before + incl - cnt;   // inside p's segment
+    // fused exchange: p's inbox segment (parity, this rank) through peer memory (NVLink stores);
+    // otherwise p's segment of the local send buffer, moved by exchange()
+    int32_t *recs = x.p2p ? reinterpret_cast<int32_t *>(
+                                x.inbox[p] + 12 * ((int64_t)(x.ipar * x.bd.world + x.rank) * x.icap))
+                          : reinterpret_cast<int32_t *>(x.sval) + 3 * x.bd.b[p];
 #pragma unroll
     for (int k = 0; k < kCompPer; k++) {
       if (v[k] == 0.0) continue;
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *
       x.R[j0 + k] = 0.0;
       pos++;
     }
+    if (x.p2p && cnt) __threadfence_system();   // the records reach the peer before the counts
     __syncthreads();  // s_w / s_base reused by the next chunk
   }
   // the last block: per-peer counts into the header, counters rewound
@@ -256,6 +261,26 @@ __global__ void k_apply_recv(double *__restrict__ F, int64_t lo, const int32_t *
     const int32_t *r = rec + 3 * k;
     const double v = __longlong_as_double(((long long)(uint32_t)r[1]) | ((long long)r[2] << 32));
     red_add_f64(F + ((int64_t)r[0] - lo), v);
+  }
+}
+
+// fused exchange, receiving side: the records every peer wrote into this rank's inbox segment
+// (parity, peer); the counts come from the gathered sweep headers (device-resident)
+__global__ void k_apply_inbox(double *__restrict__ F, int64_t lo, const char *__restrict__ inbox,
+                              int64_t icap, int ipar, const int64_t *__restrict__ ghdr, int world,
+                              int me) {
+  const int hw = 8 + world;
+  for (int q = 0; q < world; q++) {
+    if (q == me) continue;
+    const int64_t m = ghdr[(int64_t)q * hw + 8 + me];
+    const int32_t *rec =
+        reinterpret_cast<const int32_t *>(inbox + 12 * ((int64_t)(ipar * world + q) * icap));
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)gridDim.x * blockDim.x) {
+      const int32_t *r = rec + 3 * k;
+      const double v = __longlong_as_double(((long long)(uint32_t)r[1]) | ((long long)r[2] << 32));
+      red_add_f64(F + ((int64_t)r[0] - lo), v);
+    }
   }
 }
 
@@ -331,6 +356,34 @@ di_status alloc_dist(Graph &g) {
   g.sendcnt = g.hdr + 8;
   const size_t cap = (size_t)std::max<int64_t>(1, (int64_t)(G - 1) * g.n);
   DI_CK(dmalloc(&g.rid, cap * 12));          // received records
+  // fused exchange: a double-buffered inbox of G segments of (largest range) records per rank,
+  // written by the peers' compaction kernels through peer memory (collective; every rank agrees
+  // on the outcome, else all fall back to exchange())
+  g.p2p = false;
+  g.inbox.clear();
+  // (DI_P2P=0 disables it; DI_P2P_FORCE=1 creates it on one rank too, which exercises the
+  // symmetric-memory calls with nothing to send)
+  const bool want = G > 1 || (getenv("DI_P2P_FORCE") && atoi(getenv("DI_P2P_FORCE")) == 1);
+  if (want && !(getenv("DI_P2P") && atoi(getenv("DI_P2P")) == 0)) {
+    int64_t mx = 1;
+    for (int p = 0; p < G; p++) mx = std::max<int64_t>(mx, g.bounds.b[p + 1] - g.bounds.b[p]);
+    g.icap = mx;
+    std::vector<char *> peers;
+    di_status s = g.comm->make_inbox((size_t)2 * G * mx * 12, &peers);
+    int64_t *flag = reinterpret_cast<int64_t *>(g.ghdr);   // scratch before the first sweep
+    const int64_t bad = (s == DI_OK) ? 0 : 1;
+    DI_CK(cudaMemcpy(flag, &bad, 8, cudaMemcpyHostToDevice));
+    di_status s2 = g.comm->allreduce_i64(flag, 1, g.stream);
+    if (s2 != DI_OK) return s2;
+    int64_t nbad = 0;
+    DI_CK(cudaMemcpy(&nbad, flag, 8, cudaMemcpyDeviceToHost));
+    if (nbad == 0) {
+      g.inbox = peers;
+      g.p2p = true;
+    } else {
+      g.comm->free_inbox();
+    }
+  }
   return DI_OK;
 }
 
@@ -339,6 +392,9 @@ void free_dist(Graph &g) {
   for (void *q : p)
     if (q) dfree(q);
   if (g.ghdr_h) cudaFreeHost(g.ghdr_h);
+  if (g.comm) g.comm->free_inbox();
+  g.inbox.clear();
+  g.p2p = false;
   delete g.comm;
   g.comm = nullptr;
 }
@@ -392,7 +448,10 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   auto err_of = [&](double r, double e) { return paper ? r / (1.0 - d - d * e) : r; };
   bool converged = err_of(g.sc_host->r, g.sc_host->e) <= tol;
   const SweepArgs a = sweep_args(g, 0);
-  const DistArgs x = dist_args(g);
+  DistArgs x = dist_args(g);
+  const bool p2p = g.p2p && !(flags & DI_XCHG_NOP2P);
+  x.p2p = p2p ? 1 : 0;
+  int par = 0;   // inbox parity of the current sweep
   int occ = 0;
   if (g.has_loops)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push_dist<true>, kPushThreads, 0);
@@ -404,7 +463,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   std::vector<size_t> s12(G), r12(G);
   const size_t hw = (size_t)(8 + G);
   double xbytes = 0.0, xdense = 0.0;
-  int64_t xentries = 0, ndense = 0;
+  int64_t xentries = 0, ndense = 0, np2p = 0;
   // exchange choice: sparse lists unless the last sparse sweep's lists
   // (12 B per entry, all ranks) outweighed the dense reduction (8 B per remote node per rank);
   // after kDenseRun dense sweeps one sparse sweep measures the lists again
@@ -438,8 +497,10 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
            12.0 * (double)last_lists > 8.0 * (double)(G - 1) * (double)g.n_global);
       if (dense)  // no lists: the header's per-peer counts are zero
         DI_CK(cudaMemsetAsync(g.sendcnt, 0, (size_t)G * 8, g.stream));
-      else
+      else {
+        x.ipar = par;
         k_compact_remote<<<g.num_sms * 4, kCompThreads, 0, g.stream>>>(g.sc, x);
+      }
       launches += 2;
       launched++;
       // one collective for the sums and the per-peer counts of every rank
@@ -480,7 +541,15 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
           for (int q = 0; q < G; q++) last_lists += (p == q) ? 0 : g.ghdr_h[(size_t)p * hw + 8 + q];
         dense_run = 0;
       }
-      for (int p = 0; p < G && !dense; p++) {
+      if (!dense && p2p) {  // the records are already in the owners' inboxes: apply ours
+        for (int p = 0; p < G; p++) xentries += (p == me) ? 0 : g.ghdr_h[(size_t)me * hw + 8 + p];
+        k_apply_inbox<<<g.num_sms * 4, 256, 0, g.stream>>>(g.F, g.lo, g.inbox[me], g.icap, par,
+                                                          g.ghdr, G, me);
+        launches++;
+        par ^= 1;
+        np2p++;
+      }
+      for (int p = 0; p < G && !dense && !p2p; p++) {
         const int64_t ns = (p == me) ? 0 : g.ghdr_h[(size_t)me * hw + 8 + p];
         const int64_t nr = (p == me) ? 0 : g.ghdr_h[(size_t)p * hw + 8 + me];
         sb[p] = reinterpret_cast<const char *>(g.sval) + (size_t)12 * g.bounds.b[p];
@@ -490,7 +559,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
         off += nr;
         xentries += ns;
       }
-      if (!dense &&
+      if (!dense && !p2p &&
           (s = g.comm->exchange(sb.data(), s12.data(), rb.data(), r12.data(), g.stream)) != DI_OK)
         return s;
       if (off > 0) {
@@ -558,6 +627,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
     xbytes = 12.0 * (double)xentries + xdense;
     st->exchange_bytes = xbytes;
     st->dense_exchanges = ndense;
+    st->p2p_exchanges = np2p;
     st->exchange_entries = xentries;
     st->push_ms = push_ms;
     st->select_ms = select_ms;

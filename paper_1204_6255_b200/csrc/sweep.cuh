@@ -273,10 +273,20 @@ struct DistArgs {
   int64_t *isum;             // sel, nd, lk, scanned
   DistBounds bd;
   int rank;
+  // fused exchange (dist.cu): records go straight into the owner's inbox through peer memory;
+  // inbox[p] = rank p's inbox as mapped here, segment (parity, source) of icap records
+  char *inbox[kMaxWorld];
+  int64_t icap;
+  int ipar;    // cycle parity: double-buffered segments (a rank is at most one cycle ahead)
+  int p2p;     // 1: k_compact_remote writes into inbox[p]; 0: into sval (then exchange())
 };
 
 inline DistArgs dist_args(Graph &g) {
   DistArgs x;
+  for (int p = 0; p < kMaxWorld; p++) x.inbox[p] = (p < (int)g.inbox.size()) ? g.inbox[p] : nullptr;
+  x.icap = g.icap;
+  x.ipar = 0;
+  x.p2p = 0;
   x.R = g.R;
   x.sval = g.sval;
   x.tcnt = g.tcnt;

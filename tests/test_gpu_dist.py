@@ -61,11 +61,13 @@ def same_stats(sts):
         assert len({s[k] for s in sts}) == 1, (k, [s[k] for s in sts])
 
 
+@pytest.mark.parametrize("p2p", [True, False])
 @pytest.mark.parametrize("asynchronous", [False, True])
 @pytest.mark.parametrize("G", [2, 3, 4])
-def test_pins_partitioned(G, asynchronous):
+def test_pins_partitioned(G, asynchronous, p2p):
     """T1 on partitions: the exact rationals of tests/golden/pins.txt (graphs with >= G nodes),
-    bulk sweeps and asynchronous cycles (R7 on every rank, one exchange per cycle)."""
+    bulk sweeps and asynchronous cycles (R7 on every rank, one exchange per cycle); the lists
+    through peer memory (fused compaction + transfer) or through the backend's send/recv."""
     need_gpu()
     for name, n, links, X in load_pins():
         if n < G:
@@ -74,9 +76,11 @@ def test_pins_partitioned(G, asynchronous):
         dst = np.array([t for _, t in links], dtype=np.int32)
         for variant in ("sop", "cyc"):
             H, F, st, sts, _ = run(src, dst, n, G, [dict(d=D, tol=1e-16, variant=variant,
-                                                         asynchronous=asynchronous)])[0]
+                                                         asynchronous=asynchronous, p2p=p2p)])[0]
             same_stats(sts)
             assert st["converged"] == 1, (name, st)
+            assert all(s_["p2p_exchanges"] == (s_["sweeps"] - s_["dense_exchanges"] if p2p else 0)
+                       for s_ in sts)
             assert l1(H, [float(x) for x in X]) <= 1e-14, (name, variant, H)
 
 
@@ -98,17 +102,18 @@ def test_random_vs_dense_partitioned(G, asynchronous):
             assert l1(H, X) <= 1e-13, (seed, G)
 
 
+@pytest.mark.parametrize("p2p", [True, False])
 @pytest.mark.parametrize("asynchronous", [False, True])
 @pytest.mark.parametrize("G", [2, 3, 4, 8])
 @pytest.mark.parametrize("variant", ["sop", "cyc"])
-def test_north_star_parity_partitioned(G, variant, asynchronous):
+def test_north_star_parity_partitioned(G, variant, asynchronous, p2p):
     """T11 / T10 on partitions: C1 at tol 1e-10 vs the oracle (1e-9, and the G19 bound against
     the tight 1e-13 oracle run); the partition and the exchange counters are sane."""
     need_gpu()
     src, dst, n = digen.make("c1", seed=1)
     (H, F, st, sts, ranges), = run(src, dst, n, G, [dict(d=D, tol=1e-10, variant=variant,
                                                          asynchronous=asynchronous,
-                                                         exchange="sparse")])
+                                                         exchange="sparse", p2p=p2p)])
     same_stats(sts)
     assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
     Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant=variant)
@@ -127,6 +132,7 @@ def test_north_star_parity_partitioned(G, variant, asynchronous):
     for s, (lo, hi) in zip(sts, ranges):
         assert s["exchange_entries"] <= (n - (hi - lo)) * s["sweeps"]
         assert s["exchange_bytes"] == 12 * s["exchange_entries"]
+        assert s["p2p_exchanges"] == (s["sweeps"] if p2p else 0)
 
 
 @pytest.mark.parametrize("asynchronous", [False, True])
@@ -325,11 +331,15 @@ def test_invalid_partitioned_arguments():
 
 
 @pytest.mark.parametrize("asynchronous", [False, True])
-def test_nccl_backend_single_rank(asynchronous):
+def test_nccl_backend_single_rank(asynchronous, monkeypatch):
     """The NCCL backend for real on one GPU: a communicator of one rank (ncclCommInitRank,
     ncclAllReduce, grouped send/recv with no peers) runs the whole partitioned protocol with
-    nothing to exchange; C1 to the north_star gate, and the same through a group of one."""
+    nothing to exchange; C1 to the north_star gate, and the same through a group of one. With
+    DI_P2P_FORCE=1 the upload also creates the peer-memory inbox on the one rank (ncclMemAlloc,
+    a symmetric ncclCommWindowRegister, the LSA pointer read on the device), and every sweep
+    takes the fused path with no peers."""
     need_gpu()
+    monkeypatch.setenv("DI_P2P_FORCE", "1")
     import paper_1204_6255_b200 as di
     src, dst, n = digen.make("c1", seed=2)
     Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
@@ -338,6 +348,7 @@ def test_nccl_backend_single_rank(asynchronous):
     assert g.range() == (0, n)
     st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous)
     assert st["converged"] == 1 and st["exchange_entries"] == 0
+    assert st["p2p_exchanges"] == st["sweeps"]          # the window exists
     assert l1(g.history().cpu().numpy(), Ho) <= 1e-9
     st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous, exchange="dense")  # one rank: no-op
     assert st["converged"] == 1 and st["dense_exchanges"] == 0
