@@ -93,6 +93,11 @@ typedef enum {
  * pointers of one GPU for an in-process group) when the upload could create the inboxes; this
  * flag moves them with the backend's send/recv instead. */
 #define DI_XCHG_NOP2P   0x800u
+/* Asynchronous multi-GPU cycles (with DI_ASYNC on a partitioned graph): no
+ * collective between two cycles — each rank runs its cycles back to back, the remote fluid goes
+ * through peer-memory rings drained at the start of every cycle, and the ranks meet every 4
+ * cycles (drain, exact global sum F, stop test). Needs the peer-memory inboxes. */
+#define DI_DIST_ASYNC   0x1000u
 /* Block-ordered cycles (F1): each cycle visits K ordered blocks of
  * internal node ids; block b is selected against the cycle's threshold r (computed once per
  * cycle) with the live F, i.e. including the fluid pushed by blocks 0..b-1 this
@@ -127,6 +132,7 @@ typedef struct {
   double exchange_ms;           /* multi-GPU, DI_PROFILE: event time of list exchange + apply     */
   int64_t dense_exchanges;      /* multi-GPU: sweeps whose exchange took the dense fallback       */
   int64_t p2p_exchanges;        /* multi-GPU: sweeps whose lists went through peer memory (fused) */
+  int64_t meetings;             /* DI_DIST_ASYNC: collective meetings (drain + global sum F)       */
 } di_stats;
 
 /* In-process rank group: `world` emulated ranks, one host thread each, sharing one GPU. The

@@ -33,7 +33,7 @@ VARIANTS = {"sop": 0, "cyc": 1, "pi": 2, "pi_pull": 2, "pi_push": 3, "pi_col": 3
 DEDUP, DROP_SELF_LOOPS, BUILD_CSC, HOST_PTRS, LOCAL_LINKS, NO_REORDER = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 PUSH, PULL, AUTO, RESUME, PAPER_ERROR, TRACE, PROFILE, GRAPH_LOOP = 0x0, 0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
 ASYNC = 0x100
-XCHG_SPARSE, XCHG_DENSE, XCHG_NOP2P = 0x200, 0x400, 0x800
+XCHG_SPARSE, XCHG_DENSE, XCHG_NOP2P, DIST_ASYNC = 0x200, 0x400, 0x800, 0x1000
 
 
 class Stats(ctypes.Structure):
@@ -50,7 +50,7 @@ class Stats(ctypes.Structure):
         ("converged", ctypes.c_int32), ("variant", ctypes.c_int32),
         ("exchange_bytes", ctypes.c_double), ("exchange_entries", ctypes.c_int64),
         ("exchange_ms", ctypes.c_double), ("dense_exchanges", ctypes.c_int64),
-        ("p2p_exchanges", ctypes.c_int64),
+        ("p2p_exchanges", ctypes.c_int64), ("meetings", ctypes.c_int64),
     ]
 
     def as_dict(self):
@@ -224,18 +224,21 @@ class Graph:
     # -------------------------------------------------------------- solve
     def solve(self, d=0.85, tol=1e-10, variant="sop", max_sweeps=100_000, B=None, resume=False,
               paper_error=False, trace=False, profile=False, mode="push", graph_loop=False,
-              blocks=1, asynchronous=False, exchange="auto", p2p=True, raise_on_not_converged=False):
+              blocks=1, asynchronous=False, exchange="auto", p2p=True, dist_async=False,
+              raise_on_not_converged=False):
         """di_solve. Returns the di_stats dict (status under key 'status').
         blocks=K > 1: block-ordered cycles (K ordered node blocks per cycle, push only).
         exchange ("auto" | "sparse" | "dense"): remote-fluid exchange of a partitioned graph;
-        p2p=False moves the sparse lists with send/recv instead of peer-memory stores."""
+        p2p=False moves the sparse lists with send/recv instead of peer-memory stores;
+        dist_async=True (with asynchronous=True on a partitioned graph): no collective between
+        cycles, the ranks meet every 4 cycles (F2)."""
         torch = _torch()
         flags = (RESUME if resume else 0) | (PAPER_ERROR if paper_error else 0) | \
                 (TRACE if trace else 0) | (PROFILE if profile else 0) | \
                 (GRAPH_LOOP if graph_loop else 0) | {"push": PUSH, "pull": PULL, "auto": AUTO}[mode] | \
                 ((int(blocks) & 0xFF) << 16) | (ASYNC if asynchronous else 0) | \
                 {"auto": 0, "sparse": XCHG_SPARSE, "dense": XCHG_DENSE}[exchange] | \
-                (0 if p2p else XCHG_NOP2P)
+                (0 if p2p else XCHG_NOP2P) | (DIST_ASYNC if dist_async else 0)
         bp = None
         if B is not None:
             Bt = B if isinstance(B, torch.Tensor) else torch.as_tensor(np.asarray(B))

@@ -58,6 +58,10 @@ enum SweepMode { MODE_PUSH = 0, MODE_PULL = 1, MODE_AUTO = 2 };
 // Multi-GPU: rank g owns the node range [b[g], b[g+1]) (caller's numbering, and
 // internal numbering after the per-range relabelling).
 constexpr int kMaxWorld = 16;
+// Peer-memory inbox of a partitioned graph (dist.cu): per sender a segment of kRingSlots * icap
+// 12-byte records (synchronous sweeps use slots 0/1 by sweep parity; DI_DIST_ASYNC uses the
+// segment as a ring), then one 256-B control line per sender (its published ring tail).
+constexpr int kRingSlots = 4;
 struct DistBounds {
   int world;
   int64_t b[kMaxWorld + 1];
@@ -133,6 +137,9 @@ struct Graph {
   std::vector<char *> inbox;  // fused exchange: every rank's inbox as mapped here (dist.cu)
   int64_t icap = 0;          // records per inbox segment (largest owned range)
   bool p2p = false;          // the inbox exists: k_compact_remote writes through peer memory
+  double e_global = 0.0, e_cycle = 0.0;  // DI_DIST_ASYNC: global absorption (resume; last meeting)
+  unsigned long long *ring = nullptr;  // DI_DIST_ASYNC state: tsent, head, snap [kMaxWorld each],
+                                       // then 8 doubles (sent, applied, r_loc, r_loc_sync, r_sync)
   // locality relabelling: internal id = new_of[user id]; user id = old_of[internal id]
   bool reordered = false;
   int stripes = 0;           // relabelling stripes (DI_STRIPES; 0 = auto: stripes of ~1024 nodes,

@@ -171,6 +171,11 @@ __global__ void __launch_bounds__(kPushThreads) k_push_dist(const SweepArgs a, c
 // order; the receiver adds every record with a RED.
 constexpr int kCompThreads = 256, kCompPer = 16, kCompChunk = kCompThreads * kCompPer;
 
+// byte offset of the control lines in an inbox (after G segments of kRingSlots * icap records)
+__host__ __device__ inline size_t ring_ctrl_offset(int world, int64_t icap) {
+  return ((size_t)world * kRingSlots * (size_t)icap * 12 + 255) / 256 * 256;
+}
+
 __global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *sc, DistArgs x) {
   __shared__ int s_w[kCompThreads / 32];
   __shared__ unsigned long long s_base;
@@ -217,23 +222,33 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *
       s_base = total ? atomicAdd(x.tcnt + 32 * p, (unsigned long long)total) : 0ull;
     __syncthreads();
     int64_t pos = (int64_t)s_base + before + incl - cnt;   // inside p's segment
-    // fused exchange: p's inbox segment (parity, this rank) through peer memory (NVLink stores);
+    // fused exchange: p's inbox, segment of this rank, through peer memory (NVLink stores):
+    // slot `ipar` (synchronous sweeps) or the ring from the published tail (DI_DIST_ASYNC);
     // otherwise p's segment of the local send buffer, moved by exchange()
-    int32_t *recs = x.p2p ? reinterpret_cast<int32_t *>(
-                                x.inbox[p] + 12 * ((int64_t)(x.ipar * x.bd.world + x.rank) * x.icap))
+    const int64_t seg = (int64_t)x.rank * kRingSlots * x.icap;
+    const int64_t cap = (int64_t)kRingSlots * x.icap;
+    int32_t *recs = x.p2p ? reinterpret_cast<int32_t *>(x.inbox[p]) +
+                                3 * (seg + (x.ring ? 0 : (int64_t)x.ipar * x.icap))
                           : reinterpret_cast<int32_t *>(x.sval) + 3 * x.bd.b[p];
+    const int64_t t0 = x.ring ? (int64_t)x.tsent[p] : 0;
+    double sent = 0.0;
 #pragma unroll
     for (int k = 0; k < kCompPer; k++) {
       if (v[k] == 0.0) continue;
       const long long bits = __double_as_longlong(v[k]);
-      int32_t *r = recs + 3 * pos;
+      int32_t *r = recs + 3 * (x.ring ? (t0 + pos) % cap : pos);
       r[0] = (int32_t)(j0 + k);
       r[1] = (int32_t)(bits & 0xffffffffll);
       r[2] = (int32_t)(bits >> 32);
       x.R[j0 + k] = 0.0;
+      sent += v[k];
       pos++;
     }
     if (x.p2p && cnt) __threadfence_system();   // the records reach the peer before the counts
+    if (x.ring) {  // fluid that left this rank (the local r estimate, DI_DIST_ASYNC)
+      sent = warp_sum(sent);
+      if (lane == 0 && sent != 0.0) atomicAdd(x.sent, sent);
+    }
     __syncthreads();  // s_w / s_base reused by the next chunk
   }
   // the last block: per-peer counts into the header, counters rewound
@@ -248,8 +263,16 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *
   __threadfence();
   if (threadIdx.x < x.bd.world) {
     volatile unsigned long long *cn = x.tcnt + 32 * threadIdx.x;
-    x.sendcnt[threadIdx.x] = (threadIdx.x == x.rank) ? 0 : (int64_t)*cn;
+    const unsigned long long c = *cn;
+    x.sendcnt[threadIdx.x] = (threadIdx.x == x.rank) ? 0 : (int64_t)c;
     *cn = 0ull;
+    if (x.ring && threadIdx.x != x.rank) {  // publish the new tail in the owner's control line
+      const unsigned long long t = x.tsent[threadIdx.x] + c;
+      x.tsent[threadIdx.x] = t;
+      unsigned long long *ctl = reinterpret_cast<unsigned long long *>(
+          x.inbox[threadIdx.x] + ring_ctrl_offset(x.bd.world, x.icap) + 256 * (size_t)x.rank);
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ctl), "l"(t) : "memory");
+    }
   }
   if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned int *>(x.tcnt + 32 * x.bd.world) = 0u;
 }
@@ -273,8 +296,8 @@ __global__ void k_apply_inbox(double *__restrict__ F, int64_t lo, const char *__
   for (int q = 0; q < world; q++) {
     if (q == me) continue;
     const int64_t m = ghdr[(int64_t)q * hw + 8 + me];
-    const int32_t *rec =
-        reinterpret_cast<const int32_t *>(inbox + 12 * ((int64_t)(ipar * world + q) * icap));
+    const int32_t *rec = reinterpret_cast<const int32_t *>(inbox) +
+                         3 * ((int64_t)q * kRingSlots * icap + (int64_t)ipar * icap);
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
          k += (int64_t)gridDim.x * blockDim.x) {
       const int32_t *r = rec + 3 * k;
@@ -282,6 +305,86 @@ __global__ void k_apply_inbox(double *__restrict__ F, int64_t lo, const char *__
       red_add_f64(F + ((int64_t)r[0] - lo), v);
     }
   }
+}
+
+// DI_DIST_ASYNC receiving side, step 1: the tails the peers published (acquire: their records
+// are visible after it); every block of the apply then uses the same snapshot
+__global__ void k_ring_snap(const char *inbox, int world, int64_t icap, int me,
+                            unsigned long long *snap) {
+  const int q = threadIdx.x;
+  if (q >= world || q == me) return;
+  const unsigned long long *ctl = reinterpret_cast<const unsigned long long *>(
+      inbox + ring_ctrl_offset(world, icap) + 256 * (size_t)q);
+  unsigned long long t;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(t) : "l"(ctl) : "memory");
+  snap[q] = t;
+}
+
+// step 2: records [head, snap) of every peer's ring into F (RED), the fluid summed into *applied
+__global__ void k_ring_apply(double *__restrict__ F, int64_t lo, const char *__restrict__ inbox,
+                             int world, int64_t icap, int me, const unsigned long long *snap,
+                             const unsigned long long *head, double *applied) {
+  const int64_t cap = (int64_t)kRingSlots * icap;
+  double acc = 0.0;
+  for (int q = 0; q < world; q++) {
+    if (q == me) continue;
+    const int64_t h = (int64_t)head[q], m = (int64_t)snap[q] - h;
+    const int32_t *seg = reinterpret_cast<const int32_t *>(inbox) + 3 * ((int64_t)q * cap);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)gridDim.x * blockDim.x) {
+      const int32_t *r = seg + 3 * ((h + k) % cap);
+      const double v = __longlong_as_double(((long long)(uint32_t)r[1]) | ((long long)r[2] << 32));
+      red_add_f64(F + ((int64_t)r[0] - lo), v);
+      acc += v;
+    }
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0 && acc != 0.0) atomicAdd(applied, acc);
+}
+
+// step 3: the ring heads advance to the snapshot
+__global__ void k_ring_advance(int world, int me, const unsigned long long *snap,
+                               unsigned long long *head) {
+  const int q = threadIdx.x;
+  if (q < world && q != me) head[q] = snap[q];
+}
+
+// DI_DIST_ASYNC: this rank's cycle effect on its own fluid, r_loc <- r_loc - taken + pushed -
+// sent + applied, and the r of the next cycle's threshold (reading R8 in DESIGN.md): the global
+// r of the last meeting times (r_loc + sent) / r_loc at that meeting. Measured on emulated ranks
+// (tools/exp/dist_async.py): the rule on the rank's own part, r_loc / L_loc, or the decay
+// without the sent fluid, over-diffuse (C4 at G = 2: 64 and 49 eq-iter vs 44.3 with this one,
+// 44.75 for synchronous cycles); counters; the starvation guard
+__global__ void k_ring_finalize(const SweepArgs a, const DistArgs x, double *rs) {
+  if (threadIdx.x != 0) return;
+  Scalars *sc = a.sc;
+  const double taken = x.dsum[3], pushed = x.dsum[1], e = x.dsum[2];
+  const double sent = rs[0];
+  const double r_loc = rs[2] - taken + pushed - sent + rs[1];
+  rs[0] = 0.0;
+  rs[1] = 0.0;
+  rs[2] = r_loc;
+  // the global r of the last meeting, scaled by this rank's decay since; the fluid it just sent
+  // still counts (it left for the peers, it did not leave the system)
+  const double rl = (r_loc > 0.0 ? r_loc : 0.0) + sent;
+  sc->r = (rs[3] > 0.0) ? rs[4] * rl / rs[3] : rs[4];
+  sc->e = sc->e + e;
+  sc->sweeps = sc->sweeps + 1;
+  sc->selected_total = sc->selected_total + x.isum[0];
+  sc->selected_nd_total = sc->selected_nd_total + x.isum[1];
+  sc->links_total = sc->links_total + x.isum[2];
+  sc->scanned_total = sc->scanned_total + a.n;
+  const int starving = (x.isum[0] == 0 && sc->variant == DI_SOP) ? 1 : 0;
+  if (starving) sc->guards = sc->guards + 1;
+  sc->guard = starving;
+}
+
+// meeting: r_loc = r_loc at the meeting = this rank's exact sum F (resid); r = the global sum
+__global__ void k_ring_meet(Scalars *sc, const double *global, double *rs) {
+  rs[2] = sc->resid;
+  rs[3] = sc->resid;
+  rs[4] = *global;
+  sc->r = *global;
 }
 
 // dense fallback: this rank's slice of the reduced accumulators into F
@@ -369,7 +472,10 @@ di_status alloc_dist(Graph &g) {
     for (int p = 0; p < G; p++) mx = std::max<int64_t>(mx, g.bounds.b[p + 1] - g.bounds.b[p]);
     g.icap = mx;
     std::vector<char *> peers;
-    di_status s = g.comm->make_inbox((size_t)2 * G * mx * 12, &peers);
+    di_status s = g.comm->make_inbox(ring_ctrl_offset(G, mx) + (size_t)256 * G, &peers);
+    if (s == DI_OK &&  // ring tails start at 0 (the allreduce below orders it before any use)
+        cudaMemset(peers[g.rank] + ring_ctrl_offset(G, mx), 0, (size_t)256 * G) != cudaSuccess)
+      s = DI_ECUDA;
     int64_t *flag = reinterpret_cast<int64_t *>(g.ghdr);   // scratch before the first sweep
     const int64_t bad = (s == DI_OK) ? 0 : 1;
     DI_CK(cudaMemcpy(flag, &bad, 8, cudaMemcpyHostToDevice));
@@ -380,6 +486,8 @@ di_status alloc_dist(Graph &g) {
     if (nbad == 0) {
       g.inbox = peers;
       g.p2p = true;
+      DI_CK(dmalloc(&g.ring, 3 * kMaxWorld * 8 + 8 * 8));
+      DI_CK(dmemset(g.ring, 0, 3 * kMaxWorld * 8 + 8 * 8));
     } else {
       g.comm->free_inbox();
     }
@@ -388,7 +496,7 @@ di_status alloc_dist(Graph &g) {
 }
 
 void free_dist(Graph &g) {
-  void *p[] = {g.R, g.sval, g.tcnt, g.hdr, g.ghdr, g.rid};
+  void *p[] = {g.R, g.sval, g.tcnt, g.hdr, g.ghdr, g.rid, g.ring};
   for (void *q : p)
     if (q) dfree(q);
   if (g.ghdr_h) cudaFreeHost(g.ghdr_h);
@@ -408,8 +516,174 @@ di_status dist_residual(Graph &g, double *l1) {
   return DI_OK;
 }
 
+// DI_DIST_ASYNC: asynchronous cycles across ranks. Every rank runs its own
+// cycles (k_cycle<DIST>) back to back; the fluid for remote targets goes through the peer-memory
+// rings (k_compact_remote in ring mode appends and publishes the tail; each rank drains its
+// rings at the start of every cycle), so no collective separates two cycles. The ranks meet
+// every kRingSlots cycles — which bounds what a sender can have in flight to one ring — to drain
+// everything, take the exact global sum F and decide convergence; between meetings a rank's
+// DI-SOP threshold scales the last global r by its own fluid's decay (reading R8).
+di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int variant,
+                           int64_t max_sweeps, uint32_t flags, di_stats *st) {
+  const int G = g.world, me = g.rank;
+  if (!g.p2p || !g.ring)
+  {
+    set_error("di_solve: DI_DIST_ASYNC needs the peer-memory inboxes (see DI_P2P)");
+    return DI_EINVAL;
+  }
+  const bool resume = flags & DI_RESUME;
+  const int paper = (flags & DI_PAPER_ERROR) ? 1 : 0;
+  int64_t launches = 0;
+  cudaEvent_t t0, t1;
+  DI_CK(cudaEventCreate(&t0));
+  DI_CK(cudaEventCreate(&t1));
+  {
+    Scalars &s = *g.sc_host;
+    const uint32_t epoch = s.epoch ? s.epoch : 1;
+    const double e_prev = s.e;
+    memset(&s, 0, sizeof(Scalars));
+    s.epoch = epoch;
+    s.e = 0.0;   // this rank's absorption; the global e is summed at the meetings
+    s.d = d;
+    s.tol = tol;
+    s.variant = variant;
+    s.paper_err = paper;
+    s.alpha = g.alpha;
+    s.mode = MODE_PUSH;
+    (void)e_prev;
+  }
+  double e_global = resume ? g.e_global : 0.0;
+  DI_CK(cudaEventRecord(t0, g.stream));
+  DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
+  DI_CK(cudaMemsetAsync(g.R, 0, (size_t)g.n_global * 8, g.stream));
+  DI_CK(cudaMemsetAsync(g.tcnt, 0, (size_t)(G + 1) * 32 * 8, g.stream));
+  if (!resume) launch_init(g, B, d, &launches);
+  unsigned long long *tsent = g.ring, *head = g.ring + kMaxWorld, *snap = g.ring + 2 * kMaxWorld;
+  double *rs = reinterpret_cast<double *>(g.ring + 3 * kMaxWorld);
+  double *scratch = reinterpret_cast<double *>(g.hdr + 8 + g.world);
+  (void)tsent;
+  DI_CK(cudaMemsetAsync(rs, 0, 8 * 8, g.stream));
+  const char *mine = g.inbox[me];
+  auto drain = [&]() {
+    k_ring_snap<<<1, 32, 0, g.stream>>>(mine, G, g.icap, me, snap);
+    k_ring_apply<<<g.num_sms * 4, 256, 0, g.stream>>>(g.F, g.lo, mine, G, g.icap, me, snap, head,
+                                                      rs + 1);
+    k_ring_advance<<<1, 32, 0, g.stream>>>(G, me, snap, head);
+    launches += 3;
+  };
+  // a meeting: everyone's cycles and their ring appends are complete (collective 1, which also
+  // sums the dangling absorption), every ring is drained, the exact global sum F (collective 2)
+  auto meet = [&](double *r_out) -> di_status {
+    DI_CK(cudaMemcpyAsync(scratch, &g.sc->e, 8, cudaMemcpyDeviceToDevice, g.stream));
+    di_status s = g.comm->allreduce_f64(scratch, 1, g.stream);
+    if (s != DI_OK) return s;
+    double e_sum = 0.0;
+    DI_CK(cudaMemcpyAsync(&e_sum, scratch, 8, cudaMemcpyDeviceToHost, g.stream));
+    drain();
+    launch_reduce_F(g, &launches);   // this rank's exact sum F -> sc->resid
+    k_copy_resid<<<1, 1, 0, g.stream>>>(g.sc, scratch + 1);
+    if ((s = g.comm->allreduce_f64(scratch + 1, 1, g.stream)) != DI_OK) return s;
+    k_ring_meet<<<1, 1, 0, g.stream>>>(g.sc, scratch + 1, rs);
+    launches += 2;
+    DI_CK(cudaMemcpyAsync(r_out, scratch + 1, 8, cudaMemcpyDeviceToHost, g.stream));
+    DI_CK(cudaStreamSynchronize(g.stream));
+    g.e_cycle = e_sum;
+    return DI_OK;
+  };
+  auto err_of = [&](double r, double e) { return paper ? r / (1.0 - d - d * e) : r; };
+  double r_glob = 0.0;
+  di_status s = meet(&r_glob);
+  if (s != DI_OK) return s;
+  bool converged = err_of(r_glob, e_global + g.e_cycle) <= tol;
+  const SweepArgs a = sweep_args(g, 0);
+  DistArgs x = dist_args(g);
+  x.p2p = 1;
+  x.ring = 1;
+  int64_t launched = 0, meetings = 1;
+  double xentries = 0;
+  while (!converged && launched < max_sweeps) {
+    const int64_t k_end = std::min<int64_t>(max_sweeps, launched + kRingSlots);
+    for (; launched < k_end; launched++) {
+      drain();                       // what the peers sent so far
+      launch_cycle(g, &launches);    // this rank's asynchronous cycle (R7) with r from rs
+      k_compact_remote<<<g.num_sms * 4, kCompThreads, 0, g.stream>>>(g.sc, x);
+      k_ring_finalize<<<1, 32, 0, g.stream>>>(a, x, rs);
+      launches += 2;
+    }
+    if ((s = meet(&r_glob)) != DI_OK) return s;
+    meetings++;
+    converged = err_of(r_glob, e_global + g.e_cycle) <= tol;
+  }
+  // global counters (every rank reports the same totals)
+  DI_CK(cudaMemcpyAsync(g.sc_host, g.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, g.stream));
+  DI_CK(cudaStreamSynchronize(g.stream));
+  {
+    int64_t *cnt = reinterpret_cast<int64_t *>(scratch + 2);
+    const int64_t h[5] = {g.sc_host->selected_total, g.sc_host->selected_nd_total,
+                          g.sc_host->links_total, g.sc_host->scanned_total, g.sc_host->guards};
+    DI_CK(cudaMemcpyAsync(cnt, h, sizeof(h), cudaMemcpyHostToDevice, g.stream));
+    if ((s = g.comm->allreduce_i64(cnt, 5, g.stream)) != DI_OK) return s;
+    int64_t tot[5];
+    DI_CK(cudaMemcpyAsync(tot, cnt, sizeof(tot), cudaMemcpyDeviceToHost, g.stream));
+    DI_CK(cudaStreamSynchronize(g.stream));
+    Scalars &c = *g.sc_host;
+    c.selected_total = tot[0];
+    c.selected_nd_total = tot[1];
+    c.links_total = tot[2];
+    c.scanned_total = tot[3];
+    c.guards = tot[4];
+    c.resid = r_glob;
+    c.r = r_glob;
+    c.e = e_global + g.e_cycle;
+    c.sweeps = launched;
+    DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
+  }
+  g.e_global = g.sc_host->e;
+  DI_CK(cudaEventRecord(t1, g.stream));
+  DI_CK(cudaEventSynchronize(t1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  DI_CK(cudaGetLastError());
+  g.solved = true;
+  g.last_d = d;
+  g.log_n = 0;
+  (void)xentries;
+  if (st) {
+    const Scalars &c = *g.sc_host;
+    memset(st, 0, sizeof(*st));
+    st->sweeps = c.sweeps;
+    st->selected_total = c.selected_total;
+    st->link_diffusions = c.links_total;
+    st->starvation_fallbacks = c.guards;
+    st->nodes_scanned = c.scanned_total;
+    st->gpu_launches = launches;
+    st->residual_l1 = c.resid;
+    st->dangling_absorbed = c.e;
+    st->equivalent_iterations = g.l_global > 0 ? (double)c.links_total / (double)g.l_global : 0.0;
+    st->solve_ms = ms;
+    st->counted_bytes = 12.0 * c.scanned_total + 40.0 * c.selected_total + 20.0 * c.links_total;
+    st->push_bytes = 16.0 * c.selected_nd_total + 20.0 * c.links_total;
+    st->error_estimate = c.resid / (1.0 - d - d * c.e);
+    st->converged = converged ? 1 : 0;
+    st->variant = variant;
+    st->p2p_exchanges = launched;
+    st->meetings = meetings;
+  }
+  return converged ? DI_OK : DI_NOT_CONVERGED;
+}
+
 di_status solve_dist(Graph &g, double d, const double *B, double tol, int variant,
                      int64_t max_sweeps, uint32_t flags, di_stats *st) {
+  if (flags & DI_DIST_ASYNC) {
+    if (!(flags & DI_ASYNC))
+    {
+      set_error("di_solve: DI_DIST_ASYNC runs asynchronous cycles (add DI_ASYNC)");
+      return DI_EINVAL;
+    }
+    return solve_dist_async(g, d, B, tol, variant, max_sweeps, flags, st);
+  }
   const int G = g.world, me = g.rank;
   const bool resume = flags & DI_RESUME;
   const bool async = flags & DI_ASYNC;

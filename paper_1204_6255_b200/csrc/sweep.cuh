@@ -279,6 +279,9 @@ struct DistArgs {
   int64_t icap;
   int ipar;    // cycle parity: double-buffered segments (a rank is at most one cycle ahead)
   int p2p;     // 1: k_compact_remote writes into inbox[p]; 0: into sval (then exchange())
+  int ring;    // DI_DIST_ASYNC: append at the ring tail, publish it, sum the sent fluid
+  unsigned long long *tsent;  // [kMaxWorld] records sent to each owner so far (ring tails)
+  double *sent;               // fluid compacted this cycle (ring mode)
 };
 
 inline DistArgs dist_args(Graph &g) {
@@ -287,6 +290,9 @@ inline DistArgs dist_args(Graph &g) {
   x.icap = g.icap;
   x.ipar = 0;
   x.p2p = 0;
+  x.ring = 0;
+  x.tsent = g.ring;
+  x.sent = g.ring ? reinterpret_cast<double *>(g.ring + 3 * kMaxWorld) : nullptr;
   x.R = g.R;
   x.sval = g.sval;
   x.tcnt = g.tcnt;

@@ -188,6 +188,53 @@ def test_dense_exchange_partitioned(G, asynchronous):
         assert 0 < st["dense_exchanges"] < st["sweeps"]
 
 
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_dist_async(G):
+    """F2 (DI_DIST_ASYNC): asynchronous cycles on every rank with no collective between two
+    cycles; remote fluid through the peer-memory rings; meetings every 4 cycles. Exact pins, random
+    graphs vs the dense solve, C1 at the north_star gate (vs the oracle, both to 1e-10), the
+    invariant F = B + P.H - H and conservation at a max_sweeps stop (the meeting drains every
+    ring), global counters identical on every rank."""
+    need_gpu()
+    kw = dict(d=D, asynchronous=True, dist_async=True)
+    for name, n, links, X in load_pins():
+        if n < G:
+            continue
+        src = np.array([s for s, _ in links], dtype=np.int32)
+        dst = np.array([t for _, t in links], dtype=np.int32)
+        for variant in ("sop", "cyc"):
+            H, F, st, sts, _ = run(src, dst, n, G, [dict(tol=1e-16, variant=variant, **kw)])[0]
+            same_stats(sts)
+            assert st["converged"] == 1 and st["meetings"] >= 1, (name, st)
+            assert l1(H, [float(x) for x in X]) <= 1e-14, (name, variant, H)
+    for seed in range(0, 25, 3):
+        src, dst, n = digen.small_random(seed)
+        if n < G:
+            continue
+        X = defn.solve_dense(src, dst, n, D)
+        H, F, st, sts, _ = run(src, dst, n, G, [dict(tol=1e-15, variant="sop", **kw)])[0]
+        same_stats(sts)
+        assert st["converged"] == 1 and l1(H, X) <= 1e-13, seed
+    src, dst, n = digen.make("c1", seed=1)
+    P = defn.sparse_P(src, dst, n, D)
+    B = defn.uniform_B(n, D)
+    outd = np.bincount(src, minlength=n)
+    Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
+    res = run(src, dst, n, G, [dict(tol=1e-10, variant="sop", **kw),
+                               dict(tol=1e-300, variant="sop", max_sweeps=6, **kw)])
+    H, F, st, sts, _ = res[0]
+    same_stats(sts)
+    assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
+    assert abs(F.sum() - st["residual_l1"]) <= 1e-18
+    assert l1(H, Ho) <= 1e-9
+    assert st["meetings"] == -(-st["sweeps"] // 4) + 1
+    H, F, st, sts, _ = res[1]
+    assert st["sweeps"] == 6 and st["converged"] == 0 and np.all(F >= 0)
+    assert np.abs(F - (B + P @ H - H)).max() <= 1e-15
+    cons = F.sum() + (1 - D) * H[outd > 0].sum() + H[outd == 0].sum()
+    assert abs(cons - (1 - D)) <= 1e-14
+
+
 def test_cyc_neumann_partitioned():
     """T7 on partitions: bulk DI-CYC without loops is the Neumann series, F_n = P^n B and
     H_n = sum_{k<n} P^k B, whatever the partition (the exchange only moves where fluid is added)."""
