@@ -137,6 +137,7 @@ def run_ours(args):
     if args.sched != "block":
         args.blocks = 1
     use_async = args.sched == "async"
+    dist_async = use_async and world > 1 and args.dist_async   # F2: ranks meet every 4 cycles
     part = dict(rank=rank, world=world, nccl_id=nid) if world > 1 else dict(build_csc=args.mode != "push")
 
     src, dst, n, gen_s = make_graph(args.config, args.seed)
@@ -167,7 +168,7 @@ def run_ours(args):
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         st = g.solve(d=D, tol=TOL, variant=args.variant, profile=profile, mode=args.mode,
-                     blocks=args.blocks, graph_loop=graph, asynchronous=use_async)
+                     blocks=args.blocks, graph_loop=graph, asynchronous=use_async, dist_async=dist_async)
         ev1.record(stream)
         ev1.synchronize()
         assert st["converged"] == 1, st
@@ -239,7 +240,7 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         g.solve(d=D, tol=TOL, variant=args.variant, mode=args.mode, blocks=args.blocks,
-                graph_loop=use_graph, asynchronous=use_async)
+                graph_loop=use_graph, asynchronous=use_async, dist_async=dist_async)
         e1.record(stream)
         e1.synchronize()
         warm.append(e0.elapsed_time(e1))
@@ -261,7 +262,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         st = gh.solve(d=D, tol=TOL, variant=args.variant, mode=args.mode, blocks=args.blocks,
-                      asynchronous=use_async,
+                      asynchronous=use_async, dist_async=dist_async,
                       graph_loop=use_graph)
         t2 = time.perf_counter()
         H = gh.history()
@@ -298,7 +299,9 @@ def run_ours(args):
                                 "block": f"block-ordered cycles, K = {args.blocks}",
                                 "bulk": "bulk-synchronous sweeps"}[args.sched],
                    "l2": "inputs > 126 MB L2 and 512 MiB L2 flush before each step",
-                   "parallelism": f"1-D node range x{world}, NCCL (id, value) exchange" if world > 1
+                   "parallelism": (f"1-D node range x{world}, (id, value) lists (peer memory if available)"
+                                   + (", asynchronous cycles meeting every 4 (F2)" if dist_async else
+                                      ", one exchange per cycle")) if world > 1
                    else "single GPU",
                    "init_build_ms": round(init_ms, 1), "generator_s": round(gen_s, 1)},
         "time_to_tol_ms": round(ms_per_step, 3),
@@ -314,7 +317,10 @@ def run_ours(args):
         "host_loop_profiled_ms_per_step": gl_ms,
         "loop": "DI_GRAPH_LOOP (device-side while node)" if use_graph else "host loop",
         "exchange": ({"bytes_per_step_per_gpu": sum(s["exchange_bytes"] for s in stats) / len(stats),
-                      "ms_per_step": sum(s["exchange_ms"] for s in stats) / len(stats)}
+                      "ms_per_step": sum(s["exchange_ms"] for s in stats) / len(stats),
+                      "peer_memory_sweeps_per_step": sum(s["p2p_exchanges"] for s in stats) / len(stats),
+                      "dense_sweeps_per_step": sum(s["dense_exchanges"] for s in stats) / len(stats),
+                      "meetings_per_step": sum(s["meetings"] for s in stats) / len(stats)}
                      if world > 1 else None),
         "clocks": clocks,
         "cpu_baseline": cpu,
@@ -377,6 +383,8 @@ def main():
                          "per cycle (DI_BLOCKS); bulk: bulk-synchronous sweeps")
     ap.add_argument("--blocks", type=int, default=8, help="K for --sched block")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--dist-async", action="store_true",
+                    help="N > 1: asynchronous multi-GPU cycles (DI_DIST_ASYNC, SURVEY F2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-cycles", type=int, default=12)
