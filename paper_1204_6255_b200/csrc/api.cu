@@ -102,7 +102,7 @@ struct EventSet {
 
 void free_graph(Graph *g) {
   if (!g) return;
-  void *ptrs[] = {g->ppartials, g->rep, g->hub_items, g->row_ptr, g->col, g->deg, g->kloop, g->csc_ptr, g->csc_row, g->F, g->H,
+  void *ptrs[] = {g->ppartials, g->rep, g->hub_items, g->cyc_times, g->row_ptr, g->col, g->deg, g->kloop, g->csc_ptr, g->csc_row, g->F, g->H,
                   g->new_of, g->old_of, g->Bperm, g->xfer,
                   g->S, g->aux, g->sc, g->partials, g->ipartials, g->red_partials,
                   g->log_r, g->log_sel, g->log_links, g->log_mode};

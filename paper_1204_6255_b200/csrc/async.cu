@@ -537,6 +537,8 @@ static int hot_shift_of(const Graph &g) {
 
 // called by di_solve before any launch or capture (allocations are not capturable)
 di_status prepare_cycle(Graph &g) {
+  if (getenv("DI_CYC_TIMES") && !g.cyc_times)
+    DI_CK(dmalloc(&g.cyc_times, (size_t)64 * kMaxSlices * 2 * sizeof(unsigned long long)));
   const int hot = hot_shift_of(g);
   if (hot >= 0 && !g.rep) {
     const size_t rep_bytes = ((size_t)kCopies * kRepl * kRepStride + kRepl) * sizeof(double);
@@ -556,8 +558,6 @@ di_status prepare_cycle(Graph &g) {
           items.push_back(std::min(b + kHubItem, rp[k + 1]));
         }
     g.n_hub = (int)(items.size() / 3);
-    if (getenv("DI_CYC_TIMES") && !g.cyc_times)
-      DI_CK(dmalloc(&g.cyc_times, (size_t)64 * kMaxSlices * 2 * sizeof(unsigned long long)));
     if (g.n_hub > 0) {
       DI_CK(dmalloc(&g.hub_items, items.size() * sizeof(int64_t)));
       DI_CK(cudaMemcpyAsync(g.hub_items, items.data(), items.size() * sizeof(int64_t),
