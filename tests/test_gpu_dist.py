@@ -361,10 +361,39 @@ def test_async_partitioned_invariants():
     assert l1(H, X) <= (1e-13 + 1e-15) / (1 - D) + 1e-14
 
 
-def test_invalid_partitioned_arguments():
+def test_invalid_partitioned_arguments(monkeypatch):
     need_gpu()
     import paper_1204_6255_b200 as di
     src, dst, n = digen.make("c1")
+
+    def dist_async_flags(r, grp):   # F2 runs asynchronous cycles only
+        g = di.Graph(src, dst, n, rank=r, world=2, group=grp)
+        try:
+            with pytest.raises(di.DIError) as ei:
+                g.solve(dist_async=True)
+            assert ei.value.status == di.DI_EINVAL and "DI_ASYNC" in str(ei.value)
+        finally:
+            g.free()
+
+    def no_inbox(r, grp):           # F2 needs the peer-memory inboxes
+        g = di.Graph(src, dst, n, rank=r, world=2, group=grp)
+        try:
+            with pytest.raises(di.DIError) as ei:
+                g.solve(asynchronous=True, dist_async=True)
+            assert ei.value.status == di.DI_EINVAL and "inbox" in str(ei.value)
+            st = g.solve(asynchronous=True)            # the send/recv path still works
+            assert st["converged"] == 1 and st["p2p_exchanges"] == 0
+        finally:
+            g.free()
+
+    from paper_1204_6255_b200.dist import run_local_group
+    run_local_group(2, dist_async_flags)
+    monkeypatch.setenv("DI_P2P", "0")
+    run_local_group(2, no_inbox)
+    monkeypatch.delenv("DI_P2P")
+    g = di.Graph(src, dst, n)                          # one GPU: the flag is ignored
+    assert g.solve(asynchronous=True, dist_async=True)["converged"] == 1
+    g.free()
 
     def bad_csc(r, grp):
         di.Graph(src, dst, n, rank=r, world=2, group=grp, build_csc=True)
