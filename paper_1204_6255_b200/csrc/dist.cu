@@ -169,7 +169,14 @@ __global__ void __launch_bounds__(kPushThreads) k_push_dist(const SweepArgs a, c
 // atomics are per chunk, not per entry. The last block publishes the per-peer counts into the
 // sweep header and rewinds the counters. Record order inside a segment is the (free) reservation
 // order; the receiver adds every record with a RED.
-constexpr int kCompThreads = 256, kCompPer = 16, kCompChunk = kCompThreads * kCompPer;
+#ifndef DI_COMP_PER
+#define DI_COMP_PER 4
+#endif
+#ifndef DI_COMP_BPS
+#define DI_COMP_BPS 16
+#endif
+constexpr int kCompThreads = 256, kCompPer = DI_COMP_PER, kCompChunk = kCompThreads * kCompPer;
+constexpr int kCompBlocksPerSM = DI_COMP_BPS;
 
 // byte offset of the control lines in an inbox (after G segments of kRingSlots * icap records)
 __host__ __device__ inline size_t ring_ctrl_offset(int world, int64_t icap) {
@@ -178,9 +185,11 @@ __host__ __device__ inline size_t ring_ctrl_offset(int world, int64_t icap) {
 
 __global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *sc, DistArgs x) {
   __shared__ int s_w[kCompThreads / 32];
+  __shared__ double s_sent[kCompThreads / 32];
   __shared__ unsigned long long s_base;
   __shared__ bool s_last;
   if (sc->stop) return;
+  double sent = 0.0;   // ring mode: this thread's compacted fluid, over all its chunks
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // chunk index space: owners in order, chunks of kCompChunk ids inside each (own range skipped)
   int64_t nchunks = 0;
@@ -195,13 +204,16 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *
       if (cc < k) break;
       cc -= k;
     }
-    const int64_t j0 = x.bd.b[p] + cc * kCompChunk + (int64_t)threadIdx.x * kCompPer;
+    // element k of this thread: id j0 + k * kCompThreads (a warp reads 32 consecutive doubles
+    // per load: coalesced; the record order inside a segment is free)
+    const int64_t j0 = x.bd.b[p] + cc * kCompChunk + (int64_t)threadIdx.x;
     const int64_t jend = x.bd.b[p + 1];
     double v[kCompPer];
     int cnt = 0;
 #pragma unroll
     for (int k = 0; k < kCompPer; k++) {
-      v[k] = (j0 + k < jend) ? __ldcg(x.R + j0 + k) : 0.0;
+      const int64_t j = j0 + (int64_t)k * kCompThreads;
+      v[k] = (j < jend) ? __ldcs(x.R + j) : 0.0;
       cnt += (v[k] != 0.0) ? 1 : 0;
     }
     int incl = cnt;
@@ -230,31 +242,46 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *
     int32_t *recs = x.p2p ? reinterpret_cast<int32_t *>(x.inbox[p]) +
                                 3 * (seg + (x.ring ? 0 : (int64_t)x.ipar * x.icap))
                           : reinterpret_cast<int32_t *>(x.sval) + 3 * x.bd.b[p];
-    const int64_t t0 = x.ring ? (int64_t)x.tsent[p] : 0;
-    double sent = 0.0;
+    const int64_t t0 = x.ring ? (int64_t)(x.tsent[p] % (unsigned long long)cap) : 0;  // ring start
 #pragma unroll
     for (int k = 0; k < kCompPer; k++) {
       if (v[k] == 0.0) continue;
       const long long bits = __double_as_longlong(v[k]);
-      int32_t *r = recs + 3 * (x.ring ? (t0 + pos) % cap : pos);
-      r[0] = (int32_t)(j0 + k);
+      int64_t at = pos;
+      if (x.ring) {  // pos < one range <= cap: one wrap at most
+        at = t0 + pos;
+        if (at >= cap) at -= cap;
+      }
+      int32_t *r = recs + 3 * at;
+      r[0] = (int32_t)(j0 + (int64_t)k * kCompThreads);
       r[1] = (int32_t)(bits & 0xffffffffll);
       r[2] = (int32_t)(bits >> 32);
-      x.R[j0 + k] = 0.0;
+      x.R[j0 + (int64_t)k * kCompThreads] = 0.0;
       sent += v[k];
       pos++;
     }
-    if (x.p2p && cnt) __threadfence_system();   // the records reach the peer before the counts
-    if (x.ring) {  // fluid that left this rank (the local r estimate, DI_DIST_ASYNC)
-      sent = warp_sum(sent);
-      if (lane == 0 && sent != 0.0) atomicAdd(x.sent, sent);
-    }
     __syncthreads();  // s_w / s_base reused by the next chunk
   }
-  // the last block: per-peer counts into the header, counters rewound
+  if (x.ring) {  // fluid that left this rank (the local r estimate, DI_DIST_ASYNC): one atomic
+    sent = warp_sum(sent);   // per block (same-address fp64 atomics serialise in one L2 slice)
+    if (lane == 0) s_sent[warp] = sent;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kCompThreads / 32; w++) t += s_sent[w];
+      if (t != 0.0) atomicAdd(x.sent, t);
+    }
+  }
+  // the last block: per-peer counts into the header, counters rewound. Ring mode: the block's
+  // records (ordered before thread 0 by the barrier) reach the peers before the ticket, hence
+  // before the last block publishes the tails; synchronous sweeps: the kernel's completion
+  // orders them before the collective that hands the counts over
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    if (x.ring)
+      __threadfence_system();
+    else
+      __threadfence();
     s_last = atomicAdd(reinterpret_cast<unsigned int *>(x.tcnt + 32 * x.bd.world), 1u) ==
              gridDim.x - 1;
   }
@@ -561,7 +588,8 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
   unsigned long long *tsent = g.ring, *head = g.ring + kMaxWorld, *snap = g.ring + 2 * kMaxWorld;
   double *rs = reinterpret_cast<double *>(g.ring + 3 * kMaxWorld);
   double *scratch = reinterpret_cast<double *>(g.hdr + 8 + g.world);
-  (void)tsent;
+  unsigned long long sent0[kMaxWorld];   // ring tails at the start: entries sent = difference
+  DI_CK(cudaMemcpyAsync(sent0, tsent, sizeof(sent0), cudaMemcpyDeviceToHost, g.stream));
   DI_CK(cudaMemsetAsync(rs, 0, 8 * 8, g.stream));
   const char *mine = g.inbox[me];
   auto drain = [&]() {
@@ -600,13 +628,12 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
   x.p2p = 1;
   x.ring = 1;
   int64_t launched = 0, meetings = 1;
-  double xentries = 0;
   while (!converged && launched < max_sweeps) {
     const int64_t k_end = std::min<int64_t>(max_sweeps, launched + kRingSlots);
     for (; launched < k_end; launched++) {
       drain();                       // what the peers sent so far
       launch_cycle(g, &launches);    // this rank's asynchronous cycle (R7) with r from rs
-      k_compact_remote<<<g.num_sms * 4, kCompThreads, 0, g.stream>>>(g.sc, x);
+      k_compact_remote<<<g.num_sms * kCompBlocksPerSM, kCompThreads, 0, g.stream>>>(g.sc, x);
       k_ring_finalize<<<1, 32, 0, g.stream>>>(a, x, rs);
       launches += 2;
     }
@@ -639,6 +666,8 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
     DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
   }
   g.e_global = g.sc_host->e;
+  unsigned long long sent1[kMaxWorld];
+  DI_CK(cudaMemcpyAsync(sent1, tsent, sizeof(sent1), cudaMemcpyDeviceToHost, g.stream));
   DI_CK(cudaEventRecord(t1, g.stream));
   DI_CK(cudaEventSynchronize(t1));
   float ms = 0.f;
@@ -649,7 +678,6 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
   g.solved = true;
   g.last_d = d;
   g.log_n = 0;
-  (void)xentries;
   if (st) {
     const Scalars &c = *g.sc_host;
     memset(st, 0, sizeof(*st));
@@ -670,6 +698,10 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
     st->variant = variant;
     st->p2p_exchanges = launched;
     st->meetings = meetings;
+    int64_t ent = 0;
+    for (int p = 0; p < G; p++) ent += (p == me) ? 0 : (int64_t)(sent1[p] - sent0[p]);
+    st->exchange_entries = ent;
+    st->exchange_bytes = 12.0 * (double)ent;
   }
   return converged ? DI_OK : DI_NOT_CONVERGED;
 }
@@ -773,7 +805,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
         DI_CK(cudaMemsetAsync(g.sendcnt, 0, (size_t)G * 8, g.stream));
       else {
         x.ipar = par;
-        k_compact_remote<<<g.num_sms * 4, kCompThreads, 0, g.stream>>>(g.sc, x);
+        k_compact_remote<<<g.num_sms * kCompBlocksPerSM, kCompThreads, 0, g.stream>>>(g.sc, x);
       }
       launches += 2;
       launched++;

@@ -228,6 +228,9 @@ def test_dist_async(G):
     assert abs(F.sum() - st["residual_l1"]) <= 1e-18
     assert l1(H, Ho) <= 1e-9
     assert st["meetings"] == -(-st["sweeps"] // 4) + 1
+    for s_ in sts:   # lists moved through the rings, at most one entry per (remote node, cycle)
+        assert 0 < s_["exchange_entries"] <= n * s_["sweeps"]
+        assert s_["exchange_bytes"] == 12 * s_["exchange_entries"]
     H, F, st, sts, _ = res[1]
     assert st["sweeps"] == 6 and st["converged"] == 0 and np.all(F >= 0)
     assert np.abs(F - (B + P @ H - H)).max() <= 1e-15

@@ -57,7 +57,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return SO
     tmp = SO + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-I", nccl_include(), "-o", tmp, *sources(), "-ldl"]
+    # DI_NVCC_DEFS="-DNAME=V ..." (tuning experiments: compile-time knobs of the kernels)
+    defs = os.environ.get("DI_NVCC_DEFS", "").split()
+    cmd = [NVCC, *FLAGS, *defs, "-I", nccl_include(), "-o", tmp, *sources(), "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
