@@ -336,12 +336,25 @@ def cpu_baseline(src, dst, n, args, budget_cycles=None):
     `cycles` cycles of the same workload (adjacency build excluded, as the paper's Init)."""
     import oracle
     cycles = budget_cycles or args.cpu_cycles
-    H, F, st = oracle.di(src, dst, n, d=D, tol=TOL, variant=args.variant, max_cycles=cycles)
+    prev = os.sched_getaffinity(0)          # pinned to one host core (SURVEY §8(d))
+    core = min(prev)
+    os.sched_setaffinity(0, {core})
+    try:
+        H, F, st = oracle.di(src, dst, n, d=D, tol=TOL, variant=args.variant, max_cycles=cycles)
+    finally:
+        os.sched_setaffinity(0, prev)
     secs = st["solve_seconds"]
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except Exception:
+        pass
     return {"value": round(st["diffusions"] / secs / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"first {st['cycles']} sequential DI-{args.variant.upper()} cycles of {args.config} "
                       f"({st['diffusions']} link diffusions, {secs:.1f} s, loop only)",
-            "seconds": round(secs, 2)}
+            "seconds": round(secs, 2),
+            "host": {"cpu": model, "pinned_core": core, "host_cores": os.cpu_count()}}
 
 
 # ------------------------------------------------------------------ reference arm
