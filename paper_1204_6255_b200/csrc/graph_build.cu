@@ -14,6 +14,7 @@
 
 #include <cub/cub.cuh>
 
+#include "comm.cuh"
 #include "di_common.cuh"
 
 namespace di {
@@ -120,18 +121,6 @@ __global__ void k_bounds(const int64_t *__restrict__ pre, int64_t n, int world, 
   out[g] = (g == 0) ? 0 : (g == world ? n : a);
 }
 
-// first index k in sorted keys with (key >> b) >= node
-__global__ void k_key_bound(const uint64_t *__restrict__ keys, int64_t L, int b, int64_t node0,
-                            int64_t node1, int64_t *out) {
-  if (threadIdx.x > 1) return;
-  const uint64_t target = (uint64_t)(threadIdx.x == 0 ? node0 : node1) << b;
-  int64_t a = 0, c = L;
-  while (a < c) {
-    const int64_t m = (a + c) / 2;
-    if (keys[m] >= target) c = m; else a = m + 1;
-  }
-  out[threadIdx.x] = a;
-}
 
 __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
                             int64_t L, int b, const int32_t *__restrict__ new_of,
@@ -148,6 +137,16 @@ __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__re
 }
 
 // keep[k]: not (drop_self and s == t) and not (dedup and key_k == key_{k-1})
+// partitioned build: keys whose source (major) this rank owns
+__global__ void k_own_flags(const uint64_t *__restrict__ keys, int64_t L, int b, int64_t lo,
+                            int64_t hi, uint8_t *__restrict__ keep) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = (int64_t)(keys[k] >> b);
+    keep[k] = s >= lo && s < hi;
+  }
+}
+
 __global__ void k_keep_flags(const uint64_t *__restrict__ keys, int64_t L, int b, int dedup,
                              int drop_self, uint8_t *__restrict__ keep) {
   const uint64_t mask = (1ull << b) - 1;
@@ -260,7 +259,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   DI_CK(cub::DeviceRadixSort::SortKeys(nullptr, q, (uint64_t *)nullptr, (uint64_t *)nullptr,
                                        (int64_t)LL, 0, 2 * b, st));
   cub_tmp = std::max(cub_tmp, q);
-  if (dedup || drop_self) {
+  if (dedup || drop_self || world > 1) {
     DI_CK(cub::DeviceSelect::Flagged(nullptr, q, (uint64_t *)nullptr, (uint8_t *)nullptr,
                                      (uint64_t *)nullptr, (int64_t *)nullptr, (int64_t)LL, st));
     cub_tmp = std::max(cub_tmp, q);
@@ -289,7 +288,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   add(LL * 8);                        // keys_a
   add(LL * 8);                        // keys_b
   add(cub_tmp);
-  if (dedup || drop_self) add(LL);    // keep flags
+  if (dedup || drop_self || world > 1) add(LL);    // keep flags (own rows; dedup / self-loops)
   add(64);                            // bad index / counts / max / key bounds
   add((kMaxWorld + 1) * 8);           // partition bounds
   if (reorder) {
@@ -317,12 +316,11 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   }
   uint64_t *ka = ar.take<uint64_t>(LL * 8), *kb = ar.take<uint64_t>(LL * 8);
   void *tmp = ar.take<char>(cub_tmp);
-  uint8_t *keep = (dedup || drop_self) ? ar.take<uint8_t>(LL) : nullptr;
+  uint8_t *keep = (dedup || drop_self || world > 1) ? ar.take<uint8_t>(LL) : nullptr;
   char *small = ar.take<char>(64);
   unsigned long long *badb = reinterpret_cast<unsigned long long *>(small);
   int64_t *nsel = reinterpret_cast<int64_t *>(small + 16);
   uint32_t *mx = reinterpret_cast<uint32_t *>(small + 24);
-  int64_t *kbnd = reinterpret_cast<int64_t *>(small + 32);
   int64_t *bnd = ar.take<int64_t>((kMaxWorld + 1) * 8);
   unsigned long long init_bad = ~0ull;
   DI_CK(cudaMemcpyAsync(badb, &init_bad, 8, cudaMemcpyHostToDevice, st));
@@ -414,34 +412,45 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   if (L > 0) k_make_keys<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, b, g.new_of, ka);
   btrace("sync4");
 
+  // ---- partitioned: keep only this rank's rows (sources in [lo, hi): the relabelling keeps every
+  //      range in place) before sorting — each rank sorts ~L/G keys, not L
+  int64_t Ls = L;
+  if (world > 1 && L > 0) {
+    k_own_flags<<<grid_for(L, sms), 256, 0, st>>>(ka, L, b, g.lo, g.hi, keep);
+    size_t sb = cub_tmp;
+    DI_CK(cub::DeviceSelect::Flagged(tmp, sb, ka, keep, kb, nsel, (int64_t)L, st));
+    DI_CK(cudaMemcpyAsync(&Ls, nsel, 8, cudaMemcpyDeviceToHost, st));
+    DI_CK(cudaStreamSynchronize(st));
+    btrace("sync4b");
+    std::swap(ka, kb);  // ka = this rank's keys
+  }
   // ---- sort by (src, dst)
-  if (L > 0) {
+  if (Ls > 0) {
     size_t tb = cub_tmp;
-    DI_CK(cub::DeviceRadixSort::SortKeys(tmp, tb, ka, kb, (int64_t)L, 0, 2 * b, st));
+    DI_CK(cub::DeviceRadixSort::SortKeys(tmp, tb, ka, kb, (int64_t)Ls, 0, 2 * b, st));
   }
   // kb: sorted keys. Optional compaction.
-  int64_t Lk = L;
-  if (L > 0 && (dedup || drop_self)) {
-    k_keep_flags<<<grid_for(L, sms), 256, 0, st>>>(kb, L, b, dedup, drop_self, keep);
+  int64_t Lk = Ls;
+  if (Ls > 0 && (dedup || drop_self)) {
+    k_keep_flags<<<grid_for(Ls, sms), 256, 0, st>>>(kb, Ls, b, dedup, drop_self, keep);
     size_t sb = cub_tmp;
-    DI_CK(cub::DeviceSelect::Flagged(tmp, sb, kb, keep, ka, nsel, (int64_t)L, st));
+    DI_CK(cub::DeviceSelect::Flagged(tmp, sb, kb, keep, ka, nsel, (int64_t)Ls, st));
     DI_CK(cudaMemcpyAsync(&Lk, nsel, 8, cudaMemcpyDeviceToHost, st));
     DI_CK(cudaStreamSynchronize(st));
     btrace("sync5");
     std::swap(ka, kb);  // kb = compacted sorted keys
   }
   g.l_global = Lk;
-  // ---- this rank's rows: the contiguous key range of majors in [lo, hi)
-  int64_t kbeg = 0, kend = Lk;
-  if (world > 1 && Lk > 0) {
-    int64_t hb[2];
-    k_key_bound<<<1, 32, 0, st>>>(kb, Lk, b, g.lo, g.hi, kbnd);
-    DI_CK(cudaMemcpyAsync(hb, kbnd, 16, cudaMemcpyDeviceToHost, st));
+  if (world > 1) {  // the global link count after dedup / self-loop removal: sum over the ranks
+    int64_t *cnt = reinterpret_cast<int64_t *>(small + 48);
+    DI_CK(cudaMemcpyAsync(cnt, &Lk, 8, cudaMemcpyHostToDevice, st));
+    di_status cs = g.comm->allreduce_i64(cnt, 1, st);
+    if (cs != DI_OK) return cs;
+    DI_CK(cudaMemcpyAsync(&g.l_global, cnt, 8, cudaMemcpyDeviceToHost, st));
     DI_CK(cudaStreamSynchronize(st));
-    btrace("sync6");
-    kbeg = hb[0];
-    kend = hb[1];
   }
+  // ---- this rank's rows: all of kb (partitioned) or everything (one GPU)
+  const int64_t kbeg = 0, kend = Lk;
   const int64_t Ll = kend - kbeg;
   const int64_t nl = g.n;
   g.l = Ll;
