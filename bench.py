@@ -378,7 +378,7 @@ def run_reference(args):
            "config": {"workload": f"{args.config}: " + __import__("digen").CONFIGS[args.config].note,
                       "variant": "DI-" + args.variant.upper(), "d": D, "tol_l1_fluid": TOL},
            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
-                            "sample": last["sample"]},
+                            "sample": last["sample"], "host": last.get("host")},
            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
