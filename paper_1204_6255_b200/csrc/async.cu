@@ -569,14 +569,10 @@ di_status prepare_cycle(Graph &g) {
 }
 
 static int cycle_grid(const Graph &g) {
-  static int occ = 0;
-  if (occ == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cycle<false, false>, kAsyncThreads, 0);
-    if (occ < 1) occ = 1;
-  }
+  static const int occ = occupancy(k_cycle<false, false>, kAsyncThreads);  // once, thread-safe
   // DI_CYC_GRID_DIV=k (experiments with emulated ranks on one GPU): 1/k of the grid per rank, so
   // the ranks' cycles run side by side at similar rates as they would on k GPUs
-  static int div = getenv("DI_CYC_GRID_DIV") ? std::max(1, atoi(getenv("DI_CYC_GRID_DIV"))) : 1;
+  static const int div = getenv("DI_CYC_GRID_DIV") ? std::max(1, atoi(getenv("DI_CYC_GRID_DIV"))) : 1;
   return std::max(1, std::min(g.num_sms * occ, kMaxSlices) / div);
 }
 

@@ -590,11 +590,7 @@ __global__ void __launch_bounds__(kPushThreads) k_pull(const SweepArgs a) {
 
 template <bool LOOPS, int MINB>
 void launch_push_t(const Graph &g, const SweepArgs &a) {
-  static int occ = 0;
-  if (occ == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push<LOOPS, MINB>, kPushThreads, 0);
-    if (occ < 1) occ = 1;
-  }
+  static const int occ = occupancy(k_push<LOOPS, MINB>, kPushThreads);  // once, thread-safe
   k_push<LOOPS, MINB><<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a);
 }
 
@@ -690,11 +686,7 @@ void launch_push(Graph &g, int64_t *launches, int blk, int blocks) {
 
 void launch_pull(Graph &g, int64_t *launches) {
   const SweepArgs a = sweep_args(g, 0);
-  static int occ = 0;
-  if (occ == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pull, kPushThreads, 0);
-    if (occ < 1) occ = 1;
-  }
+  static const int occ = occupancy(k_pull, kPushThreads);
   k_pull<<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a);
   *launches += 1;
 }

@@ -67,6 +67,15 @@ __device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// resident blocks per SM of a kernel (>= 1); callers keep it in a function-local static, whose
+// initialisation C++ makes thread-safe (emulated ranks launch from several host threads)
+template <typename K>
+inline int occupancy(K kernel, int threads) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0);
+  return occ < 1 ? 1 : occ;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T x) {
 #pragma unroll
