@@ -137,13 +137,35 @@ __global__ void k_make_keys(const int32_t *__restrict__ src, const int32_t *__re
 }
 
 // keep[k]: not (drop_self and s == t) and not (dedup and key_k == key_{k-1})
-// partitioned build: keys whose source (major) this rank owns
-__global__ void k_own_flags(const uint64_t *__restrict__ keys, int64_t L, int b, int64_t lo,
-                            int64_t hi, uint8_t *__restrict__ keep) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = (int64_t)(keys[k] >> b);
-    keep[k] = s >= lo && s < hi;
+// partitioned build: the keys of the links whose source this rank owns (caller's numbering
+// [lo, hi)), appended in any order (the sort follows); one counter reservation per warp
+__global__ void k_make_own_keys(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                                int64_t L, int b, int64_t lo, int64_t hi,
+                                const int32_t *__restrict__ new_of, uint64_t *__restrict__ keys,
+                                unsigned long long *count) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t k0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; k0 < L;
+       k0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = k0 + lane;
+    int32_t s = 0, t = 0;
+    bool own = false;
+    if (k < L) {
+      s = src[k];
+      own = s >= lo && s < hi;
+      if (own) t = dst[k];
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, own);
+    unsigned long long base = 0;
+    if (lane == 0 && m) base = atomicAdd(count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (own) {
+      if (new_of) {
+        s = new_of[s];
+        t = new_of[t];
+      }
+      keys[base + __popc(m & ((1u << lane) - 1))] =
+          ((uint64_t)(uint32_t)s << b) | (uint64_t)(uint32_t)t;
+    }
   }
 }
 
@@ -255,11 +277,16 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
 
   btrace("start");
   // ---- one arena for every temporary: CUB temp sizes first (null pointers: size queries only)
+  // (partitioned: the link keys, their sort and the compaction live in a second arena sized by
+  //  this rank's own links, allocated once the partition is known)
+  const bool part = world > 1;
   size_t cub_tmp = 0, q = 0;
-  DI_CK(cub::DeviceRadixSort::SortKeys(nullptr, q, (uint64_t *)nullptr, (uint64_t *)nullptr,
-                                       (int64_t)LL, 0, 2 * b, st));
-  cub_tmp = std::max(cub_tmp, q);
-  if (dedup || drop_self || world > 1) {
+  if (!part) {
+    DI_CK(cub::DeviceRadixSort::SortKeys(nullptr, q, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                         (int64_t)LL, 0, 2 * b, st));
+    cub_tmp = std::max(cub_tmp, q);
+  }
+  if (!part && (dedup || drop_self)) {
     DI_CK(cub::DeviceSelect::Flagged(nullptr, q, (uint64_t *)nullptr, (uint8_t *)nullptr,
                                      (uint64_t *)nullptr, (int64_t *)nullptr, (int64_t)LL, st));
     cub_tmp = std::max(cub_tmp, q);
@@ -285,10 +312,12 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     add(LL * 4);
     add(LL * 4);
   }
-  add(LL * 8);                        // keys_a
-  add(LL * 8);                        // keys_b
+  if (!part) {
+    add(LL * 8);                      // keys_a
+    add(LL * 8);                      // keys_b
+  }
   add(cub_tmp);
-  if (dedup || drop_self || world > 1) add(LL);    // keep flags (own rows; dedup / self-loops)
+  if (!part && (dedup || drop_self)) add(LL);    // keep flags (dedup / self-loops)
   add(64);                            // bad index / counts / max / key bounds
   add((kMaxWorld + 1) * 8);           // partition bounds
   if (reorder) {
@@ -314,9 +343,10 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     s_dev = hs;
     d_dev = hd;
   }
-  uint64_t *ka = ar.take<uint64_t>(LL * 8), *kb = ar.take<uint64_t>(LL * 8);
+  uint64_t *ka = part ? nullptr : ar.take<uint64_t>(LL * 8);
+  uint64_t *kb = part ? nullptr : ar.take<uint64_t>(LL * 8);
   void *tmp = ar.take<char>(cub_tmp);
-  uint8_t *keep = (dedup || drop_self || world > 1) ? ar.take<uint8_t>(LL) : nullptr;
+  uint8_t *keep = (!part && (dedup || drop_self)) ? ar.take<uint8_t>(LL) : nullptr;
   char *small = ar.take<char>(64);
   unsigned long long *badb = reinterpret_cast<unsigned long long *>(small);
   int64_t *nsel = reinterpret_cast<int64_t *>(small + 16);
@@ -356,8 +386,10 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   bd.b[0] = 0;
   bd.b[1] = n;
   int64_t *od = (world > 1) ? ar.take<int64_t>((nn + 1) * 8) : nullptr;
+  const int64_t *pre_dev = nullptr;   // out-degree prefix in the caller's numbering (partitioned)
   if (world > 1) {
     int64_t *pre = ar.take<int64_t>((nn + 1) * 8);
+    pre_dev = pre;
     DI_CK(cudaMemsetAsync(od, 0, (nn + 1) * 8, st));
     if (L > 0) k_outdeg<<<grid_for(L, sms), 256, 0, st>>>(s_dev, L, od);
     size_t cb = cub_tmp;
@@ -409,21 +441,43 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     k_place<<<grid_for(n, sms), 256, 0, st>>>(sorted, n, bd, pp, g.new_of, g.old_of);
     g.reordered = true;
   }
-  if (L > 0) k_make_keys<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, b, g.new_of, ka);
+  // ---- partitioned: only this rank's links (sources in [lo, hi) of the caller's numbering; the
+  //      relabelling keeps every range in place) get keys, in a second arena of ~L/G keys
+  int64_t Ls = L;
+  Arena ar2;
+  if (part) {
+    int64_t pe[2] = {0, 0};   // own links = out-degree prefix at the range ends
+    DI_CK(cudaMemcpyAsync(&pe[0], pre_dev + g.lo, 8, cudaMemcpyDeviceToHost, st));
+    DI_CK(cudaMemcpyAsync(&pe[1], pre_dev + g.hi, 8, cudaMemcpyDeviceToHost, st));
+    DI_CK(cudaStreamSynchronize(st));
+    Ls = pe[1] - pe[0];
+    const size_t LS = (size_t)(Ls > 0 ? Ls : 1);
+    size_t t2 = 0;
+    DI_CK(cub::DeviceRadixSort::SortKeys(nullptr, q, (uint64_t *)nullptr, (uint64_t *)nullptr,
+                                         (int64_t)LS, 0, 2 * b, st));
+    t2 = std::max(t2, q);
+    if (dedup || drop_self) {
+      DI_CK(cub::DeviceSelect::Flagged(nullptr, q, (uint64_t *)nullptr, (uint8_t *)nullptr,
+                                       (uint64_t *)nullptr, (int64_t *)nullptr, (int64_t)LS, st));
+      t2 = std::max(t2, q);
+    }
+    DI_CK(dmalloc(&ar2.base, 2 * Arena::up(LS * 8) + Arena::up(t2) + Arena::up(LS) + 256));
+    ka = ar2.take<uint64_t>(LS * 8);
+    kb = ar2.take<uint64_t>(LS * 8);
+    tmp = ar2.take<char>(t2);
+    keep = ar2.take<uint8_t>(LS);
+    cub_tmp = t2;
+    unsigned long long *cnt = reinterpret_cast<unsigned long long *>(small + 48);
+    DI_CK(cudaMemsetAsync(cnt, 0, 8, st));
+    if (L > 0)
+      k_make_own_keys<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, b, g.lo, g.hi, g.new_of,
+                                                        ka, cnt);
+    btrace("sync4b");
+  } else if (L > 0) {
+    k_make_keys<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, b, g.new_of, ka);
+  }
   btrace("sync4");
 
-  // ---- partitioned: keep only this rank's rows (sources in [lo, hi): the relabelling keeps every
-  //      range in place) before sorting — each rank sorts ~L/G keys, not L
-  int64_t Ls = L;
-  if (world > 1 && L > 0) {
-    k_own_flags<<<grid_for(L, sms), 256, 0, st>>>(ka, L, b, g.lo, g.hi, keep);
-    size_t sb = cub_tmp;
-    DI_CK(cub::DeviceSelect::Flagged(tmp, sb, ka, keep, kb, nsel, (int64_t)L, st));
-    DI_CK(cudaMemcpyAsync(&Ls, nsel, 8, cudaMemcpyDeviceToHost, st));
-    DI_CK(cudaStreamSynchronize(st));
-    btrace("sync4b");
-    std::swap(ka, kb);  // ka = this rank's keys
-  }
   // ---- sort by (src, dst)
   if (Ls > 0) {
     size_t tb = cub_tmp;
