@@ -4,14 +4,15 @@
 // node i pushes to a later node j is diffused by j in the same cycle. Bulk sweeps (R1) lose that
 // (fluid waits for the next sweep); block-ordered cycles (R5) recover part of it at the price of
 // 2K kernel boundaries per cycle. Here one persistent grid runs the whole cycle:
-//   - CTAs take tiles of 1024 consecutive nodes in increasing order from a global counter;
+//   - CTAs take tiles of kCycTile (512) consecutive nodes in increasing order from a global
+//     counter (hub items of the hottest rows are claimed right after tile 0, see below);
 //   - a node is selected against the cycle's threshold t = r/L (r once per cycle) and
 //     its fluid is TAKEN with an atomic exchange F_i <- 0, so fluid that other CTAs push into
 //     F_i concurrently is never lost: it is either in the exchanged value or stays in F_i for
 //     the next visit (any diffusion order keeps F = B + P.H - H);
-//   - the CTA pushes the tile's rows immediately: rows of <= 8 links by the selecting thread,
-//     rows of 9-128 links by 8-lane groups, longer rows as 1024-link chunks, claimed by the CTA's
-//     warps from one shared-memory row list (mid rows from its front, long rows from its back).
+//   - the CTA pushes the tile's rows immediately from shared-memory lists: rows of <= 16 links
+//     a lane each (32 per warp claim), 17-256 links by 8-lane groups (front of the row list),
+//     longer rows as 1024-link chunks claimed by the CTA's warps (back of the row list).
 // The order of diffusions is the dynamic order of the tiles, so iterates are not reproducible
 // bit for bit (like every fp64-atomic push); the fixed point and the tolerance are those of the
 // paper's method. The last CTA reduces the per-CTA sums, applies r_{c+1} = r_c - taken + pushed,
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         }
       }
     } else {
-    // ---- select: 4 consecutive nodes per thread, F and row extents
+    // ---- select: kCycItems consecutive nodes per thread, F and row extents
     const int64_t base = tile * (int64_t)kCycTile + (int64_t)threadIdx.x * kCycItems;
     double f[kCycItems];
     int64_t rb[kCycItems + 1];
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       }
       rb[kCycItems] = base < a.n ? a.row_ptr[a.n] : 0;
     }
-    // the selection test for the 4 nodes first, then all their exchanges in flight together
+    // the selection test for the thread's nodes first, then all their exchanges in flight together
     // (one round trip per tile instead of one per selected node)
     int o4[kCycItems];
     bool hub4[kCycItems];
