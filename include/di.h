@@ -148,7 +148,9 @@ typedef struct di_group_s *di_group;
 typedef struct {
   int32_t rank, world;        /* 0 <= rank < world <= 16                                        */
   const void *nccl_unique_id; /* 128-byte ncclUniqueId, identical on every rank (host pointer),
-                                 from di_nccl_unique_id on one rank; NULL with a group            */
+                                 from di_nccl_unique_id on one rank; NULL with a group. Graphs
+                                 uploaded with the same id share one NCCL communicator, kept
+                                 until the process exits (an id initialises one communicator) */
   di_group group;             /* in-process group from di_group_create, else NULL                */
 } di_dist;
 

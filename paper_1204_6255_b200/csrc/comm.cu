@@ -5,6 +5,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "comm.cuh"
@@ -93,14 +95,18 @@ __global__ void k_window_peers(ncclWindow_t w, int world, char **out) {
     out[p] = static_cast<char *>(ncclGetPeerPointer(w, 0, p));
 }
 
+// Communicators by unique id: an ncclUniqueId initialises exactly one communicator (a second
+// ncclCommInitRank with the same id is not supported), so every graph uploaded with the same
+// (id, rank, world) shares one, e.g. the e2e uploads of bench.py at N > 1. They live until the
+// process exits and are never destroyed (NCCL may already be unloaded at static destruction).
+std::mutex g_comm_mu;
+std::map<std::string, ncclComm_t> *g_comms = new std::map<std::string, ncclComm_t>();
+
 struct NcclComm : Comm {
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;   // shared (g_comms), not owned
   void *ibuf = nullptr;
   ncclWindow_t iwin = nullptr;
-  ~NcclComm() override {
-    free_inbox();
-    if (comm) nccl().CommDestroy(comm);
-  }
+  ~NcclComm() override { free_inbox(); }
   di_status make_inbox(size_t bytes, std::vector<char *> *peers) override {
     const NcclApi &a = nccl();
     if (!a.MemAlloc || !a.MemFree || !a.CommWindowRegister || !a.CommWindowDeregister) {
@@ -310,16 +316,25 @@ di_status make_nccl_comm(const void *unique_id, int rank, int world, Comm **out)
   }
   ncclUniqueId id;
   memcpy(&id, unique_id, sizeof(id));
+  std::string key(reinterpret_cast<const char *>(&id), sizeof(id));
+  key += ":" + std::to_string(rank) + "/" + std::to_string(world);
+  std::lock_guard<std::mutex> lk(g_comm_mu);
+  ncclComm_t comm = nullptr;
+  auto it = g_comms->find(key);
+  if (it != g_comms->end()) {
+    comm = it->second;
+  } else {
+    ncclResult_t r = a.CommInitRank(&comm, world, id, rank);
+    if (r != ncclSuccess) {
+      set_error(std::string("ncclCommInitRank: ") + a.GetErrorString(r));
+      return DI_ENCCL;
+    }
+    (*g_comms)[key] = comm;
+  }
   NcclComm *c = new NcclComm();
   c->rank = rank;
   c->world = world;
-  ncclResult_t r = a.CommInitRank(&c->comm, world, id, rank);
-  if (r != ncclSuccess) {
-    set_error(std::string("ncclCommInitRank: ") + a.GetErrorString(r));
-    c->comm = nullptr;
-    delete c;
-    return DI_ENCCL;
-  }
+  c->comm = comm;
   *out = c;
   return DI_OK;
 }

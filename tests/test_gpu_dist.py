@@ -432,7 +432,14 @@ def test_nccl_backend_single_rank(asynchronous, monkeypatch):
     st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous, exchange="dense")  # one rank: no-op
     assert st["converged"] == 1 and st["dense_exchanges"] == 0
     assert g.residual() <= 1e-10
+    g2 = di.Graph(src, dst, n, rank=0, world=1, nccl_id=nid)   # same id: the same communicator
+    assert g2.solve(d=D, tol=1e-10, asynchronous=asynchronous)["converged"] == 1
     g.free()
+    g2.free()
+    g3 = di.Graph(src, dst, n, rank=0, world=1, nccl_id=nid)   # ... also after both were freed
+    st = g3.solve(d=D, tol=1e-10, asynchronous=asynchronous)
+    assert st["converged"] == 1 and l1(g3.history().cpu().numpy(), Ho) <= 1e-9
+    g3.free()
     grp = di.LocalGroup(1)
     g = di.Graph(src, dst, n, rank=0, world=1, group=grp)
     st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous)
