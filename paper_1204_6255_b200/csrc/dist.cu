@@ -628,11 +628,28 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
   x.p2p = 1;
   x.ring = 1;
   int64_t launched = 0, meetings = 1;
+  const bool prof = flags & DI_PROFILE;   // events around every cycle kernel (roofline)
+  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  if (prof) {
+    DI_CK(cudaEventCreate(&pe0));
+    DI_CK(cudaEventCreate(&pe1));
+  }
+  double push_ms = 0.0;
+  int64_t push_launches = 0;
   while (!converged && launched < max_sweeps) {
     const int64_t k_end = std::min<int64_t>(max_sweeps, launched + kRingSlots);
     for (; launched < k_end; launched++) {
       drain();                       // what the peers sent so far
+      if (prof) DI_CK(cudaEventRecord(pe0, g.stream));
       launch_cycle(g, &launches);    // this rank's asynchronous cycle (R7) with r from rs
+      if (prof) {
+        DI_CK(cudaEventRecord(pe1, g.stream));
+        DI_CK(cudaEventSynchronize(pe1));
+        float c_ms = 0.f;
+        cudaEventElapsedTime(&c_ms, pe0, pe1);
+        push_ms += c_ms;
+        push_launches++;
+      }
       k_compact_remote<<<g.num_sms * kCompBlocksPerSM, kCompThreads, 0, g.stream>>>(g.sc, x);
       k_ring_finalize<<<1, 32, 0, g.stream>>>(a, x, rs);
       launches += 2;
@@ -666,6 +683,8 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
     DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
   }
   g.e_global = g.sc_host->e;
+  if (pe0) cudaEventDestroy(pe0);
+  if (pe1) cudaEventDestroy(pe1);
   unsigned long long sent1[kMaxWorld];
   DI_CK(cudaMemcpyAsync(sent1, tsent, sizeof(sent1), cudaMemcpyDeviceToHost, g.stream));
   DI_CK(cudaEventRecord(t1, g.stream));
@@ -698,6 +717,8 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
     st->variant = variant;
     st->p2p_exchanges = launched;
     st->meetings = meetings;
+    st->push_ms = push_ms;
+    st->push_launches = push_launches;
     int64_t ent = 0;
     for (int p = 0; p < G; p++) ent += (p == me) ? 0 : (int64_t)(sent1[p] - sent0[p]);
     st->exchange_entries = ent;

@@ -221,7 +221,9 @@ def test_dist_async(G):
     outd = np.bincount(src, minlength=n)
     Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
     res = run(src, dst, n, G, [dict(tol=1e-10, variant="sop", **kw),
-                               dict(tol=1e-300, variant="sop", max_sweeps=6, **kw)])
+                               dict(tol=1e-300, variant="sop", max_sweeps=6, **kw),
+                               dict(tol=1e-10, variant="sop", profile=True, **kw)])
+    assert res[2][2]["push_launches"] == res[2][2]["sweeps"] and res[2][2]["push_ms"] > 0
     H, F, st, sts, _ = res[0]
     same_stats(sts)
     assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
