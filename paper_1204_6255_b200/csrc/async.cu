@@ -61,7 +61,10 @@ constexpr int kAsyncChunk = DI_ASYNC_CHUNK;  // longer rows: chunks of this many
 // in its own 128-B line (copies sharing a line serialise like one address: tools/micro/hot.cu,
 // profiles/micro_hot.txt), and the last CTA of the cycle folds the copies into F.
 constexpr int kRepl = kHotRanks;
-constexpr int kCopies = 16;
+#ifndef DI_HOT_COPIES
+#define DI_HOT_COPIES 16
+#endif
+constexpr int kCopies = DI_HOT_COPIES;
 constexpr int kRepStride = 16;  // doubles between accumulators: one 128-B line each
 
 // Hub items. On R-MAT graphs the hottest targets are also the largest rows (node 0 of C4 has

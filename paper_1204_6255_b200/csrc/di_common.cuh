@@ -33,7 +33,10 @@ constexpr int kMaxSlices = 4096;   // finaliser slices (= push/pull grid size, <
 constexpr int kMaxBlocks = 256;    // block-ordered sweeps: sub-sweeps per cycle
 // Skewed in-degrees (async.cu): when the top node takes more than kReplShare of the links, the
 // kHotRanks hottest nodes are placed first and their REDs spread over replicated accumulators.
-constexpr int kHotRanks = 64;
+#ifndef DI_HOT_RANKS
+#define DI_HOT_RANKS 64
+#endif
+constexpr int kHotRanks = DI_HOT_RANKS;
 constexpr double kReplShare = 0.0005;
 
 enum BinId { BIN_T = 0, BIN_G = 1, BIN_W = 2, BIN_C = 3 };
