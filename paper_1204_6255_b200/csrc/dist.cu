@@ -553,8 +553,7 @@ di_status dist_residual(Graph &g, double *l1) {
 di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int variant,
                            int64_t max_sweeps, uint32_t flags, di_stats *st) {
   const int G = g.world, me = g.rank;
-  if (!g.p2p || !g.ring)
-  {
+  if (!g.p2p || !g.ring) {
     set_error("di_solve: DI_DIST_ASYNC needs the peer-memory inboxes (see DI_P2P)");
     return DI_EINVAL;
   }
@@ -567,17 +566,15 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
   {
     Scalars &s = *g.sc_host;
     const uint32_t epoch = s.epoch ? s.epoch : 1;
-    const double e_prev = s.e;
     memset(&s, 0, sizeof(Scalars));
     s.epoch = epoch;
-    s.e = 0.0;   // this rank's absorption; the global e is summed at the meetings
+    s.e = 0.0;   // this rank's absorption; the global e is summed at the meetings (g.e_global)
     s.d = d;
     s.tol = tol;
     s.variant = variant;
     s.paper_err = paper;
     s.alpha = g.alpha;
     s.mode = MODE_PUSH;
-    (void)e_prev;
   }
   double e_global = resume ? g.e_global : 0.0;
   DI_CK(cudaEventRecord(t0, g.stream));
@@ -731,7 +728,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
                      int64_t max_sweeps, uint32_t flags, di_stats *st) {
   if (flags & DI_DIST_ASYNC) {
     if (!(flags & DI_ASYNC))
-    {
+    {  // F2 runs R7 cycles on every rank
       set_error("di_solve: DI_DIST_ASYNC runs asynchronous cycles (add DI_ASYNC)");
       return DI_EINVAL;
     }
