@@ -56,8 +56,11 @@ typedef enum {
 #define DI_DROP_SELF_LOOPS  0x2u  /* drop i -> i links (default folds them)            */
 #define DI_BUILD_CSC        0x4u  /* also build the in-link (CSC) index: pull variant, PI, GS     */
 #define DI_HOST_PTRS        0x8u  /* src/dst are host pointers (copied inside the call)           */
-#define DI_LOCAL_LINKS      0x10u /* reserved (multi-GPU, each rank passing only its own links):
-                                     not available in this build, DI_EINVAL                       */
+#define DI_LOCAL_LINKS      0x10u /* partitioned: this rank passes only the links whose source is
+                                     in its node range dist->lo..hi (caller's numbering; the
+                                     ranges of the ranks must tile [0, n) in rank order); the
+                                     in-degrees are summed across ranks. Without it every rank
+                                     passes the full list and the library balances the ranges */
 #define DI_NO_REORDER       0x20u /* keep the caller's node numbering internally (default relabels
                                      by descending in-degree for L2 locality; results are always
                                      returned in the caller's numbering)                          */
@@ -152,6 +155,7 @@ typedef struct {
                                  uploaded with the same id share one NCCL communicator, kept
                                  until the process exits (an id initialises one communicator) */
   di_group group;             /* in-process group from di_group_create, else NULL                */
+  int64_t lo, hi;             /* DI_LOCAL_LINKS: this rank's node range [lo, hi); else ignored   */
 } di_dist;
 
 /* Fill out128 (host, 128 bytes) with a fresh ncclUniqueId (call on one rank, broadcast the bytes,
@@ -174,7 +178,9 @@ di_status di_group_abort(di_group grp);
  *  stream   : cudaStream_t the handle will use (NULL = legacy default stream).
  *  dist     : NULL for one GPU; otherwise every rank calls collectively with the same link list
  *             and owns the node range returned by di_graph_range (1-D partition).
- *             Partitioned graphs: no DI_BUILD_CSC / DI_LOCAL_LINKS (DI_EINVAL), n_nodes >= world.
+ *             Partitioned graphs: no DI_BUILD_CSC (DI_EINVAL), n_nodes >= world; with DI_LOCAL_LINKS a
+ *             link whose source lies outside dist->lo..hi, or ranges that do not tile [0, n), fail
+ *             on every rank with DI_EINVAL.
  * Layout built in HBM: CSR row_ptr int64[n+1], col int32[L] sorted by (src, dst); deg int32[n];
  * kloop int32[n] (self-loop multiplicity); optional CSC (col_ptr int64[n+1], row int32[L]).
  * Errors: DI_EINVAL (sizes, an id outside [0, n): the message names the first bad index),

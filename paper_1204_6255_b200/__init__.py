@@ -59,7 +59,7 @@ class Stats(ctypes.Structure):
 
 class Dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
-                ("group", ctypes.c_void_p)]
+                ("group", ctypes.c_void_p), ("lo", ctypes.c_int64), ("hi", ctypes.c_int64)]
 
 
 _vp, _i64, _u32, _dbl, _ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_double, ctypes.c_int
@@ -171,15 +171,19 @@ class Graph:
 
     Partitioned: pass rank/world and either nccl_id (bytes from nccl_unique_id(),
     one process per GPU) or group (a LocalGroup, one thread per emulated rank). Every rank passes
-    the full link list and owns the node range self.range(); history()/residual(return_F) are
-    that rank's slice, residual() and solve() are collective."""
+    the full link list and owns the node range self.range() — or, with local_range=(lo, hi),
+    only the links whose source lies in its own range [lo, hi) (DI_LOCAL_LINKS; the ranges tile
+    [0, n) in rank order); history()/residual(return_F) are that rank's slice, residual() and
+    solve() are collective."""
 
     def __init__(self, src, dst, n, dedup=False, drop_self_loops=False, build_csc=False,
-                 reorder=True, stream=None, rank=0, world=1, nccl_id=None, group=None):
+                 reorder=True, stream=None, rank=0, world=1, nccl_id=None, group=None,
+                 local_range=None):
         torch = _torch()
         self.n = int(n)
         flags = (DEDUP if dedup else 0) | (DROP_SELF_LOOPS if drop_self_loops else 0) | \
-                (BUILD_CSC if build_csc else 0) | (0 if reorder else NO_REORDER)
+                (BUILD_CSC if build_csc else 0) | (0 if reorder else NO_REORDER) | \
+                (LOCAL_LINKS if local_range is not None else 0)
         keep = []
         if isinstance(src, torch.Tensor) and src.is_cuda:
             s = src.to(torch.int32).contiguous()
@@ -208,9 +212,10 @@ class Graph:
         self._group = group
         if int(world) > 1 or nccl_id is not None or group is not None:
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+            lo, hi = local_range if local_range is not None else (0, 0)
             dist = Dist(int(rank), int(world),
                         ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None,
-                        group._h if group is not None else None)
+                        group._h if group is not None else None, int(lo), int(hi))
         _check(_lib.di_graph_upload(ps, pt, m, self.n, flags, self.stream.cuda_stream,
                                     ctypes.byref(dist) if dist is not None else None, ctypes.byref(h)))
         del keep

@@ -261,12 +261,15 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
   // partitioned: any rank of a communicator, including a communicator of one rank (which runs
   // the whole multi-GPU protocol with nothing to exchange: tests the NCCL backend on one GPU)
   const bool partitioned = dist && (world > 1 || grp || dist->nccl_unique_id);
+  if (!partitioned && (flags & DI_LOCAL_LINKS))
+    return fail(DI_EINVAL, "di_graph_upload: DI_LOCAL_LINKS is for partitioned graphs");
   if (partitioned) {
     if (n_nodes < world) return fail(DI_EINVAL, "di_graph_upload: fewer nodes than ranks");
-    if (flags & (DI_BUILD_CSC | DI_LOCAL_LINKS))
-      return fail(DI_EINVAL, "di_graph_upload: DI_BUILD_CSC and DI_LOCAL_LINKS are single-GPU / "
-                             "not available on a partitioned graph (every rank passes the full link "
-                             "list; sweeps are push-only)");
+    if (flags & DI_BUILD_CSC)
+      return fail(DI_EINVAL, "di_graph_upload: DI_BUILD_CSC is single-GPU (partitioned sweeps are "
+                             "push-only)");
+    if ((flags & DI_LOCAL_LINKS) && !(dist->lo >= 0 && dist->lo < dist->hi && dist->hi <= n_nodes))
+      return fail(DI_EINVAL, "di_graph_upload: DI_LOCAL_LINKS needs 0 <= dist->lo < dist->hi <= n");
     if (!grp && !dist->nccl_unique_id)
       return fail(DI_EINVAL, "di_graph_upload: dist needs an NCCL unique id or a di_group");
     if (grp && grp->world != world)
@@ -301,6 +304,11 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
       std::lock_guard<std::mutex> lk(g->group->m);
       g->group->handles++;
     }
+  }
+  if (partitioned && (flags & DI_LOCAL_LINKS)) {
+    g->local_links = true;
+    g->local_lo = dist->lo;
+    g->local_hi = dist->hi;
   }
   if (const char *e = getenv("DI_RED_HINT")) g->red_hint = atoi(e);
   if (const char *e = getenv("DI_PUSH_OCC")) g->push_occ = atoi(e);

@@ -148,6 +148,10 @@ struct NcclComm : Comm {
     DI_NCK(nccl().AllReduce(dev, dev, (size_t)count, ncclInt64, ncclSum, comm, st));
     return DI_OK;
   }
+  di_status allreduce_u32(uint32_t *dev, int64_t count, cudaStream_t st) override {
+    DI_NCK(nccl().AllReduce(dev, dev, (size_t)count, ncclUint32, ncclSum, comm, st));
+    return DI_OK;
+  }
   di_status allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
     DI_NCK(nccl().AllGather(send, recv, bytes, ncclUint8, comm, st));
     return DI_OK;
@@ -196,7 +200,7 @@ struct GroupComm : Comm {
     return DI_ESTATE;
   }
   template <typename T>
-  di_status allreduce(T *dev, int count, cudaStream_t st, std::vector<std::vector<T>> &stage) {
+  di_status allreduce(T *dev, int64_t count, cudaStream_t st, std::vector<std::vector<T>> &stage) {
     std::vector<T> &mine = stage[rank];
     mine.assign((size_t)count, T(0));
     DI_CK(cudaMemcpyAsync(mine.data(), dev, (size_t)count * sizeof(T), cudaMemcpyDeviceToHost, st));
@@ -204,7 +208,7 @@ struct GroupComm : Comm {
     if (!g->barrier()) return aborted();
     std::vector<T> sum((size_t)count, T(0));
     for (int p = 0; p < world; p++)  // rank order: every rank computes the identical sum
-      for (int k = 0; k < count; k++) sum[k] += stage[p][k];
+      for (int64_t k = 0; k < count; k++) sum[k] += stage[p][k];
     if (!g->barrier()) return aborted();  // nobody restages before everyone has summed
     DI_CK(cudaMemcpyAsync(dev, sum.data(), (size_t)count * sizeof(T), cudaMemcpyHostToDevice, st));
     DI_CK(cudaStreamSynchronize(st));
@@ -215,6 +219,9 @@ struct GroupComm : Comm {
   }
   di_status allreduce_i64(int64_t *dev, int count, cudaStream_t st) override {
     return allreduce(dev, count, st, g->red_i);
+  }
+  di_status allreduce_u32(uint32_t *dev, int64_t count, cudaStream_t st) override {
+    return allreduce(dev, count, st, g->red_u);
   }
   di_status allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) override {
     std::vector<char> &mine = g->gat[rank];

@@ -28,6 +28,7 @@ struct Comm {
   // for the group backend, NCCL's order for NCCL)
   virtual di_status allreduce_f64(double *dev, int count, cudaStream_t st) = 0;
   virtual di_status allreduce_i64(int64_t *dev, int count, cudaStream_t st) = 0;
+  virtual di_status allreduce_u32(uint32_t *dev, int64_t count, cudaStream_t st) = 0;
   // every rank's `bytes` from `send` into recv[rank * bytes ...] on every rank
   virtual di_status allgather(const void *send, void *recv, size_t bytes, cudaStream_t st) = 0;
   // grouped point-to-point: to every peer p != rank send sbytes[p] bytes from sbuf[p] and receive
@@ -58,6 +59,7 @@ struct Group {
   uint64_t gen = 0;
   std::vector<std::vector<double>> red_f;    // allreduce staging, one host vector per rank
   std::vector<std::vector<int64_t>> red_i;
+  std::vector<std::vector<uint32_t>> red_u;
   std::vector<std::vector<char>> gat;        // allgather staging
   std::vector<std::vector<const void *>> sptr;  // sptr[src][dst]
   std::vector<std::vector<size_t>> sbytes;
@@ -66,7 +68,7 @@ struct Group {
   int handles = 0;                           // graphs built on this group (for di_group_free)
   bool aborted = false;                      // di_group_abort: every barrier fails from now on
   explicit Group(int w)
-      : world(w), red_f(w), red_i(w), gat(w), sptr(w, std::vector<const void *>(w, nullptr)),
+      : world(w), red_f(w), red_i(w), red_u(w), gat(w), sptr(w, std::vector<const void *>(w, nullptr)),
         sbytes(w, std::vector<size_t>(w, 0)), dsend(w, nullptr),
         inbox(w, nullptr) {}
   // false once the group is aborted (a rank failed: the others must not wait for it forever)

@@ -137,6 +137,8 @@ struct Graph {
   int red_hint = 1;         // L2 evict_last hint on the push's REDs into F (DI_RED_HINT=0 disables)
   int rank = 0, world = 1;
   bool partitioned = false;  // built with a communicator (dist.cu path), even of one rank
+  bool local_links = false;  // DI_LOCAL_LINKS: this rank's links only, range [local_lo, local_hi)
+  int64_t local_lo = 0, local_hi = 0;
   std::vector<char *> inbox;  // fused exchange: every rank's inbox as mapped here (dist.cu)
   int64_t icap = 0;          // records per inbox segment (largest owned range)
   bool p2p = false;          // the inbox exists: k_compact_remote writes through peer memory

@@ -21,13 +21,14 @@ namespace di {
 namespace {
 
 // id validation (first bad link index) and, for the locality relabelling, in-degrees
+// every id in [0, n); sources in [s_lo, s_hi) ([0, n), or the rank's range with DI_LOCAL_LINKS)
 __global__ void k_validate(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
-                           int64_t L, int64_t n, unsigned long long *__restrict__ bad,
-                           uint32_t *__restrict__ indeg) {
+                           int64_t L, int64_t n, int64_t s_lo, int64_t s_hi,
+                           unsigned long long *__restrict__ bad, uint32_t *__restrict__ indeg) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = src[k], t = dst[k];
-    if (s < 0 || s >= n || t < 0 || t >= n)
+    if (s < s_lo || s >= s_hi || t < 0 || t >= n)
       atomicMin(bad, (unsigned long long)k);
     else if (indeg)
       atomicAdd(indeg + t, 1u);
@@ -327,8 +328,8 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     add(nn * 4);                      // iota
     add(nn * 4);                      // sorted ranks
   }
-  if (world > 1) add((nn + 1) * 8);   // out-degrees (partition bounds)
-  if (world > 1) add((nn + 1) * 8);              // prefix
+  if (world > 1 && !g.local_links) add((nn + 1) * 8);   // out-degrees (partition bounds)
+  if (world > 1 && !g.local_links) add((nn + 1) * 8);   // prefix
   Arena ar;
   DI_CK(dmalloc(&ar.base, total));
   ar.cap = total;
@@ -359,12 +360,28 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     indeg = ar.take<uint32_t>(nn * 4);
     DI_CK(cudaMemsetAsync(indeg, 0, nn * 4, st));
   }
+  const bool local = g.local_links;   // DI_LOCAL_LINKS: this rank's links, sources in its range
+  const int64_t s_lo = local ? g.local_lo : 0, s_hi = local ? g.local_hi : n;
   if (L > 0)
-    k_validate<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, n, badb, indeg);
+    k_validate<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, n, s_lo, s_hi, badb, indeg);
   unsigned long long bad = 0;
   DI_CK(cudaMemcpyAsync(&bad, badb, 8, cudaMemcpyDeviceToHost, st));
   DI_CK(cudaStreamSynchronize(st));
   btrace("sync1");
+  if (local) {  // every rank learns whether any rank failed (no rank may leave a collective)
+    int64_t *flag = reinterpret_cast<int64_t *>(small + 48);
+    const int64_t mine = bad != ~0ull ? 1 : 0;
+    DI_CK(cudaMemcpyAsync(flag, &mine, 8, cudaMemcpyHostToDevice, st));
+    di_status cs = g.comm->allreduce_i64(flag, 1, st);
+    if (cs != DI_OK) return cs;
+    int64_t any = 0;
+    DI_CK(cudaMemcpyAsync(&any, flag, 8, cudaMemcpyDeviceToHost, st));
+    DI_CK(cudaStreamSynchronize(st));
+    if (any && bad == ~0ull) {
+      set_error("di_graph_upload: another rank's link list failed validation (DI_LOCAL_LINKS)");
+      return DI_EINVAL;
+    }
+  }
   if (bad != ~0ull) {
     int32_t sv = 0, dv = 0;
     if (host) {
@@ -374,10 +391,19 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
       cudaMemcpy(&sv, src + bad, 4, cudaMemcpyDeviceToHost);
       cudaMemcpy(&dv, dst + bad, 4, cudaMemcpyDeviceToHost);
     }
-    set_error("di_graph_upload: link " + std::to_string(bad) + " (" + std::to_string(sv) +
-              " -> " + std::to_string(dv) + ") has a node id outside [0, " + std::to_string(n) +
-              ")");
+    if (local && (sv < s_lo || sv >= s_hi) && sv >= 0 && sv < n)
+      set_error("di_graph_upload: link " + std::to_string(bad) + " (" + std::to_string(sv) +
+                " -> " + std::to_string(dv) + ") has a source outside this rank's range [" +
+                std::to_string(s_lo) + ", " + std::to_string(s_hi) + ") (DI_LOCAL_LINKS)");
+    else
+      set_error("di_graph_upload: link " + std::to_string(bad) + " (" + std::to_string(sv) +
+                " -> " + std::to_string(dv) + ") has a node id outside [0, " + std::to_string(n) +
+                ")");
     return DI_EINVAL;
+  }
+  if (local && reorder) {  // in-degrees over every rank's links
+    di_status cs = g.comm->allreduce_u32(indeg, n, st);
+    if (cs != DI_OK) return cs;
   }
   // ---- multi-GPU: 1-D node ranges in the caller's numbering, balanced on counted sweep bytes
   //      (SURVEY §8(e)); every rank holds the full link list and computes the same bounds
@@ -385,9 +411,30 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   bd.world = world;
   bd.b[0] = 0;
   bd.b[1] = n;
-  int64_t *od = (world > 1) ? ar.take<int64_t>((nn + 1) * 8) : nullptr;
+  int64_t *od = (world > 1 && !local) ? ar.take<int64_t>((nn + 1) * 8) : nullptr;
   const int64_t *pre_dev = nullptr;   // out-degree prefix in the caller's numbering (partitioned)
-  if (world > 1) {
+  if (local) {  // the ranges the callers chose: gathered, checked to tile [0, n) in rank order
+    int64_t *rr = reinterpret_cast<int64_t *>(bnd);
+    const int64_t mine[2] = {g.local_lo, g.local_hi};
+    DI_CK(cudaMemcpyAsync(rr, mine, 16, cudaMemcpyHostToDevice, st));
+    int64_t *all = reinterpret_cast<int64_t *>(tmp);
+    di_status cs = g.comm->allgather(rr, all, 16, st);
+    if (cs != DI_OK) return cs;
+    std::vector<int64_t> h((size_t)2 * world);
+    DI_CK(cudaMemcpyAsync(h.data(), all, 16 * (size_t)world, cudaMemcpyDeviceToHost, st));
+    DI_CK(cudaStreamSynchronize(st));
+    bool ok = h[0] == 0 && h[2 * (world - 1) + 1] == n;
+    for (int r = 0; r < world; r++) {
+      ok = ok && h[2 * r] < h[2 * r + 1];
+      if (r > 0) ok = ok && h[2 * r] == h[2 * r - 1];
+      bd.b[r] = h[2 * r];
+    }
+    bd.b[world] = n;
+    if (!ok) {
+      set_error("di_graph_upload: DI_LOCAL_LINKS ranges do not tile [0, n) in rank order");
+      return DI_EINVAL;
+    }
+  } else if (world > 1) {
     int64_t *pre = ar.take<int64_t>((nn + 1) * 8);
     pre_dev = pre;
     DI_CK(cudaMemsetAsync(od, 0, (nn + 1) * 8, st));
@@ -447,10 +494,12 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   Arena ar2;
   if (part) {
     int64_t pe[2] = {0, 0};   // own links = out-degree prefix at the range ends
-    DI_CK(cudaMemcpyAsync(&pe[0], pre_dev + g.lo, 8, cudaMemcpyDeviceToHost, st));
-    DI_CK(cudaMemcpyAsync(&pe[1], pre_dev + g.hi, 8, cudaMemcpyDeviceToHost, st));
-    DI_CK(cudaStreamSynchronize(st));
-    Ls = pe[1] - pe[0];
+    if (!local) {
+      DI_CK(cudaMemcpyAsync(&pe[0], pre_dev + g.lo, 8, cudaMemcpyDeviceToHost, st));
+      DI_CK(cudaMemcpyAsync(&pe[1], pre_dev + g.hi, 8, cudaMemcpyDeviceToHost, st));
+      DI_CK(cudaStreamSynchronize(st));
+    }
+    Ls = local ? L : pe[1] - pe[0];   // DI_LOCAL_LINKS: every link passed is this rank's
     const size_t LS = (size_t)(Ls > 0 ? Ls : 1);
     size_t t2 = 0;
     DI_CK(cub::DeviceRadixSort::SortKeys(nullptr, q, (uint64_t *)nullptr, (uint64_t *)nullptr,

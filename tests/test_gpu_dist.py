@@ -240,6 +240,78 @@ def test_dist_async(G):
     assert abs(cons - (1 - D)) <= 1e-14
 
 
+@pytest.mark.parametrize("G", [2, 3])
+def test_local_links(G):
+    """DI_LOCAL_LINKS: every rank passes only the links of its own sources, for node ranges the
+    caller chose (equal node counts here, not the library's balanced ranges); in-degrees are
+    summed across ranks. C1 to the north_star gate (synchronous cycles, F2), a random graph with
+    loops and duplicates vs the dense solve; a link outside the range or ranges that do not tile
+    [0, n) fail on every rank."""
+    need_gpu()
+    import paper_1204_6255_b200 as di
+    from paper_1204_6255_b200.dist import assemble, run_local_group
+
+    def solve_local(src, dst, n, solves, cut=None):
+        bounds = [n * r // G for r in range(G + 1)] if cut is None else cut
+
+        def fn(r, grp):
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                lo, hi = bounds[r], bounds[r + 1]
+                m = (src >= lo) & (src < hi)
+                g = di.Graph(src[m], dst[m], n, rank=r, world=G, group=grp, stream=stream,
+                             local_range=(lo, hi))
+                assert g.range() == (lo, hi)
+                out = []
+                for sk in solves:
+                    st = g.solve(**sk)
+                    out.append((g.history().cpu().numpy(), st))
+                g.free()
+            return (lo, hi), out
+
+        res = run_local_group(G, fn)
+        return [(assemble([o[k][0] for _, o in res], [rg for rg, _ in res], n), [o[k][1] for _, o in res])
+                for k in range(len(solves))]
+
+    src, dst, n = digen.make("c1", seed=1)
+    Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
+    for H, sts in solve_local(src, dst, n, [dict(d=D, tol=1e-10, asynchronous=True),
+                                            dict(d=D, tol=1e-10, asynchronous=True, dist_async=True),
+                                            dict(d=D, tol=1e-10)]):
+        same_stats(sts)
+        assert sts[0]["converged"] == 1 and l1(H, Ho) <= 1e-9
+        assert sts[0]["equivalent_iterations"] == sts[0]["link_diffusions"] / len(src)
+    s2, t2, n2 = digen.small_random(5, n_max=300)
+    X = defn.solve_dense(s2, t2, n2, D) if n2 <= 64 else oracle.di(s2, t2, n2, d=D, tol=1e-15)[0]
+    (H, sts), = solve_local(s2, t2, n2, [dict(d=D, tol=1e-15, asynchronous=True)])
+    assert sts[0]["converged"] == 1 and l1(H, X) <= 1e-13 * max(1, n2 / 64)
+
+    def bad_link(r, grp):   # rank 0 passes one link of rank 1's range: every rank fails
+        lo, hi = [0, n // 2, n][r], [n // 2, n, n][r]
+        m = (src >= lo) & (src < hi)
+        s_, t_ = src[m], dst[m]
+        if r == 0:
+            s_ = np.concatenate([s_, np.array([n - 1], np.int32)])
+            t_ = np.concatenate([t_, np.array([0], np.int32)])
+        with pytest.raises(di.DIError) as ei:
+            di.Graph(s_, t_, n, rank=r, world=2, group=grp, local_range=(lo, hi))
+        assert ei.value.status == di.DI_EINVAL
+        return str(ei.value)
+
+    msgs = run_local_group(2, bad_link)
+    assert "outside this rank's range" in msgs[0] and "another rank" in msgs[1]
+
+    def gap(r, grp):        # ranges [0, n/2) and [n/2 + 1, n): not a tiling
+        lo, hi = [(0, n // 2), (n // 2 + 1, n)][r]
+        m = (src >= lo) & (src < hi)
+        with pytest.raises(di.DIError) as ei:
+            di.Graph(src[m], dst[m], n, rank=r, world=2, group=grp, local_range=(lo, hi))
+        assert ei.value.status == di.DI_EINVAL and "tile" in str(ei.value)
+
+    run_local_group(2, gap)
+
+
 def test_cyc_neumann_partitioned():
     """T7 on partitions: bulk DI-CYC without loops is the Neumann series, F_n = P^n B and
     H_n = sum_{k<n} P^k B, whatever the partition (the exchange only moves where fluid is added)."""

@@ -48,6 +48,14 @@ def _worker(rank, world, port, q):
             H = gather_to_rank0(g.history().cpu().numpy(), g.lo, g.hi, n)
             out.append((kw, st, None if H is None else H.tolist()))
         g.free()
+        # DI_LOCAL_LINKS: this process passes only its own sources' links (equal node ranges)
+        lo, hi = n * r // w, n * (r + 1) // w
+        m = (src >= lo) & (src < hi)
+        gl = di.Graph(src[m], dst[m], n, rank=r, world=w, nccl_id=nid, local_range=(lo, hi))
+        st = gl.solve(d=D, tol=1e-10, variant="sop", asynchronous=True)
+        H = gather_to_rank0(gl.history().cpu().numpy(), gl.lo, gl.hi, n)
+        out.append((dict(local_links=True), st, None if H is None else H.tolist()))
+        gl.free()
         q.put((rank, out))
         tdist.barrier()
         tdist.destroy_process_group()
@@ -75,7 +83,7 @@ def test_nccl_multiprocess_partitioned():
         assert not isinstance(o, str), o
     src, dst, n = digen.make("c1", seed=1)
     Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
-    for k, kw in enumerate(CASES):
+    for k, kw in enumerate(CASES + [dict(local_links=True)]):
         sts = [res[r][k][1] for r in range(world)]
         assert all(s["converged"] == 1 for s in sts), (kw, sts)
         assert len({s["link_diffusions"] for s in sts}) == 1, kw   # global counters
