@@ -399,7 +399,7 @@ def main():
     ap.add_argument("--dist-async", action="store_true",
                     help="N > 1: asynchronous multi-GPU cycles (DI_DIST_ASYNC, SURVEY F2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-cycles", type=int, default=12)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
