@@ -454,10 +454,27 @@ def test_trace_log():
 
 
 @pytest.mark.slow
+def test_c3_async_vs_oracle():
+    """The north_star gate at C3's full size (host-block graph, 8.4M nodes, ~99M links, Zipf hot
+    targets: replicated accumulators on), the bench's launch configuration against the sequential
+    CPU oracle, both to ||F||_1 <= 1e-10."""
+    need_gpu()
+    src, dst, n = digen.make("c3")
+    g = upload(src, dst, n)
+    st = g.solve(d=D, tol=1e-10, variant="sop", asynchronous=True, graph_loop=True)
+    assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
+    H = g.history().cpu().numpy()
+    g.free()
+    Ho, _, sto = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
+    assert l1(H, Ho) <= 1e-9
+
+
+@pytest.mark.slow
 def test_c4_full_size_properties():
     """C4 at full size, first in the bench's launch configuration (asynchronous cycles in the
-    device-side graph loop), then bulk sweeps with the push/pull choice: converged residual,
-    sampled invariant F_i = B_i + (P.H)_i - H_i on 2000 nodes, conservation, and
+    device-side graph loop), then bulk sweeps with the push/pull choice: the north_star gate
+    against the sequential CPU oracle (both to ||F||_1 <= 1e-10), converged residual, sampled
+    invariant F_i = B_i + (P.H)_i - H_i on 2000 nodes, conservation, and
     ||X - H||_1 <= ||F||_1/(1-d) by construction."""
     need_gpu()
     src, dst, n = digen.make("c4")
@@ -466,12 +483,16 @@ def test_c4_full_size_properties():
     sample = rng.choice(n, 2000, replace=False)
     out = np.bincount(src, minlength=n).astype(np.float64)
     insample = np.isin(dst, sample)
+    Ho = None
     for kw in (dict(asynchronous=True, graph_loop=True), dict(mode="auto")):
         st = g.solve(d=D, tol=1e-10, variant="sop", **kw)
         assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
         if "mode" in kw:
             assert 0 < st["pull_sweeps"] < st["sweeps"]
         H = g.history().cpu().numpy()
+        if Ho is None:   # the north_star gate on the bench's workload and launch configuration
+            Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
+        assert l1(H, Ho) <= 1e-9, kw
         _, F = g.residual(return_F=True)
         F = F.cpu().numpy()
         assert np.all(F >= 0) and np.all(H >= 0)
