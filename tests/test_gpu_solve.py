@@ -503,3 +503,28 @@ def test_c4_full_size_properties():
         cons = F.sum() + (1 - D) * H[out > 0].sum() + H[out == 0].sum()
         assert abs(cons - (1 - D)) <= 1e-12, kw
     g.free()
+    # the partitioned path at the same size: 4 emulated ranks on this GPU (fused peer-memory
+    # exchange; then asynchronous multi-GPU cycles), the same gate against the same oracle run
+    import torch
+    import paper_1204_6255_b200 as di
+    from paper_1204_6255_b200.dist import assemble, run_local_group
+    s_d, t_d = torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda()
+
+    def rank(r, grp):
+        torch.cuda.set_device(0)
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            gr = di.Graph(s_d, t_d, n, rank=r, world=4, group=grp, stream=stream)
+            out_ = []
+            for kw in (dict(asynchronous=True), dict(asynchronous=True, dist_async=True)):
+                st = gr.solve(d=D, tol=1e-10, variant="sop", **kw)
+                out_.append((gr.history().cpu().numpy(), st))
+            rg = (gr.lo, gr.hi)
+            gr.free()
+        return rg, out_
+
+    res = run_local_group(4, rank)
+    for k in range(2):
+        H = assemble([o[k][0] for _, o in res], [rg for rg, _ in res], n)
+        assert res[0][1][k][1]["converged"] == 1
+        assert l1(H, Ho) <= 1e-9, k
