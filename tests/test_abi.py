@@ -49,3 +49,30 @@ def test_no_oracle_in_product():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert not re.search(r"\boracle\b\s*(import|\.)|import\s+oracle|di_oracle|libdioracle", txt), f
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of di_stats and di_dist have the C layout of include/di.h (size and
+    every field offset), compiled here with gcc."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    import paper_1204_6255_b200 as di
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    checks = []
+    for cname, py in (("di_stats", di.Stats), ("di_dist", di.Dist)):
+        checks.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            checks.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stddef.h>\n#include <stdio.h>\n#include \"di.h\"\nint main(void) {\n"
+                   + "\n".join(checks) + "\nreturn 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(root, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split("\n")
+    got = {tuple(line.split()[:2]): int(line.split()[2]) for line in out if line.strip()}
+    for cname, py in (("di_stats", di.Stats), ("di_dist", di.Dist)):
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
