@@ -413,7 +413,7 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   const bool async = flags & DI_ASYNC;
   if (async && (mode != MODE_PUSH || blocks > 1))
     return fail(DI_EINVAL, "di_solve: DI_ASYNC runs push cycles without DI_BLOCKS");
-  if (async) {
+  {  // replicated hot accumulators (every push schedule) and, for DI_ASYNC, the hub items
     di_status ps = prepare_cycle(g);
     if (ps != DI_OK) return ps;
   }

@@ -61,11 +61,7 @@ constexpr int kAsyncChunk = DI_ASYNC_CHUNK;  // longer rows: chunks of this many
 // in its own 128-B line (copies sharing a line serialise like one address: tools/micro/hot.cu,
 // profiles/micro_hot.txt), and the last CTA of the cycle folds the copies into F.
 constexpr int kRepl = kHotRanks;
-#ifndef DI_HOT_COPIES
-#define DI_HOT_COPIES 16
-#endif
-constexpr int kCopies = DI_HOT_COPIES;
-constexpr int kRepStride = 16;  // doubles between accumulators: one 128-B line each
+constexpr int kCopies = kRepCopies;
 
 // Hub items. On R-MAT graphs the hottest targets are also the largest rows (node 0 of C4 has
 // ~240k out-links): pushed by the CTA that takes tile 0 they would make it the straggler of

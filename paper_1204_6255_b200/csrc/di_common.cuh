@@ -37,6 +37,11 @@ constexpr int kMaxBlocks = 256;    // block-ordered sweeps: sub-sweeps per cycle
 #define DI_HOT_RANKS 64
 #endif
 constexpr int kHotRanks = DI_HOT_RANKS;
+#ifndef DI_HOT_COPIES
+#define DI_HOT_COPIES 16
+#endif
+constexpr int kRepCopies = DI_HOT_COPIES;  // copies of each hot accumulator (chosen by warp)
+constexpr int kRepStride = 16;             // doubles between accumulators: one 128-B line each
 constexpr double kReplShare = 0.0005;
 
 enum BinId { BIN_T = 0, BIN_G = 1, BIN_W = 2, BIN_C = 3 };

@@ -383,6 +383,9 @@ __device__ __forceinline__ void push_rows_warp(const SweepArgs &a, int b, int64_
   const Entry *__restrict__ ent = a.fr.ent[b];
   const int32_t *__restrict__ col = a.col;
   double *__restrict__ F = a.F;
+  double *__restrict__ rep = a.rep;   // replicated hot accumulators (j < hot_lim)
+  const int32_t hot_lim = a.hot_shift > 0 ? a.hot_shift : 0;
+  const int copy = (int)(((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) % kRepCopies);
   Entry nx = ent[w];
   for (int64_t u = w; u < U; u += W) {
     const Entry en = nx;
@@ -397,8 +400,8 @@ __device__ __forceinline__ void push_rows_warp(const SweepArgs &a, int b, int64_
       int4 x0 = make_int4(0, 0, 0, 0), x1 = make_int4(0, 0, 0, 0);
       if (v0 < nvec) x0 = ld_col4(col + a0 + 4 * (int64_t)v0, pol);
       if (v1 < nvec) x1 = ld_col4(col + a0 + 4 * (int64_t)v1, pol);
-      if (v0 < nvec) red_group<LOOPS>(F, x0, a0 + 4 * (int64_t)v0, beg, end, gi, en.v, fpol);
-      if (v1 < nvec) red_group<LOOPS>(F, x1, a0 + 4 * (int64_t)v1, beg, end, gi, en.v, fpol);
+      if (v0 < nvec) red_group<LOOPS>(F, rep, hot_lim, copy, x0, a0 + 4 * (int64_t)v0, beg, end, gi, en.v, fpol);
+      if (v1 < nvec) red_group<LOOPS>(F, rep, hot_lim, copy, x1, a0 + 4 * (int64_t)v1, beg, end, gi, en.v, fpol);
     }
   }
 }
@@ -417,6 +420,9 @@ __global__ void __launch_bounds__(kPushThreads, MINB) k_push(const SweepArgs a) 
   const int64_t w = (int64_t)blockIdx.x * (kPushThreads / 32) + (threadIdx.x >> 5);
   const int32_t *__restrict__ col = a.col;
   double *__restrict__ F = a.F;
+  double *__restrict__ rep = a.rep;   // replicated hot accumulators (j < hot_lim)
+  const int32_t hot_lim = a.hot_shift > 0 ? a.hot_shift : 0;
+  const int copy = (int)(((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) % kRepCopies);
   int64_t U[kBins];
 #pragma unroll
   for (int b = 0; b < kBins; b++) U[b] = (int64_t)sc->bin_fill[b][0];
@@ -437,8 +443,8 @@ __global__ void __launch_bounds__(kPushThreads, MINB) k_push(const SweepArgs a) 
       int4 x0 = make_int4(0, 0, 0, 0), x1 = make_int4(0, 0, 0, 0);
       if (sub < nvec) x0 = ld_col4(col + a0 + 4 * sub, pol);
       if (sub + 8 < nvec) x1 = ld_col4(col + a0 + 4 * (sub + 8), pol);
-      if (sub < nvec) red_group<LOOPS>(F, x0, a0 + 4 * sub, beg, end, gi, en.v, fpol);
-      if (sub + 8 < nvec) red_group<LOOPS>(F, x1, a0 + 4 * (sub + 8), beg, end, gi, en.v, fpol);
+      if (sub < nvec) red_group<LOOPS>(F, rep, hot_lim, copy, x0, a0 + 4 * sub, beg, end, gi, en.v, fpol);
+      if (sub + 8 < nvec) red_group<LOOPS>(F, rep, hot_lim, copy, x1, a0 + 4 * (sub + 8), beg, end, gi, en.v, fpol);
     }
   }
   // ---- bin T (1..8 links): one thread per row; <= 3 int4 groups
@@ -455,9 +461,9 @@ __global__ void __launch_bounds__(kPushThreads, MINB) k_push(const SweepArgs a) 
       int4 x1 = make_int4(0, 0, 0, 0), x2 = make_int4(0, 0, 0, 0);
       if (nvec > 1) x1 = ld_col4(col + a0 + 4, pol);
       if (nvec > 2) x2 = ld_col4(col + a0 + 8, pol);
-      red_group<LOOPS>(F, x0, a0, beg, end, gi, en.v, fpol);
-      if (nvec > 1) red_group<LOOPS>(F, x1, a0 + 4, beg, end, gi, en.v, fpol);
-      if (nvec > 2) red_group<LOOPS>(F, x2, a0 + 8, beg, end, gi, en.v, fpol);
+      red_group<LOOPS>(F, rep, hot_lim, copy, x0, a0, beg, end, gi, en.v, fpol);
+      if (nvec > 1) red_group<LOOPS>(F, rep, hot_lim, copy, x1, a0 + 4, beg, end, gi, en.v, fpol);
+      if (nvec > 2) red_group<LOOPS>(F, rep, hot_lim, copy, x2, a0 + 8, beg, end, gi, en.v, fpol);
     }
   }
   // ---- every block reduces its slice of the select partials; the last block to finish

@@ -243,7 +243,22 @@ __device__ __forceinline__ void apply_sweep(const SweepArgs &a, const SweepSums 
   vs->ticket = 0;
 }
 
+// the replicated hot accumulators into F, cleared (every push kernel's last block, all threads)
+__device__ __forceinline__ void fold_replicas(const SweepArgs &a, int nthreads) {
+  if (a.hot_shift <= 0 || !a.rep) return;
+  for (int k = threadIdx.x; k < a.hot_shift; k += nthreads) {
+    double acc = 0.0;
+    for (int c = 0; c < kRepCopies; c++) {
+      double *p = a.rep + (int64_t)(c * kHotRanks + k) * kRepStride;
+      acc += __ldcg(p);
+      *p = 0.0;
+    }
+    if (acc != 0.0) a.F[k] += acc;
+  }
+}
+
 __device__ __forceinline__ void finalize_sweep(const SweepArgs &a, int P, int nthreads) {
+  fold_replicas(a, nthreads);
   const SweepSums x = reduce_partials(a, P, nthreads);
   if (threadIdx.x == 0) apply_sweep(a, x);
 }
@@ -252,13 +267,21 @@ __device__ __forceinline__ void finalize_sweep(const SweepArgs &a, int P, int nt
 // group outside [beg, end) are masked. The col array carries 8 elements of tail padding.
 // Each valid target j != i receives v with a fire-and-forget RED.
 template <bool LOOPS>
-__device__ __forceinline__ void red_group(double *__restrict__ F, int4 x, int64_t p0, int64_t beg,
-                                          int64_t end, int32_t gi, double v, uint64_t fpol) {
+// Hot ids j < hot_lim (replicated accumulators, async.cu; 0 when off) go to copy `copy` of j.
+__device__ __forceinline__ void red_group(double *__restrict__ F, double *__restrict__ rep,
+                                          int32_t hot_lim, int copy, int4 x, int64_t p0,
+                                          int64_t beg, int64_t end, int32_t gi, double v,
+                                          uint64_t fpol) {
   const int32_t jj[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
   for (int c = 0; c < 4; c++) {
     const int64_t p = p0 + c;
-    if (p >= beg && p < end && (!LOOPS || jj[c] != gi)) red_add_f64_hint(F + jj[c], v, fpol);
+    if (p >= beg && p < end && (!LOOPS || jj[c] != gi)) {
+      if (jj[c] < hot_lim)
+        red_add_f64(rep + (int64_t)(copy * kHotRanks + jj[c]) * kRepStride, v);
+      else
+        red_add_f64_hint(F + jj[c], v, fpol);
+    }
   }
 }
 
@@ -321,8 +344,11 @@ inline SweepArgs sweep_args(Graph &g, int test_mode, int blk = 0, int blocks = 1
   a.blk = blk;
   a.blocks = blocks;
   a.ppartials = g.ppartials;
-  a.hot_shift = -1;
-  a.rep = nullptr;
+  // replicated hot accumulators (one GPU, hot placement on, allocated by prepare_cycle)
+  a.hot_shift = (g.rep && g.reordered && g.hot_acc && !g.partitioned && g.hot_count > 0)
+                    ? (int)g.hot_count
+                    : -1;
+  a.rep = g.rep;
   a.hub = nullptr;
   a.n_hub = 0;
   a.times = nullptr;
