@@ -399,8 +399,11 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     }
     return solve_dist(g, d, Bint, tol, (int)v, max_sweeps, flags, st);
   }
-  if (v == DI_PI_PULL || v == DI_PI_PUSH || v == DI_GS_BLOCK)
+  if (v == DI_PI_PULL || v == DI_PI_PUSH || v == DI_GS_BLOCK) {
+    di_status ps = prepare_cycle(g);   // PI' push uses the replicated hot accumulators too
+    if (ps != DI_OK) return ps;
     return run_comparator(g, d, tol, (int)v, max_sweeps, flags, st);
+  }
   const int mode = (flags & DI_PULL) ? MODE_PULL : ((flags & DI_AUTO) ? MODE_AUTO : MODE_PUSH);
   if (mode != MODE_PUSH && !g.has_csc)
     return fail(DI_EINVAL, "di_solve: DI_PULL / DI_AUTO need the CSC (upload with DI_BUILD_CSC)");

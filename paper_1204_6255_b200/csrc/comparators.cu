@@ -19,6 +19,7 @@
 
 #include "di_common.cuh"
 #include "kern_util.cuh"
+#include "sweep.cuh"
 
 namespace di {
 namespace {
@@ -37,7 +38,31 @@ struct CmpArgs {
   int64_t pe_count[kPullBins];
   PullEntry *re[kPullBins];  // static out-row entries for PI' (j = source row id)
   int64_t re_count[kPullBins];
+  double *rep;               // replicated accumulators of the hot ids j < hot_lim (PI' push)
+  int32_t hot_lim;
 };
+
+// PI' scatter of t into xn[j]: a hot id (j < hot_lim) goes to copy `copy` of its replicated
+// accumulator (same-address REDs serialise in one L2 slice), folded by k_pi_fold
+__device__ __forceinline__ void pi_add(const CmpArgs &a, double *__restrict__ xn, int32_t j,
+                                       double t, int copy, uint64_t fpol) {
+  if (j < a.hot_lim)
+    red_add_f64(a.rep + (int64_t)(copy * kHotRanks + j) * kRepStride, t);
+  else
+    red_add_f64_hint(xn + j, t, fpol);
+}
+
+__global__ void k_pi_fold(const CmpArgs a, double *__restrict__ xn) {
+  for (int k = threadIdx.x; k < a.hot_lim; k += blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < kRepCopies; c++) {
+      double *p = a.rep + (int64_t)(c * kHotRanks + k) * kRepStride;
+      acc += *p;
+      *p = 0.0;
+    }
+    if (acc != 0.0) xn[k] += acc;
+  }
+}
 
 // y_i = d*x_i/out_i (0 for dangling: l_out is empty), xn_i = (1-d)/N
 __global__ void k_pi_prep(const CmpArgs a, const double *__restrict__ x, double *__restrict__ y,
@@ -106,6 +131,7 @@ __global__ void __launch_bounds__(kCmpThreads) k_pi_push(const CmpArgs a, const 
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * (kCmpThreads / 32);
   const int64_t w = (int64_t)blockIdx.x * (kCmpThreads / 32) + (threadIdx.x >> 5);
+  const int copy = (int)(w % kRepCopies);
   for (int b = kPullBins - 1; b >= 2; b--) {
     for (int64_t u = w; u < a.re_count[b]; u += W) {
       const PullEntry en = a.re[b][u];
@@ -119,7 +145,7 @@ __global__ void __launch_bounds__(kCmpThreads) k_pi_push(const CmpArgs a, const 
 #pragma unroll
         for (int c = 0; c < 4; c++) {
           const int64_t p = a0 + 4 * (int64_t)v + c;
-          if (p >= beg && p < end) red_add_f64_hint(xn + jj[c], t, fpol);
+          if (p >= beg && p < end) pi_add(a, xn, jj[c], t, copy, fpol);
         }
       }
     }
@@ -136,7 +162,7 @@ __global__ void __launch_bounds__(kCmpThreads) k_pi_push(const CmpArgs a, const 
 #pragma unroll
         for (int c = 0; c < 4; c++) {
           const int64_t p = a0 + 4 * (int64_t)v + c;
-          if (p >= beg && p < end) red_add_f64_hint(xn + jj[c], t, fpol);
+          if (p >= beg && p < end) pi_add(a, xn, jj[c], t, copy, fpol);
         }
       }
     }
@@ -304,6 +330,11 @@ di_status run_comparator(Graph &g, double d, double tol, int variant, int64_t ma
   a.b = (1.0 - d) / (double)g.n_global;
   a.sc = g.sc;
   a.partials = g.cmp_partials;
+  {  // the replicated hot accumulators of the push schedules (prepare_cycle), when present
+    const SweepArgs sa = sweep_args(g, 0);
+    a.rep = sa.rep;
+    a.hot_lim = sa.hot_shift > 0 ? sa.hot_shift : 0;
+  }
   for (int b = 0; b < kPullBins; b++) {
     a.pe[b] = g.pe[b];
     a.pe_count[b] = g.pe_count[b];
@@ -325,10 +356,15 @@ di_status run_comparator(Graph &g, double d, double tol, int variant, int64_t ma
     launches++;
     while (err > tol && iters < max_sweeps) {
       k_pi_prep<<<grid, 256, 0, s>>>(a, x, y, xn);
-      if (variant == DI_PI_PULL)
+      if (variant == DI_PI_PULL) {
         k_pi_pull<<<grid, kCmpThreads, 0, s>>>(a, y, xn);
-      else
+      } else {
         k_pi_push<<<grid, kCmpThreads, 0, s>>>(a, y, xn);
+        if (a.hot_lim > 0) {  // the hot ids' replicated accumulators into xn
+          k_pi_fold<<<1, 256, 0, s>>>(a, xn);
+          launches++;
+        }
+      }
       k_sum<<<grid, kCmpThreads, 0, s>>>(a, xn, &g.sc->resid);
       k_pi_fix<<<grid, kCmpThreads, 0, s>>>(a, xn, x);
       launches += 4;
