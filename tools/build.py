@@ -59,15 +59,37 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = SO + f".tmp{os.getpid()}"
     # DI_NVCC_DEFS="-DNAME=V ..." (tuning experiments: compile-time knobs of the kernels)
     defs = os.environ.get("DI_NVCC_DEFS", "").split()
-    cmd = [NVCC, *FLAGS, *defs, "-I", nccl_include(), "-o", tmp, *sources(), "-ldl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    # one nvcc per translation unit, in parallel, then one link
+    objdir = os.path.join(HERE, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+    procs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + f".{os.getpid()}.o")
+        cmd = [NVCC, *cflags, *defs, "-I", nccl_include(), "-c", "-o", obj, src]
+        procs.append((obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    log, objs, failed = [], [], False
+    for obj, p in procs:
+        out, err = p.communicate()
+        log.append(err)
+        objs.append(obj)
+        if p.returncode != 0:
+            failed = True
+            sys.stderr.write(out + err)
+    if failed:
+        raise RuntimeError("nvcc failed building libdi.so")
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+            "-o", tmp, *objs, "-ldl"]
+    res = subprocess.run(link, capture_output=True, text=True)
+    for obj in objs:
+        os.remove(obj)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libdi.so")
+        raise RuntimeError("nvcc failed linking libdi.so")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("".join(log))
     with open(os.path.join(HERE, "ptxas.log"), "w") as f:
-        f.write(res.stderr)
+        f.write("".join(log))
     os.replace(tmp, SO)
     return SO
 
