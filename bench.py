@@ -108,6 +108,24 @@ def make_graph(cfg, seed):
     return src, dst, n, time.time() - t
 
 
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_cmd(gpus, argv, port=None):
+    """The torch.distributed.run command that runs this bench with one rank per GPU."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port or free_port()}",
+            os.path.abspath(__file__), *argv]
+
+
+def spawn(gpus, argv):
+    return subprocess.call(spawn_cmd(gpus, argv))
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -122,6 +140,12 @@ def run_ours(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the process group has {world} rank(s); "
+                         f"launch with torchrun --nproc-per-node {args.gpus}, or without WORLD_SIZE "
+                         "(bench.py then spawns the ranks itself)")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: --gpus {world} but only {torch.cuda.device_count()} CUDA device(s)")
     torch.cuda.set_device(local)
     nid = None
     if world > 1:
@@ -140,19 +164,46 @@ def run_ours(args):
     dist_async = use_async and world > 1 and args.dist_async   # F2: ranks meet every 4 cycles
     part = dict(rank=rank, world=world, nccl_id=nid) if world > 1 else dict(build_csc=args.mode != "push")
 
-    src, dst, n, gen_s = make_graph(args.config, args.seed)
-    L = len(src)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
+    if world > 1:
+        # every rank draws only the links of its own source range (equal node ranges; the R-MAT
+        # ids are Feistel-relabelled) on its GPU, and uploads them with DI_LOCAL_LINKS: no rank
+        # holds the whole link list (C5: 2.16e9 links; ~270e6 per rank at N = 8)
+        import digen
+        n = digen.CONFIGS[args.config].n
+        lo, hi = digen.node_ranges(n, world)[rank]
+        t = time.time()
+        if digen.CONFIGS[args.config].kind == "rmat":
+            s_d, t_d, _ = digen.make_range_gpu(args.config, lo, hi, seed=args.seed, device=dev)
+        else:   # host-block recipe: host generator, own sources kept
+            src_all, dst_all, _ = digen.make(args.config, seed=args.seed)
+            keep = (src_all >= lo) & (src_all < hi)
+            s_d = torch.from_numpy(src_all[keep]).to(dev)
+            t_d = torch.from_numpy(dst_all[keep]).to(dev)
+            del src_all, dst_all, keep
+        torch.cuda.synchronize()
+        gen_s = time.time() - t
+        part["local_range"] = (lo, hi)
+        src = dst = None
+        L_local = torch.tensor([s_d.numel()], dtype=torch.int64, device=dev)
+        dist.all_reduce(L_local)
+        L = int(L_local.item())
+    else:
+        src, dst, n, gen_s = make_graph(args.config, args.seed)
+        L = len(src)
+        s_d = torch.from_numpy(src).to(dev)
+        t_d = torch.from_numpy(dst).to(dev)
 
     # ---- a0 build ("Init"), device pointers
-    s_d = torch.from_numpy(src).to(dev)
-    t_d = torch.from_numpy(dst).to(dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     g = di.Graph(s_d, t_d, n, stream=stream, **part)
     torch.cuda.synchronize()
     init_ms = (time.perf_counter() - t0) * 1e3
+    if world > 1:   # the rank's own links, pinned on the host for the e2e steps
+        src_p = s_d.cpu().pin_memory()
+        dst_p = t_d.cpu().pin_memory()
     del s_d, t_d
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -247,9 +298,11 @@ def run_ours(args):
     warm_ms = round(statistics.median(warm), 3)
 
     # ---- e2e through the C ABI with host buffers (H2D of the link list, build, solve, D2H of H)
-    src_p = torch.from_numpy(src).pin_memory()
-    dst_p = torch.from_numpy(dst).pin_memory()
+    if world == 1:
+        src_p = torch.from_numpy(src).pin_memory()
+        dst_p = torch.from_numpy(dst).pin_memory()
     n_local = g.n_local
+    h2d_bytes = 8 * int(src_p.numel())
     H_host = torch.empty(n_local, dtype=torch.float64).pin_memory()
     e2e_ms, e2e_links = [], 0
     g.free()
@@ -311,8 +364,9 @@ def run_ours(args):
         "hbm_frac_counted_whole_solve": round(counted / (tot_ms * 1e-3) / 1e9 / peak, 4),
         "roofline": roofline,
         "e2e": {"value": round(e2e_val, 3) if e2e_val else None, "unit": UNIT, "ms_per_step": round(statistics.mean(e2e_ms), 2) if e2e_ms else None,
-                "h2d_bytes_per_step": 8 * L, "d2h_bytes_per_step": 8 * n_local,
-                "includes": "pinned host link list -> di_graph_upload(DI_HOST_PTRS) build -> di_solve -> H to host"},
+                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": 8 * n_local,
+                "includes": ("pinned host link list -> di_graph_upload(DI_HOST_PTRS) build -> di_solve -> H to host"
+                             + (" (per rank: its own source range, DI_LOCAL_LINKS; bytes per rank)" if world > 1 else ""))},
         "gpu_launches": gpu_launches,
         "host_loop_profiled_ms_per_step": gl_ms,
         "loop": "DI_GRAPH_LOOP (device-side while node)" if use_graph else "host loop",
@@ -357,6 +411,26 @@ def cpu_baseline(src, dst, n, args, budget_cycles=None):
             "host": {"cpu": model, "pinned_core": core, "host_cores": os.cpu_count()}}
 
 
+def launch_check(args):
+    """The launch path without a GPU: the same spawn and the same world == --gpus assertion as the
+    bench, then one gloo all-gather of the ranks; rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the process group has {world} rank(s)")
+    if world > 1:
+        dist.init_process_group("gloo")
+        got = [None] * world
+        dist.all_gather_object(got, (rank, os.getpid()))
+        dist.destroy_process_group()
+    else:
+        got = [(0, os.getpid())]
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "ranks": [r for r, _ in got],
+                          "pids": len({p for _, p in got})}), flush=True)
+
+
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
     rank, world, _ = dist_env()
@@ -372,7 +446,8 @@ def run_reference(args):
             times.append(cb["seconds"] * 1e3)
             last = cb
     value = statistics.mean(vals)
-    out = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    out = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": max(world, args.gpus),
+           "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(statistics.mean(times), 1), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": f"{args.config}: " + __import__("digen").CONFIGS[args.config].note,
@@ -402,7 +477,18 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-cycles", type=int, default=12)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="only check the launch: N ranks over gloo (CPU), world == --gpus, rank 0 prints "
+                         "one JSON line (tests/test_bench_launch.py)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        # one process per GPU: re-launch this command under torch.distributed.run (rendezvous on
+        # 127.0.0.1); rank 0 prints the JSON line, the exit code is the launcher's
+        sys.exit(spawn(args.gpus, sys.argv[1:]))
+    if args.launch_check:
+        return launch_check(args)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

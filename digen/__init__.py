@@ -18,15 +18,43 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libdigen.so")
 _SRC = os.path.join(_HERE, "gen.c")
+_GPU_SO = os.path.join(_HERE, "libdigen_gpu.so")
+_GPU_SRC = os.path.join(_HERE, "gen_gpu.cu")
+_NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
 def build(force: bool = False) -> str:
-    """Compile gen.c into libdigen.so (gcc, host code)."""
+    """Compile gen.c into libdigen.so (gcc, host code) and gen_gpu.cu into libdigen_gpu.so (nvcc,
+    sm_100a; per-source-range generation for partitioned runs) when nvcc is present."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
         tmp = _SO + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-pthread", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _SO)
+    if os.path.exists(_NVCC) and (force or not os.path.exists(_GPU_SO)
+                                  or os.path.getmtime(_GPU_SO) < os.path.getmtime(_GPU_SRC)):
+        tmp = _GPU_SO + f".tmp{os.getpid()}"
+        subprocess.check_call([_NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "--fmad=false",
+                               "-Xcompiler", "-fPIC", "-shared", "-o", tmp, _GPU_SRC])
+        os.replace(tmp, _GPU_SO)
     return _SO
+
+
+_gpu_lib = None
+
+
+def _G():
+    global _gpu_lib
+    if _gpu_lib is None:
+        build()
+        if not os.path.exists(_GPU_SO):
+            raise RuntimeError(f"{_GPU_SO} is missing (needs nvcc)")
+        lib = ctypes.CDLL(_GPU_SO)
+        vp, i64, dbl, u64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_uint64, ctypes.c_int
+        lib.digen_rmat_range_gpu.restype = ci
+        lib.digen_rmat_range_gpu.argtypes = [i64, i64, dbl, dbl, dbl, u64, dbl, dbl, dbl, ci, ci, i64, i64,
+                                             vp, i64, ctypes.POINTER(i64), vp]
+        _gpu_lib = lib
+    return _gpu_lib
 
 
 _lib = None
@@ -130,6 +158,53 @@ def make(name: str, seed: int = 1, n: int | None = None, threads: int = 0):
     else:
         src, dst = host_block(nn, seed=seed, threads=threads, **p)
     return src, dst, nn
+
+
+def node_ranges(n: int, world: int):
+    """Equal node ranges [n*g/world, n*(g+1)/world) (the R-MAT + repair ids are Feistel-relabelled,
+    so equal ranges carry about equal link counts)."""
+    return [(n * g // world, n * (g + 1) // world) for g in range(world)]
+
+
+def make_range_gpu(name: str, lo: int, hi: int, seed: int = 1, n: int | None = None, device=None):
+    """The links of config `name` (an R-MAT config) whose source lies in [lo, hi), generated on the
+    GPU: torch int32 CUDA tensors (src, dst) sorted by (src, dst), deduplicated, no self-loops —
+    exactly `make(name)`'s links with a source in [lo, hi) (tests/test_gpu_digen.py), without
+    drawing the rest of the graph on the host (C5 at G = 8: ~270M links per rank)."""
+    import torch
+    cfg = CONFIGS[name]
+    if cfg.kind != "rmat":
+        raise ValueError(f"make_range_gpu: {name} is not an R-MAT config")
+    nn = cfg.n if n is None else int(n)
+    p = dict(cfg.params)
+    m = p.pop("m")
+    if n is not None:
+        m = int(round(m * nn / cfg.n))
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    stream = torch.cuda.current_stream(dev)
+    lib = _G()
+    cap = int(1.15 * (m + nn) * (hi - lo) / max(nn, 1)) + 4096
+    for _ in range(3):
+        keys = torch.empty(cap, dtype=torch.int64, device=dev)
+        cnt = ctypes.c_int64(0)
+        rc = lib.digen_rmat_range_gpu(nn, m, p.get("a", 0.57), p.get("b", 0.19), p.get("c", 0.19), seed,
+                                      p.get("p_dangling", 0.0), p.get("p_zero_in", 0.0),
+                                      p.get("chain_heads", 0.0), 1, int(p.get("repair_in", True)),
+                                      int(lo), int(hi), keys.data_ptr(), cap, ctypes.byref(cnt),
+                                      stream.cuda_stream)
+        if rc != 0:
+            raise RuntimeError(f"digen_rmat_range_gpu failed ({rc})")
+        if cnt.value <= cap:
+            break
+        cap = int(cnt.value * 1.05) + 4096
+    keys = keys[:cnt.value]
+    keys, _ = torch.sort(keys)
+    keys = torch.unique_consecutive(keys)
+    src = (keys >> 32).to(torch.int32)
+    dst = (keys & 0xFFFFFFFF).to(torch.int32)
+    del keys
+    keep = src != dst
+    return src[keep].contiguous(), dst[keep].contiguous(), nn
 
 
 def transpose(src: np.ndarray, dst: np.ndarray):
