@@ -181,9 +181,15 @@ def make_range_gpu(name: str, lo: int, hi: int, seed: int = 1, n: int | None = N
     if n is not None:
         m = int(round(m * nn / cfg.n))
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    expect = (m + nn) * (hi - lo) / max(nn, 1)
+    if expect > 1.0e9:   # torch.sort takes < 2^31 keys: sub-ranges, concatenated in order
+        k = int(expect // 1.0e9) + 1
+        parts = [make_range_gpu(name, lo + (hi - lo) * q // k, lo + (hi - lo) * (q + 1) // k, seed, n, dev)
+                 for q in range(k)]
+        return torch.cat([p_[0] for p_ in parts]), torch.cat([p_[1] for p_ in parts]), nn
     stream = torch.cuda.current_stream(dev)
     lib = _G()
-    cap = int(1.15 * (m + nn) * (hi - lo) / max(nn, 1)) + 4096
+    cap = int(1.15 * expect) + 4096
     for _ in range(3):
         keys = torch.empty(cap, dtype=torch.int64, device=dev)
         cnt = ctypes.c_int64(0)

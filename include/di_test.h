@@ -26,6 +26,22 @@ di_status di_test_select(di_graph g, const double *F_in, const double *H_in, dou
                          int64_t bin_off[5], double scal[3], int64_t counts[2], double *F_out,
                          double *H_out);
 
+/* Run ONE asynchronous cycle of the bench's kernel (k_cycle, DI_ASYNC; SURVEY §8(a) a2-a6 fused)
+ * in its record mode on a caller snapshot F_in, H_in (host, n entries, caller's numbering) with
+ * the cycle's threshold fluid r: every node is tested against (r/L)*#out_i (DI_SOP) or 0
+ * (DI_CYC) and its fluid taken and folded exactly as in the product kernel, in
+ * the same launch configuration, but nothing is pushed: the kernel writes T_out[i] = T_i and
+ * v_out[i] = T_i*d/#out_i (0 for dangling nodes) for the selected nodes and leaves both 0
+ * elsewhere (T_i > 0 for every selected node). With no push nothing else changes F during the
+ * cycle, so the result must equal the oracle's bulk sweep on the same snapshot bit for bit.
+ * Outputs (host, caller's numbering; any may be NULL): T_out, v_out, F_out, H_out (n each);
+ * scal[3] = q (r - sum of taken fluid), s (sum v*(#out - k)), e (dangling transit);
+ * counts[2] = |S| (selected, dangling included), links(S). Single-GPU graphs (DI_EINVAL else).
+ * Leaves the handle's F and H set to F_out and H_out. */
+di_status di_test_cycle(di_graph g, const double *F_in, const double *H_in, double r, double d,
+                        di_variant v, double *T_out, double *v_out, double scal[3],
+                        int64_t counts[2], double *F_out, double *H_out);
+
 /* Internal numbering: old_of[k] = caller id of internal node k (identity with DI_NO_REORDER). */
 di_status di_test_perm(di_graph g, int32_t *old_of);
 

@@ -93,6 +93,8 @@ _lib.di_group_free.restype = _ci
 _lib.di_group_free.argtypes = [_vp]
 _lib.di_test_select.restype = _ci
 _lib.di_test_select.argtypes = [_vp, _vp, _vp, _dbl, _dbl, _ci, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
+_lib.di_test_cycle.restype = _ci
+_lib.di_test_cycle.argtypes = [_vp, _vp, _vp, _dbl, _dbl, _ci, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.di_test_csr.restype = _ci
 _lib.di_test_csr.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.di_test_perm.restype = _ci
@@ -104,7 +106,7 @@ EXPORTED = ["di_graph_upload", "di_graph_range", "di_graph_links", "di_solve", "
             "di_history", "di_sweep_log", "di_graph_free", "di_last_error",
             "di_nccl_unique_id", "di_group_create", "di_group_free", "di_group_abort",
             "di_set_threshold_scale",
-            "di_test_select", "di_test_csr", "di_test_bins", "di_test_perm"]
+            "di_test_select", "di_test_cycle", "di_test_csr", "di_test_bins", "di_test_perm"]
 
 
 class DIError(RuntimeError):
@@ -332,6 +334,23 @@ class Graph:
         m = int(off[4])
         return dict(ids=ids[:m].copy(), vals=vals[:m].copy(), chunk=chunk[:m].copy(), bin_off=off.copy(),
                     q=scal[0], s=scal[1], e=scal[2], selected=int(cnt[0]), links=int(cnt[1]), F=Fo, H=Ho)
+
+    def test_cycle(self, F, H, r, d=0.85, variant="sop"):
+        """di_test_cycle: one record-mode cycle of k_cycle on the snapshot (F, H) with threshold
+        fluid r; returns T, v (0 where not selected), F, H after, q, s, e, selected, links."""
+        F = np.ascontiguousarray(F, dtype=np.float64)
+        H = np.ascontiguousarray(H, dtype=np.float64)
+        T = np.empty(self.n, dtype=np.float64)
+        v = np.empty(self.n, dtype=np.float64)
+        Fo = np.empty(self.n, dtype=np.float64)
+        Ho = np.empty(self.n, dtype=np.float64)
+        scal = np.empty(3, dtype=np.float64)
+        cnt = np.empty(2, dtype=np.int64)
+        _check(_lib.di_test_cycle(self._h, F.ctypes.data, H.ctypes.data, float(r), float(d), VARIANTS[variant],
+                                  T.ctypes.data, v.ctypes.data, scal.ctypes.data, cnt.ctypes.data,
+                                  Fo.ctypes.data, Ho.ctypes.data))
+        return dict(T=T, v=v, F=Fo, H=Ho, q=scal[0], s=scal[1], e=scal[2], selected=int(cnt[0]),
+                    links=int(cnt[1]))
 
     def free(self):
         if getattr(self, "_h", None):

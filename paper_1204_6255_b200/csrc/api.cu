@@ -684,6 +684,82 @@ di_status di_test_csr(di_graph h, int64_t *row_ptr, int32_t *col, int32_t *deg, 
   return DI_OK;
 }
 
+di_status di_test_cycle(di_graph h, const double *F_in, const double *H_in, double r, double d,
+                        di_variant v, double *T_out, double *v_out, double scal[3], int64_t counts[2],
+                        double *F_out, double *H_out) {
+  Graph *gp = (Graph *)h;
+  if (!gp || !F_in || !H_in) return fail(DI_EINVAL, "di_test_cycle: NULL argument");
+  if (v != DI_SOP && v != DI_CYC) return fail(DI_EINVAL, "di_test_cycle: DI_SOP or DI_CYC");
+  Graph &g = *gp;
+  if (g.partitioned) return fail(DI_EINVAL, "di_test_cycle: single-GPU graphs only");
+  AllocScope as(g.stream);
+  {
+    di_status ps = prepare_cycle(g);
+    if (ps != DI_OK) return ps;
+  }
+  const size_t n = (size_t)g.n;
+  std::vector<int32_t> old_of;
+  std::vector<double> Fi(n), Hi(n);
+  if (g.reordered) {
+    old_of.resize(n);
+    DI_CK(cudaMemcpy(old_of.data(), g.old_of, n * 4, cudaMemcpyDeviceToHost));
+  }
+  for (size_t k = 0; k < n; k++) {
+    const size_t u = g.reordered ? (size_t)old_of[k] : k;
+    Fi[k] = F_in[u];
+    Hi[k] = H_in[u];
+  }
+  DI_CK(cudaMemcpy(g.F, Fi.data(), n * 8, cudaMemcpyHostToDevice));
+  DI_CK(cudaMemcpy(g.H, Hi.data(), n * 8, cudaMemcpyHostToDevice));
+  double *rec = nullptr;
+  DI_CK(dmalloc(&rec, 2 * n * 8 + 16));
+  DI_CK(cudaMemsetAsync(rec, 0, 2 * n * 8 + 16, g.stream));
+  {
+    Scalars &s = *g.sc_host;
+    const uint32_t epoch = s.epoch ? s.epoch : 1;
+    memset(&s, 0, sizeof(Scalars));
+    s.epoch = epoch;
+    s.r = r;
+    s.d = d;
+    s.alpha = g.alpha;
+    s.tol = 1e-300;
+    s.variant = (int32_t)v;
+  }
+  DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
+  int64_t launches = 0;
+  launch_cycle_test(g, rec, rec + n, &launches);
+  di_status s = sync_scalars(g);
+  if (s != DI_OK) {
+    dfree(rec);
+    return s;
+  }
+  DI_CK(cudaGetLastError());
+  std::vector<double> Tr(n), vr(n), Fo(n), Ho(n);
+  DI_CK(cudaMemcpy(Tr.data(), rec, n * 8, cudaMemcpyDeviceToHost));
+  DI_CK(cudaMemcpy(vr.data(), rec + n, n * 8, cudaMemcpyDeviceToHost));
+  DI_CK(cudaMemcpy(Fo.data(), g.F, n * 8, cudaMemcpyDeviceToHost));
+  DI_CK(cudaMemcpy(Ho.data(), g.H, n * 8, cudaMemcpyDeviceToHost));
+  dfree(rec);
+  for (size_t k = 0; k < n; k++) {
+    const size_t u = g.reordered ? (size_t)old_of[k] : k;
+    if (T_out) T_out[u] = Tr[k];
+    if (v_out) v_out[u] = vr[k];
+    if (F_out) F_out[u] = Fo[k];
+    if (H_out) H_out[u] = Ho[k];
+  }
+  const Scalars &c = *g.sc_host;
+  if (scal) {
+    scal[0] = c.q;
+    scal[1] = c.s;
+    scal[2] = c.e_sw;
+  }
+  if (counts) {
+    counts[0] = c.selected_total;
+    counts[1] = c.links_total;
+  }
+  return DI_OK;
+}
+
 di_status di_test_select(di_graph h, const double *F_in, const double *H_in, double r, double d,
                          di_variant v, int32_t *ids, double *vals, int32_t *chunk, int64_t cap,
                          int64_t bin_off[5], double scal[3], int64_t counts[2], double *F_out,

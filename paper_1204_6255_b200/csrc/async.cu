@@ -121,7 +121,10 @@ __device__ __forceinline__ double take_fluid(double *p) {
       (long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
 }
 
-template <bool LOOPS, bool DIST>
+// TEST (di_test_cycle, include/di_test.h): the selection records (T, v) per node in a.rec_T /
+// a.rec_v instead of pushing, so that the select-and-take step of this kernel can be compared bit
+// for bit with the oracle's bulk sweep on a frozen F (no push: nothing changes F during the cycle)
+template <bool LOOPS, bool DIST, bool TEST = false>
 __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const SweepArgs a, const DistArgs x) {
   constexpr int NW = kAsyncThreads / 32;
   __shared__ int64_t s_rb[kCycTile];   // long rows of the tile: first link
@@ -273,12 +276,21 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       acc_sel++;
       if (o == 0) {
         acc_e += T;
+        if (TEST) {
+          a.rec_T[i] = T;
+          a.rec_v[i] = 0.0;
+        }
         continue;
       }
       const double v = __ddiv_rn(__dmul_rn(T, d), (double)o);
       acc_s += __dmul_rn(v, (double)(o - kl[j]));
       acc_lk += o;
       acc_nd++;
+      if (TEST) {
+        a.rec_T[i] = T;
+        a.rec_v[i] = v;
+        continue;
+      }
       if (hub4[j]) {
         hv[i] = v;
         __threadfence();
@@ -603,6 +615,26 @@ void report_cycle_times(Graph &g, int64_t cycles) {
   }
   fprintf(stderr, "[DI_CYC_TIMES] %lld cycles, grid %d: span %.1f us, start skew %.1f us, tail (max - median end) %.1f us, mean CTA busy %.1f us\n",
           (long long)nc, grid, span / nc / 1e3, skew / nc / 1e3, tail / nc / 1e3, busy / nc / 1e3);
+}
+
+// di_test_cycle: one cycle of the select-and-take step on the current (F, H), recording (T, v)
+void launch_cycle_test(Graph &g, double *rec_T, double *rec_v, int64_t *launches) {
+  SweepArgs a = sweep_args(g, 1);
+  a.ntiles = (g.n + kCycTile - 1) / kCycTile;
+  a.hot_shift = g.rep ? hot_shift_of(g) : -1;
+  a.rep = g.rep;
+  a.times = nullptr;
+  a.hub = nullptr;
+  a.n_hub = 0;   // hub rows are recorded like the others (nothing is pushed)
+  a.rec_T = rec_T;
+  a.rec_v = rec_v;
+  DistArgs x{};
+  const int grid = cycle_grid(g);
+  if (g.has_loops)
+    k_cycle<true, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+  else
+    k_cycle<false, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+  *launches += 1;
 }
 
 void launch_cycle(Graph &g, int64_t *launches) {

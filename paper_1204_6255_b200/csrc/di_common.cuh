@@ -274,6 +274,7 @@ void launch_loop_cond(Graph &g, cudaGraphConditionalHandle h);
 // async.cu
 void report_cycle_times(Graph &g, int64_t cycles);
 void launch_cycle(Graph &g, int64_t *launches);
+void launch_cycle_test(Graph &g, double *rec_T, double *rec_v, int64_t *launches);
 di_status prepare_cycle(Graph &g);
 di_status alloc_pull(Graph &g);
 di_status alloc_dist(Graph &g);

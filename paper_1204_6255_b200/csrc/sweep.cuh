@@ -38,6 +38,7 @@ struct SweepArgs {
   const int64_t *hub;   // DI_ASYNC hub items (async.cu), n_hub of them
   int n_hub;
   unsigned long long *times;  // DI_CYC_TIMES diagnostic (async.cu), nullptr = off
+  double *rec_T, *rec_v;      // di_test_cycle records (async.cu, TEST instantiation only)
 };
 
 // What one sweep moved: r_{n+1} = q + s (a2), dangling absorption e, counters.
@@ -352,6 +353,8 @@ inline SweepArgs sweep_args(Graph &g, int test_mode, int blk = 0, int blocks = 1
   a.hub = nullptr;
   a.n_hub = 0;
   a.times = nullptr;
+  a.rec_T = nullptr;
+  a.rec_v = nullptr;
   a.F = g.F;
   a.H = g.H;
   a.deg = g.deg;

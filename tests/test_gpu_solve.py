@@ -528,3 +528,31 @@ def test_c4_full_size_properties():
         H = assemble([o[k][0] for _, o in res], [rg for rg, _ in res], n)
         assert res[0][1][k][1]["converged"] == 1
         assert l1(H, Ho) <= 1e-9, k
+
+
+@pytest.mark.parametrize("axis", ["transpose", "loops"])
+def test_paper_axes_c2_async_vs_oracle(axis):
+    """F3's paper axes at C2's full size, on the bench's path (asynchronous cycles in the
+    device-side graph loop): Dataset 1bis is P^T (every link reversed) and Dataset 1
+    has O/N = 0.204 self-loop nodes (Table 1; fold P:259-263, reading G6), here 20 % of
+    the nodes with out-links get one self-loop (the LOOPS instantiation of k_cycle). North_star
+    gate against the sequential CPU oracle (both to ||F||_1 <= 1e-10), and against the tight
+    oracle run (G19); DI-SOP and DI-CYC; the bulk push sweep too."""
+    need_gpu()
+    src, dst, n = digen.make("c2")
+    if axis == "transpose":
+        src, dst = digen.transpose(src, dst)
+    else:
+        src, dst = digen.add_self_loops(src, dst, n, frac=0.2)
+        assert digen.stats(src, dst, n)["o_over_n"] > 0.15
+    g = upload(src, dst, n)
+    for variant in ("sop", "cyc"):
+        Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant=variant)
+        Ht, _, _ = oracle.di(src, dst, n, d=D, tol=1e-13, variant=variant)
+        for kw in (dict(asynchronous=True, graph_loop=True), dict()):
+            st = g.solve(d=D, tol=1e-10, variant=variant, **kw)
+            assert st["converged"] == 1 and st["residual_l1"] <= 1e-10, (axis, variant, kw)
+            H = g.history().cpu().numpy()
+            assert l1(H, Ho) <= 1e-9, (axis, variant, kw)
+            assert l1(H, Ht) <= 1e-10 / (1 - D) + 1e-13 / (1 - D), (axis, variant, kw)
+    g.free()
