@@ -188,6 +188,30 @@ di_status di_group_abort(di_group grp);
 di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_links, int64_t n_nodes,
                           uint32_t flags, void *stream, const di_dist *dist, di_graph *out);
 
+/* Process-wide tuning and diagnostic options. Every knob of the library is one of these (there are
+ * no environment variables). Upload-time options (marked U) apply to graphs uploaded afterwards;
+ * the others are read when used. Not for the inner loop: the call takes a mutex.
+ *   name             default  range     meaning
+ *   "red_hint"       1        0..1      U: L2 evict_last policy on the push's REDs into F
+ *   "push_occ"       4        1..32     U: resident blocks per SM of the bulk push kernel
+ *   "auto_ratio"     0.35     >= 0      U: DI_AUTO pulls a sweep whose links(S) exceed ratio * L
+ *   "stripes"        0        >= 0      U: relabelling stripes (0: ~1024-node stripes, prime count;
+ *                                          1: plain descending in-degree order)
+ *   "hot_acc"        1        0..1      U: replicated accumulators for the 64 hottest targets
+ *   "repl_share"     0.0005   0..1      U: top in-degree share of L that turns them on
+ *   "cold_bins"      -1       -1..1     U: cold bins of DI_ASYNC on one GPU (-1: when F > 2 x L2;
+ *                                          0 off; 1 on): pushes to targets beyond the first tier
+ *                                          are binned by target slice and applied slice by slice
+ *   "cold_tier"      0        >= 0      U: first-tier size in nodes (0: half the L2 in bytes)
+ *   "cycle_grid_div" 1        1..4096   U: DI_ASYNC grid divided by k (emulated-rank studies)
+ *   "cycle_times"    0        0..1      U: per-CTA start/end times of each cycle, summary on stderr
+ *   "p2p"            1        0..1      U: peer-memory inboxes for the partitioned exchange
+ *   "p2p_force"      0        0..1      U: create the inbox on a one-rank communicator too
+ *   "build_trace"    0        0..1      host timestamps of the build phases on stderr
+ * DI_EINVAL for an unknown name or a value out of range (integers must be integral). */
+di_status di_set_option(const char *name, double value);
+di_status di_get_option(const char *name, double *value);
+
 /* DI-SOP threshold scale: later solves select F_i > alpha * (r/L) * #out_i.
  * alpha = 1 (the default) is the paper's rule and computes bit for bit the same
  * threshold; alpha > 1 diffuses fewer, larger amounts. alpha must be finite and > 0 (DI_EINVAL).

@@ -81,6 +81,10 @@ _lib.di_graph_free.restype = _ci
 _lib.di_graph_free.argtypes = [_vp]
 _lib.di_last_error.restype = ctypes.c_char_p
 _lib.di_last_error.argtypes = []
+_lib.di_set_option.restype = _ci
+_lib.di_set_option.argtypes = [ctypes.c_char_p, _dbl]
+_lib.di_get_option.restype = _ci
+_lib.di_get_option.argtypes = [ctypes.c_char_p, ctypes.POINTER(_dbl)]
 _lib.di_set_threshold_scale.restype = _ci
 _lib.di_set_threshold_scale.argtypes = [_vp, _dbl]
 _lib.di_nccl_unique_id.restype = _ci
@@ -105,7 +109,7 @@ _lib.di_test_bins.argtypes = [_vp]
 EXPORTED = ["di_graph_upload", "di_graph_range", "di_graph_links", "di_solve", "di_residual",
             "di_history", "di_sweep_log", "di_graph_free", "di_last_error",
             "di_nccl_unique_id", "di_group_create", "di_group_free", "di_group_abort",
-            "di_set_threshold_scale",
+            "di_set_threshold_scale", "di_set_option", "di_get_option",
             "di_test_select", "di_test_cycle", "di_test_csr", "di_test_bins", "di_test_perm"]
 
 
@@ -131,6 +135,32 @@ def _stream_ptr(stream):
     if stream is None:
         stream = torch.cuda.current_stream()
     return stream.cuda_stream
+
+
+def set_option(name: str, value) -> None:
+    """di_set_option: process-wide tuning/diagnostic option (include/di.h lists them)."""
+    _check(_lib.di_set_option(name.encode(), float(value)))
+
+
+def get_option(name: str) -> float:
+    v = _dbl()
+    _check(_lib.di_get_option(name.encode(), ctypes.byref(v)))
+    return v.value
+
+
+class option:
+    """Context manager: `with di.option("cold_bins", 1): ...` sets an option and restores it."""
+
+    def __init__(self, name, value):
+        self.name, self.value = name, value
+
+    def __enter__(self):
+        self.prev = get_option(self.name)
+        set_option(self.name, self.value)
+        return self
+
+    def __exit__(self, *a):
+        set_option(self.name, self.prev)
 
 
 def nccl_unique_id() -> bytes:

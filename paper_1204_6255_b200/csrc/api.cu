@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -17,6 +18,13 @@
 #include "di_common.cuh"
 
 namespace di {
+
+static std::mutex g_opt_mu;
+static Options g_opt;
+Options options() {
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  return g_opt;
+}
 
 static thread_local std::string g_err;
 void set_error(const std::string &msg) { g_err = msg; }
@@ -38,7 +46,7 @@ cudaError_t dmalloc_bytes(void **p, size_t bytes) {
     }
     prepared = dev;
   }
-  static const bool trace = getenv("DI_BUILD_TRACE") && atoi(getenv("DI_BUILD_TRACE"));
+  const bool trace = options().build_trace != 0;
   const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 1, alloc_stream());
   // the buffer is then usable on any stream (some host paths touch it with synchronous copies)
@@ -102,7 +110,7 @@ struct EventSet {
 
 void free_graph(Graph *g) {
   if (!g) return;
-  void *ptrs[] = {g->ppartials, g->rep, g->hub_items, g->cyc_times, g->row_ptr, g->col, g->deg, g->kloop, g->csc_ptr, g->csc_row, g->F, g->H,
+  void *ptrs[] = {g->cold_rec, g->cold_off, g->cold_top, g->cold_fill, g->ppartials, g->rep, g->hub_items, g->cyc_times, g->row_ptr, g->col, g->deg, g->kloop, g->csc_ptr, g->csc_row, g->F, g->H,
                   g->new_of, g->old_of, g->Bperm, g->xfer,
                   g->S, g->aux, g->sc, g->partials, g->ipartials, g->red_partials,
                   g->log_r, g->log_sel, g->log_links, g->log_mode};
@@ -268,8 +276,8 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
     if (flags & DI_BUILD_CSC)
       return fail(DI_EINVAL, "di_graph_upload: DI_BUILD_CSC is single-GPU (partitioned sweeps are "
                              "push-only)");
-    if ((flags & DI_LOCAL_LINKS) && !(dist->lo >= 0 && dist->lo < dist->hi && dist->hi <= n_nodes))
-      return fail(DI_EINVAL, "di_graph_upload: DI_LOCAL_LINKS needs 0 <= dist->lo < dist->hi <= n");
+    // (a DI_LOCAL_LINKS range outside [0, n) is reported by the collective validation in
+    //  build_graph, on every rank: a rank must not leave before the communicator exists)
     if (!grp && !dist->nccl_unique_id)
       return fail(DI_EINVAL, "di_graph_upload: dist needs an NCCL unique id or a di_group");
     if (grp && grp->world != world)
@@ -310,12 +318,21 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
     g->local_lo = dist->lo;
     g->local_hi = dist->hi;
   }
-  if (const char *e = getenv("DI_RED_HINT")) g->red_hint = atoi(e);
-  if (const char *e = getenv("DI_PUSH_OCC")) g->push_occ = atoi(e);
-  if (const char *e = getenv("DI_AUTO_RATIO")) g->auto_ratio = atof(e);
-  if (const char *e = getenv("DI_STRIPES")) g->stripes = atoi(e);
-  if (const char *e = getenv("DI_HOT_ACC")) g->hot_acc = atoi(e);
-  if (const char *e = getenv("DI_REPL_SHARE")) g->repl_share = atof(e);
+  {
+    const Options o = options();
+    g->red_hint = o.red_hint;
+    g->push_occ = o.push_occ;
+    g->auto_ratio = o.auto_ratio;
+    g->stripes = o.stripes;
+    g->hot_acc = o.hot_acc;
+    g->repl_share = o.repl_share;
+    g->cold_mode = o.cold_bins;
+    g->cold_tier = o.cold_tier;
+    g->grid_div = o.cycle_grid_div;
+    g->cycle_times = o.cycle_times;
+    g->p2p_opt = o.p2p;
+    g->p2p_force = o.p2p_force;
+  }
   di_status s = build_graph(*g, src, dst, n_links, flags);
   if (s == DI_OK) s = alloc_state(*g);
   if (s == DI_OK) s = alloc_pull(*g);
@@ -325,6 +342,70 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
     return s;
   }
   *out = (di_graph)g;
+  return DI_OK;
+}
+
+namespace {
+struct OptDesc {
+  const char *name;
+  double lo, hi;
+  bool integer;
+};
+const OptDesc kOpts[] = {
+    {"red_hint", 0, 1, true},       {"push_occ", 1, 32, true},    {"auto_ratio", 0, 1e9, false},
+    {"stripes", 0, 2147483647.0, true}, {"hot_acc", 0, 1, true},  {"repl_share", 0, 1, false},
+    {"cold_bins", -1, 1, true},     {"cold_tier", 0, 2147483647.0, true},
+    {"cycle_grid_div", 1, 4096, true}, {"cycle_times", 0, 1, true}, {"p2p", 0, 1, true},
+    {"p2p_force", 0, 1, true},      {"build_trace", 0, 1, true},
+};
+}  // namespace
+
+di_status di_set_option(const char *name, double value) {
+  if (!name) return fail(DI_EINVAL, "di_set_option: NULL name");
+  const std::string n(name);
+  const OptDesc *d = nullptr;
+  for (const auto &k : kOpts)
+    if (n == k.name) d = &k;
+  if (!d) return fail(DI_EINVAL, "di_set_option: unknown option '" + n + "'");
+  if (!std::isfinite(value) || value < d->lo || value > d->hi || (d->integer && value != std::floor(value)))
+    return fail(DI_EINVAL, "di_set_option: value out of range for '" + n + "'");
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  Options &o = g_opt;
+  const int iv = (int)value;
+  if (n == "red_hint") o.red_hint = iv;
+  else if (n == "push_occ") o.push_occ = iv;
+  else if (n == "auto_ratio") o.auto_ratio = value;
+  else if (n == "stripes") o.stripes = iv;
+  else if (n == "hot_acc") o.hot_acc = iv;
+  else if (n == "repl_share") o.repl_share = value;
+  else if (n == "cold_bins") o.cold_bins = iv;
+  else if (n == "cold_tier") o.cold_tier = (int64_t)value;
+  else if (n == "cycle_grid_div") o.cycle_grid_div = iv;
+  else if (n == "cycle_times") o.cycle_times = iv;
+  else if (n == "p2p") o.p2p = iv;
+  else if (n == "p2p_force") o.p2p_force = iv;
+  else if (n == "build_trace") o.build_trace = iv;
+  return DI_OK;
+}
+
+di_status di_get_option(const char *name, double *value) {
+  if (!name || !value) return fail(DI_EINVAL, "di_get_option: NULL argument");
+  const std::string n(name);
+  const Options o = options();
+  if (n == "red_hint") *value = o.red_hint;
+  else if (n == "push_occ") *value = o.push_occ;
+  else if (n == "auto_ratio") *value = o.auto_ratio;
+  else if (n == "stripes") *value = o.stripes;
+  else if (n == "hot_acc") *value = o.hot_acc;
+  else if (n == "repl_share") *value = o.repl_share;
+  else if (n == "cold_bins") *value = o.cold_bins;
+  else if (n == "cold_tier") *value = (double)o.cold_tier;
+  else if (n == "cycle_grid_div") *value = o.cycle_grid_div;
+  else if (n == "cycle_times") *value = o.cycle_times;
+  else if (n == "p2p") *value = o.p2p;
+  else if (n == "p2p_force") *value = o.p2p_force;
+  else if (n == "build_trace") *value = o.build_trace;
+  else return fail(DI_EINVAL, "di_get_option: unknown option '" + n + "'");
   return DI_OK;
 }
 
@@ -400,8 +481,10 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
     return solve_dist(g, d, Bint, tol, (int)v, max_sweeps, flags, st);
   }
   if (v == DI_PI_PULL || v == DI_PI_PUSH || v == DI_GS_BLOCK) {
-    di_status ps = prepare_cycle(g);   // PI' push uses the replicated hot accumulators too
-    if (ps != DI_OK) return ps;
+    if (v == DI_PI_PUSH) {   // PI' push uses the replicated hot accumulators too
+      di_status ps = prepare_cycle(g, false);
+      if (ps != DI_OK) return ps;
+    }
     return run_comparator(g, d, tol, (int)v, max_sweeps, flags, st);
   }
   const int mode = (flags & DI_PULL) ? MODE_PULL : ((flags & DI_AUTO) ? MODE_AUTO : MODE_PUSH);
@@ -416,8 +499,8 @@ di_status di_solve(di_graph h, double d, const double *B, double tol, di_variant
   const bool async = flags & DI_ASYNC;
   if (async && (mode != MODE_PUSH || blocks > 1))
     return fail(DI_EINVAL, "di_solve: DI_ASYNC runs push cycles without DI_BLOCKS");
-  {  // replicated hot accumulators (every push schedule) and, for DI_ASYNC, the hub items
-    di_status ps = prepare_cycle(g);
+  {  // replicated hot accumulators (every push schedule) and, for DI_ASYNC, the cold bins
+    di_status ps = prepare_cycle(g, async);
     if (ps != DI_OK) return ps;
   }
   const bool resume = flags & DI_RESUME;
@@ -694,7 +777,7 @@ di_status di_test_cycle(di_graph h, const double *F_in, const double *H_in, doub
   if (g.partitioned) return fail(DI_EINVAL, "di_test_cycle: single-GPU graphs only");
   AllocScope as(g.stream);
   {
-    di_status ps = prepare_cycle(g);
+    di_status ps = prepare_cycle(g, false);
     if (ps != DI_OK) return ps;
   }
   const size_t n = (size_t)g.n;

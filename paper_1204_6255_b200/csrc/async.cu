@@ -121,12 +121,87 @@ __device__ __forceinline__ double take_fluid(double *p) {
       (long long)atomicExch(reinterpret_cast<unsigned long long *>(p), 0ull));
 }
 
+__device__ __forceinline__ void st_cold(ColdRec *r, int32_t j, double v) {
+  const long long b = __double_as_longlong(v);
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(r), "r"(j), "r"(0),
+               "r"((int)(b & 0xffffffffll)), "r"((int)(b >> 32))
+               : "memory");
+}
+
+// Cold bins: warp-collective — all 32 lanes call it, `cold` marks the lanes with a
+// record (j, v). Lanes of one bin are grouped (match.any); the group's leader takes their slots
+// from the warp's current chunk of that bin (cb/ce: next slot and chunk end, relative to the bin's
+// region, in shared memory), reserving a fresh kColdChunk-record chunk with one global atomic when
+// the current one runs out (its fill, kColdChunk, is recorded then; partially filled chunks record
+// theirs at the end of the cycle). Records of one group land in consecutive slots: one coalesced
+// 16-B-per-lane store.
+__device__ __forceinline__ void cold_append(const SweepArgs &a, int32_t *cb, int32_t *ce,
+                                            const int64_t *coff, bool cold, int32_t j, double v,
+                                            int lane) {
+  if (__ballot_sync(0xffffffffu, cold) == 0u) return;
+  const int b = cold ? (int)(((int64_t)j - a.cold_lo) >> a.cold_shift) : -1;
+  const unsigned peers = __match_any_sync(0xffffffffu, b);
+  const int leader = __ffs(peers) - 1;
+  int pos0 = 0, avail = 0, nb = 0;
+  if (cold && lane == leader) {
+    const int cnt = __popc(peers);
+    pos0 = cb[b];
+    avail = ce[b] - pos0;
+    if (avail >= cnt) {
+      cb[b] = pos0 + cnt;
+    } else {
+      if (ce[b] > 0) a.cold_fill[(coff[b] + ce[b]) / kColdChunk - 1] = kColdChunk;
+      nb = (int)atomicAdd(a.cold_top + 16 * b, (unsigned long long)kColdChunk);
+      cb[b] = nb + (cnt - avail);
+      ce[b] = nb + kColdChunk;
+    }
+  }
+  pos0 = __shfl_sync(0xffffffffu, pos0, leader);
+  avail = __shfl_sync(0xffffffffu, avail, leader);
+  nb = __shfl_sync(0xffffffffu, nb, leader);
+  if (cold) {
+    const int rk = __popc(peers & ((1u << lane) - 1u));
+    const int pos = rk < avail ? pos0 + rk : nb + (rk - avail);
+    st_cold(a.cold_rec + coff[b] + pos, j, v);
+  }
+}
+
+// COLD push of one int4 group (warp-collective: every lane calls it; `valid` = the lane has a
+// group): hot ids to the replicated accumulators, first-tier targets (j < cold_lo) a RED into F,
+// cold targets a record of their bin.
+template <bool LOOPS>
+__device__ __forceinline__ void push_group_cold(const SweepArgs &a, double *__restrict__ rep,
+                                                int32_t hot_lim, int copy, int4 q, int64_t p0,
+                                                int64_t beg, int64_t end, bool valid, int32_t gi,
+                                                double v, uint64_t fpol, int32_t *cb, int32_t *ce,
+                                                const int64_t *coff, int lane) {
+  const int32_t jj[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    const int64_t p = p0 + c;
+    const int32_t j = jj[c];
+    const bool ok = valid && p >= beg && p < end && (!LOOPS || j != gi);
+    const bool cold = ok && (int64_t)j >= a.cold_lo;
+    if (ok && !cold) {
+      if (j < hot_lim)
+        red_add_f64(rep + (int64_t)(copy * kRepl + j) * kRepStride, v);
+      else
+        red_add_f64_hint(a.F + j, v, fpol);
+    }
+    cold_append(a, cb, ce, coff, cold, j, v, lane);
+  }
+}
+
 // TEST (di_test_cycle, include/di_test.h): the selection records (T, v) per node in a.rec_T /
 // a.rec_v instead of pushing, so that the select-and-take step of this kernel can be compared bit
 // for bit with the oracle's bulk sweep on a frozen F (no push: nothing changes F during the cycle)
-template <bool LOOPS, bool DIST, bool TEST = false>
+// COLD: cold bins on (single GPU, F several times the L2)
+template <bool LOOPS, bool DIST, bool TEST = false, bool COLD = false>
 __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const SweepArgs a, const DistArgs x) {
   constexpr int NW = kAsyncThreads / 32;
+  constexpr int NCB = COLD ? kColdBins : 1;
+  __shared__ int32_t s_ccb[NW][NCB], s_cce[NW][NCB];   // COLD: per-warp chunk state per bin
+  __shared__ int64_t s_coff[NCB];
   __shared__ int64_t s_rb[kCycTile];   // long rows of the tile: first link
   __shared__ int32_t s_ro[kCycTile];   // #links
   __shared__ double s_rv[kCycTile];    // v = T d / o
@@ -163,6 +238,14 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   double *__restrict__ F = a.F;
   double acc_tk = 0.0, acc_s = 0.0, acc_e = 0.0;
   long long acc_sel = 0, acc_nd = 0, acc_lk = 0;
+  int32_t *ccb = s_ccb[warp], *cce = s_cce[warp];
+  if (COLD) {
+    if (lane < NCB) {
+      ccb[lane] = 0;
+      cce[lane] = 0;
+    }
+    if (threadIdx.x < NCB) s_coff[threadIdx.x] = threadIdx.x < a.cold_nbins ? a.cold_off[threadIdx.x] : 0;
+  }
 
   for (;;) {
     if (threadIdx.x == 0) {
@@ -369,7 +452,10 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
 #pragma unroll
           for (int k = 0; k < 4; k++) {
             const int vi = vb + 32 * k + lane;
-            if (vi < nvec)
+            if constexpr (COLD)
+              push_group_cold<LOOPS>(a, rep, hot_lim, copy, xq[k], a0 + 4 * (int64_t)vi, beg, end,
+                                     vi < nvec, gi, v, fpol, ccb, cce, s_coff, lane);
+            else if (vi < nvec)
               push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, xq[k], a0 + 4 * (int64_t)vi,
                                       beg, end, gi, v, fpol);
           }
@@ -386,7 +472,26 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         q = __shfl_sync(0xffffffffu, q, 0);
         if (q >= nsmall) break;
         const int k = q + lane;
-        if (k < nsmall) {
+        if constexpr (COLD) {   // warp-collective pushes: every lane runs the NG groups
+          const bool has = k < nsmall;
+          const int li = has ? s_si[k] : 0;
+          const double v = has ? s_sv[k] : 0.0;
+          const int64_t sb = has ? s_sb[k] : 0;
+          const int64_t beg = sb >> 8, end = beg + (sb & 255), a0 = beg & ~3ll;
+          const int nvec = has ? (int)((end - a0 + 3) >> 2) : 0;
+          const int32_t gi = LOOPS ? (int32_t)(tb + li + a.lo) : -1;
+          constexpr int NG = (kAsyncSmall + 6) / 4;
+          int4 xs[NG];
+#pragma unroll
+          for (int u = 0; u < NG; u++) {
+            xs[u] = make_int4(0, 0, 0, 0);
+            if (u < nvec) xs[u] = ld_col4(col + a0 + 4 * u, pol);
+          }
+#pragma unroll
+          for (int u = 0; u < NG; u++)
+            push_group_cold<LOOPS>(a, rep, hot_lim, copy, xs[u], a0 + 4 * u, beg, end, u < nvec, gi, v,
+                                   fpol, ccb, cce, s_coff, lane);
+        } else if (k < nsmall) {
           const int li = s_si[k];
           const double v = s_sv[k];
           const int64_t sb = s_sb[k];
@@ -417,7 +522,24 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         q = __shfl_sync(0xffffffffu, q, 0);
         if (q >= nmid) break;
         const int k = q + (lane >> 3);
-        if (k < nmid) {
+        if constexpr (COLD) {   // warp-collective: every lane runs the warp's longest row's steps
+          const bool has = k < nmid;
+          const int64_t beg = has ? s_rb[k] : 0, end = has ? beg + s_ro[k] : 0, a0 = beg & ~3ll;
+          const int nvec = has ? (int)((end - a0 + 3) >> 2) : 0;
+          const double v = has ? s_rv[k] : 0.0;
+          const int32_t gi = LOOPS && has ? (int32_t)(tile * kCycTile + s_ri[k] + a.lo) : -1;
+          const int maxn = __reduce_max_sync(0xffffffffu, nvec);
+          for (int b0 = 0; b0 < maxn; b0 += 16) {
+            const int vb = b0 + sub;
+            int4 x0 = make_int4(0, 0, 0, 0), x1 = make_int4(0, 0, 0, 0);
+            if (vb < nvec) x0 = ld_col4(col + a0 + 4 * (int64_t)vb, pol);
+            if (vb + 8 < nvec) x1 = ld_col4(col + a0 + 4 * (int64_t)(vb + 8), pol);
+            push_group_cold<LOOPS>(a, rep, hot_lim, copy, x0, a0 + 4 * (int64_t)vb, beg, end, vb < nvec,
+                                   gi, v, fpol, ccb, cce, s_coff, lane);
+            push_group_cold<LOOPS>(a, rep, hot_lim, copy, x1, a0 + 4 * (int64_t)(vb + 8), beg, end,
+                                   vb + 8 < nvec, gi, v, fpol, ccb, cce, s_coff, lane);
+          }
+        } else if (k < nmid) {
           const int64_t beg = s_rb[k], end = beg + s_ro[k], a0 = beg & ~3ll;
           const int nvec = (int)((end - a0 + 3) >> 2);   // <= 33
           const double v = s_rv[k];
@@ -436,6 +558,10 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       }
     }
     __syncthreads();
+  }
+  if (COLD && lane == 0) {  // the warp's open chunks: their fill for k_cold_apply
+    for (int b = 0; b < a.cold_nbins; b++)
+      if (cce[b] > 0) a.cold_fill[(s_coff[b] + cce[b]) / kColdChunk - 1] = kColdChunk - (cce[b] - ccb[b]);
   }
   // ---- this CTA's sums (fixed order inside the CTA) -> ppartials[blockIdx.x]
   acc_tk = warp_sum(acc_tk);
@@ -540,6 +666,58 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   vs->ticket = 0;
 }
 
+// Cold bins, after the cycle: the records of bin 0, then bin 1, ... (every block takes a contiguous
+// share of each bin, so the grid walks the bins together and the slice of F being updated stays
+// in L2), each a RED into F; the last block rewinds the bins. Chunks past their fill are skipped.
+__global__ void __launch_bounds__(256) k_cold_apply(double *__restrict__ F, const ColdRec *__restrict__ rec,
+                                                    const int64_t *__restrict__ off,
+                                                    unsigned long long *top,
+                                                    const int32_t *__restrict__ fill, int nbins) {
+  __shared__ bool s_last;
+  const uint64_t pol = policy_evict_first();
+  for (int b = 0; b < nbins; b++) {
+    const int64_t m = (int64_t)*reinterpret_cast<volatile unsigned long long *>(top + 16 * b);
+    if (m == 0) continue;
+    const int64_t base = off[b];
+    const int64_t per = (m + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * per, r1 = r0 + per < m ? r0 + per : m;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+      const int64_t gr = base + r;   // regions are chunk-aligned
+      if ((int)(r % kColdChunk) >= __ldg(fill + gr / kColdChunk)) continue;
+      int4 q;
+      asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                   : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+                   : "l"(rec + gr), "l"(pol));
+      red_add_f64(F + q.x, __hiloint2double(q.w, q.z));
+    }
+  }
+  __syncthreads();
+  unsigned int *ticket = reinterpret_cast<unsigned int *>(top + 16 * kColdBins);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  if (threadIdx.x < nbins) top[16 * threadIdx.x] = 0ull;
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+// cold-target counts per bin (static: the CSR), for the bin regions of the arena
+__global__ void k_cold_hist(const int32_t *__restrict__ col, int64_t L, int64_t cold_lo, int shift,
+                            unsigned long long *cnt) {
+  __shared__ unsigned int h[kColdBins];
+  if (threadIdx.x < kColdBins) h[threadIdx.x] = 0u;
+  __syncthreads();
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = col[k];
+    if (j >= cold_lo) atomicAdd(&h[(j - cold_lo) >> shift], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < kColdBins && h[threadIdx.x]) atomicAdd(cnt + threadIdx.x, (unsigned long long)h[threadIdx.x]);
+}
+
 }  // namespace
 
 // number of hot ids (replicated accumulators) for this graph, or -1 when off
@@ -547,9 +725,52 @@ static int hot_shift_of(const Graph &g) {
   return (g.reordered && g.hot_acc && !g.partitioned && g.hot_count > 0) ? (int)g.hot_count : -1;
 }
 
+static int cycle_grid(const Graph &g);
+
+// cold bins: the arena of bin regions (cold in-links of the slice + one chunk per warp of the
+// grid), chunk fills and counters; once per graph (the CSR is static)
+static di_status prepare_cold(Graph &g) {
+  if (g.cold_rec || g.partitioned || !(g.cold_lo < g.n)) return DI_OK;
+  const int64_t ncold = g.n - g.cold_lo;
+  int s = kColdMinShift;
+  while ((((ncold + (1ll << s) - 1) >> s)) > kColdBins) s++;
+  g.cold_shift = s;
+  g.cold_nbins = (int)((ncold + (1ll << s) - 1) >> s);
+  unsigned long long *cnt = nullptr;
+  DI_CK(dmalloc(&cnt, kColdBins * 8));
+  DI_CK(cudaMemsetAsync(cnt, 0, kColdBins * 8, g.stream));
+  if (g.l > 0)
+    k_cold_hist<<<g.num_sms * 8, 256, 0, g.stream>>>(g.col, g.l, g.cold_lo, s, cnt);
+  std::vector<unsigned long long> hc(kColdBins);
+  DI_CK(cudaMemcpyAsync(hc.data(), cnt, kColdBins * 8, cudaMemcpyDeviceToHost, g.stream));
+  DI_CK(cudaStreamSynchronize(g.stream));
+  dfree(cnt);
+  const int64_t slack = (int64_t)cycle_grid(g) * (kAsyncThreads / 32) * kColdChunk;
+  std::vector<int64_t> off(kColdBins + 1, 0);
+  for (int b = 0; b < g.cold_nbins; b++) {
+    const int64_t cap = ((int64_t)hc[b] + slack + kColdChunk - 1) / kColdChunk * kColdChunk;
+    if (cap >= (1ll << 31)) return DI_ENOMEM;   // positions inside a bin region are 32-bit
+    off[b + 1] = off[b] + cap;
+  }
+  for (int b = g.cold_nbins; b < kColdBins; b++) off[b + 1] = off[b];
+  const int64_t total = off[g.cold_nbins];
+  DI_CK(dmalloc(&g.cold_rec, (size_t)total * sizeof(ColdRec)));
+  DI_CK(dmalloc(&g.cold_fill, (size_t)(total / kColdChunk + 1) * 4));
+  DI_CK(dmalloc(&g.cold_off, (kColdBins + 1) * 8));
+  DI_CK(cudaMemcpyAsync(g.cold_off, off.data(), (kColdBins + 1) * 8, cudaMemcpyHostToDevice, g.stream));
+  DI_CK(dmalloc(&g.cold_top, (kColdBins + 1) * 16 * 8));
+  DI_CK(cudaMemsetAsync(g.cold_top, 0, (kColdBins + 1) * 16 * 8, g.stream));
+  DI_CK(cudaStreamSynchronize(g.stream));
+  return DI_OK;
+}
+
 // called by di_solve before any launch or capture (allocations are not capturable)
-di_status prepare_cycle(Graph &g) {
-  if (getenv("DI_CYC_TIMES") && !g.cyc_times)
+di_status prepare_cycle(Graph &g, bool async) {
+  if (async) {
+    di_status cs = prepare_cold(g);
+    if (cs != DI_OK) return cs;
+  }
+  if (g.cycle_times && !g.cyc_times)
     DI_CK(dmalloc(&g.cyc_times, (size_t)64 * kMaxSlices * 2 * sizeof(unsigned long long)));
   const int hot = hot_shift_of(g);
   if (hot >= 0 && !g.rep) {
@@ -582,13 +803,12 @@ di_status prepare_cycle(Graph &g) {
 
 static int cycle_grid(const Graph &g) {
   static const int occ = occupancy(k_cycle<false, false>, kAsyncThreads);  // once, thread-safe
-  // DI_CYC_GRID_DIV=k (experiments with emulated ranks on one GPU): 1/k of the grid per rank, so
-  // the ranks' cycles run side by side at similar rates as they would on k GPUs
-  static const int div = getenv("DI_CYC_GRID_DIV") ? std::max(1, atoi(getenv("DI_CYC_GRID_DIV"))) : 1;
-  return std::max(1, std::min(g.num_sms * occ, kMaxSlices) / div);
+  // option cycle_grid_div = k (experiments with emulated ranks on one GPU): 1/k of the grid per
+  // rank, so the ranks' cycles run side by side at similar rates as they would on k GPUs
+  return std::max(1, std::min(g.num_sms * occ, kMaxSlices) / std::max(1, g.grid_div));
 }
 
-// DI_CYC_TIMES diagnostic: per cycle, the spread of CTA start and end times (stderr)
+// option cycle_times (diagnostic): per cycle, the spread of CTA start and end times (stderr)
 void report_cycle_times(Graph &g, int64_t cycles) {
   if (!g.cyc_times || cycles <= 0) return;
   const int grid = cycle_grid(g);
@@ -613,7 +833,7 @@ void report_cycle_times(Graph &g, int64_t cycles) {
     tail += e1 - emed;
     busy += b / grid;
   }
-  fprintf(stderr, "[DI_CYC_TIMES] %lld cycles, grid %d: span %.1f us, start skew %.1f us, tail (max - median end) %.1f us, mean CTA busy %.1f us\n",
+  fprintf(stderr, "[di cycle_times] %lld cycles, grid %d: span %.1f us, start skew %.1f us, tail (max - median end) %.1f us, mean CTA busy %.1f us\n",
           (long long)nc, grid, span / nc / 1e3, skew / nc / 1e3, tail / nc / 1e3, busy / nc / 1e3);
 }
 
@@ -639,6 +859,16 @@ void launch_cycle_test(Graph &g, double *rec_T, double *rec_v, int64_t *launches
 
 void launch_cycle(Graph &g, int64_t *launches) {
   SweepArgs a = sweep_args(g, 0);
+  const bool cold = g.cold_rec && !g.partitioned;
+  if (cold) {
+    a.cold_lo = g.cold_lo;
+    a.cold_shift = g.cold_shift;
+    a.cold_nbins = g.cold_nbins;
+    a.cold_rec = g.cold_rec;
+    a.cold_off = g.cold_off;
+    a.cold_top = g.cold_top;
+    a.cold_fill = g.cold_fill;
+  }
   a.ntiles = (g.n + kCycTile - 1) / kCycTile;
   const bool dist = g.partitioned;
   DistArgs x{};
@@ -656,6 +886,14 @@ void launch_cycle(Graph &g, int64_t *launches) {
       k_cycle<true, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
     else
       k_cycle<false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+  } else if (cold) {
+    if (g.has_loops)
+      k_cycle<true, false, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+    else
+      k_cycle<false, false, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+    k_cold_apply<<<g.num_sms * 8, 256, 0, g.stream>>>(g.F, g.cold_rec, g.cold_off, g.cold_top,
+                                                      g.cold_fill, g.cold_nbins);
+    *launches += 1;
   } else {
     if (g.has_loops)
       k_cycle<true, false><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 
@@ -99,8 +100,17 @@ __global__ void k_window_peers(ncclWindow_t w, int world, char **out) {
 // ncclCommInitRank with the same id is not supported), so every graph uploaded with the same
 // (id, rank, world) shares one, e.g. the e2e uploads of bench.py at N > 1. They live until the
 // process exits and are never destroyed (NCCL may already be unloaded at static destruction).
+// The map's mutex is held only to find / insert an entry; the collective ncclCommInitRank runs
+// outside it, once per entry (std::call_once), so ranks driven by threads of one process do not
+// wait for each other's initialisation behind the mutex.
+struct CommEntry {
+  std::once_flag once;
+  ncclComm_t comm = nullptr;
+  ncclResult_t res = ncclSuccess;
+};
 std::mutex g_comm_mu;
-std::map<std::string, ncclComm_t> *g_comms = new std::map<std::string, ncclComm_t>();
+std::map<std::string, std::shared_ptr<CommEntry>> *g_comms =
+    new std::map<std::string, std::shared_ptr<CommEntry>>();
 
 struct NcclComm : Comm {
   ncclComm_t comm = nullptr;   // shared (g_comms), not owned
@@ -325,19 +335,19 @@ di_status make_nccl_comm(const void *unique_id, int rank, int world, Comm **out)
   memcpy(&id, unique_id, sizeof(id));
   std::string key(reinterpret_cast<const char *>(&id), sizeof(id));
   key += ":" + std::to_string(rank) + "/" + std::to_string(world);
-  std::lock_guard<std::mutex> lk(g_comm_mu);
-  ncclComm_t comm = nullptr;
-  auto it = g_comms->find(key);
-  if (it != g_comms->end()) {
-    comm = it->second;
-  } else {
-    ncclResult_t r = a.CommInitRank(&comm, world, id, rank);
-    if (r != ncclSuccess) {
-      set_error(std::string("ncclCommInitRank: ") + a.GetErrorString(r));
-      return DI_ENCCL;
-    }
-    (*g_comms)[key] = comm;
+  std::shared_ptr<CommEntry> e;
+  {
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    std::shared_ptr<CommEntry> &slot = (*g_comms)[key];
+    if (!slot) slot = std::make_shared<CommEntry>();
+    e = slot;
   }
+  std::call_once(e->once, [&] { e->res = a.CommInitRank(&e->comm, world, id, rank); });
+  if (e->res != ncclSuccess) {
+    set_error(std::string("ncclCommInitRank: ") + a.GetErrorString(e->res));
+    return DI_ENCCL;
+  }
+  ncclComm_t comm = e->comm;
   NcclComm *c = new NcclComm();
   c->rank = rank;
   c->world = world;

@@ -44,6 +44,23 @@ constexpr int kRepCopies = DI_HOT_COPIES;  // copies of each hot accumulator (ch
 constexpr int kRepStride = 16;             // doubles between accumulators: one 128-B line each
 constexpr double kReplShare = 0.0005;
 
+// Cold bins (async.cu): on one GPU, when F is larger than kColdF_L2 times the L2,
+// the relabelling puts a first tier of kColdHotL2 x L2 bytes of nodes (by in-degree) right after
+// the hot ids; REDs to them stay in L2, and a push to a node beyond them (a "cold" target: mostly
+// an L2 miss, ~22 G random REDs/s into 1 GB) is appended as a 16-B record to the bin of its
+// slice of 2^shift nodes (at most kColdBins slices), then applied slice by slice after the cycle
+// (k_cold_apply: the slice's F lines stay in L2 while its records stream through).
+constexpr int kColdBins = 32;
+constexpr int kColdChunk = 64;          // records per warp chunk (one 1 KB run of a bin)
+constexpr double kColdF_L2 = 2.0;
+constexpr double kColdHotL2 = 0.5;
+constexpr int kColdMinShift = 16;
+struct __align__(16) ColdRec {
+  int32_t j;     // internal target id (-1: none)
+  int32_t pad;
+  double v;
+};
+
 enum BinId { BIN_T = 0, BIN_G = 1, BIN_W = 2, BIN_C = 3 };
 
 // Pull (CSC) variant, SURVEY §8(a) a5': static bins of target rows by in-degree.
@@ -74,6 +91,25 @@ struct DistBounds {
   int world;
   int64_t b[kMaxWorld + 1];
 };
+
+// Process-wide tuning / diagnostic options (di_set_option, include/di.h). Upload-time options are
+// copied into each graph by di_graph_upload; the rest are read when used.
+struct Options {
+  int red_hint = 1;          // "red_hint": L2 evict_last policy on the push's REDs into F
+  int push_occ = 4;          // "push_occ": k_push resident blocks per SM
+  double auto_ratio = 0.35;  // "auto_ratio": DI_AUTO pulls a sweep with links(S) > ratio * L
+  int stripes = 0;           // "stripes": relabelling stripes (0 auto, 1 plain degree order)
+  int hot_acc = 1;           // "hot_acc": replicated accumulators for the hottest targets
+  double repl_share = kReplShare;  // "repl_share": top in-degree share that turns them on
+  int cold_bins = -1;        // "cold_bins": -1 auto (F > 2 L2), 0 off, 1 on (one GPU, DI_ASYNC)
+  int64_t cold_tier = 0;     // "cold_tier": first-tier size in nodes (0: half the L2 in bytes)
+  int cycle_grid_div = 1;    // "cycle_grid_div": 1/k of k_cycle's grid (emulated-rank studies)
+  int cycle_times = 0;       // "cycle_times": per-CTA start/end times of each cycle (stderr)
+  int p2p = 1;               // "p2p": peer-memory inboxes for the partitioned exchange
+  int p2p_force = 0;         // "p2p_force": create the inbox on a one-rank communicator too
+  int build_trace = 0;       // "build_trace": host timestamps of the build phases (stderr)
+};
+Options options();           // a snapshot of the current options
 
 // Device-resident sweep state. Every field is written only by the "last block" of the
 // select kernel (the finaliser) or by the host between solves, so kernels never race on it.
@@ -138,8 +174,8 @@ struct Graph {
   int64_t l_global = 0;
   bool has_loops = false;
   bool has_csc = false;
-  int push_occ = 4;         // k_push min blocks per SM (DI_PUSH_OCC)
-  int red_hint = 1;         // L2 evict_last hint on the push's REDs into F (DI_RED_HINT=0 disables)
+  int push_occ = 4;         // k_push min blocks per SM (option push_occ)
+  int red_hint = 1;         // L2 evict_last hint on the push's REDs into F (option red_hint)
   int rank = 0, world = 1;
   bool partitioned = false;  // built with a communicator (dist.cu path), even of one rank
   bool local_links = false;  // DI_LOCAL_LINKS: this rank's links only, range [local_lo, local_hi)
@@ -152,17 +188,31 @@ struct Graph {
                                        // then 8 doubles (sent, applied, r_loc, r_loc_sync, r_sync)
   // locality relabelling: internal id = new_of[user id]; user id = old_of[internal id]
   bool reordered = false;
-  int stripes = 0;           // relabelling stripes (DI_STRIPES; 0 = auto: stripes of ~1024 nodes,
+  int stripes = 0;           // relabelling stripes (option stripes; 0 = auto: stripes of ~1024 nodes,
                              // 1 = plain degree order)
   int64_t hot_count = 0;     // skewed graphs: the hot_count hottest nodes are internal ids 0..
   double alpha = 1.0;        // DI-SOP threshold scale
-  double repl_share = kReplShare;  // top in-degree share that turns hot placement on (DI_REPL_SHARE)
-  int hot_acc = 1;           // DI_ASYNC: replicated accumulators for the hottest targets (DI_HOT_ACC)
+  double repl_share = kReplShare;  // top in-degree share that turns hot placement on (option repl_share)
+  int hot_acc = 1;           // replicated accumulators for the hottest targets, every single-GPU
+                             // push schedule and PI' (option hot_acc)
+  int grid_div = 1;          // option cycle_grid_div
+  int cycle_times = 0;       // option cycle_times
+  int p2p_opt = 1, p2p_force = 0;  // options p2p, p2p_force
   double *rep = nullptr;     // replicated accumulators, then hv[kHotRanks] (async.cu)
-  unsigned long long *cyc_times = nullptr;  // DI_CYC_TIMES diagnostic: per-CTA start/end per cycle
+  unsigned long long *cyc_times = nullptr;  // option cycle_times: per-CTA start/end per cycle
   int64_t *hub_items = nullptr;  // DI_ASYNC hub items: (row, first link, end link) triples
   int n_hub = 0;
   int64_t max_indeg = 0;     // largest in-degree (set by the relabelling pass)
+  // cold bins (async.cu): internal ids >= cold_lo are cold (cold_lo == n: off)
+  int cold_mode = -1;        // -1 auto (F > kColdF_L2 x L2), 0 off, 1 on (di_set_option)
+  int64_t cold_tier = 0;     // > 0: first-tier size in nodes instead of kColdHotL2 x L2 / 8
+  int64_t l2_bytes = 0;
+  int64_t cold_lo = INT64_MAX;
+  int cold_shift = 0, cold_nbins = 0;
+  ColdRec *cold_rec = nullptr;     // arena: bin b's region starts at record cold_off[b]
+  int64_t *cold_off = nullptr;     // device [kColdBins + 1]
+  unsigned long long *cold_top = nullptr;  // device: records reserved per bin (one line each)
+  int32_t *cold_fill = nullptr;    // device: records written per chunk, chunk k of the arena
   int32_t *new_of = nullptr, *old_of = nullptr;
   double *Bperm = nullptr;   // B in internal order (custom B)
   double *xfer = nullptr;    // scratch for permuted copies
@@ -180,7 +230,7 @@ struct Graph {
   PullEntry *re[kPullBins] = {nullptr, nullptr, nullptr, nullptr};  // PI' static out-rows
   int64_t re_count[kPullBins] = {0, 0, 0, 0};
   double *cmp_partials = nullptr;
-  double auto_ratio = 0.35; // DI_AUTO threshold on links(S_n)/L (DI_AUTO_RATIO)
+  double auto_ratio = 0.35; // DI_AUTO threshold on links(S_n)/L (option auto_ratio)
   // state
   double *F = nullptr, *H = nullptr;
   double *S = nullptr;       // pull mode: dense per-node sent value
@@ -275,7 +325,7 @@ void launch_loop_cond(Graph &g, cudaGraphConditionalHandle h);
 void report_cycle_times(Graph &g, int64_t cycles);
 void launch_cycle(Graph &g, int64_t *launches);
 void launch_cycle_test(Graph &g, double *rec_T, double *rec_v, int64_t *launches);
-di_status prepare_cycle(Graph &g);
+di_status prepare_cycle(Graph &g, bool async);
 di_status alloc_pull(Graph &g);
 di_status alloc_dist(Graph &g);
 // dist.cu

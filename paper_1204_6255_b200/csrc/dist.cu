@@ -491,10 +491,10 @@ di_status alloc_dist(Graph &g) {
   // on the outcome, else all fall back to exchange())
   g.p2p = false;
   g.inbox.clear();
-  // (DI_P2P=0 disables it; DI_P2P_FORCE=1 creates it on one rank too, which exercises the
+  // (option p2p = 0 disables it; p2p_force = 1 creates it on one rank too, which exercises the
   // symmetric-memory calls with nothing to send)
-  const bool want = G > 1 || (getenv("DI_P2P_FORCE") && atoi(getenv("DI_P2P_FORCE")) == 1);
-  if (want && !(getenv("DI_P2P") && atoi(getenv("DI_P2P")) == 0)) {
+  const bool want = G > 1 || g.p2p_force == 1;
+  if (want && g.p2p_opt != 0) {
     int64_t mx = 1;
     for (int p = 0; p < G; p++) mx = std::max<int64_t>(mx, g.bounds.b[p + 1] - g.bounds.b[p]);
     g.icap = mx;
@@ -554,7 +554,7 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
                            int64_t max_sweeps, uint32_t flags, di_stats *st) {
   const int G = g.world, me = g.rank;
   if (!g.p2p || !g.ring) {
-    set_error("di_solve: DI_DIST_ASYNC needs the peer-memory inboxes (see DI_P2P)");
+    set_error("di_solve: DI_DIST_ASYNC needs the peer-memory inboxes (option p2p)");
     return DI_EINVAL;
   }
   const bool resume = flags & DI_RESUME;

@@ -44,10 +44,24 @@ __global__ void k_validate(const int32_t *__restrict__ src, const int32_t *__res
 // maps onto fewer slices (C4: 16384 stripes 65.7 ms, 16411 63.1 ms). Multi-GPU: the sorted order
 // is (owner range, rank) and every range is placed on its own, so a rank's internal ids stay in
 // the node range it owns.
+// Two-tier placement (graphs whose F exceeds the L2 several times, DESIGN.md §6 "cold bins"): the
+// first tier[g] ranks after the hot ones fill the prefix [lo + hot, lo + hot + tier) — striped
+// among themselves (stripes2 stripes) — so that "hot target" is the plain test j < cold_lo, and
+// the remaining ranks are striped over the rest of the range.
 struct PlaceParams {
   int64_t hot[kMaxWorld];
   int64_t stripes[kMaxWorld];
+  int64_t tier[kMaxWorld];
+  int64_t stripes2[kMaxWorld];
 };
+
+__device__ __forceinline__ int64_t stripe_pos(int64_t q, int64_t m, int64_t P) {
+  if (P < 1) P = 1;
+  if (P > m) P = m;
+  const int64_t M = m / P, rem = m % P;
+  const int64_t s = q % P, idx = q / P;
+  return s * M + (s < rem ? s : rem) + idx;
+}
 
 __global__ void k_place(const int32_t *__restrict__ sorted_old, int64_t n, DistBounds bd,
                         PlaceParams pp, int32_t *__restrict__ new_of, int32_t *__restrict__ old_of) {
@@ -57,16 +71,14 @@ __global__ void k_place(const int32_t *__restrict__ sorted_old, int64_t n, DistB
     while (g + 1 < bd.world && r >= bd.b[g + 1]) g++;
     const int64_t lo = bd.b[g], rr = r - lo, hot = pp.hot[g];
     int64_t k;
+    const int64_t tier = pp.tier[g];
     if (rr < hot) {
       k = lo + rr;
+    } else if (rr < hot + tier) {   // first tier: striped inside the prefix
+      k = lo + hot + stripe_pos(rr - hot, tier, pp.stripes2[g]);
     } else {
-      const int64_t m = bd.b[g + 1] - lo - hot, q = rr - hot;
-      int64_t P = pp.stripes[g];
-      if (P < 1) P = 1;
-      if (P > m) P = m;
-      const int64_t M = m / P, rem = m % P;
-      const int64_t s = q % P, idx = q / P;
-      k = lo + hot + s * M + (s < rem ? s : rem) + idx;
+      const int64_t m = bd.b[g + 1] - lo - hot - tier, q = rr - hot - tier;
+      k = lo + hot + tier + stripe_pos(q, m, pp.stripes[g]);
     }
     const int32_t o = sorted_old[r];
     new_of[o] = (int32_t)k;
@@ -221,9 +233,9 @@ __global__ void k_swap_keys(const uint64_t *__restrict__ in, int64_t L, int b,
   }
 }
 
-// DI_BUILD_TRACE=1: host timestamps of the build phases on stderr (diagnostics)
+// option build_trace = 1: host timestamps of the build phases on stderr (diagnostics)
 void btrace(const char *what) {
-  static const bool on = getenv("DI_BUILD_TRACE") && atoi(getenv("DI_BUILD_TRACE"));
+  const bool on = options().build_trace != 0;
   if (!on) return;
   static thread_local std::chrono::steady_clock::time_point t0;
   const auto now = std::chrono::steady_clock::now();
@@ -362,7 +374,9 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   }
   const bool local = g.local_links;   // DI_LOCAL_LINKS: this rank's links, sources in its range
   const int64_t s_lo = local ? g.local_lo : 0, s_hi = local ? g.local_hi : n;
-  if (L > 0)
+  // a range outside [0, n) fails on every rank, in the collective below
+  const bool bad_range = local && !(s_lo >= 0 && s_lo < s_hi && s_hi <= n);
+  if (L > 0 && !bad_range)
     k_validate<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, n, s_lo, s_hi, badb, indeg);
   unsigned long long bad = 0;
   DI_CK(cudaMemcpyAsync(&bad, badb, 8, cudaMemcpyDeviceToHost, st));
@@ -370,15 +384,21 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   btrace("sync1");
   if (local) {  // every rank learns whether any rank failed (no rank may leave a collective)
     int64_t *flag = reinterpret_cast<int64_t *>(small + 48);
-    const int64_t mine = bad != ~0ull ? 1 : 0;
+    const int64_t mine = (bad != ~0ull || bad_range) ? 1 : 0;
     DI_CK(cudaMemcpyAsync(flag, &mine, 8, cudaMemcpyHostToDevice, st));
     di_status cs = g.comm->allreduce_i64(flag, 1, st);
     if (cs != DI_OK) return cs;
     int64_t any = 0;
     DI_CK(cudaMemcpyAsync(&any, flag, 8, cudaMemcpyDeviceToHost, st));
     DI_CK(cudaStreamSynchronize(st));
+    if (bad_range) {
+      set_error("di_graph_upload: DI_LOCAL_LINKS needs 0 <= dist->lo < dist->hi <= n, got [" +
+                std::to_string(s_lo) + ", " + std::to_string(s_hi) + ")");
+      return DI_EINVAL;
+    }
     if (any && bad == ~0ull) {
-      set_error("di_graph_upload: another rank's link list failed validation (DI_LOCAL_LINKS)");
+      set_error("di_graph_upload: another rank's link list or range failed validation "
+                "(DI_LOCAL_LINKS)");
       return DI_EINVAL;
     }
   }
@@ -478,12 +498,28 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     bool skewed = !g.partitioned && g.hot_acc && L > 0 &&
                   (double)top > g.repl_share * (double)L && n > 4 * kHotRanks;
     g.hot_count = skewed ? kHotRanks : 0;
+    // cold bins (single GPU, F several times the L2): a first tier of ~kColdHotL2 of the L2 in
+    // nodes takes the prefix after the hot ids; targets beyond it are "cold" (async.cu)
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g.device);
+    if (l2 <= 0) l2 = 126 << 20;
+    g.l2_bytes = l2;
+    int64_t tier = 0;
+    if (!g.partitioned && g.cold_mode != 0 &&
+        (g.cold_mode == 1 || (double)n * 8.0 > kColdF_L2 * (double)l2)) {
+      tier = std::min<int64_t>(n - g.hot_count, (int64_t)(kColdHotL2 * (double)l2 / 8.0));
+      if (g.cold_tier > 0) tier = std::min<int64_t>(n - g.hot_count, g.cold_tier);
+      if (tier < 0) tier = 0;
+    }
+    g.cold_lo = (tier > 0 && g.hot_count + tier < n) ? g.hot_count + tier : n;
     PlaceParams pp;
     for (int r = 0; r < world; r++) {
       const int64_t m = bd.b[r + 1] - bd.b[r];
       pp.hot[r] = (r == 0) ? g.hot_count : 0;
+      pp.tier[r] = (r == 0 && g.cold_lo < n) ? tier : 0;
+      pp.stripes2[r] = prime_at_most(std::max<int64_t>(1, pp.tier[r] >> 10));
       pp.stripes[r] = g.stripes > 0 ? (int64_t)g.stripes
-                                     : prime_at_most(std::max<int64_t>(1, (m - pp.hot[r]) >> 10));
+                                     : prime_at_most(std::max<int64_t>(1, (m - pp.hot[r] - pp.tier[r]) >> 10));
     }
     k_place<<<grid_for(n, sms), 256, 0, st>>>(sorted, n, bd, pp, g.new_of, g.old_of);
     g.reordered = true;

@@ -33,12 +33,21 @@ struct SweepArgs {
   int64_t t0, t1;
   int blk, blocks;
   double *ppartials;    // 8 per finaliser slice: q, s, e, taken, sel, nd, links, 0
-  int hot_shift;        // DI_ASYNC replicated hot accumulators (async.cu), -1 = off
+  int hot_shift;        // replicated hot accumulators: number of hot ids, -1 = off (every
+                        // single-GPU push schedule and PI' use them; top share > kReplShare = 0.05 %)
   double *rep;
   const int64_t *hub;   // DI_ASYNC hub items (async.cu), n_hub of them
   int n_hub;
-  unsigned long long *times;  // DI_CYC_TIMES diagnostic (async.cu), nullptr = off
+  unsigned long long *times;  // option cycle_times diagnostic (async.cu), nullptr = off
   double *rec_T, *rec_v;      // di_test_cycle records (async.cu, TEST instantiation only)
+  // cold bins (async.cu COLD instantiation): targets j >= cold_lo become records of bin
+  // (j - cold_lo) >> cold_shift in region cold_off[b] of the arena
+  int64_t cold_lo;
+  int cold_shift, cold_nbins;
+  ColdRec *cold_rec;
+  const int64_t *cold_off;
+  unsigned long long *cold_top;
+  int32_t *cold_fill;
 };
 
 // What one sweep moved: r_{n+1} = q + s (a2), dangling absorption e, counters.
@@ -267,8 +276,8 @@ __device__ __forceinline__ void finalize_sweep(const SweepArgs &a, int P, int nt
 // Column ids are read as aligned int4 groups (one LSU instruction per 4 links); elements of a
 // group outside [beg, end) are masked. The col array carries 8 elements of tail padding.
 // Each valid target j != i receives v with a fire-and-forget RED.
+// Hot ids j < hot_lim (replicated accumulators; 0 when off) go to copy `copy` of j.
 template <bool LOOPS>
-// Hot ids j < hot_lim (replicated accumulators, async.cu; 0 when off) go to copy `copy` of j.
 __device__ __forceinline__ void red_group(double *__restrict__ F, double *__restrict__ rep,
                                           int32_t hot_lim, int copy, int4 x, int64_t p0,
                                           int64_t beg, int64_t end, int32_t gi, double v,
@@ -355,6 +364,13 @@ inline SweepArgs sweep_args(Graph &g, int test_mode, int blk = 0, int blocks = 1
   a.times = nullptr;
   a.rec_T = nullptr;
   a.rec_v = nullptr;
+  a.cold_lo = INT64_MAX;
+  a.cold_shift = 0;
+  a.cold_nbins = 0;
+  a.cold_rec = nullptr;
+  a.cold_off = nullptr;
+  a.cold_top = nullptr;
+  a.cold_fill = nullptr;
   a.F = g.F;
   a.H = g.H;
   a.deg = g.deg;

@@ -65,7 +65,7 @@ def test_reorder_relabelling(name):
     old_of = g.test_perm()
     indeg = np.bincount(dst, minlength=n)
     ranked = np.argsort(-indeg, kind="stable")           # rank r -> caller id
-    # placement (graph_build.cu k_place): on a skewed graph (top in-degree > 0.25 % of the links)
+    # placement (graph_build.cu k_place): on a skewed graph (top in-degree > 0.05 % of the links, kReplShare)
     # the 64 hottest ranks come first; the rest in P stripes, P = largest prime <= (n - hot)/1024
     hot = 64 if (indeg.max() > 0.0005 * len(src) and n > 256) else 0
 

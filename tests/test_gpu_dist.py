@@ -311,6 +311,17 @@ def test_local_links(G):
 
     run_local_group(2, gap)
 
+    def empty_range(r, grp):   # rank 1 passes an empty range: both ranks fail, neither hangs
+        lo, hi = [(0, n), (n, n)][r]
+        m = (src >= lo) & (src < hi)
+        with pytest.raises(di.DIError) as ei:
+            di.Graph(src[m], dst[m], n, rank=r, world=2, group=grp, local_range=(lo, hi))
+        assert ei.value.status == di.DI_EINVAL
+        return str(ei.value)
+
+    msgs = run_local_group(2, empty_range)
+    assert "another rank" in msgs[0] and "0 <= dist->lo < dist->hi" in msgs[1]
+
 
 def test_cyc_neumann_partitioned():
     """T7 on partitions: bulk DI-CYC without loops is the Neumann series, F_n = P^n B and
@@ -465,9 +476,8 @@ def test_invalid_partitioned_arguments(monkeypatch):
 
     from paper_1204_6255_b200.dist import run_local_group
     run_local_group(2, dist_async_flags)
-    monkeypatch.setenv("DI_P2P", "0")
-    run_local_group(2, no_inbox)
-    monkeypatch.delenv("DI_P2P")
+    with di.option("p2p", 0):
+        run_local_group(2, no_inbox)
     g = di.Graph(src, dst, n)                          # one GPU: the flag is ignored
     assert g.solve(asynchronous=True, dist_async=True)["converged"] == 1
     g.free()
@@ -488,36 +498,39 @@ def test_nccl_backend_single_rank(asynchronous, monkeypatch):
     """The NCCL backend for real on one GPU: a communicator of one rank (ncclCommInitRank,
     ncclAllReduce, grouped send/recv with no peers) runs the whole partitioned protocol with
     nothing to exchange; C1 to the north_star gate, and the same through a group of one. With
-    DI_P2P_FORCE=1 the upload also creates the peer-memory inbox on the one rank (ncclMemAlloc,
+    the option p2p_force = 1 the upload also creates the peer-memory inbox on the one rank (ncclMemAlloc,
     a symmetric ncclCommWindowRegister, the LSA pointer read on the device), and every sweep
     takes the fused path with no peers."""
     need_gpu()
-    monkeypatch.setenv("DI_P2P_FORCE", "1")
     import paper_1204_6255_b200 as di
-    src, dst, n = digen.make("c1", seed=2)
-    Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
-    nid = di.nccl_unique_id()
-    g = di.Graph(src, dst, n, rank=0, world=1, nccl_id=nid)
-    assert g.range() == (0, n)
-    st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous)
-    assert st["converged"] == 1 and st["exchange_entries"] == 0
-    assert st["p2p_exchanges"] == st["sweeps"]          # the window exists
-    assert l1(g.history().cpu().numpy(), Ho) <= 1e-9
-    st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous, exchange="dense")  # one rank: no-op
-    assert st["converged"] == 1 and st["dense_exchanges"] == 0
-    assert g.residual() <= 1e-10
-    g2 = di.Graph(src, dst, n, rank=0, world=1, nccl_id=nid)   # same id: the same communicator
-    assert g2.solve(d=D, tol=1e-10, asynchronous=asynchronous)["converged"] == 1
-    g.free()
-    g2.free()
-    g3 = di.Graph(src, dst, n, rank=0, world=1, nccl_id=nid)   # ... also after both were freed
-    st = g3.solve(d=D, tol=1e-10, asynchronous=asynchronous)
-    assert st["converged"] == 1 and l1(g3.history().cpu().numpy(), Ho) <= 1e-9
-    g3.free()
-    grp = di.LocalGroup(1)
-    g = di.Graph(src, dst, n, rank=0, world=1, group=grp)
-    st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous)
-    assert st["converged"] == 1
-    assert l1(g.history().cpu().numpy(), Ho) <= 1e-9
-    g.free()
-    grp.free()
+    di.set_option("p2p_force", 1)
+    try:
+        src, dst, n = digen.make("c1", seed=2)
+        Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
+        nid = di.nccl_unique_id()
+        g = di.Graph(src, dst, n, rank=0, world=1, nccl_id=nid)
+        assert g.range() == (0, n)
+        st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous)
+        assert st["converged"] == 1 and st["exchange_entries"] == 0
+        assert st["p2p_exchanges"] == st["sweeps"]          # the window exists
+        assert l1(g.history().cpu().numpy(), Ho) <= 1e-9
+        st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous, exchange="dense")  # one rank: no-op
+        assert st["converged"] == 1 and st["dense_exchanges"] == 0
+        assert g.residual() <= 1e-10
+        g2 = di.Graph(src, dst, n, rank=0, world=1, nccl_id=nid)   # same id: the same communicator
+        assert g2.solve(d=D, tol=1e-10, asynchronous=asynchronous)["converged"] == 1
+        g.free()
+        g2.free()
+        g3 = di.Graph(src, dst, n, rank=0, world=1, nccl_id=nid)   # ... also after both were freed
+        st = g3.solve(d=D, tol=1e-10, asynchronous=asynchronous)
+        assert st["converged"] == 1 and l1(g3.history().cpu().numpy(), Ho) <= 1e-9
+        g3.free()
+        grp = di.LocalGroup(1)
+        g = di.Graph(src, dst, n, rank=0, world=1, group=grp)
+        st = g.solve(d=D, tol=1e-10, asynchronous=asynchronous)
+        assert st["converged"] == 1
+        assert l1(g.history().cpu().numpy(), Ho) <= 1e-9
+        g.free()
+        grp.free()
+    finally:
+        di.set_option("p2p_force", 0)

@@ -9,7 +9,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
 src, dst, n = digen.make(cfg)
 s_d, t_d = torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda()
 for stripes, reorder in [(int(x), True) for x in (sys.argv[2] if len(sys.argv) > 2 else "4096,1,64,256,16384").split(",")]:
-    os.environ["DI_STRIPES"] = str(stripes)
+    __import__("paper_1204_6255_b200").set_option("stripes", float(str(stripes)))
     g = di.Graph(s_d, t_d, n, reorder=reorder)
     g.solve(d=0.85, tol=1e-10, asynchronous=True)
     sts = [g.solve(d=0.85, tol=1e-10, asynchronous=True) for _ in range(3)]

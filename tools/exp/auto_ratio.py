@@ -9,7 +9,7 @@ s_d, t_d = torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda()
 import paper_1204_6255_b200 as di
 res = {}
 for ratio in [0.35, 0.5, 0.65, 0.8, 2.0]:
-    os.environ["DI_AUTO_RATIO"] = str(ratio)
+    __import__("paper_1204_6255_b200").set_option("auto_ratio", float(str(ratio)))
     g = di.Graph(s_d, t_d, n, build_csc=True)
     g.solve(d=0.85, tol=1e-10, mode="auto")
     ts = []

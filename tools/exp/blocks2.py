@@ -1,4 +1,5 @@
-"""Experiment: block-ordered cycles with push / pull / auto sub-sweeps (+ agreement of H)."""
+"""(Round-1 experiment: some knobs it sets no longer exist; kept as the record of that run.)
+Experiment: block-ordered cycles with push / pull / auto sub-sweeps (+ agreement of H)."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)

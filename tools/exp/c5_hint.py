@@ -7,7 +7,7 @@ import digen
 import paper_1204_6255_b200 as di
 src, dst, n = digen.make("c5")
 for hint in ("1", "0"):
-    os.environ["DI_RED_HINT"] = hint
+    __import__("paper_1204_6255_b200").set_option("red_hint", float(hint))
     g = di.Graph(src, dst, n)
     st = g.solve(d=0.85, tol=1e-10, asynchronous=True, graph_loop=True)
     st = g.solve(d=0.85, tol=1e-10, asynchronous=True, graph_loop=True)

@@ -1,5 +1,5 @@
 """Experiment: k_cycle grid size vs order (a smaller grid is a narrower window of tiles in flight,
-closer to the paper's sequential cycle, with less parallelism). DI_CYC_GRID_DIV is read once per
+closer to the paper's sequential cycle, with less parallelism). the cycle_grid_div option is read per
 process, so each setting runs in its own process (see the loop in the gpurun command)."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -13,6 +13,6 @@ for cfg in sys.argv[1].split(","):
     g.solve(d=0.85, tol=1e-10, asynchronous=True, graph_loop=True)
     sts = [g.solve(d=0.85, tol=1e-10, asynchronous=True, graph_loop=True) for _ in range(5)]
     st = min(sts, key=lambda s: s["solve_ms"])
-    print(cfg, "div", os.environ.get("DI_CYC_GRID_DIV", "1"), "ms", round(st["solve_ms"], 3), "cycles", st["sweeps"],
+    print(cfg, "div", __import__("paper_1204_6255_b200").get_option("cycle_grid_div"), "ms", round(st["solve_ms"], 3), "cycles", st["sweeps"],
           "eq", round(st["equivalent_iterations"], 2), flush=True)
     g.free()

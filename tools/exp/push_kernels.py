@@ -1,4 +1,5 @@
-"""Experiment: k_push (0) vs k_push_b (1): solve time on a config for K in a list; H agreement."""
+"""(Round-1 experiment: some knobs it sets no longer exist; kept as the record of that run.)
+Experiment: k_push (0) vs k_push_b (1): solve time on a config for K in a list; H agreement."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)

@@ -1,4 +1,5 @@
-"""Experiment: k_push occupancy (DI_PUSH_OCC) and red hint on C4 block-ordered solve."""
+"""(Round-1 experiment: some knobs it sets no longer exist; kept as the record of that run.)
+Experiment: k_push occupancy (DI_PUSH_OCC) and red hint on C4 block-ordered solve."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
@@ -11,9 +12,9 @@ s_d, t_d = torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda()
 CASES = [(4, 1, 4096, 0), (4, 1, 4096, 1), (4, 1, 16384, 0), (4, 1, 16384, 1), (4, 1, 2048, 1), (4, 1, 8192, 1)]
 for occ, hint, stripes, rot in CASES:
     os.environ["DI_STRIPE_ROT"] = str(rot)
-    os.environ["DI_PUSH_OCC"] = str(occ)
-    os.environ["DI_RED_HINT"] = str(hint)
-    os.environ["DI_STRIPES"] = str(stripes)
+    __import__("paper_1204_6255_b200").set_option("push_occ", float(str(occ)))
+    __import__("paper_1204_6255_b200").set_option("red_hint", float(str(hint)))
+    __import__("paper_1204_6255_b200").set_option("stripes", float(str(stripes)))
     g = di.Graph(s_d, t_d, n)
     for K in (1, 8):
         g.solve(d=0.85, tol=1e-10, blocks=K)

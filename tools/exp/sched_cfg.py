@@ -12,6 +12,6 @@ for cfg in (sys.argv[1] if len(sys.argv) > 1 else "c3").split(","):
     for name, kw in (("bulk", {}), ("block8", dict(blocks=8)), ("async", dict(asynchronous=True))):
         g.solve(d=0.85, tol=1e-10, graph_loop=True, **kw)
         st = min((g.solve(d=0.85, tol=1e-10, graph_loop=True, **kw) for _ in range(3)), key=lambda s: s["solve_ms"])
-        print(cfg, os.environ.get("DI_HOT_ACC", "1"), name, "ms", round(st["solve_ms"], 2), "sweeps", st["sweeps"],
+        print(cfg, __import__("paper_1204_6255_b200").get_option("hot_acc"), name, "ms", round(st["solve_ms"], 2), "sweeps", st["sweeps"],
               "eq", round(st["equivalent_iterations"], 2), flush=True)
     g.free()

@@ -1,5 +1,5 @@
 """Experiment: run-to-run variance of the host-pointer upload (the e2e outliers): 12 uploads of C4
-from pinned host memory with DI_BUILD_TRACE phase times."""
+from pinned host memory with the build_trace option's phase times."""
 import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
