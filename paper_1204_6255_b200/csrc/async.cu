@@ -128,41 +128,49 @@ __device__ __forceinline__ void st_cold(ColdRec *r, int32_t j, double v) {
                : "memory");
 }
 
-// Cold bins: warp-collective — all 32 lanes call it, `cold` marks the lanes with a
-// record (j, v). Lanes of one bin are grouped (match.any); the group's leader takes their slots
-// from the warp's current chunk of that bin (cb/ce: next slot and chunk end, relative to the bin's
-// region, in shared memory), reserving a fresh kColdChunk-record chunk with one global atomic when
-// the current one runs out (its fill, kColdChunk, is recorded then; partially filled chunks record
-// theirs at the end of the cycle). Records of one group land in consecutive slots: one coalesced
-// 16-B-per-lane store.
-__device__ __forceinline__ void cold_append(const SweepArgs &a, int32_t *cb, int32_t *ce,
-                                            const int64_t *coff, bool cold, int32_t j, double v,
-                                            int lane) {
-  if (__ballot_sync(0xffffffffu, cold) == 0u) return;
-  const int b = cold ? (int)(((int64_t)j - a.cold_lo) >> a.cold_shift) : -1;
-  const unsigned peers = __match_any_sync(0xffffffffu, b);
-  const int leader = __ffs(peers) - 1;
-  int pos0 = 0, avail = 0, nb = 0;
-  if (cold && lane == leader) {
-    const int cnt = __popc(peers);
-    pos0 = cb[b];
-    avail = ce[b] - pos0;
-    if (avail >= cnt) {
-      cb[b] = pos0 + cnt;
-    } else {
-      if (ce[b] > 0) a.cold_fill[(coff[b] + ce[b]) / kColdChunk - 1] = kColdChunk;
-      nb = (int)atomicAdd(a.cold_top + 16 * b, (unsigned long long)kColdChunk);
-      cb[b] = nb + (cnt - avail);
-      ce[b] = nb + kColdChunk;
+// Cold bins. Every warp owns one chunk of kColdChunk records per bin at a time
+// (shared memory: its start inside the bin's region, and the number of slots taken). A lane with
+// a cold target takes a slot with one shared-memory atomic and stores its 16-B record; when a
+// chunk runs out, the lanes that got no slot keep their records and the warp — at the end of the
+// int4 group, where it is converged — records the full chunk's fill, reserves a fresh chunk for
+// each exhausted bin (one global atomic per kColdChunk records) and retries them. Partially filled
+// chunks record their fill at the end of the cycle; k_cold_apply reads the fills.
+__device__ __noinline__ void cold_refill(int nbins, int32_t *__restrict__ fill,
+                                         unsigned long long *top, int32_t *cnt, int32_t *base,
+                                         const int64_t *coff, int lane) {
+  for (int b = lane; b < nbins; b += 32) {
+    if (cnt[b] >= kColdChunk) {
+      if (base[b] >= 0) fill[(coff[b] + base[b]) / kColdChunk] = kColdChunk;
+      base[b] = (int32_t)atomicAdd(top + 16 * b, (unsigned long long)kColdChunk);
+      cnt[b] = 0;
     }
   }
-  pos0 = __shfl_sync(0xffffffffu, pos0, leader);
-  avail = __shfl_sync(0xffffffffu, avail, leader);
-  nb = __shfl_sync(0xffffffffu, nb, leader);
-  if (cold) {
-    const int rk = __popc(peers & ((1u << lane) - 1u));
-    const int pos = rk < avail ? pos0 + rk : nb + (rk - avail);
-    st_cold(a.cold_rec + coff[b] + pos, j, v);
+  __syncwarp();
+}
+
+__device__ __forceinline__ bool cold_put(ColdRec *rec, int64_t cold_lo, int shift, int32_t *cnt,
+                                         const int32_t *base, const int64_t *coff, int32_t j,
+                                         double v) {
+  const int b = (int)(((int64_t)j - cold_lo) >> shift);
+  const int p = atomicAdd(cnt + b, 1);
+  if (p >= kColdChunk) return false;
+  st_cold(rec + coff[b] + base[b] + p, j, v);
+  return true;
+}
+
+// the records of an int4 group that found their chunk full (warp-collective; rare: once per
+// kColdChunk records of a bin and warp). Scalar arguments only: a reference to the kernel's
+// parameter block would make the compiler copy it to the stack.
+__device__ __noinline__ void cold_retry(ColdRec *rec, int64_t cold_lo, int shift, int nbins,
+                                        int32_t *fill, unsigned long long *top, int32_t *cnt,
+                                        int32_t *base, const int64_t *coff, int4 q, unsigned pending,
+                                        double v, int lane) {
+  const int32_t jj[4] = {q.x, q.y, q.z, q.w};
+  while (__any_sync(0xffffffffu, pending != 0u)) {
+    cold_refill(nbins, fill, top, cnt, base, coff, lane);
+    for (int c = 0; c < 4; c++)
+      if ((pending >> c) & 1u)
+        if (cold_put(rec, cold_lo, shift, cnt, base, coff, jj[c], v)) pending &= ~(1u << c);
   }
 }
 
@@ -173,23 +181,27 @@ template <bool LOOPS>
 __device__ __forceinline__ void push_group_cold(const SweepArgs &a, double *__restrict__ rep,
                                                 int32_t hot_lim, int copy, int4 q, int64_t p0,
                                                 int64_t beg, int64_t end, bool valid, int32_t gi,
-                                                double v, uint64_t fpol, int32_t *cb, int32_t *ce,
+                                                double v, uint64_t fpol, int32_t *cnt, int32_t *base,
                                                 const int64_t *coff, int lane) {
   const int32_t jj[4] = {q.x, q.y, q.z, q.w};
+  unsigned pending = 0u;
 #pragma unroll
   for (int c = 0; c < 4; c++) {
     const int64_t p = p0 + c;
     const int32_t j = jj[c];
-    const bool ok = valid && p >= beg && p < end && (!LOOPS || j != gi);
-    const bool cold = ok && (int64_t)j >= a.cold_lo;
-    if (ok && !cold) {
-      if (j < hot_lim)
+    if (valid && p >= beg && p < end && (!LOOPS || j != gi)) {
+      if ((int64_t)j >= a.cold_lo) {
+        if (!cold_put(a.cold_rec, a.cold_lo, a.cold_shift, cnt, base, coff, j, v)) pending |= 1u << c;
+      } else if (j < hot_lim) {
         red_add_f64(rep + (int64_t)(copy * kRepl + j) * kRepStride, v);
-      else
+      } else {
         red_add_f64_hint(a.F + j, v, fpol);
+      }
     }
-    cold_append(a, cb, ce, coff, cold, j, v, lane);
   }
+  if (__any_sync(0xffffffffu, pending != 0u))
+    cold_retry(a.cold_rec, a.cold_lo, a.cold_shift, a.cold_nbins, a.cold_fill, a.cold_top, cnt, base,
+               coff, q, pending, v, lane);
 }
 
 // TEST (di_test_cycle, include/di_test.h): the selection records (T, v) per node in a.rec_T /
@@ -200,7 +212,7 @@ template <bool LOOPS, bool DIST, bool TEST = false, bool COLD = false>
 __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const SweepArgs a, const DistArgs x) {
   constexpr int NW = kAsyncThreads / 32;
   constexpr int NCB = COLD ? kColdBins : 1;
-  __shared__ int32_t s_ccb[NW][NCB], s_cce[NW][NCB];   // COLD: per-warp chunk state per bin
+  __shared__ int32_t s_ccb[NW][NCB], s_cce[NW][NCB];   // COLD: per-warp chunk (slots taken, start)
   __shared__ int64_t s_coff[NCB];
   __shared__ int64_t s_rb[kCycTile];   // long rows of the tile: first link
   __shared__ int32_t s_ro[kCycTile];   // #links
@@ -241,8 +253,8 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   int32_t *ccb = s_ccb[warp], *cce = s_cce[warp];
   if (COLD) {
     if (lane < NCB) {
-      ccb[lane] = 0;
-      cce[lane] = 0;
+      ccb[lane] = kColdChunk;   // slots taken in the current chunk (full: none yet)
+      cce[lane] = -1;           // its start inside the bin's region (-1: none)
     }
     if (threadIdx.x < NCB) s_coff[threadIdx.x] = threadIdx.x < a.cold_nbins ? a.cold_off[threadIdx.x] : 0;
   }
@@ -259,6 +271,15 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         } else {
           tl = c - a.n_hub;
         }
+      }
+      if (COLD && it < 0 && tl < a.ntiles) {
+        // the first-tier (hot) tiles are spread evenly over the cycle instead of all coming
+        // first: a hot node is then visited after the pushes of the tiles before it, as in the
+        // one-tier striped order (claim 0 stays tile 0: the hub rows' tile). Bijection of
+        // [0, ntiles): claim c is hot iff ceil((c+1)H/T) > ceil(cH/T)
+        const int64_t H = a.cold_hot_tiles, T = a.ntiles;
+        const int64_t h0 = (tl * H + T - 1) / T, h1 = ((tl + 1) * H + T - 1) / T;
+        tl = (h1 > h0) ? h0 : H + (tl - h0);
       }
       s_tile = tl;
       s_item = it;
@@ -561,7 +582,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   }
   if (COLD && lane == 0) {  // the warp's open chunks: their fill for k_cold_apply
     for (int b = 0; b < a.cold_nbins; b++)
-      if (cce[b] > 0) a.cold_fill[(s_coff[b] + cce[b]) / kColdChunk - 1] = kColdChunk - (cce[b] - ccb[b]);
+      if (cce[b] >= 0) a.cold_fill[(s_coff[b] + cce[b]) / kColdChunk] = min(ccb[b], kColdChunk);
   }
   // ---- this CTA's sums (fixed order inside the CTA) -> ppartials[blockIdx.x]
   acc_tk = warp_sum(acc_tk);
@@ -861,6 +882,7 @@ void launch_cycle(Graph &g, int64_t *launches) {
   SweepArgs a = sweep_args(g, 0);
   const bool cold = g.cold_rec && !g.partitioned;
   if (cold) {
+    a.cold_hot_tiles = (g.cold_lo + kCycTile - 1) / kCycTile;
     a.cold_lo = g.cold_lo;
     a.cold_shift = g.cold_shift;
     a.cold_nbins = g.cold_nbins;

@@ -142,6 +142,10 @@ struct __align__(256) Scalars {
   unsigned int hub_flag;     // DI_ASYNC hub items: tile 0 published hv[] for cycle hub_want + 1
   unsigned int hub_want;     //   (advanced by the last CTA of every cycle)
   double alpha;              // DI-SOP threshold scale (di_set_threshold_scale; 1 = P:298)
+  // partitioned sweeps, counted on the device by k_dist_finalize (the batched peer-memory loop
+  // reads them once per batch): entries this rank sent, all ranks' entries of the last sweep,
+  // sweeps whose lists went through peer memory
+  int64_t x_entries, x_lists_last, x_p2p;
 };
 
 // One push work item: a row (or a kChunk-link chunk of a hub row) of a selected node.

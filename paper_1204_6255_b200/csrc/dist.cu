@@ -16,9 +16,12 @@
 //   6. k_apply_recv — F[j - lo] += value (RED: several peers may send the same j).
 //   7. k_dist_finalize — the single-GPU finaliser on the global sums: every rank takes the same
 //      stop / guard decision.
-// The host reads the counts after step 4 (one synchronisation per sweep: NCCL needs the receive
-// sizes on the host). The collectives are NCCL send/recv + allreduce (comm.cu), or the
-// in-process group backend for emulated ranks on one GPU.
+// With send/recv (step 5) the host reads the counts after step 4 (one synchronisation per sweep:
+// NCCL needs the receive sizes on the host). With the peer-memory inboxes (the default) steps 3 and
+// 5 are one kernel and the apply takes its counts from the gathered headers on the device, so the
+// host enqueues batches of sweeps and reads the device state once per batch (the stop flag,
+// counters and the dense/sparse choice), like the single-GPU loop. The collectives are NCCL
+// (comm.cu), or the in-process group backend for emulated ranks on one GPU.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -318,7 +321,8 @@ __global__ void k_apply_recv(double *__restrict__ F, int64_t lo, const int32_t *
 // (parity, peer); the counts come from the gathered sweep headers (device-resident)
 __global__ void k_apply_inbox(double *__restrict__ F, int64_t lo, const char *__restrict__ inbox,
                               int64_t icap, int ipar, const int64_t *__restrict__ ghdr, int world,
-                              int me) {
+                              int me, const Scalars *sc) {
+  if (sc->stop) return;   // batched loop: a sweep after convergence (stale headers) does nothing
   const int hw = 8 + world;
   for (int q = 0; q < world; q++) {
     if (q == me) continue;
@@ -425,9 +429,24 @@ __global__ void k_apply_dense(double *__restrict__ F, const double *__restrict__
 
 // the single-GPU finaliser on the sums of the gathered headers (rank order: every rank computes
 // the same values bit for bit)
-__global__ void k_dist_finalize(const SweepArgs a, const int64_t *ghdr, int world, int async) {
+__global__ void k_dist_finalize(const SweepArgs a, const int64_t *ghdr, int world, int async,
+                                int me, int p2p) {
   if (threadIdx.x != 0 || a.sc->stop) return;
   const int hw = 8 + world;
+  {  // exchange counters (entries this rank sent; every rank's entries of this sweep)
+    int64_t mine = 0, all = 0;
+    for (int p = 0; p < world; p++)
+      for (int q = 0; q < world; q++)
+        if (p != q) {
+          const int64_t c = ghdr[(int64_t)p * hw + 8 + q];
+          all += c;
+          if (p == me) mine += c;
+        }
+    volatile Scalars *vs = a.sc;
+    vs->x_entries = vs->x_entries + mine;
+    vs->x_lists_last = all;
+    if (p2p) vs->x_p2p = vs->x_p2p + 1;
+  }
   double d[4] = {0.0, 0.0, 0.0, 0.0};
   int64_t c[4] = {0, 0, 0, 0};
   for (int p = 0; p < world; p++) {
@@ -803,8 +822,57 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
     for (auto &e : pe) DI_CK(cudaEventCreate(&e));
   double push_ms = 0.0, select_ms = 0.0, xchg_ms = 0.0;
   int64_t push_launches = 0;
+  int64_t batch = 4;
+  double r_prev = g.sc_host->r;
   while (!converged && launched < max_sweeps) {
-    while (launched < max_sweeps) {
+    // ---- batched sweeps through peer memory: no host synchronisation inside a batch
+    const bool batched = p2p && !prof && !force_dense &&
+                         !(!force_sparse && last_lists >= 0 &&
+                           12.0 * (double)last_lists > 8.0 * (double)(G - 1) * (double)g.n_global);
+    if (batched) {
+      const int64_t k = std::min<int64_t>(batch, max_sweeps - launched);
+      const int64_t sw0 = g.sc_host->sweeps;
+      for (int64_t j = 0; j < k; j++) {
+        if (!async) launch_select(g, 0, &launches);
+        if (async)
+          launch_cycle(g, &launches);
+        else if (g.has_loops)
+          k_push_dist<true><<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a, x);
+        else
+          k_push_dist<false><<<g.num_sms * occ, kPushThreads, 0, g.stream>>>(a, x);
+        x.ipar = par;
+        k_compact_remote<<<g.num_sms * kCompBlocksPerSM, kCompThreads, 0, g.stream>>>(g.sc, x);
+        if ((s = g.comm->allgather(g.hdr, g.ghdr, (size_t)hw * 8, g.stream)) != DI_OK) return s;
+        k_apply_inbox<<<g.num_sms * 4, 256, 0, g.stream>>>(g.F, g.lo, g.inbox[me], g.icap, par,
+                                                          g.ghdr, G, me, g.sc);
+        k_dist_finalize<<<1, 32, 0, g.stream>>>(a, g.ghdr, G, async ? 1 : 0, me, 1);
+        launches += 4;
+        par ^= 1;
+      }
+      launched += k;
+      DI_CK(cudaMemcpyAsync(g.sc_host, g.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, g.stream));
+      DI_CK(cudaStreamSynchronize(g.stream));   // once per batch
+      DI_CK(cudaGetLastError());
+      const int64_t real = g.sc_host->sweeps - sw0;
+      last_lists = g.sc_host->x_lists_last;
+      if (g.sc_host->stop) {
+        launched = g.sc_host->sweeps;
+      } else if (launched < max_sweeps) {
+        // next batch: the sweeps left predicted from the decay of r (as on one GPU)
+        const double r_now = g.sc_host->r;
+        int64_t next = 8;
+        if (real > 0 && r_now > 0.0 && r_prev > r_now) {
+          const double rate = std::pow(r_now / r_prev, 1.0 / (double)real);
+          const double target = paper ? tol * (1.0 - d) : tol;
+          if (rate < 1.0 && rate > 0.0)
+            next = (int64_t)std::ceil(std::max(1.0, std::log(target / r_now) / std::log(rate)));
+        }
+        batch = std::max<int64_t>(1, std::min<int64_t>(next, 32));
+        r_prev = r_now;
+        continue;
+      }
+    }
+    while (!batched && launched < max_sweeps) {
       if (prof) DI_CK(cudaEventRecord(pe[0], g.stream));
       if (!async) launch_select(g, 0, &launches);
       if (prof) DI_CK(cudaEventRecord(pe[1], g.stream));
@@ -868,7 +936,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       if (!dense && p2p) {  // the records are already in the owners' inboxes: apply ours
         for (int p = 0; p < G; p++) xentries += (p == me) ? 0 : g.ghdr_h[(size_t)me * hw + 8 + p];
         k_apply_inbox<<<g.num_sms * 4, 256, 0, g.stream>>>(g.F, g.lo, g.inbox[me], g.icap, par,
-                                                          g.ghdr, G, me);
+                                                          g.ghdr, G, me, g.sc);
         launches++;
         par ^= 1;
         np2p++;
@@ -890,7 +958,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
         k_apply_recv<<<grid_of(off, g.num_sms), 256, 0, g.stream>>>(g.F, g.lo, g.rid, off);
         launches++;
       }
-      k_dist_finalize<<<1, 32, 0, g.stream>>>(a, g.ghdr, G, async ? 1 : 0);
+      k_dist_finalize<<<1, 32, 0, g.stream>>>(a, g.ghdr, G, async ? 1 : 0, me, 0);
       launches++;
       if (prof) {  // exchange of the lists + apply (the counts exchange is in the sync above)
         DI_CK(cudaEventRecord(pe[0], g.stream));
@@ -948,11 +1016,11 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
     st->error_estimate = c.resid / (1.0 - d - d * c.e);
     st->converged = converged ? 1 : 0;
     st->variant = variant;
-    xbytes = 12.0 * (double)xentries + xdense;
+    xbytes = 12.0 * (double)c.x_entries + xdense;
     st->exchange_bytes = xbytes;
     st->dense_exchanges = ndense;
-    st->p2p_exchanges = np2p;
-    st->exchange_entries = xentries;
+    st->p2p_exchanges = np2p + c.x_p2p;
+    st->exchange_entries = c.x_entries;
     st->push_ms = push_ms;
     st->select_ms = select_ms;
     st->push_launches = push_launches;

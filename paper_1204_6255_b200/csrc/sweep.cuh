@@ -43,6 +43,7 @@ struct SweepArgs {
   // cold bins (async.cu COLD instantiation): targets j >= cold_lo become records of bin
   // (j - cold_lo) >> cold_shift in region cold_off[b] of the arena
   int64_t cold_lo;
+  int64_t cold_hot_tiles;   // tiles holding first-tier ids (interleaved over the cycle)
   int cold_shift, cold_nbins;
   ColdRec *cold_rec;
   const int64_t *cold_off;
@@ -365,6 +366,7 @@ inline SweepArgs sweep_args(Graph &g, int test_mode, int blk = 0, int blocks = 1
   a.rec_T = nullptr;
   a.rec_v = nullptr;
   a.cold_lo = INT64_MAX;
+  a.cold_hot_tiles = 0;
   a.cold_shift = 0;
   a.cold_nbins = 0;
   a.cold_rec = nullptr;

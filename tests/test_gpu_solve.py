@@ -556,3 +556,58 @@ def test_paper_axes_c2_async_vs_oracle(axis):
             assert l1(H, Ho) <= 1e-9, (axis, variant, kw)
             assert l1(H, Ht) <= 1e-10 / (1 - D) + 1e-13 / (1 - D), (axis, variant, kw)
     g.free()
+
+
+def _skewed_hub_graph(seed, n=4096 * 8, self_loop_on_hot=True):
+    """Targets with 4 %, 2 %, 1 % of all links (replicated accumulators on) that are also hub rows
+    of 30000 / 9000 / 100 links; one hot hub row carries a self-loop (fold, G6)."""
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, n, 6 * n).astype(np.int32)
+    dst = rng.integers(0, n, 6 * n).astype(np.int32)
+    m = len(src)
+    for hub, share, out in ((77, 0.04, 30000), (5000, 0.02, 9000), (123, 0.01, 100)):
+        k = int(share * m)
+        tgt = rng.choice(n, out, replace=False).astype(np.int32)
+        src = np.concatenate([src, rng.integers(0, n, k).astype(np.int32), np.full(out, hub, np.int32)])
+        dst = np.concatenate([dst, np.full(k, hub, np.int32), tgt])
+    if self_loop_on_hot:
+        src = np.concatenate([src, np.array([77, 5000], np.int32)])
+        dst = np.concatenate([dst, np.array([77, 5000], np.int32)])
+    return src, dst, n
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(mode="auto"), dict(blocks=8), dict(mode="pull")],
+                         ids=["bulk_push", "auto", "blocks8", "pull"])
+def test_hot_accumulators_every_schedule(kw):
+    """The replicated hot accumulators are folded by every push schedule (bulk k_push, the DI_AUTO
+    push/pull mix, block-ordered sub-sweeps), not only by the asynchronous cycle: skewed in-degrees
+    (hot placement on), hot targets that are hub rows, self-loops on hot hubs."""
+    need_gpu()
+    src, dst, n = _skewed_hub_graph(21)
+    g = upload(src, dst, n, build_csc=True)
+    for variant in ("sop", "cyc"):
+        X, _, _ = oracle.di(src, dst, n, d=D, tol=1e-15, variant=variant)
+        for rep in range(2):
+            st = g.solve(d=D, tol=1e-13, variant=variant, **kw)
+            assert st["converged"] == 1
+            assert l1(g.history().cpu().numpy(), X) <= (1e-13 + 1e-15) / (1 - D) + 1e-14, (variant, rep)
+    g.free()
+
+
+def test_hot_accumulators_pi_push():
+    """PI' (push comparator) scatters through the same replicated accumulators (k_pi_fold): on the
+    skewed hub graph with self-loops it matches the oracle's PI' loop and the normalised dense
+    solution."""
+    need_gpu()
+    src, dst, n = _skewed_hub_graph(22)
+    g = upload(src, dst, n, build_csc=True)
+    target = 1e-12
+    st = g.solve(d=D, tol=target, variant="pi_push")
+    x = g.history().cpu().numpy()
+    xo, sto = oracle.pi_col(src, dst, n, d=D, target=target)
+    assert st["converged"] == 1 and abs(st["sweeps"] - sto["cycles"]) <= 1
+    if st["sweeps"] == sto["cycles"]:
+        assert l1(x, xo) <= 1e-12
+    Xs = defn.solve_sparse(src, dst, n, D)
+    assert l1(x, Xs / Xs.sum()) <= 1e-10
+    g.free()
