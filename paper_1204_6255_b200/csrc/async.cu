@@ -183,12 +183,13 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, double *__re
                                                 int64_t beg, int64_t end, bool valid, int32_t gi,
                                                 double v, uint64_t fpol, int32_t *cnt, int32_t *base,
                                                 const int64_t *coff, int lane) {
-  const int32_t jj[4] = {q.x, q.y, q.z, q.w};
   unsigned pending = 0u;
-#pragma unroll
+  // not unrolled: the COLD kernel's code must stay small enough for the instruction cache (with
+  // the four targets unrolled at every call site, half the stall samples were no_instruction)
+#pragma unroll 1
   for (int c = 0; c < 4; c++) {
     const int64_t p = p0 + c;
-    const int32_t j = jj[c];
+    const int32_t j = c == 0 ? q.x : (c == 1 ? q.y : (c == 2 ? q.z : q.w));
     if (valid && p >= beg && p < end && (!LOOPS || j != gi)) {
       if ((int64_t)j >= a.cold_lo) {
         if (!cold_put(a.cold_rec, a.cold_lo, a.cold_shift, cnt, base, coff, j, v)) pending |= 1u << c;
@@ -690,13 +691,26 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
 // Cold bins, after the cycle: the records of bin 0, then bin 1, ... (every block takes a contiguous
 // share of each bin, so the grid walks the bins together and the slice of F being updated stays
 // in L2), each a RED into F; the last block rewinds the bins. Chunks past their fill are skipped.
+// The grid is co-resident (at most the resident blocks of the device) and the blocks meet at a
+// barrier between two bins, so that the whole grid works on one slice of F at a time.
 __global__ void __launch_bounds__(256) k_cold_apply(double *__restrict__ F, const ColdRec *__restrict__ rec,
                                                     const int64_t *__restrict__ off,
                                                     unsigned long long *top,
                                                     const int32_t *__restrict__ fill, int nbins) {
   __shared__ bool s_last;
   const uint64_t pol = policy_evict_first();
+  unsigned int *bar = reinterpret_cast<unsigned int *>(top + 16 * kColdBins) + 32;
   for (int b = 0; b < nbins; b++) {
+    if (b > 0) {  // grid barrier: every block done with bin b - 1
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        const unsigned want = (unsigned)b * gridDim.x;
+        while (ld_acquire_u32(bar) < want) __nanosleep(32);
+      }
+      __syncthreads();
+    }
     const int64_t m = (int64_t)*reinterpret_cast<volatile unsigned long long *>(top + 16 * b);
     if (m == 0) continue;
     const int64_t base = off[b];
@@ -721,7 +735,10 @@ __global__ void __launch_bounds__(256) k_cold_apply(double *__restrict__ F, cons
   __syncthreads();
   if (!s_last) return;
   if (threadIdx.x < nbins) top[16 * threadIdx.x] = 0ull;
-  if (threadIdx.x == 0) *ticket = 0u;
+  if (threadIdx.x == 0) {
+    *ticket = 0u;
+    *bar = 0u;   // every block has passed its last barrier (they all reached the ticket)
+  }
 }
 
 // cold-target counts per bin (static: the CSR), for the bin regions of the arena
@@ -779,8 +796,8 @@ static di_status prepare_cold(Graph &g) {
   DI_CK(dmalloc(&g.cold_fill, (size_t)(total / kColdChunk + 1) * 4));
   DI_CK(dmalloc(&g.cold_off, (kColdBins + 1) * 8));
   DI_CK(cudaMemcpyAsync(g.cold_off, off.data(), (kColdBins + 1) * 8, cudaMemcpyHostToDevice, g.stream));
-  DI_CK(dmalloc(&g.cold_top, (kColdBins + 1) * 16 * 8));
-  DI_CK(cudaMemsetAsync(g.cold_top, 0, (kColdBins + 1) * 16 * 8, g.stream));
+  DI_CK(dmalloc(&g.cold_top, (kColdBins + 2) * 16 * 8));   // + ticket line + barrier line
+  DI_CK(cudaMemsetAsync(g.cold_top, 0, (kColdBins + 2) * 16 * 8, g.stream));
   DI_CK(cudaStreamSynchronize(g.stream));
   return DI_OK;
 }
@@ -878,6 +895,12 @@ void launch_cycle_test(Graph &g, double *rec_T, double *rec_v, int64_t *launches
   *launches += 1;
 }
 
+// k_cold_apply's grid: co-resident blocks only (its blocks wait for each other between bins)
+static int cold_apply_grid(const Graph &g) {
+  static const int occ = occupancy(k_cold_apply, 256);
+  return g.num_sms * std::min(occ, 8);
+}
+
 void launch_cycle(Graph &g, int64_t *launches) {
   SweepArgs a = sweep_args(g, 0);
   const bool cold = g.cold_rec && !g.partitioned;
@@ -913,8 +936,8 @@ void launch_cycle(Graph &g, int64_t *launches) {
       k_cycle<true, false, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
     else
       k_cycle<false, false, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
-    k_cold_apply<<<g.num_sms * 8, 256, 0, g.stream>>>(g.F, g.cold_rec, g.cold_off, g.cold_top,
-                                                      g.cold_fill, g.cold_nbins);
+    k_cold_apply<<<cold_apply_grid(g), 256, 0, g.stream>>>(g.F, g.cold_rec, g.cold_off, g.cold_top,
+                                                           g.cold_fill, g.cold_nbins);
     *launches += 1;
   } else {
     if (g.has_loops)
