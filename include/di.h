@@ -136,6 +136,9 @@ typedef struct {
   int64_t dense_exchanges;      /* multi-GPU: sweeps whose exchange took the dense fallback       */
   int64_t p2p_exchanges;        /* multi-GPU: sweeps whose lists went through peer memory (fused) */
   int64_t meetings;             /* DI_DIST_ASYNC: collective meetings (drain + global sum F)       */
+  int64_t exchange_cold;        /* multi-GPU compact path: 16-B records of pushes to cold remote
+                                   targets this rank wrote into the owners' inboxes (slots
+                                   reserved); exchange_bytes = 12 entries + 16 cold (+ dense)     */
 } di_stats;
 
 /* In-process rank group: `world` emulated ranks, one host thread each, sharing one GPU. The
@@ -208,6 +211,12 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
  *   "p2p"            1        0..1      U: peer-memory inboxes for the partitioned exchange
  *   "p2p_force"      0        0..1      U: create the inbox on a one-rank communicator too
  *   "build_trace"    0        0..1      host timestamps of the build phases on stderr
+ *   "remote_compact" 1        0..1      U: partitioned DI_ASYNC cycles through peer memory keep a
+ *                                          compact accumulator for the hot targets of the other
+ *                                          ranges and write pushes to colder remote targets as
+ *                                          records straight into the owner's inbox (0: the
+ *                                          global-size accumulator and its compaction scan)
+ *   "remote_tier"    0        >= 0      U: hot remote targets per range (0: half the L2 over G)
  * DI_EINVAL for an unknown name or a value out of range (integers must be integral). */
 di_status di_set_option(const char *name, double value);
 di_status di_get_option(const char *name, double *value);

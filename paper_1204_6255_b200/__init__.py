@@ -51,6 +51,7 @@ class Stats(ctypes.Structure):
         ("exchange_bytes", ctypes.c_double), ("exchange_entries", ctypes.c_int64),
         ("exchange_ms", ctypes.c_double), ("dense_exchanges", ctypes.c_int64),
         ("p2p_exchanges", ctypes.c_int64), ("meetings", ctypes.c_int64),
+        ("exchange_cold", ctypes.c_int64),
     ]
 
     def as_dict(self):

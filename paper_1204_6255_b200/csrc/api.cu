@@ -332,6 +332,8 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
     g->cycle_times = o.cycle_times;
     g->p2p_opt = o.p2p;
     g->p2p_force = o.p2p_force;
+    g->remote_compact = o.remote_compact;
+    g->remote_tier = o.remote_tier;
   }
   di_status s = build_graph(*g, src, dst, n_links, flags);
   if (s == DI_OK) s = alloc_state(*g);
@@ -357,6 +359,7 @@ const OptDesc kOpts[] = {
     {"cold_bins", -1, 1, true},     {"cold_tier", 0, 2147483647.0, true},
     {"cycle_grid_div", 1, 4096, true}, {"cycle_times", 0, 1, true}, {"p2p", 0, 1, true},
     {"p2p_force", 0, 1, true},      {"build_trace", 0, 1, true},
+    {"remote_compact", 0, 1, true}, {"remote_tier", 0, 2147483647.0, true},
 };
 }  // namespace
 
@@ -385,6 +388,8 @@ di_status di_set_option(const char *name, double value) {
   else if (n == "p2p") o.p2p = iv;
   else if (n == "p2p_force") o.p2p_force = iv;
   else if (n == "build_trace") o.build_trace = iv;
+  else if (n == "remote_compact") o.remote_compact = iv;
+  else if (n == "remote_tier") o.remote_tier = (int64_t)value;
   return DI_OK;
 }
 
@@ -405,6 +410,8 @@ di_status di_get_option(const char *name, double *value) {
   else if (n == "p2p") *value = o.p2p;
   else if (n == "p2p_force") *value = o.p2p_force;
   else if (n == "build_trace") *value = o.build_trace;
+  else if (n == "remote_compact") *value = o.remote_compact;
+  else if (n == "remote_tier") *value = (double)o.remote_tier;
   else return fail(DI_EINVAL, "di_get_option: unknown option '" + n + "'");
   return DI_OK;
 }

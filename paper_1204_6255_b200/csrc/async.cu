@@ -135,55 +135,66 @@ __device__ __forceinline__ void st_cold(ColdRec *r, int32_t j, double v) {
 // int4 group, where it is converged — records the full chunk's fill, reserves a fresh chunk for
 // each exhausted bin (one global atomic per kColdChunk records) and retries them. Partially filled
 // chunks record their fill at the end of the cycle; k_cold_apply reads the fills.
-__device__ __noinline__ void cold_refill(int nbins, int32_t *__restrict__ fill,
-                                         unsigned long long *top, int32_t *cnt, int32_t *base,
-                                         const int64_t *coff, int lane) {
+// Per-bin pointers (shared memory): the bin's region of records, its chunk fills, its counter.
+// One GPU: the bins of target slices in the arena. Partitioned (compact remote path): bin p is
+// owner p, the region this sender's cold records take in p's inbox (parity of the cycle).
+__device__ __noinline__ void cold_refill(int nbins, int32_t *const *fptr,
+                                         unsigned long long *const *tptr, int32_t *cnt,
+                                         int32_t *base, int lane) {
   for (int b = lane; b < nbins; b += 32) {
-    if (cnt[b] >= kColdChunk) {
-      if (base[b] >= 0) fill[(coff[b] + base[b]) / kColdChunk] = kColdChunk;
-      base[b] = (int32_t)atomicAdd(top + 16 * b, (unsigned long long)kColdChunk);
+    if (cnt[b] >= kColdChunk && tptr[b]) {   // (partitioned: no bin for the own range)
+      if (base[b] >= 0) fptr[b][base[b] / kColdChunk] = kColdChunk;
+      base[b] = (int32_t)atomicAdd(tptr[b], (unsigned long long)kColdChunk);
       cnt[b] = 0;
     }
   }
   __syncwarp();
 }
 
-__device__ __forceinline__ bool cold_put(ColdRec *rec, int64_t cold_lo, int shift, int32_t *cnt,
-                                         const int32_t *base, const int64_t *coff, int32_t j,
-                                         double v) {
-  const int b = (int)(((int64_t)j - cold_lo) >> shift);
+__device__ __forceinline__ bool cold_put(ColdRec *const *cptr, int32_t *cnt, const int32_t *base,
+                                         int b, int32_t j, double v) {
   const int p = atomicAdd(cnt + b, 1);
   if (p >= kColdChunk) return false;
-  st_cold(rec + coff[b] + base[b] + p, j, v);
+  st_cold(cptr[b] + base[b] + p, j, v);
   return true;
 }
 
 // the records of an int4 group that found their chunk full (warp-collective; rare: once per
-// kColdChunk records of a bin and warp). Scalar arguments only: a reference to the kernel's
-// parameter block would make the compiler copy it to the stack.
-__device__ __noinline__ void cold_retry(ColdRec *rec, int64_t cold_lo, int shift, int nbins,
-                                        int32_t *fill, unsigned long long *top, int32_t *cnt,
-                                        int32_t *base, const int64_t *coff, int4 q, unsigned pending,
+// kColdChunk records of a bin and warp); bins packed 5 bits per target. Scalar and shared-memory
+// arguments only: a reference to the kernel's parameter block would make the compiler copy it
+// to the stack.
+__device__ __noinline__ void cold_retry(int nbins, ColdRec *const *cptr, int32_t *const *fptr,
+                                        unsigned long long *const *tptr, int32_t *cnt,
+                                        int32_t *base, int4 q, unsigned pending, unsigned bins,
                                         double v, int lane) {
   const int32_t jj[4] = {q.x, q.y, q.z, q.w};
   while (__any_sync(0xffffffffu, pending != 0u)) {
-    cold_refill(nbins, fill, top, cnt, base, coff, lane);
+    cold_refill(nbins, fptr, tptr, cnt, base, lane);
     for (int c = 0; c < 4; c++)
       if ((pending >> c) & 1u)
-        if (cold_put(rec, cold_lo, shift, cnt, base, coff, jj[c], v)) pending &= ~(1u << c);
+        if (cold_put(cptr, cnt, base, (int)((bins >> (5 * c)) & 31u), jj[c], v)) pending &= ~(1u << c);
   }
 }
 
+struct ColdSm {   // the warp's chunk state and the block's per-bin pointers (shared memory)
+  int32_t *cnt, *base;
+  ColdRec *const *cptr;
+  int32_t *const *fptr;
+  unsigned long long *const *tptr;
+};
+
 // COLD push of one int4 group (warp-collective: every lane calls it; `valid` = the lane has a
-// group): hot ids to the replicated accumulators, first-tier targets (j < cold_lo) a RED into F,
-// cold targets a record of their bin.
-template <bool LOOPS>
-__device__ __forceinline__ void push_group_cold(const SweepArgs &a, double *__restrict__ rep,
-                                                int32_t hot_lim, int copy, int4 q, int64_t p0,
-                                                int64_t beg, int64_t end, bool valid, int32_t gi,
-                                                double v, uint64_t fpol, int32_t *cnt, int32_t *base,
-                                                const int64_t *coff, int lane) {
-  unsigned pending = 0u;
+// group). One GPU: hot ids to the replicated accumulators, first-tier targets (j < cold_lo) a
+// RED into F, cold targets a record of their slice's bin. Partitioned (DIST): local targets a RED
+// into F, hot remote targets (the first rt[p] ids of owner p's range) a RED into the compact
+// accumulator, colder remote targets a record into owner p's inbox.
+template <bool LOOPS, bool DIST>
+__device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistArgs &x,
+                                                double *__restrict__ rep, int32_t hot_lim, int copy,
+                                                int4 q, int64_t p0, int64_t beg, int64_t end,
+                                                bool valid, int32_t gi, double v, uint64_t fpol,
+                                                const ColdSm &cs, int lane) {
+  unsigned pending = 0u, bins = 0u;
   // not unrolled: the COLD kernel's code must stay small enough for the instruction cache (with
   // the four targets unrolled at every call site, half the stall samples were no_instruction)
 #pragma unroll 1
@@ -191,8 +202,27 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, double *__re
     const int64_t p = p0 + c;
     const int32_t j = c == 0 ? q.x : (c == 1 ? q.y : (c == 2 ? q.z : q.w));
     if (valid && p >= beg && p < end && (!LOOPS || j != gi)) {
-      if ((int64_t)j >= a.cold_lo) {
-        if (!cold_put(a.cold_rec, a.cold_lo, a.cold_shift, cnt, base, coff, j, v)) pending |= 1u << c;
+      if (DIST) {
+        const int64_t jl = (int64_t)j - a.lo;
+        if (jl >= 0 && jl < a.n) {
+          red_add_f64_hint(a.F + jl, v, fpol);
+        } else {
+          int pp = 0;
+          while (pp + 1 < x.bd.world && (int64_t)j >= x.bd.b[pp + 1]) pp++;
+          const int64_t off = (int64_t)j - x.bd.b[pp];
+          if (off < x.rt[pp]) {
+            red_add_f64_hint(x.racc + x.hoff[pp] + off, v, fpol);
+          } else if (!cold_put(cs.cptr, cs.cnt, cs.base, pp, j, v)) {
+            pending |= 1u << c;
+            bins |= (unsigned)pp << (5 * c);
+          }
+        }
+      } else if ((int64_t)j >= a.cold_lo) {
+        const int bb = (int)(((int64_t)j - a.cold_lo) >> a.cold_shift);
+        if (!cold_put(cs.cptr, cs.cnt, cs.base, bb, j, v)) {
+          pending |= 1u << c;
+          bins |= (unsigned)bb << (5 * c);
+        }
       } else if (j < hot_lim) {
         red_add_f64(rep + (int64_t)(copy * kRepl + j) * kRepStride, v);
       } else {
@@ -201,8 +231,8 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, double *__re
     }
   }
   if (__any_sync(0xffffffffu, pending != 0u))
-    cold_retry(a.cold_rec, a.cold_lo, a.cold_shift, a.cold_nbins, a.cold_fill, a.cold_top, cnt, base,
-               coff, q, pending, v, lane);
+    cold_retry(DIST ? x.bd.world : a.cold_nbins, cs.cptr, cs.fptr, cs.tptr, cs.cnt, cs.base, q,
+               pending, bins, v, lane);
 }
 
 // TEST (di_test_cycle, include/di_test.h): the selection records (T, v) per node in a.rec_T /
@@ -214,7 +244,9 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   constexpr int NW = kAsyncThreads / 32;
   constexpr int NCB = COLD ? kColdBins : 1;
   __shared__ int32_t s_ccb[NW][NCB], s_cce[NW][NCB];   // COLD: per-warp chunk (slots taken, start)
-  __shared__ int64_t s_coff[NCB];
+  __shared__ ColdRec *s_cptr[NCB];
+  __shared__ int32_t *s_fptr[NCB];
+  __shared__ unsigned long long *s_tptr[NCB];
   __shared__ int64_t s_rb[kCycTile];   // long rows of the tile: first link
   __shared__ int32_t s_ro[kCycTile];   // #links
   __shared__ double s_rv[kCycTile];    // v = T d / o
@@ -252,13 +284,30 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   double acc_tk = 0.0, acc_s = 0.0, acc_e = 0.0;
   long long acc_sel = 0, acc_nd = 0, acc_lk = 0;
   int32_t *ccb = s_ccb[warp], *cce = s_cce[warp];
+  const int cnb = DIST ? x.bd.world : a.cold_nbins;
   if (COLD) {
     if (lane < NCB) {
       ccb[lane] = kColdChunk;   // slots taken in the current chunk (full: none yet)
       cce[lane] = -1;           // its start inside the bin's region (-1: none)
     }
-    if (threadIdx.x < NCB) s_coff[threadIdx.x] = threadIdx.x < a.cold_nbins ? a.cold_off[threadIdx.x] : 0;
+    const int b = threadIdx.x;
+    if (b < NCB) {
+      s_cptr[b] = nullptr;
+      s_fptr[b] = nullptr;
+      s_tptr[b] = nullptr;
+      if (!DIST && b < a.cold_nbins) {
+        s_cptr[b] = a.cold_rec + a.cold_off[b];
+        s_fptr[b] = a.cold_fill + a.cold_off[b] / kColdChunk;
+        s_tptr[b] = a.cold_top + 16 * b;
+      } else if (DIST && b < x.bd.world && b != x.rank) {
+        const int64_t slot = 2 * (int64_t)x.rank + x.ipar;
+        s_cptr[b] = reinterpret_cast<ColdRec *>(x.inbox[b] + x.cold_off0) + slot * x.ccap;
+        s_fptr[b] = reinterpret_cast<int32_t *>(x.inbox[b] + x.fill_off0) + slot * (x.ccap / kColdChunk);
+        s_tptr[b] = x.ctop + 16 * b;
+      }
+    }
   }
+  const ColdSm cs{ccb, cce, s_cptr, s_fptr, s_tptr};
 
   for (;;) {
     if (threadIdx.x == 0) {
@@ -475,8 +524,8 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           for (int k = 0; k < 4; k++) {
             const int vi = vb + 32 * k + lane;
             if constexpr (COLD)
-              push_group_cold<LOOPS>(a, rep, hot_lim, copy, xq[k], a0 + 4 * (int64_t)vi, beg, end,
-                                     vi < nvec, gi, v, fpol, ccb, cce, s_coff, lane);
+              push_group_cold<LOOPS, DIST>(a, x, rep, hot_lim, copy, xq[k], a0 + 4 * (int64_t)vi, beg, end,
+                                     vi < nvec, gi, v, fpol, cs, lane);
             else if (vi < nvec)
               push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, xq[k], a0 + 4 * (int64_t)vi,
                                       beg, end, gi, v, fpol);
@@ -511,8 +560,8 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           }
 #pragma unroll
           for (int u = 0; u < NG; u++)
-            push_group_cold<LOOPS>(a, rep, hot_lim, copy, xs[u], a0 + 4 * u, beg, end, u < nvec, gi, v,
-                                   fpol, ccb, cce, s_coff, lane);
+            push_group_cold<LOOPS, DIST>(a, x, rep, hot_lim, copy, xs[u], a0 + 4 * u, beg, end, u < nvec, gi, v,
+                                   fpol, cs, lane);
         } else if (k < nsmall) {
           const int li = s_si[k];
           const double v = s_sv[k];
@@ -556,10 +605,10 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
             int4 x0 = make_int4(0, 0, 0, 0), x1 = make_int4(0, 0, 0, 0);
             if (vb < nvec) x0 = ld_col4(col + a0 + 4 * (int64_t)vb, pol);
             if (vb + 8 < nvec) x1 = ld_col4(col + a0 + 4 * (int64_t)(vb + 8), pol);
-            push_group_cold<LOOPS>(a, rep, hot_lim, copy, x0, a0 + 4 * (int64_t)vb, beg, end, vb < nvec,
-                                   gi, v, fpol, ccb, cce, s_coff, lane);
-            push_group_cold<LOOPS>(a, rep, hot_lim, copy, x1, a0 + 4 * (int64_t)(vb + 8), beg, end,
-                                   vb + 8 < nvec, gi, v, fpol, ccb, cce, s_coff, lane);
+            push_group_cold<LOOPS, DIST>(a, x, rep, hot_lim, copy, x0, a0 + 4 * (int64_t)vb, beg, end, vb < nvec,
+                                   gi, v, fpol, cs, lane);
+            push_group_cold<LOOPS, DIST>(a, x, rep, hot_lim, copy, x1, a0 + 4 * (int64_t)(vb + 8), beg, end,
+                                   vb + 8 < nvec, gi, v, fpol, cs, lane);
           }
         } else if (k < nmid) {
           const int64_t beg = s_rb[k], end = beg + s_ro[k], a0 = beg & ~3ll;
@@ -581,9 +630,9 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
     }
     __syncthreads();
   }
-  if (COLD && lane == 0) {  // the warp's open chunks: their fill for k_cold_apply
-    for (int b = 0; b < a.cold_nbins; b++)
-      if (cce[b] >= 0) a.cold_fill[(s_coff[b] + cce[b]) / kColdChunk] = min(ccb[b], kColdChunk);
+  if (COLD && lane == 0) {  // the warp's open chunks: their fill for the apply kernels
+    for (int b = 0; b < cnb; b++)
+      if (cce[b] >= 0) s_fptr[b][cce[b] / kColdChunk] = min(ccb[b], kColdChunk);
   }
   // ---- this CTA's sums (fixed order inside the CTA) -> ppartials[blockIdx.x]
   acc_tk = warp_sum(acc_tk);
@@ -846,6 +895,9 @@ static int cycle_grid(const Graph &g) {
   return std::max(1, std::min(g.num_sms * occ, kMaxSlices) / std::max(1, g.grid_div));
 }
 
+// warps of k_cycle's grid (the cold regions reserve one chunk per warp of slack)
+int64_t cycle_warps(const Graph &g) { return (int64_t)cycle_grid(g) * (kAsyncThreads / 32); }
+
 // option cycle_times (diagnostic): per cycle, the spread of CTA start and end times (stderr)
 void report_cycle_times(Graph &g, int64_t cycles) {
   if (!g.cyc_times || cycles <= 0) return;
@@ -926,7 +978,15 @@ void launch_cycle(Graph &g, int64_t *launches) {
     a.n_hub = g.n_hub;
   }
   const int grid = cycle_grid(g);
-  if (dist) {
+  if (dist && g.cur_compact) {  // hot remote accumulator + cold records into the owners' inboxes
+    x.ipar = g.cur_par;
+    x.compact = 1;
+    a.cold_hot_tiles = (g.rtier[g.rank] + kCycTile - 1) / kCycTile;
+    if (g.has_loops)
+      k_cycle<true, true, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+    else
+      k_cycle<false, true, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+  } else if (dist) {
     if (g.has_loops)
       k_cycle<true, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
     else

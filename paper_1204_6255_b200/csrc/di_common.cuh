@@ -108,6 +108,8 @@ struct Options {
   int p2p = 1;               // "p2p": peer-memory inboxes for the partitioned exchange
   int p2p_force = 0;         // "p2p_force": create the inbox on a one-rank communicator too
   int build_trace = 0;       // "build_trace": host timestamps of the build phases (stderr)
+  int remote_compact = 1;    // "remote_compact": hot remote accumulator + cold records (P2P)
+  int64_t remote_tier = 0;   // "remote_tier": hot remote targets per range (0: auto)
 };
 Options options();           // a snapshot of the current options
 
@@ -145,7 +147,7 @@ struct __align__(256) Scalars {
   // partitioned sweeps, counted on the device by k_dist_finalize (the batched peer-memory loop
   // reads them once per batch): entries this rank sent, all ranks' entries of the last sweep,
   // sweeps whose lists went through peer memory
-  int64_t x_entries, x_lists_last, x_p2p;
+  int64_t x_entries, x_lists_last, x_p2p, x_cold;
 };
 
 // One push work item: a row (or a kChunk-link chunk of a hub row) of a selected node.
@@ -277,6 +279,16 @@ struct Graph {
   double *dsum = nullptr;
   int64_t *isum = nullptr;
   int32_t *rid = nullptr;         // received 12-byte records, capacity (world-1) * n
+  // compact remote path (dist.cu, async.cu)
+  int remote_compact = 1;         // option remote_compact
+  int64_t remote_tier = 0;        // option remote_tier (0: auto)
+  int64_t rtier[kMaxWorld] = {0}; // hot remote targets at the start of every range
+  double *racc = nullptr;         // their accumulator, sum of rtier
+  int64_t ccap = 0;               // cold records per (sender, parity) inbox region
+  size_t cold_off0 = 0, fill_off0 = 0;
+  unsigned long long *ctop = nullptr;
+  bool R_ready = false;           // R (global-size accumulator) allocated: bulk / ring / send-recv
+  int cur_par = 0, cur_compact = 0;  // solve_dist -> launch_cycle: inbox parity, compact path
 };
 
 // ---------------------------------------------------------------- device memory
@@ -332,6 +344,7 @@ void launch_cycle_test(Graph &g, double *rec_T, double *rec_v, int64_t *launches
 di_status prepare_cycle(Graph &g, bool async);
 di_status alloc_pull(Graph &g);
 di_status alloc_dist(Graph &g);
+int64_t cycle_warps(const Graph &g);
 // dist.cu
 di_status solve_dist(Graph &g, double d, const double *B, double tol, int variant,
                      int64_t max_sweeps, uint32_t flags, di_stats *st);

@@ -195,28 +195,32 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *
   double sent = 0.0;   // ring mode: this thread's compacted fluid, over all its chunks
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // chunk index space: owners in order, chunks of kCompChunk ids inside each (own range skipped)
+  // (compact path: the segment of owner p is its hot prefix rt[p] in racc, L2-resident; else R's
+  //  whole range of p)
   int64_t nchunks = 0;
   for (int p = 0; p < x.bd.world; p++)
-    if (p != x.rank) nchunks += (x.bd.b[p + 1] - x.bd.b[p] + kCompChunk - 1) / kCompChunk;
+    if (p != x.rank)
+      nchunks += ((x.compact ? x.rt[p] : x.bd.b[p + 1] - x.bd.b[p]) + kCompChunk - 1) / kCompChunk;
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     int p = 0;
     int64_t cc = c;
     for (; p < x.bd.world; p++) {
       if (p == x.rank) continue;
-      const int64_t k = (x.bd.b[p + 1] - x.bd.b[p] + kCompChunk - 1) / kCompChunk;
+      const int64_t k = ((x.compact ? x.rt[p] : x.bd.b[p + 1] - x.bd.b[p]) + kCompChunk - 1) / kCompChunk;
       if (cc < k) break;
       cc -= k;
     }
     // element k of this thread: id j0 + k * kCompThreads (a warp reads 32 consecutive doubles
     // per load: coalesced; the record order inside a segment is free)
+    double *src = x.compact ? x.racc + x.hoff[p] - x.bd.b[p] : x.R;   // indexed by global id
     const int64_t j0 = x.bd.b[p] + cc * kCompChunk + (int64_t)threadIdx.x;
-    const int64_t jend = x.bd.b[p + 1];
+    const int64_t jend = x.bd.b[p] + (x.compact ? x.rt[p] : x.bd.b[p + 1] - x.bd.b[p]);
     double v[kCompPer];
     int cnt = 0;
 #pragma unroll
     for (int k = 0; k < kCompPer; k++) {
       const int64_t j = j0 + (int64_t)k * kCompThreads;
-      v[k] = (j < jend) ? __ldcs(x.R + j) : 0.0;
+      v[k] = (j < jend) ? (x.compact ? __ldcg(src + j) : __ldcs(src + j)) : 0.0;
       cnt += (v[k] != 0.0) ? 1 : 0;
     }
     int incl = cnt;
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *
       r[0] = (int32_t)(j0 + (int64_t)k * kCompThreads);
       r[1] = (int32_t)(bits & 0xffffffffll);
       r[2] = (int32_t)(bits >> 32);
-      x.R[j0 + (int64_t)k * kCompThreads] = 0.0;
+      src[j0 + (int64_t)k * kCompThreads] = 0.0;
       sent += v[k];
       pos++;
     }
@@ -296,6 +300,13 @@ __global__ void __launch_bounds__(kCompThreads) k_compact_remote(const Scalars *
     const unsigned long long c = *cn;
     x.sendcnt[threadIdx.x] = (threadIdx.x == x.rank) ? 0 : (int64_t)c;
     *cn = 0ull;
+    if (x.compact) {  // cold records reserved in the owner's inbox this cycle (k_cycle)
+      volatile unsigned long long *ct = x.ctop + 16 * threadIdx.x;
+      x.coldcnt[threadIdx.x] = (threadIdx.x == x.rank) ? 0 : (int64_t)*ct;
+      *ct = 0ull;
+    } else if (x.coldcnt) {
+      x.coldcnt[threadIdx.x] = 0;
+    }
     if (x.ring && threadIdx.x != x.rank) {  // publish the new tail in the owner's control line
       const unsigned long long t = x.tsent[threadIdx.x] + c;
       x.tsent[threadIdx.x] = t;
@@ -321,9 +332,23 @@ __global__ void k_apply_recv(double *__restrict__ F, int64_t lo, const int32_t *
 // (parity, peer); the counts come from the gathered sweep headers (device-resident)
 __global__ void k_apply_inbox(double *__restrict__ F, int64_t lo, const char *__restrict__ inbox,
                               int64_t icap, int ipar, const int64_t *__restrict__ ghdr, int world,
-                              int me, const Scalars *sc) {
+                              int me, const Scalars *sc, int64_t ccap, size_t cold_off0,
+                              size_t fill_off0) {
   if (sc->stop) return;   // batched loop: a sweep after convergence (stale headers) does nothing
-  const int hw = 8 + world;
+  const int hw = hdr_words(world);
+  for (int q = 0; q < world; q++) {   // compact path: the cold records sender q wrote (16 B)
+    if (q == me || ccap == 0) continue;
+    const int64_t mc = ghdr[(int64_t)q * hw + 8 + world + me];
+    const ColdRec *rec = reinterpret_cast<const ColdRec *>(inbox + cold_off0) + (2 * q + ipar) * ccap;
+    const int32_t *fill = reinterpret_cast<const int32_t *>(inbox + fill_off0) +
+                          (2 * q + ipar) * (ccap / kColdChunk);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < mc;
+         k += (int64_t)gridDim.x * blockDim.x) {
+      if ((int)(k % kColdChunk) >= fill[k / kColdChunk]) continue;
+      const int4 r = *reinterpret_cast<const int4 *>(rec + k);
+      red_add_f64(F + ((int64_t)r.x - lo), __hiloint2double(r.w, r.z));
+    }
+  }
   for (int q = 0; q < world; q++) {
     if (q == me) continue;
     const int64_t m = ghdr[(int64_t)q * hw + 8 + me];
@@ -432,18 +457,22 @@ __global__ void k_apply_dense(double *__restrict__ F, const double *__restrict__
 __global__ void k_dist_finalize(const SweepArgs a, const int64_t *ghdr, int world, int async,
                                 int me, int p2p) {
   if (threadIdx.x != 0 || a.sc->stop) return;
-  const int hw = 8 + world;
+  const int hw = hdr_words(world);
   {  // exchange counters (entries this rank sent; every rank's entries of this sweep)
-    int64_t mine = 0, all = 0;
+    int64_t mine = 0, all = 0, cold = 0;
     for (int p = 0; p < world; p++)
       for (int q = 0; q < world; q++)
         if (p != q) {
           const int64_t c = ghdr[(int64_t)p * hw + 8 + q];
           all += c;
-          if (p == me) mine += c;
+          if (p == me) {
+            mine += c;
+            cold += ghdr[(int64_t)p * hw + 8 + world + q];
+          }
         }
     volatile Scalars *vs = a.sc;
     vs->x_entries = vs->x_entries + mine;
+    vs->x_cold = vs->x_cold + cold;
     vs->x_lists_last = all;
     if (p2p) vs->x_p2p = vs->x_p2p + 1;
   }
@@ -476,7 +505,7 @@ int grid_of(int64_t n, int sms) {
 // global sum F (exact local tree sum, then the allreduce); set_r: also r = that sum
 di_status global_sum_F(Graph &g, int set_r, int64_t *launches) {
   launch_reduce_F(g, launches);
-  double *scratch = reinterpret_cast<double *>(g.hdr + 8 + g.world);
+  double *scratch = reinterpret_cast<double *>(g.hdr + hdr_words(g.world));
   k_copy_resid<<<1, 1, 0, g.stream>>>(g.sc, scratch);
   di_status s = g.comm->allreduce_f64(scratch, 1, g.stream);
   if (s != DI_OK) return s;
@@ -485,26 +514,94 @@ di_status global_sum_F(Graph &g, int set_r, int64_t *launches) {
   return DI_OK;
 }
 
+// links of this rank whose target is a cold remote target (j outside [lo, hi) and not in its
+// owner's hot prefix), per owner: the capacity of the cold regions of the inboxes
+__global__ void k_cold_remote_count(const int32_t *__restrict__ col, int64_t L, DistBounds bd,
+                                    int me, const int64_t *rt, unsigned long long *cnt) {
+  __shared__ unsigned int h[kMaxWorld];
+  if (threadIdx.x < kMaxWorld) h[threadIdx.x] = 0u;
+  __syncthreads();
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = col[k];
+    int p = 0;
+    while (p + 1 < bd.world && j >= bd.b[p + 1]) p++;
+    if (p != me && j - bd.b[p] >= rt[p]) atomicAdd(&h[p], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < bd.world && h[threadIdx.x]) atomicAdd(cnt + threadIdx.x, (unsigned long long)h[threadIdx.x]);
+}
+
 }  // namespace
 
-di_status alloc_dist(Graph &g) {
+// the global-size remote accumulator and the send/recv buffers: only the bulk partitioned sweep,
+// the asynchronous multi-GPU cycles (rings), the send/recv and dense exchanges use them
+di_status ensure_R(Graph &g) {
+  if (g.R_ready) return DI_OK;
   const int64_t N = g.n_global;
   const int G = g.world;
   DI_CK(dmalloc(&g.R, (size_t)N * 8));
   DI_CK(dmemset(g.R, 0, (size_t)N * 8));
   DI_CK(dmalloc(&g.sval, (size_t)N * 12));   // send records, segment p at record b[p]
+  const size_t cap = (size_t)std::max<int64_t>(1, (int64_t)(G - 1) * g.n);
+  DI_CK(dmalloc(&g.rid, cap * 12));          // received records
+  g.R_ready = true;
+  return DI_OK;
+}
+
+di_status alloc_dist(Graph &g) {
+  const int G = g.world;
   DI_CK(dmalloc(&g.tcnt, (size_t)(G + 1) * 32 * 8));   // + the compaction's block ticket
   DI_CK(dmemset(g.tcnt, 0, (size_t)(G + 1) * 32 * 8));
-  const size_t hw = (size_t)(8 + G);
-  DI_CK(dmalloc(&g.hdr, 8 * 8 + hw * 8));   // +8 words: global_sum_F's scratch at dsum[3..]
+  const size_t hw = (size_t)hdr_words(G);
+  DI_CK(dmalloc(&g.hdr, 8 * 8 + hw * 8));   // +8 words: global_sum_F's scratch after the header
   DI_CK(dmemset(g.hdr, 0, 8 * 8 + hw * 8));
   DI_CK(dmalloc(&g.ghdr, (size_t)G * hw * 8));
   DI_CK(cudaMallocHost(&g.ghdr_h, (size_t)G * hw * 8));
   g.dsum = reinterpret_cast<double *>(g.hdr);
   g.isum = g.hdr + 4;
   g.sendcnt = g.hdr + 8;
-  const size_t cap = (size_t)std::max<int64_t>(1, (int64_t)(G - 1) * g.n);
-  DI_CK(dmalloc(&g.rid, cap * 12));          // received records
+  // compact remote path: accumulator of the hot remote targets, cold-record counters, and the
+  // capacity of the inboxes' cold regions (the largest count of any sender -> owner pair plus
+  // one chunk per warp of the sender's cycle grid; allgathered: the same on every rank)
+  int64_t rsum = 0;
+  for (int p = 0; p < G; p++) rsum += g.rtier[p];
+  const bool compact_ok = g.reordered && g.remote_compact && rsum > 0;
+  g.ccap = 0;
+  if (compact_ok) {
+    DI_CK(dmalloc(&g.racc, (size_t)rsum * 8));
+    DI_CK(dmemset(g.racc, 0, (size_t)rsum * 8));
+    DI_CK(dmalloc(&g.ctop, (size_t)2 * kMaxWorld * 16 * 8));
+    DI_CK(dmemset(g.ctop, 0, (size_t)2 * kMaxWorld * 16 * 8));
+    int64_t *rtd = nullptr;
+    unsigned long long *cnt = nullptr;
+    DI_CK(dmalloc(&rtd, kMaxWorld * 8));
+    DI_CK(dmalloc(&cnt, (size_t)G * G * 8));
+    DI_CK(cudaMemcpyAsync(rtd, g.rtier, kMaxWorld * 8, cudaMemcpyHostToDevice, g.stream));
+    DI_CK(cudaMemsetAsync(cnt, 0, (size_t)G * G * 8, g.stream));
+    if (g.l > 0)
+      k_cold_remote_count<<<g.num_sms * 8, 256, 0, g.stream>>>(g.col, g.l, g.bounds, g.rank, rtd,
+                                                                cnt + (size_t)g.rank * G);
+    std::vector<int64_t> mine(G);
+    DI_CK(cudaMemcpyAsync(mine.data(), cnt + (size_t)g.rank * G, (size_t)G * 8, cudaMemcpyDeviceToHost,
+                          g.stream));
+    DI_CK(cudaStreamSynchronize(g.stream));
+    const int64_t slack = cycle_warps(g) * (int64_t)kColdChunk;
+    for (int p = 0; p < G; p++) mine[p] += slack;
+    DI_CK(cudaMemcpy(cnt + (size_t)g.rank * G, mine.data(), (size_t)G * 8, cudaMemcpyHostToDevice));
+    di_status s0 = g.comm->allgather(cnt + (size_t)g.rank * G, cnt, (size_t)G * 8, g.stream);
+    if (s0 != DI_OK) return s0;
+    std::vector<int64_t> all((size_t)G * G);
+    DI_CK(cudaMemcpyAsync(all.data(), cnt, (size_t)G * G * 8, cudaMemcpyDeviceToHost, g.stream));
+    DI_CK(cudaStreamSynchronize(g.stream));
+    dfree(rtd);
+    dfree(cnt);
+    int64_t mx = kColdChunk;
+    for (int q = 0; q < G; q++)
+      for (int p = 0; p < G; p++)
+        if (p != q) mx = std::max<int64_t>(mx, all[(size_t)q * G + p]);
+    g.ccap = (mx + kColdChunk - 1) / kColdChunk * kColdChunk;
+  }
   // fused exchange: a double-buffered inbox of G segments of (largest range) records per rank,
   // written by the peers' compaction kernels through peer memory (collective; every rank agrees
   // on the outcome, else all fall back to exchange())
@@ -517,8 +614,13 @@ di_status alloc_dist(Graph &g) {
     int64_t mx = 1;
     for (int p = 0; p < G; p++) mx = std::max<int64_t>(mx, g.bounds.b[p + 1] - g.bounds.b[p]);
     g.icap = mx;
+    // [G segments of kRingSlots x icap 12-B records][G control lines][cold regions: per sender 2
+    // parities x ccap 16-B records][their chunk fills: per sender 2 x ccap / kColdChunk int32]
+    g.cold_off0 = (ring_ctrl_offset(G, mx) + (size_t)256 * G + 255) / 256 * 256;
+    g.fill_off0 = (g.cold_off0 + (size_t)G * 2 * (size_t)g.ccap * sizeof(ColdRec) + 255) / 256 * 256;
+    const size_t ibytes = g.fill_off0 + (size_t)G * 2 * (size_t)(g.ccap / kColdChunk) * 4 + 256;
     std::vector<char *> peers;
-    di_status s = g.comm->make_inbox(ring_ctrl_offset(G, mx) + (size_t)256 * G, &peers);
+    di_status s = g.comm->make_inbox(ibytes, &peers);
     if (s == DI_OK &&  // ring tails start at 0 (the allreduce below orders it before any use)
         cudaMemset(peers[g.rank] + ring_ctrl_offset(G, mx), 0, (size_t)256 * G) != cudaSuccess)
       s = DI_ECUDA;
@@ -542,7 +644,7 @@ di_status alloc_dist(Graph &g) {
 }
 
 void free_dist(Graph &g) {
-  void *p[] = {g.R, g.sval, g.tcnt, g.hdr, g.ghdr, g.rid, g.ring};
+  void *p[] = {g.R, g.sval, g.tcnt, g.hdr, g.ghdr, g.rid, g.ring, g.racc, g.ctop};
   for (void *q : p)
     if (q) dfree(q);
   if (g.ghdr_h) cudaFreeHost(g.ghdr_h);
@@ -557,7 +659,7 @@ di_status dist_residual(Graph &g, double *l1) {
   int64_t launches = 0;
   di_status s = global_sum_F(g, 0, &launches);
   if (s != DI_OK) return s;
-  DI_CK(cudaMemcpyAsync(l1, g.hdr + 8 + g.world, 8, cudaMemcpyDeviceToHost, g.stream));
+  DI_CK(cudaMemcpyAsync(l1, g.hdr + hdr_words(g.world), 8, cudaMemcpyDeviceToHost, g.stream));
   DI_CK(cudaStreamSynchronize(g.stream));
   return DI_OK;
 }
@@ -596,6 +698,11 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
     s.mode = MODE_PUSH;
   }
   double e_global = resume ? g.e_global : 0.0;
+  g.cur_compact = 0;
+  {
+    di_status rs = ensure_R(g);   // the rings compact the global-size accumulator
+    if (rs != DI_OK) return rs;
+  }
   DI_CK(cudaEventRecord(t0, g.stream));
   DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
   DI_CK(cudaMemsetAsync(g.R, 0, (size_t)g.n_global * 8, g.stream));
@@ -603,7 +710,7 @@ di_status solve_dist_async(Graph &g, double d, const double *B, double tol, int 
   if (!resume) launch_init(g, B, d, &launches);
   unsigned long long *tsent = g.ring, *head = g.ring + kMaxWorld, *snap = g.ring + 2 * kMaxWorld;
   double *rs = reinterpret_cast<double *>(g.ring + 3 * kMaxWorld);
-  double *scratch = reinterpret_cast<double *>(g.hdr + 8 + g.world);
+  double *scratch = reinterpret_cast<double *>(g.hdr + hdr_words(g.world));
   unsigned long long sent0[kMaxWorld];   // ring tails at the start: entries sent = difference
   DI_CK(cudaMemcpyAsync(sent0, tsent, sizeof(sent0), cudaMemcpyDeviceToHost, g.stream));
   DI_CK(cudaMemsetAsync(rs, 0, 8 * 8, g.stream));
@@ -776,10 +883,26 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
     s.trace = (flags & DI_TRACE) ? 1 : 0;
     s.mode = MODE_PUSH;
   }
+  // the compact remote path (hot remote accumulator + cold records into the owners' inboxes):
+  // asynchronous cycles through peer memory; everything else uses the global-size accumulator
+  const bool p2p = g.p2p && !(flags & DI_XCHG_NOP2P);
+  const bool compact = async && p2p && g.racc && g.ccap > 0 && !(flags & DI_XCHG_DENSE);
+  if (!compact) {
+    di_status rs = ensure_R(g);
+    if (rs != DI_OK) return rs;
+  }
   DI_CK(cudaEventRecord(t0, g.stream));
   DI_CK(cudaMemcpyAsync(g.sc, g.sc_host, sizeof(Scalars), cudaMemcpyHostToDevice, g.stream));
-  DI_CK(cudaMemsetAsync(g.R, 0, (size_t)g.n_global * 8, g.stream));
+  if (compact) {
+    int64_t rsum = 0;
+    for (int p = 0; p < G; p++) rsum += g.rtier[p];
+    DI_CK(cudaMemsetAsync(g.racc, 0, (size_t)rsum * 8, g.stream));
+    DI_CK(cudaMemsetAsync(g.ctop, 0, (size_t)2 * kMaxWorld * 16 * 8, g.stream));
+  } else {
+    DI_CK(cudaMemsetAsync(g.R, 0, (size_t)g.n_global * 8, g.stream));
+  }
   DI_CK(cudaMemsetAsync(g.tcnt, 0, (size_t)(G + 1) * 32 * 8, g.stream));
+  g.cur_compact = compact ? 1 : 0;
   di_status s = DI_OK;
   if (!resume) {
     launch_init(g, B, d, &launches);  // F = B (local slice), H = 0; local sum
@@ -792,8 +915,8 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   bool converged = err_of(g.sc_host->r, g.sc_host->e) <= tol;
   const SweepArgs a = sweep_args(g, 0);
   DistArgs x = dist_args(g);
-  const bool p2p = g.p2p && !(flags & DI_XCHG_NOP2P);
   x.p2p = p2p ? 1 : 0;
+  x.compact = compact ? 1 : 0;
   int par = 0;   // inbox parity of the current sweep
   int occ = 0;
   if (g.has_loops)
@@ -804,7 +927,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   std::vector<const void *> sb(G);
   std::vector<void *> rb(G);
   std::vector<size_t> s12(G), r12(G);
-  const size_t hw = (size_t)(8 + G);
+  const size_t hw = (size_t)hdr_words(G);
   double xbytes = 0.0, xdense = 0.0;
   int64_t xentries = 0, ndense = 0, np2p = 0;
   // exchange choice: sparse lists unless the last sparse sweep's lists
@@ -812,7 +935,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   // after kDenseRun dense sweeps one sparse sweep measures the lists again
   constexpr int kDenseRun = 4;
   const bool force_dense = (flags & DI_XCHG_DENSE) && G > 1;
-  const bool force_sparse = (flags & DI_XCHG_SPARSE) || G == 1;
+  const bool force_sparse = (flags & DI_XCHG_SPARSE) || G == 1 || compact;
   int64_t last_lists = -1;
   int dense_run = 0;
   int64_t launched = 0;
@@ -834,6 +957,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       const int64_t sw0 = g.sc_host->sweeps;
       for (int64_t j = 0; j < k; j++) {
         if (!async) launch_select(g, 0, &launches);
+        g.cur_par = par;   // the cold regions written by this cycle
         if (async)
           launch_cycle(g, &launches);
         else if (g.has_loops)
@@ -844,7 +968,8 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
         k_compact_remote<<<g.num_sms * kCompBlocksPerSM, kCompThreads, 0, g.stream>>>(g.sc, x);
         if ((s = g.comm->allgather(g.hdr, g.ghdr, (size_t)hw * 8, g.stream)) != DI_OK) return s;
         k_apply_inbox<<<g.num_sms * 4, 256, 0, g.stream>>>(g.F, g.lo, g.inbox[me], g.icap, par,
-                                                          g.ghdr, G, me, g.sc);
+                                                          g.ghdr, G, me, g.sc, compact ? g.ccap : 0,
+                                                          g.cold_off0, g.fill_off0);
         k_dist_finalize<<<1, 32, 0, g.stream>>>(a, g.ghdr, G, async ? 1 : 0, me, 1);
         launches += 4;
         par ^= 1;
@@ -876,6 +1001,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       if (prof) DI_CK(cudaEventRecord(pe[0], g.stream));
       if (!async) launch_select(g, 0, &launches);
       if (prof) DI_CK(cudaEventRecord(pe[1], g.stream));
+      g.cur_par = par;
       if (async)
         launch_cycle(g, &launches);   // the asynchronous cycle on this rank's range (R7)
       else if (g.has_loops)
@@ -936,7 +1062,8 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       if (!dense && p2p) {  // the records are already in the owners' inboxes: apply ours
         for (int p = 0; p < G; p++) xentries += (p == me) ? 0 : g.ghdr_h[(size_t)me * hw + 8 + p];
         k_apply_inbox<<<g.num_sms * 4, 256, 0, g.stream>>>(g.F, g.lo, g.inbox[me], g.icap, par,
-                                                          g.ghdr, G, me, g.sc);
+                                                          g.ghdr, G, me, g.sc, compact ? g.ccap : 0,
+                                                          g.cold_off0, g.fill_off0);
         launches++;
         par ^= 1;
         np2p++;
@@ -1016,11 +1143,12 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
     st->error_estimate = c.resid / (1.0 - d - d * c.e);
     st->converged = converged ? 1 : 0;
     st->variant = variant;
-    xbytes = 12.0 * (double)c.x_entries + xdense;
+    xbytes = 12.0 * (double)c.x_entries + 16.0 * (double)c.x_cold + xdense;
     st->exchange_bytes = xbytes;
     st->dense_exchanges = ndense;
     st->p2p_exchanges = np2p + c.x_p2p;
     st->exchange_entries = c.x_entries;
+    st->exchange_cold = c.x_cold;
     st->push_ms = push_ms;
     st->select_ms = select_ms;
     st->push_launches = push_launches;

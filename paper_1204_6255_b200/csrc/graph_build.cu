@@ -517,6 +517,15 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
       const int64_t m = bd.b[r + 1] - bd.b[r];
       pp.hot[r] = (r == 0) ? g.hot_count : 0;
       pp.tier[r] = (r == 0 && g.cold_lo < n) ? tier : 0;
+      // partitioned: the hot remote targets of every range first (compact remote accumulator,
+      // dist.cu); the same on every rank (bounds, world and the L2 size of this GPU type)
+      g.rtier[r] = 0;
+      if (g.partitioned && g.remote_compact) {
+        const int64_t want = g.remote_tier > 0 ? g.remote_tier
+                                               : (int64_t)(kColdHotL2 * (double)l2 / 8.0 / world);
+        g.rtier[r] = std::max<int64_t>(0, std::min<int64_t>(m, want));
+        pp.tier[r] = g.rtier[r] < m ? g.rtier[r] : 0;
+      }
       pp.stripes2[r] = prime_at_most(std::max<int64_t>(1, pp.tier[r] >> 10));
       pp.stripes[r] = g.stripes > 0 ? (int64_t)g.stripes
                                      : prime_at_most(std::max<int64_t>(1, (m - pp.hot[r] - pp.tier[r]) >> 10));

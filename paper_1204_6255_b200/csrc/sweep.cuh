@@ -316,6 +316,18 @@ struct DistArgs {
   int ring;    // DI_DIST_ASYNC: append at the ring tail, publish it, sum the sent fluid
   unsigned long long *tsent;  // [kMaxWorld] records sent to each owner so far (ring tails)
   double *sent;               // fluid compacted this cycle (ring mode)
+  // compact remote path: the first rt[p] ids of every range p are its hot remote
+  // targets, accumulated in racc[hoff[p] + (j - b[p])] (L2-resident); a push to a colder remote
+  // target is a 16-B record written straight into the owner's inbox (cold region of this
+  // sender, parity ipar), in warp chunks reserved with the counters ctop[2p + parity]
+  int compact;                // 1: this path (k_cycle<DIST, COLD>, k_compact_remote over racc)
+  double *racc;
+  int64_t rt[kMaxWorld];
+  int64_t hoff[kMaxWorld + 1];
+  int64_t ccap;               // cold records per (sender, parity) region of an inbox
+  size_t cold_off0, fill_off0;  // byte offsets of the cold regions / their chunk fills in an inbox
+  unsigned long long *ctop;   // [2 * kMaxWorld] one line each
+  int64_t *coldcnt;           // [world] (view into the sweep header, after sendcnt)
 };
 
 inline DistArgs dist_args(Graph &g) {
@@ -335,8 +347,24 @@ inline DistArgs dist_args(Graph &g) {
   x.isum = g.isum;
   x.bd = g.bounds;
   x.rank = g.rank;
+  x.compact = 0;
+  x.racc = g.racc;
+  x.hoff[0] = 0;
+  for (int p = 0; p < kMaxWorld; p++) {
+    x.rt[p] = p < g.world ? g.rtier[p] : 0;
+    x.hoff[p + 1] = x.hoff[p] + x.rt[p];
+  }
+  x.ccap = g.ccap;
+  x.cold_off0 = g.cold_off0;
+  x.fill_off0 = g.fill_off0;
+  x.ctop = g.ctop;
+  x.coldcnt = g.sendcnt ? g.sendcnt + g.world : nullptr;
   return x;
 }
+
+// sweep header words per rank: 8 sums, then per peer the compact records and the cold records
+// sent to it; global_sum_F's scratch follows the header
+__host__ __device__ inline int hdr_words(int world) { return 8 + 2 * world; }
 
 
 // A push to a target j that another rank owns: an fp64 RED into the remote accumulator R[j]
