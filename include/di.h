@@ -217,6 +217,8 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
  *                                          records straight into the owner's inbox (0: the
  *                                          global-size accumulator and its compaction scan)
  *   "remote_tier"    0        >= 0      U: hot remote targets per range (0: half the L2 over G)
+ *   "long_lanes"     1        0..1      U: DI_ASYNC long rows (> 256 links) with lane-consecutive
+ *                                          targets (0: int4 groups per lane)
  * DI_EINVAL for an unknown name or a value out of range (integers must be integral). */
 di_status di_set_option(const char *name, double value);
 di_status di_get_option(const char *name, double *value);

@@ -334,6 +334,7 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
     g->p2p_force = o.p2p_force;
     g->remote_compact = o.remote_compact;
     g->remote_tier = o.remote_tier;
+    g->long_lanes = o.long_lanes;
   }
   di_status s = build_graph(*g, src, dst, n_links, flags);
   if (s == DI_OK) s = alloc_state(*g);
@@ -360,6 +361,7 @@ const OptDesc kOpts[] = {
     {"cycle_grid_div", 1, 4096, true}, {"cycle_times", 0, 1, true}, {"p2p", 0, 1, true},
     {"p2p_force", 0, 1, true},      {"build_trace", 0, 1, true},
     {"remote_compact", 0, 1, true}, {"remote_tier", 0, 2147483647.0, true},
+    {"long_lanes", 0, 1, true},
 };
 }  // namespace
 
@@ -390,6 +392,7 @@ di_status di_set_option(const char *name, double value) {
   else if (n == "build_trace") o.build_trace = iv;
   else if (n == "remote_compact") o.remote_compact = iv;
   else if (n == "remote_tier") o.remote_tier = (int64_t)value;
+  else if (n == "long_lanes") o.long_lanes = iv;
   return DI_OK;
 }
 
@@ -412,6 +415,7 @@ di_status di_get_option(const char *name, double *value) {
   else if (n == "build_trace") *value = o.build_trace;
   else if (n == "remote_compact") *value = o.remote_compact;
   else if (n == "remote_tier") *value = (double)o.remote_tier;
+  else if (n == "long_lanes") *value = o.long_lanes;
   else return fail(DI_EINVAL, "di_get_option: unknown option '" + n + "'");
   return DI_OK;
 }

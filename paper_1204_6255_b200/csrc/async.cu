@@ -512,6 +512,30 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         const int32_t gi = LOOPS ? (int32_t)(tile * kCycTile + s_ri[slot] + a.lo) : -1;
         const int64_t a0 = beg & ~3ll;
         const int nvec = (int)((end - a0 + 3) >> 2);
+        if (!COLD && !DIST && a.long_lanes) {
+          // lane-consecutive targets: lane l takes links beg + 32u + l, so the 32 REDs of one
+          // instruction go to 32 consecutive (sorted) targets of the row, which share L2 lines
+          // where the row is dense in the hot ids; scalar coalesced loads, no masked lanes
+          for (int64_t p0 = beg; p0 < end; p0 += 32 * 8) {
+            int32_t jj[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+              const int64_t p = p0 + 32 * u + lane;
+              jj[u] = p < end ? ld_col(col + p, pol) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+              const int32_t j = jj[u];
+              if (j >= 0 && (!LOOPS || j != gi)) {
+                if (j < hot_lim)
+                  red_add_f64(rep + (int64_t)(copy * kRepl + j) * kRepStride, v);
+                else
+                  red_add_f64_hint(F + j, v, fpol);
+              }
+            }
+          }
+          continue;
+        }
         for (int vb = 0; vb < nvec; vb += 128) {
           int4 xq[4];
 #pragma unroll
@@ -955,6 +979,7 @@ static int cold_apply_grid(const Graph &g) {
 
 void launch_cycle(Graph &g, int64_t *launches) {
   SweepArgs a = sweep_args(g, 0);
+  a.long_lanes = g.long_lanes;
   const bool cold = g.cold_rec && !g.partitioned;
   if (cold) {
     a.cold_hot_tiles = (g.cold_lo + kCycTile - 1) / kCycTile;

@@ -110,6 +110,7 @@ struct Options {
   int build_trace = 0;       // "build_trace": host timestamps of the build phases (stderr)
   int remote_compact = 1;    // "remote_compact": hot remote accumulator + cold records (P2P)
   int64_t remote_tier = 0;   // "remote_tier": hot remote targets per range (0: auto)
+  int long_lanes = 1;        // "long_lanes": k_cycle long rows with lane-consecutive targets
 };
 Options options();           // a snapshot of the current options
 
@@ -288,7 +289,8 @@ struct Graph {
   size_t cold_off0 = 0, fill_off0 = 0;
   unsigned long long *ctop = nullptr;
   bool R_ready = false;           // R (global-size accumulator) allocated: bulk / ring / send-recv
-  int cur_par = 0, cur_compact = 0;  // solve_dist -> launch_cycle: inbox parity, compact path
+  int cur_par = 0, cur_compact = 0;
+  int long_lanes = 1;             // option long_lanes  // solve_dist -> launch_cycle: inbox parity, compact path
 };
 
 // ---------------------------------------------------------------- device memory

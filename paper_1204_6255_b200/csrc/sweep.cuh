@@ -45,6 +45,7 @@ struct SweepArgs {
   int64_t cold_lo;
   int64_t cold_hot_tiles;   // tiles holding first-tier ids (interleaved over the cycle)
   int cold_shift, cold_nbins;
+  int long_lanes;           // k_cycle long rows: lane-consecutive targets (option long_lanes)
   ColdRec *cold_rec;
   const int64_t *cold_off;
   unsigned long long *cold_top;
@@ -395,6 +396,7 @@ inline SweepArgs sweep_args(Graph &g, int test_mode, int blk = 0, int blocks = 1
   a.rec_v = nullptr;
   a.cold_lo = INT64_MAX;
   a.cold_hot_tiles = 0;
+  a.long_lanes = 0;
   a.cold_shift = 0;
   a.cold_nbins = 0;
   a.cold_rec = nullptr;
