@@ -181,7 +181,15 @@ struct ColdSm {   // the warp's chunk state and the block's per-bin pointers (sh
   ColdRec *const *cptr;
   int32_t *const *fptr;
   unsigned long long *const *tptr;
+  // partitioned: range bounds, hot-prefix sizes and accumulator offsets per owner, and the owner
+  // of every 2^oshift-id bucket (shared memory: per-lane indexed loads from the parameter block
+  // serialise in the constant cache)
+  const int64_t *b, *rt, *hoff;
+  const int8_t *otab;
+  int oshift;
 };
+
+constexpr int kOwnerTab = 1024;   // owner lookup buckets (partitioned COLD cycles)
 
 // COLD push of one int4 group (warp-collective: every lane calls it; `valid` = the lane has a
 // group). One GPU: hot ids to the replicated accumulators, first-tier targets (j < cold_lo) a
@@ -207,11 +215,11 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistAr
         if (jl >= 0 && jl < a.n) {
           red_add_f64_hint(a.F + jl, v, fpol);
         } else {
-          int pp = 0;
-          while (pp + 1 < x.bd.world && (int64_t)j >= x.bd.b[pp + 1]) pp++;
-          const int64_t off = (int64_t)j - x.bd.b[pp];
-          if (off < x.rt[pp]) {
-            red_add_f64_hint(x.racc + x.hoff[pp] + off, v, fpol);
+          int pp = cs.otab[j >> cs.oshift];   // owner of the bucket's first id, then forward
+          while ((int64_t)j >= cs.b[pp + 1]) pp++;
+          const int64_t off = (int64_t)j - cs.b[pp];
+          if (off < cs.rt[pp]) {
+            red_add_f64_hint(x.racc + cs.hoff[pp] + off, v, fpol);
           } else if (!cold_put(cs.cptr, cs.cnt, cs.base, pp, j, v)) {
             pending |= 1u << c;
             bins |= (unsigned)pp << (5 * c);
@@ -247,6 +255,10 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   __shared__ ColdRec *s_cptr[NCB];
   __shared__ int32_t *s_fptr[NCB];
   __shared__ unsigned long long *s_tptr[NCB];
+  constexpr int NDW = (COLD && DIST) ? kMaxWorld + 1 : 1;
+  constexpr int NOT = (COLD && DIST) ? kOwnerTab + 1 : 1;
+  __shared__ int64_t s_db[NDW], s_drt[NDW], s_dhoff[NDW];
+  __shared__ int8_t s_otab[NOT];
   __shared__ int64_t s_rb[kCycTile];   // long rows of the tile: first link
   __shared__ int32_t s_ro[kCycTile];   // #links
   __shared__ double s_rv[kCycTile];    // v = T d / o
@@ -307,7 +319,24 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       }
     }
   }
-  const ColdSm cs{ccb, cce, s_cptr, s_fptr, s_tptr};
+  int oshift = 0;
+  if (COLD && DIST) {
+    const int G = x.bd.world;
+    const int64_t N = x.bd.b[G];
+    while ((N >> oshift) >= kOwnerTab) oshift++;
+    for (int k = threadIdx.x; k <= G; k += blockDim.x) {
+      s_db[k] = k < G ? x.bd.b[k] : INT64_MAX;   // b[G] = +inf: the forward scan stops there
+      s_drt[k] = k < G ? x.rt[k] : 0;
+      s_dhoff[k] = x.hoff[k];
+    }
+    for (int k = threadIdx.x; k <= kOwnerTab; k += blockDim.x) {
+      const int64_t id = (int64_t)k << oshift;
+      int p = 0;
+      while (p + 1 < G && id >= x.bd.b[p + 1]) p++;
+      s_otab[k] = (int8_t)p;
+    }
+  }
+  const ColdSm cs{ccb, cce, s_cptr, s_fptr, s_tptr, s_db, s_drt, s_dhoff, s_otab, oshift};
 
   for (;;) {
     if (threadIdx.x == 0) {
