@@ -166,8 +166,8 @@ __device__ __forceinline__ bool cold_put(ColdRec *const *cptr, int32_t *cnt, con
 __device__ __noinline__ void cold_retry(int nbins, ColdRec *const *cptr, int32_t *const *fptr,
                                         unsigned long long *const *tptr, int32_t *cnt,
                                         int32_t *base, int4 q, unsigned pending, unsigned bins,
-                                        double v, int lane) {
-  const int32_t jj[4] = {q.x, q.y, q.z, q.w};
+                                        double v, int lane, int32_t dec) {
+  const int32_t jj[4] = {q.x - dec, q.y - dec, q.z - dec, q.w - dec};   // (dec: column encoding)
   while (__any_sync(0xffffffffu, pending != 0u)) {
     cold_refill(nbins, fptr, tptr, cnt, base, lane);
     for (int c = 0; c < 4; c++)
@@ -187,6 +187,7 @@ struct ColdSm {   // the warp's chunk state and the block's per-bin pointers (sh
   const int64_t *b, *rt, *hoff;
   const int8_t *otab;
   int oshift;
+  int64_t rsum;   // hot remote slots (sum of rt)
 };
 
 constexpr int kOwnerTab = 1024;   // owner lookup buckets (partitioned COLD cycles)
@@ -211,16 +212,18 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistAr
     const int32_t j = c == 0 ? q.x : (c == 1 ? q.y : (c == 2 ? q.z : q.w));
     if (valid && p >= beg && p < end && (!LOOPS || j != gi)) {
       if (DIST) {
-        const int64_t jl = (int64_t)j - a.lo;
-        if (jl >= 0 && jl < a.n) {
-          red_add_f64_hint(a.F + jl, v, fpol);
+        // the compact path's encoded column (dist.cu k_encode_col): [0, n) local ids, then the
+        // hot remote targets' accumulator slots, then n + R + global id for colder remote targets
+        const uint32_t e = (uint32_t)j;
+        if (e < (uint32_t)a.n) {
+          red_add_f64_hint(a.F + e, v, fpol);
+        } else if (e < (uint32_t)(a.n + cs.rsum)) {
+          red_add_f64_hint(x.racc + (e - (uint32_t)a.n), v, fpol);
         } else {
-          int pp = cs.otab[j >> cs.oshift];   // owner of the bucket's first id, then forward
-          while ((int64_t)j >= cs.b[pp + 1]) pp++;
-          const int64_t off = (int64_t)j - cs.b[pp];
-          if (off < cs.rt[pp]) {
-            red_add_f64_hint(x.racc + cs.hoff[pp] + off, v, fpol);
-          } else if (!cold_put(cs.cptr, cs.cnt, cs.base, pp, j, v)) {
+          const int32_t gj = (int32_t)(e - (uint32_t)(a.n + cs.rsum));
+          int pp = cs.otab[gj >> cs.oshift];   // owner of the bucket's first id, then forward
+          while ((int64_t)gj >= cs.b[pp + 1]) pp++;
+          if (!cold_put(cs.cptr, cs.cnt, cs.base, pp, gj, v)) {
             pending |= 1u << c;
             bins |= (unsigned)pp << (5 * c);
           }
@@ -240,7 +243,7 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistAr
   }
   if (__any_sync(0xffffffffu, pending != 0u))
     cold_retry(DIST ? x.bd.world : a.cold_nbins, cs.cptr, cs.fptr, cs.tptr, cs.cnt, cs.base, q,
-               pending, bins, v, lane);
+               pending, bins, v, lane, DIST ? (int32_t)(a.n + cs.rsum) : 0);
 }
 
 // TEST (di_test_cycle, include/di_test.h): the selection records (T, v) per node in a.rec_T /
@@ -336,7 +339,11 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       s_otab[k] = (int8_t)p;
     }
   }
-  const ColdSm cs{ccb, cce, s_cptr, s_fptr, s_tptr, s_db, s_drt, s_dhoff, s_otab, oshift};
+  const ColdSm cs{ccb, cce, s_cptr, s_fptr, s_tptr, s_db, s_drt, s_dhoff, s_otab, oshift,
+                  (COLD && DIST) ? x.hoff[x.bd.world] : 0};
+  // the row's own id in the column's numbering (self-loop test): the compact path's columns are
+  // encoded with local ids, the others hold global ids
+  const int64_t gbase = (COLD && DIST) ? 0 : a.lo;
 
   for (;;) {
     if (threadIdx.x == 0) {
@@ -538,7 +545,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         const int64_t beg = rbeg + (int64_t)(c - s_rp[lo]) * kAsyncChunk;
         const int64_t end = min(rbeg + (int64_t)s_ro[slot], beg + kAsyncChunk);
         const double v = s_rv[slot];
-        const int32_t gi = LOOPS ? (int32_t)(tile * kCycTile + s_ri[slot] + a.lo) : -1;
+        const int32_t gi = LOOPS ? (int32_t)(tile * kCycTile + s_ri[slot] + gbase) : -1;
         const int64_t a0 = beg & ~3ll;
         const int nvec = (int)((end - a0 + 3) >> 2);
         if (!COLD && !DIST && a.long_lanes) {
@@ -603,7 +610,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           const int64_t sb = has ? s_sb[k] : 0;
           const int64_t beg = sb >> 8, end = beg + (sb & 255), a0 = beg & ~3ll;
           const int nvec = has ? (int)((end - a0 + 3) >> 2) : 0;
-          const int32_t gi = LOOPS ? (int32_t)(tb + li + a.lo) : -1;
+          const int32_t gi = LOOPS ? (int32_t)(tb + li + gbase) : -1;
           constexpr int NG = (kAsyncSmall + 6) / 4;
           int4 xs[NG];
 #pragma unroll
@@ -621,7 +628,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           const int64_t sb = s_sb[k];
           const int64_t beg = sb >> 8, end = beg + (sb & 255), a0 = beg & ~3ll;
           const int nvec = (int)((end - a0 + 3) >> 2);
-          const int32_t gi = LOOPS ? (int32_t)(tb + li + a.lo) : -1;
+          const int32_t gi = LOOPS ? (int32_t)(tb + li + gbase) : -1;
           constexpr int NG = (kAsyncSmall + 6) / 4;   // aligned int4 groups of a short row
           int4 xs[NG];
 #pragma unroll
@@ -651,7 +658,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           const int64_t beg = has ? s_rb[k] : 0, end = has ? beg + s_ro[k] : 0, a0 = beg & ~3ll;
           const int nvec = has ? (int)((end - a0 + 3) >> 2) : 0;
           const double v = has ? s_rv[k] : 0.0;
-          const int32_t gi = LOOPS && has ? (int32_t)(tile * kCycTile + s_ri[k] + a.lo) : -1;
+          const int32_t gi = LOOPS && has ? (int32_t)(tile * kCycTile + s_ri[k] + gbase) : -1;
           const int maxn = __reduce_max_sync(0xffffffffu, nvec);
           for (int b0 = 0; b0 < maxn; b0 += 16) {
             const int vb = b0 + sub;
@@ -667,7 +674,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           const int64_t beg = s_rb[k], end = beg + s_ro[k], a0 = beg & ~3ll;
           const int nvec = (int)((end - a0 + 3) >> 2);   // <= 33
           const double v = s_rv[k];
-          const int32_t gi = LOOPS ? (int32_t)(tile * kCycTile + s_ri[k] + a.lo) : -1;
+          const int32_t gi = LOOPS ? (int32_t)(tile * kCycTile + s_ri[k] + gbase) : -1;
           for (int vb = sub; vb < nvec; vb += 16) {
             const int4 x0 = ld_col4(col + a0 + 4 * (int64_t)vb, pol);
             int4 x1 = make_int4(0, 0, 0, 0);
@@ -1035,6 +1042,7 @@ void launch_cycle(Graph &g, int64_t *launches) {
   if (dist && g.cur_compact) {  // hot remote accumulator + cold records into the owners' inboxes
     x.ipar = g.cur_par;
     x.compact = 1;
+    a.col = g.ccol;
     a.cold_hot_tiles = (g.rtier[g.rank] + kCycTile - 1) / kCycTile;
     if (g.has_loops)
       k_cycle<true, true, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);

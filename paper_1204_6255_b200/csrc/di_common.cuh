@@ -288,6 +288,7 @@ struct Graph {
   int64_t ccap = 0;               // cold records per (sender, parity) inbox region
   size_t cold_off0 = 0, fill_off0 = 0;
   unsigned long long *ctop = nullptr;
+  int32_t *ccol = nullptr;        // the CSR columns encoded for the compact path (dist.cu)
   bool R_ready = false;           // R (global-size accumulator) allocated: bulk / ring / send-recv
   int cur_par = 0, cur_compact = 0;
   int long_lanes = 1;             // option long_lanes  // solve_dist -> launch_cycle: inbox parity, compact path

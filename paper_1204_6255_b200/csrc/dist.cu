@@ -532,6 +532,29 @@ __global__ void k_cold_remote_count(const int32_t *__restrict__ col, int64_t L, 
   if (threadIdx.x < bd.world && h[threadIdx.x]) atomicAdd(cnt + threadIdx.x, (unsigned long long)h[threadIdx.x]);
 }
 
+// The compact path's column encoding (one pass at upload): a local target j becomes j - lo, a
+// hot remote target (within the first rt[p] ids of its owner's range p) becomes n + hoff[p] +
+// (j - b[p]) — its accumulator slot after the n local ids — and a colder remote target n + R + j
+// (R = sum of rt): the push then needs two compares, and an owner lookup only for cold targets.
+__global__ void k_encode_col(const int32_t *__restrict__ col, int64_t L, int64_t lo, int64_t n,
+                             DistBounds bd, const int64_t *rt, const int64_t *hoff, int64_t R,
+                             int32_t *__restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = col[k];
+    int64_t e;
+    if (j >= lo && j < lo + n) {
+      e = j - lo;
+    } else {
+      int p = 0;
+      while (p + 1 < bd.world && j >= bd.b[p + 1]) p++;
+      const int64_t off = j - bd.b[p];
+      e = off < rt[p] ? n + hoff[p] + off : n + R + j;
+    }
+    out[k] = (int32_t)e;
+  }
+}
+
 }  // namespace
 
 // the global-size remote accumulator and the send/recv buffers: only the bulk partitioned sweep,
@@ -601,6 +624,26 @@ di_status alloc_dist(Graph &g) {
       for (int p = 0; p < G; p++)
         if (p != q) mx = std::max<int64_t>(mx, all[(size_t)q * G + p]);
     g.ccap = (mx + kColdChunk - 1) / kColdChunk * kColdChunk;
+    // the encoded columns (the encoding must fit int32: n + R + N < 2^31; the same on every rank)
+    if ((double)g.n_global + (double)rsum + (double)g.n_global >= 2147483647.0) {
+      g.ccap = 0;   // no compact path on this graph
+    } else {
+      int64_t hoff[kMaxWorld + 1];
+      hoff[0] = 0;
+      for (int p = 0; p < G; p++) hoff[p + 1] = hoff[p] + g.rtier[p];
+      int64_t *dv = nullptr;
+      DI_CK(dmalloc(&dv, 2 * (kMaxWorld + 1) * 8));
+      DI_CK(cudaMemcpyAsync(dv, g.rtier, kMaxWorld * 8, cudaMemcpyHostToDevice, g.stream));
+      DI_CK(cudaMemcpyAsync(dv + kMaxWorld + 1, hoff, (kMaxWorld + 1) * 8, cudaMemcpyHostToDevice,
+                            g.stream));
+      DI_CK(dmalloc(&g.ccol, (size_t)(g.l + 8) * 4));
+      DI_CK(cudaMemsetAsync(g.ccol + g.l, 0, 8 * 4, g.stream));
+      if (g.l > 0)
+        k_encode_col<<<g.num_sms * 8, 256, 0, g.stream>>>(g.col, g.l, g.lo, g.n, g.bounds, dv,
+                                                           dv + kMaxWorld + 1, rsum, g.ccol);
+      DI_CK(cudaStreamSynchronize(g.stream));
+      dfree(dv);
+    }
   }
   // fused exchange: a double-buffered inbox of G segments of (largest range) records per rank,
   // written by the peers' compaction kernels through peer memory (collective; every rank agrees
@@ -644,7 +687,7 @@ di_status alloc_dist(Graph &g) {
 }
 
 void free_dist(Graph &g) {
-  void *p[] = {g.R, g.sval, g.tcnt, g.hdr, g.ghdr, g.rid, g.ring, g.racc, g.ctop};
+  void *p[] = {g.R, g.sval, g.tcnt, g.hdr, g.ghdr, g.rid, g.ring, g.racc, g.ctop, g.ccol};
   for (void *q : p)
     if (q) dfree(q);
   if (g.ghdr_h) cudaFreeHost(g.ghdr_h);
