@@ -204,42 +204,51 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistAr
                                                 bool valid, int32_t gi, double v, uint64_t fpol,
                                                 const ColdSm &cs, int lane) {
   unsigned pending = 0u, bins = 0u;
+  auto one = [&](int c, int32_t j) {
+    const int64_t p = p0 + c;
+    if (!(valid && p >= beg && p < end && (!LOOPS || j != gi))) return;
+    if (DIST) {
+      // the compact path's encoded column (dist.cu k_encode_col): [0, n) local ids, then the hot
+      // remote targets' accumulator slots, then n + R + global id for colder remote targets
+      const uint32_t e = (uint32_t)j;
+      if (e < (uint32_t)a.n) {
+        red_add_f64_hint(a.F + e, v, fpol);
+      } else if (e < (uint32_t)(a.n + cs.rsum)) {
+        red_add_f64_hint(x.racc + (e - (uint32_t)a.n), v, fpol);
+      } else {
+        const int32_t gj = (int32_t)(e - (uint32_t)(a.n + cs.rsum));
+        int pp = cs.otab[gj >> cs.oshift];   // owner of the bucket's first id, then forward
+        while ((int64_t)gj >= cs.b[pp + 1]) pp++;
+        if (!cold_put(cs.cptr, cs.cnt, cs.base, pp, gj, v)) {
+          pending |= 1u << c;
+          bins |= (unsigned)pp << (5 * c);
+        }
+      }
+    } else if ((int64_t)j >= a.cold_lo) {
+      const int bb = (int)(((int64_t)j - a.cold_lo) >> a.cold_shift);
+      if (!cold_put(cs.cptr, cs.cnt, cs.base, bb, j, v)) {
+        pending |= 1u << c;
+        bins |= (unsigned)bb << (5 * c);
+      }
+    } else if (j < hot_lim) {
+      red_add_f64(rep + (int64_t)(copy * kRepl + j) * kRepStride, v);
+    } else {
+      red_add_f64_hint(a.F + j, v, fpol);
+    }
+  };
+#ifdef DI_COLD_UNROLL_DIST
+  if (DIST) {   // experiment: the four targets unrolled in the partitioned kernel
+    one(0, q.x);
+    one(1, q.y);
+    one(2, q.z);
+    one(3, q.w);
+  } else
+#endif
+  {
   // not unrolled: the COLD kernel's code must stay small enough for the instruction cache (with
   // the four targets unrolled at every call site, half the stall samples were no_instruction)
 #pragma unroll 1
-  for (int c = 0; c < 4; c++) {
-    const int64_t p = p0 + c;
-    const int32_t j = c == 0 ? q.x : (c == 1 ? q.y : (c == 2 ? q.z : q.w));
-    if (valid && p >= beg && p < end && (!LOOPS || j != gi)) {
-      if (DIST) {
-        // the compact path's encoded column (dist.cu k_encode_col): [0, n) local ids, then the
-        // hot remote targets' accumulator slots, then n + R + global id for colder remote targets
-        const uint32_t e = (uint32_t)j;
-        if (e < (uint32_t)a.n) {
-          red_add_f64_hint(a.F + e, v, fpol);
-        } else if (e < (uint32_t)(a.n + cs.rsum)) {
-          red_add_f64_hint(x.racc + (e - (uint32_t)a.n), v, fpol);
-        } else {
-          const int32_t gj = (int32_t)(e - (uint32_t)(a.n + cs.rsum));
-          int pp = cs.otab[gj >> cs.oshift];   // owner of the bucket's first id, then forward
-          while ((int64_t)gj >= cs.b[pp + 1]) pp++;
-          if (!cold_put(cs.cptr, cs.cnt, cs.base, pp, gj, v)) {
-            pending |= 1u << c;
-            bins |= (unsigned)pp << (5 * c);
-          }
-        }
-      } else if ((int64_t)j >= a.cold_lo) {
-        const int bb = (int)(((int64_t)j - a.cold_lo) >> a.cold_shift);
-        if (!cold_put(cs.cptr, cs.cnt, cs.base, bb, j, v)) {
-          pending |= 1u << c;
-          bins |= (unsigned)bb << (5 * c);
-        }
-      } else if (j < hot_lim) {
-        red_add_f64(rep + (int64_t)(copy * kRepl + j) * kRepStride, v);
-      } else {
-        red_add_f64_hint(a.F + j, v, fpol);
-      }
-    }
+    for (int c = 0; c < 4; c++) one(c, c == 0 ? q.x : (c == 1 ? q.y : (c == 2 ? q.z : q.w)));
   }
   if (__any_sync(0xffffffffu, pending != 0u))
     cold_retry(DIST ? x.bd.world : a.cold_nbins, cs.cptr, cs.fptr, cs.tptr, cs.cnt, cs.base, q,

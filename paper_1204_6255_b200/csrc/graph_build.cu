@@ -7,11 +7,14 @@
 // Everything is integer work and bit-exact (tests/test_gpu_build.py compares byte for byte
 // with a numpy lexsort). The radix sort is CUB's (a library sort, like cuBLAS for a plain
 // GEMM); every other step is a kernel below.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
 
+#include <cub/device/device_segmented_sort.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
 #include <cub/cub.cuh>
 
 #include "comm.cuh"
@@ -214,6 +217,65 @@ __global__ void k_csr_from_sorted(const uint64_t *__restrict__ keys, int64_t L, 
   }
 }
 
+// ---- row-sort build (one GPU, links kept as given): instead of sorting 64-bit (src, dst) keys,
+// a counting sort by source (out-degrees -> row offsets -> scatter) and a sort inside each row
+// (CUB segmented sort). Out-degrees in the caller's numbering, counted during validation (links
+// are often grouped by source: the lanes of a warp with the same source add once).
+__global__ void k_outdeg_agg(const int32_t *__restrict__ src, int64_t L, uint32_t *__restrict__ od) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t k0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; k0 < L;
+       k0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = k0 + lane;
+    const int32_t s = k < L ? src[k] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, s);
+    if (s >= 0 && lane == __ffs(peers) - 1) atomicAdd(od + s, (uint32_t)__popc(peers));
+  }
+}
+
+// out-degree of internal row k (the scan input of the row offsets)
+__global__ void k_new_deg(const uint32_t *__restrict__ od, const int32_t *__restrict__ old_of,
+                          int64_t n, int64_t *__restrict__ deg) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    deg[k] = od[old_of ? old_of[k] : k];
+  if (blockIdx.x == 0 && threadIdx.x == 0) deg[n] = 0;
+}
+
+// each link to the next free slot of its (internal) row; self-loops counted per row
+__global__ void k_scatter_rows(const int32_t *__restrict__ src, const int32_t *__restrict__ dst,
+                               int64_t L, const int32_t *__restrict__ new_of,
+                               unsigned long long *__restrict__ cursor, int32_t *__restrict__ out,
+                               int32_t *__restrict__ kloop) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t k0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; k0 < L;
+       k0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = k0 + lane;
+    int32_t s = -1, t = 0;
+    if (k < L) {
+      s = src[k];
+      t = dst[k];
+      if (new_of) {
+        s = new_of[s];
+        t = new_of[t];
+      }
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, s);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long base = 0;
+    if (s >= 0 && lane == leader) base = atomicAdd(cursor + s, (unsigned long long)__popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (s >= 0) {
+      out[base + __popc(peers & ((1u << lane) - 1))] = t;
+      if (s == t) atomicAdd(kloop + s, 1);
+    }
+  }
+}
+
+struct MinusBase {
+  int64_t base;
+  __host__ __device__ int operator()(int64_t x) const { return (int)(x - base); }
+};
+
 __global__ void k_deg(const int64_t *__restrict__ ptr, int64_t n, int32_t *__restrict__ deg,
                       const int32_t *__restrict__ kloop, int *__restrict__ any_loop) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -285,6 +347,8 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   const bool reorder = !(flags & DI_NO_REORDER);
   const int dedup = (flags & DI_DEDUP) ? 1 : 0, drop_self = (flags & DI_DROP_SELF_LOOPS) ? 1 : 0;
   const size_t LL = (size_t)(L > 0 ? L : 1);
+  // one GPU, links kept as given, no CSC: counting sort by source + segmented sort of the rows
+  const bool rowsort = world == 1 && !dedup && !drop_self && !(flags & DI_BUILD_CSC) && L > 0;
   int wb = 0;
   while ((1 << wb) < world) wb++;
 
@@ -294,9 +358,19 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   //  this rank's own links, allocated once the partition is known)
   const bool part = world > 1;
   size_t cub_tmp = 0, q = 0;
-  if (!part) {
+  if (!part && !rowsort) {
     DI_CK(cub::DeviceRadixSort::SortKeys(nullptr, q, (uint64_t *)nullptr, (uint64_t *)nullptr,
                                          (int64_t)LL, 0, 2 * b, st));
+    cub_tmp = std::max(cub_tmp, q);
+  }
+  constexpr int64_t kSegMax = 1ll << 30;   // items per segmented-sort call (its counts are int)
+  if (rowsort) {
+    cub::TransformInputIterator<int, MinusBase, const int64_t *> it(nullptr, MinusBase{0});
+    DI_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, q, (const int32_t *)nullptr, (int32_t *)nullptr,
+                                             (int)std::min<int64_t>(L, kSegMax), (int)n, it, it, st));
+    cub_tmp = std::max(cub_tmp, q);
+    DI_CK(cub::DeviceScan::ExclusiveSum(nullptr, q, (int64_t *)nullptr, (int64_t *)nullptr, n + 1,
+                                        st));
     cub_tmp = std::max(cub_tmp, q);
   }
   if (!part && (dedup || drop_self)) {
@@ -325,9 +399,14 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     add(LL * 4);
     add(LL * 4);
   }
-  if (!part) {
+  if (!part && !rowsort) {
     add(LL * 8);                      // keys_a
     add(LL * 8);                      // keys_b
+  }
+  if (rowsort) {
+    add(LL * 4);                      // rows before their sort
+    add(nn * 4);                      // out-degrees (caller's numbering)
+    add((nn + 1) * 8);                // row degrees, then the scatter cursors
   }
   add(cub_tmp);
   if (!part && (dedup || drop_self)) add(LL);    // keep flags (dedup / self-loops)
@@ -356,8 +435,11 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     s_dev = hs;
     d_dev = hd;
   }
-  uint64_t *ka = part ? nullptr : ar.take<uint64_t>(LL * 8);
-  uint64_t *kb = part ? nullptr : ar.take<uint64_t>(LL * 8);
+  uint64_t *ka = (part || rowsort) ? nullptr : ar.take<uint64_t>(LL * 8);
+  uint64_t *kb = (part || rowsort) ? nullptr : ar.take<uint64_t>(LL * 8);
+  int32_t *craw = rowsort ? ar.take<int32_t>(LL * 4) : nullptr;
+  uint32_t *odeg = rowsort ? ar.take<uint32_t>(nn * 4) : nullptr;
+  int64_t *cursor = rowsort ? ar.take<int64_t>((nn + 1) * 8) : nullptr;
   void *tmp = ar.take<char>(cub_tmp);
   uint8_t *keep = (!part && (dedup || drop_self)) ? ar.take<uint8_t>(LL) : nullptr;
   char *small = ar.take<char>(64);
@@ -378,6 +460,10 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   const bool bad_range = local && !(s_lo >= 0 && s_lo < s_hi && s_hi <= n);
   if (L > 0 && !bad_range)
     k_validate<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, n, s_lo, s_hi, badb, indeg);
+  if (rowsort) {
+    DI_CK(cudaMemsetAsync(odeg, 0, nn * 4, st));
+    k_outdeg_agg<<<grid_for(L, sms), 256, 0, st>>>(s_dev, L, odeg);
+  }
   unsigned long long bad = 0;
   DI_CK(cudaMemcpyAsync(&bad, badb, 8, cudaMemcpyDeviceToHost, st));
   DI_CK(cudaStreamSynchronize(st));
@@ -567,10 +653,64 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
       k_make_own_keys<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, b, g.lo, g.hi, g.new_of,
                                                         ka, cnt);
     btrace("sync4b");
-  } else if (L > 0) {
+  } else if (L > 0 && !rowsort) {
     k_make_keys<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, b, g.new_of, ka);
   }
   btrace("sync4");
+  if (rowsort) {  // (bad ids were rejected above: every link is valid here)
+    g.l_global = L;
+    g.l = L;
+    const int64_t nl = g.n;
+    DI_CK(dmalloc(&g.row_ptr, ((size_t)nl + 1) * 8));
+    DI_CK(dmalloc(&g.col, ((size_t)L + 8) * 4));   // +8: the push reads aligned int4 groups
+    DI_CK(cudaMemsetAsync(g.col + L, 0, 8 * 4, st));
+    DI_CK(dmalloc(&g.deg, (size_t)nl * 4));
+    DI_CK(dmalloc(&g.kloop, (size_t)nl * 4));
+    DI_CK(cudaMemsetAsync(g.kloop, 0, (size_t)nl * 4, st));
+    k_new_deg<<<grid_for(nl, sms), 256, 0, st>>>(odeg, g.reordered ? g.old_of : nullptr, nl, cursor);
+    size_t sb = cub_tmp;
+    DI_CK(cub::DeviceScan::ExclusiveSum(tmp, sb, cursor, g.row_ptr, nl + 1, st));
+    DI_CK(cudaMemcpyAsync(cursor, g.row_ptr, ((size_t)nl + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    k_scatter_rows<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, g.reordered ? g.new_of : nullptr,
+                                                    reinterpret_cast<unsigned long long *>(cursor),
+                                                    craw, g.kloop);
+    // rows sorted by target, in calls of at most kSegMax links (whole rows; a row longer than
+    // kSegMax alone gets its own call); the row offsets as ints relative to the call's first link
+    std::vector<int64_t> rp;
+    if (L > kSegMax) {
+      rp.resize((size_t)nl + 1);
+      DI_CK(cudaMemcpyAsync(rp.data(), g.row_ptr, ((size_t)nl + 1) * 8, cudaMemcpyDeviceToHost, st));
+      DI_CK(cudaStreamSynchronize(st));
+    }
+    int64_t r0 = 0;
+    while (r0 < nl) {
+      int64_t r1 = nl;
+      if (L > kSegMax) {   // the largest r1 with rp[r1] - rp[r0] <= kSegMax (at least one row)
+        r1 = std::upper_bound(rp.begin() + r0 + 1, rp.end(), rp[r0] + kSegMax) - rp.begin() - 1;
+        if (r1 <= r0) r1 = r0 + 1;
+      }
+      const int64_t base = L > kSegMax ? rp[r0] : 0, cnt = (L > kSegMax ? rp[r1] : L) - base;
+      if (cnt > 0) {
+        if (cnt > INT32_MAX) return (set_error("di_graph_upload: a row of more than 2^31 links"), DI_EINVAL);
+        cub::TransformInputIterator<int, MinusBase, const int64_t *> b0(g.row_ptr + r0, MinusBase{base});
+        cub::TransformInputIterator<int, MinusBase, const int64_t *> b1(g.row_ptr + r0 + 1, MinusBase{base});
+        size_t tb = cub_tmp;
+        DI_CK(cub::DeviceSegmentedSort::SortKeys(tmp, tb, craw + base, g.col + base, (int)cnt,
+                                                 (int)(r1 - r0), b0, b1, st));
+      }
+      r0 = r1;
+    }
+    int *any_loop = reinterpret_cast<int *>(small);
+    DI_CK(cudaMemsetAsync(any_loop, 0, 4, st));
+    k_deg<<<grid_for(nl, sms), 256, 0, st>>>(g.row_ptr, nl, g.deg, g.kloop, any_loop);
+    int hl = 0;
+    DI_CK(cudaMemcpyAsync(&hl, any_loop, 4, cudaMemcpyDeviceToHost, st));
+    DI_CK(cudaStreamSynchronize(st));
+    btrace("sync7");
+    DI_CK(cudaGetLastError());
+    g.has_loops = hl != 0;
+    return DI_OK;
+  }
 
   // ---- sort by (src, dst)
   if (Ls > 0) {
