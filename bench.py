@@ -445,7 +445,12 @@ def e2e_pipelined(di, src_p, dst_p, n, dev, args, use_async, use_graph):
     import threading
     import torch
     steps = args.e2e_steps + 2
-    streams = [torch.cuda.Stream(dev) for _ in range(3)]
+    # the uploads run on low-priority streams: the block scheduler serves the solve's kernels
+    # first, the build's kernels fill what the solve leaves, and the copy engine is idle otherwise
+    lo_prio, hi_prio = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
+        else (0, -1)
+    streams = [torch.cuda.Stream(dev, priority=lo_prio) for _ in range(3)]
+    solve_streams = [torch.cuda.Stream(dev, priority=hi_prio) for _ in range(3)]
     H_host = torch.empty(n, dtype=torch.float64).pin_memory()
     q = queue.Queue(maxsize=1)
     err = []
@@ -469,10 +474,14 @@ def e2e_pipelined(di, src_p, dst_p, n, dev, args, use_async, use_graph):
         k, g = q.get()
         if g is None:
             raise err[0]
-        st = g.solve(d=D, tol=TOL, variant=args.variant, asynchronous=use_async, graph_loop=use_graph)
-        H = g.history()
-        H_host.copy_(H, non_blocking=True)
-        g.stream.synchronize()
+        g.set_stream(solve_streams[k % 3])   # the solve on a high-priority stream
+        with torch.cuda.stream(g.stream):
+            # host loop: a new handle's CUDA-graph loop would be captured and instantiated while the
+            # other thread's upload runs, which stalled the solve by ~40 ms per step (measured)
+            st = g.solve(d=D, tol=TOL, variant=args.variant, asynchronous=use_async, graph_loop=False)
+            H = g.history()
+            H_host.copy_(H, non_blocking=True)
+            g.stream.synchronize()
         assert st["converged"] == 1
         g.free()
         del H

@@ -219,6 +219,9 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
  *   "remote_tier"    0        >= 0      U: hot remote targets per range (0: half the L2 over G)
  *   "long_lanes"     1        0..1      U: DI_ASYNC long rows (> 256 links) with lane-consecutive
  *                                          targets (0: int4 groups per lane)
+ *   "row_sort"       1        0..1      U: one-GPU build without DI_DEDUP / DI_DROP_SELF_LOOPS /
+ *                                          DI_BUILD_CSC by a counting sort on sources and a
+ *                                          segmented sort of the rows (0: 64-bit key radix sort)
  * DI_EINVAL for an unknown name or a value out of range (integers must be integral). */
 di_status di_set_option(const char *name, double value);
 di_status di_get_option(const char *name, double *value);
@@ -228,6 +231,12 @@ di_status di_get_option(const char *name, double *value);
  * threshold; alpha > 1 diffuses fewer, larger amounts. alpha must be finite and > 0 (DI_EINVAL).
  * On a partitioned graph every rank must set the same value. */
 di_status di_set_threshold_scale(di_graph g, double alpha);
+
+/* Move the handle to another stream (cudaStream_t; NULL = legacy default stream): waits for the
+ * work enqueued on the current stream, then every later call of this handle enqueues on `stream`
+ * (e.g. upload on a low-priority stream while another graph solves, then solve on a high-priority
+ * one). Not thread-safe with other calls on the same handle. */
+di_status di_graph_set_stream(di_graph g, void *stream);
 
 /* Node slice [lo, hi) owned by this rank ([0, n) on one GPU). */
 di_status di_graph_range(di_graph g, int64_t *lo, int64_t *hi);

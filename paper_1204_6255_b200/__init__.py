@@ -66,6 +66,8 @@ class Dist(ctypes.Structure):
 _vp, _i64, _u32, _dbl, _ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_double, ctypes.c_int
 _lib.di_graph_upload.restype = _ci
 _lib.di_graph_upload.argtypes = [_vp, _vp, _i64, _i64, _u32, _vp, _vp, ctypes.POINTER(_vp)]
+_lib.di_graph_set_stream.restype = _ci
+_lib.di_graph_set_stream.argtypes = [_vp, _vp]
 _lib.di_graph_range.restype = _ci
 _lib.di_graph_range.argtypes = [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
 _lib.di_graph_links.restype = _ci
@@ -107,7 +109,7 @@ _lib.di_test_perm.argtypes = [_vp, _vp]
 _lib.di_test_bins.restype = _ci
 _lib.di_test_bins.argtypes = [_vp]
 
-EXPORTED = ["di_graph_upload", "di_graph_range", "di_graph_links", "di_solve", "di_residual",
+EXPORTED = ["di_graph_upload", "di_graph_set_stream", "di_graph_range", "di_graph_links", "di_solve", "di_residual",
             "di_history", "di_sweep_log", "di_graph_free", "di_last_error",
             "di_nccl_unique_id", "di_group_create", "di_group_free", "di_group_abort",
             "di_set_threshold_scale", "di_set_option", "di_get_option",
@@ -318,6 +320,11 @@ class Graph:
     def set_threshold_scale(self, alpha):
         """DI-SOP threshold scale alpha (F_i > alpha * r/L * #out_i; 1 = the paper's rule)."""
         _check(_lib.di_set_threshold_scale(self._h, float(alpha)))
+
+    def set_stream(self, stream):
+        """di_graph_set_stream: later calls of this handle enqueue on `stream` (a torch stream)."""
+        _check(_lib.di_graph_set_stream(self._h, stream.cuda_stream))
+        self.stream = stream
 
     def range(self):
         lo, hi = _i64(), _i64()

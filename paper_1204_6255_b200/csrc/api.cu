@@ -335,6 +335,7 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
     g->remote_compact = o.remote_compact;
     g->remote_tier = o.remote_tier;
     g->long_lanes = o.long_lanes;
+    g->row_sort = o.row_sort;
   }
   di_status s = build_graph(*g, src, dst, n_links, flags);
   if (s == DI_OK) s = alloc_state(*g);
@@ -361,7 +362,7 @@ const OptDesc kOpts[] = {
     {"cycle_grid_div", 1, 4096, true}, {"cycle_times", 0, 1, true}, {"p2p", 0, 1, true},
     {"p2p_force", 0, 1, true},      {"build_trace", 0, 1, true},
     {"remote_compact", 0, 1, true}, {"remote_tier", 0, 2147483647.0, true},
-    {"long_lanes", 0, 1, true},
+    {"long_lanes", 0, 1, true},     {"row_sort", 0, 1, true},
 };
 }  // namespace
 
@@ -393,6 +394,7 @@ di_status di_set_option(const char *name, double value) {
   else if (n == "remote_compact") o.remote_compact = iv;
   else if (n == "remote_tier") o.remote_tier = (int64_t)value;
   else if (n == "long_lanes") o.long_lanes = iv;
+  else if (n == "row_sort") o.row_sort = iv;
   return DI_OK;
 }
 
@@ -416,6 +418,7 @@ di_status di_get_option(const char *name, double *value) {
   else if (n == "remote_compact") *value = o.remote_compact;
   else if (n == "remote_tier") *value = (double)o.remote_tier;
   else if (n == "long_lanes") *value = o.long_lanes;
+  else if (n == "row_sort") *value = o.row_sort;
   else return fail(DI_EINVAL, "di_get_option: unknown option '" + n + "'");
   return DI_OK;
 }
@@ -426,6 +429,14 @@ di_status di_set_threshold_scale(di_graph h, double alpha) {
   if (!(alpha > 0.0) || !std::isfinite(alpha))
     return fail(DI_EINVAL, "di_set_threshold_scale: alpha must be finite and > 0");
   g->alpha = alpha;
+  return DI_OK;
+}
+
+di_status di_graph_set_stream(di_graph h, void *stream) {
+  Graph *g = (Graph *)h;
+  if (!g) return fail(DI_EINVAL, "di_graph_set_stream: NULL handle");
+  DI_CK(cudaStreamSynchronize(g->stream));   // the old stream's work is done before the switch
+  g->stream = (cudaStream_t)stream;
   return DI_OK;
 }
 

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <string>
 
+#include <cub/device/device_segmented_radix_sort.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
 #include <cub/cub.cuh>
@@ -271,6 +272,97 @@ __global__ void k_scatter_rows(const int32_t *__restrict__ src, const int32_t *_
   }
 }
 
+// Rows sorted by target after the scatter (craw -> col), by size class (the CUB segmented sort
+// took 33 ms on C4's 16.7M rows): rows of <= 16 links one thread each (insertion sort in
+// registers/L1; rows of 0-1 links copied), 17-256 links one warp each (WarpMergeSort), 257-4096
+// one block each (BlockRadixSort in shared memory), longer rows by a CUB segmented radix sort.
+constexpr int kRsSmall = 16, kRsMid = 256, kRsBig = 4096;
+__global__ void k_rowsort_small(const int64_t *__restrict__ ptr, int64_t n,
+                                const int32_t *__restrict__ in, int32_t *__restrict__ out,
+                                int32_t *__restrict__ mid, int32_t *__restrict__ big,
+                                int32_t *__restrict__ huge, unsigned long long *__restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; i0 < n;
+       i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + lane;
+    int64_t b = 0, len = -1;
+    if (i < n) {
+      b = ptr[i];
+      len = ptr[i + 1] - b;
+    }
+    if (len >= 0 && len <= kRsSmall) {
+      int32_t a[kRsSmall];
+      for (int k = 0; k < len; k++) {
+        const int32_t x = in[b + k];
+        int m = k;
+        while (m > 0 && a[m - 1] > x) {
+          a[m] = a[m - 1];
+          m--;
+        }
+        a[m] = x;
+      }
+      for (int k = 0; k < len; k++) out[b + k] = a[k];
+    }
+    // the longer rows into their class lists (one reservation per class and warp)
+    const int cls = len <= kRsSmall ? -1 : (len <= kRsMid ? 0 : (len <= kRsBig ? 1 : 2));
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      const unsigned m = __ballot_sync(0xffffffffu, cls == c);
+      if (!m) continue;
+      unsigned long long base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(cnt + 16 * c, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      if (cls == c) {
+        int32_t *lst = c == 0 ? mid : (c == 1 ? big : huge);
+        lst[base + __popc(m & ((1u << lane) - 1))] = (int32_t)i;
+      }
+    }
+  }
+}
+
+__global__ void k_rowsort_mid(const int64_t *__restrict__ ptr, const int32_t *__restrict__ rows,
+                              int64_t nrows, const int32_t *__restrict__ in, int32_t *__restrict__ out) {
+  using WS = cub::WarpMergeSort<int32_t, kRsMid / 32, 32>;
+  __shared__ typename WS::TempStorage ts[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * (int64_t)8 + warp;
+  if (r >= nrows) return;
+  const int64_t i = rows[r], b = ptr[i], len = ptr[i + 1] - b;
+  int32_t k[kRsMid / 32];
+#pragma unroll
+  for (int u = 0; u < kRsMid / 32; u++) {   // blocked arrangement: lane owns 8 consecutive slots
+    const int64_t p = (int64_t)lane * (kRsMid / 32) + u;
+    k[u] = p < len ? in[b + p] : INT32_MAX;
+  }
+  WS(ts[warp]).Sort(k, [](int32_t x, int32_t y) { return x < y; });
+#pragma unroll
+  for (int u = 0; u < kRsMid / 32; u++) {
+    const int64_t p = (int64_t)lane * (kRsMid / 32) + u;
+    if (p < len) out[b + p] = k[u];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_rowsort_big(const int64_t *__restrict__ ptr,
+                                                     const int32_t *__restrict__ rows, int bits,
+                                                     const int32_t *__restrict__ in,
+                                                     int32_t *__restrict__ out) {
+  using BS = cub::BlockRadixSort<uint32_t, 256, kRsBig / 256>;
+  __shared__ typename BS::TempStorage ts;
+  const int64_t i = rows[blockIdx.x], b = ptr[i], len = ptr[i + 1] - b;
+  uint32_t k[kRsBig / 256];
+#pragma unroll
+  for (int u = 0; u < kRsBig / 256; u++) {
+    const int64_t p = (int64_t)threadIdx.x * (kRsBig / 256) + u;
+    k[u] = p < len ? (uint32_t)in[b + p] : (1u << bits);   // padding sorts last
+  }
+  BS(ts).Sort(k, 0, bits + 1);
+#pragma unroll
+  for (int u = 0; u < kRsBig / 256; u++) {
+    const int64_t p = (int64_t)threadIdx.x * (kRsBig / 256) + u;
+    if (p < len) out[b + p] = (int32_t)k[u];
+  }
+}
+
 struct MinusBase {
   int64_t base;
   __host__ __device__ int operator()(int64_t x) const { return (int)(x - base); }
@@ -348,7 +440,8 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   const int dedup = (flags & DI_DEDUP) ? 1 : 0, drop_self = (flags & DI_DROP_SELF_LOOPS) ? 1 : 0;
   const size_t LL = (size_t)(L > 0 ? L : 1);
   // one GPU, links kept as given, no CSC: counting sort by source + segmented sort of the rows
-  const bool rowsort = world == 1 && !dedup && !drop_self && !(flags & DI_BUILD_CSC) && L > 0;
+  const bool rowsort = g.row_sort && world == 1 && !dedup && !drop_self && !(flags & DI_BUILD_CSC) &&
+                       L > 0;
   int wb = 0;
   while ((1 << wb) < world) wb++;
 
@@ -365,9 +458,11 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   }
   constexpr int64_t kSegMax = 1ll << 30;   // items per segmented-sort call (its counts are int)
   if (rowsort) {
-    cub::TransformInputIterator<int, MinusBase, const int64_t *> it(nullptr, MinusBase{0});
-    DI_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, q, (const int32_t *)nullptr, (int32_t *)nullptr,
-                                             (int)std::min<int64_t>(L, kSegMax), (int)n, it, it, st));
+    DI_CK(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, q, (const int32_t *)nullptr,
+                                                  (int32_t *)nullptr, (int)std::min<int64_t>(L, kSegMax),
+                                                  (int)std::min<int64_t>(n, L / kRsBig + 1),
+                                                  (const int32_t *)nullptr, (const int32_t *)nullptr, 0,
+                                                  2 * b, st));
     cub_tmp = std::max(cub_tmp, q);
     DI_CK(cub::DeviceScan::ExclusiveSum(nullptr, q, (int64_t *)nullptr, (int64_t *)nullptr, n + 1,
                                         st));
@@ -406,7 +501,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   if (rowsort) {
     add(LL * 4);                      // rows before their sort
     add(nn * 4);                      // out-degrees (caller's numbering)
-    add((nn + 1) * 8);                // row degrees, then the scatter cursors
+    add((nn + 1) * 8 + 1024);         // row degrees, the scatter cursors, then the row-class lists
   }
   add(cub_tmp);
   if (!part && (dedup || drop_self)) add(LL);    // keep flags (dedup / self-loops)
@@ -439,7 +534,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   uint64_t *kb = (part || rowsort) ? nullptr : ar.take<uint64_t>(LL * 8);
   int32_t *craw = rowsort ? ar.take<int32_t>(LL * 4) : nullptr;
   uint32_t *odeg = rowsort ? ar.take<uint32_t>(nn * 4) : nullptr;
-  int64_t *cursor = rowsort ? ar.take<int64_t>((nn + 1) * 8) : nullptr;
+  int64_t *cursor = rowsort ? ar.take<int64_t>((nn + 1) * 8 + 1024) : nullptr;
   void *tmp = ar.take<char>(cub_tmp);
   uint8_t *keep = (!part && (dedup || drop_self)) ? ar.take<uint8_t>(LL) : nullptr;
   char *small = ar.take<char>(64);
@@ -671,34 +766,81 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     size_t sb = cub_tmp;
     DI_CK(cub::DeviceScan::ExclusiveSum(tmp, sb, cursor, g.row_ptr, nl + 1, st));
     DI_CK(cudaMemcpyAsync(cursor, g.row_ptr, ((size_t)nl + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    if (options().build_trace) {
+      cudaStreamSynchronize(st);
+      btrace("rs_scan");
+    }
     k_scatter_rows<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, g.reordered ? g.new_of : nullptr,
                                                     reinterpret_cast<unsigned long long *>(cursor),
                                                     craw, g.kloop);
-    // rows sorted by target, in calls of at most kSegMax links (whole rows; a row longer than
-    // kSegMax alone gets its own call); the row offsets as ints relative to the call's first link
-    std::vector<int64_t> rp;
-    if (L > kSegMax) {
-      rp.resize((size_t)nl + 1);
-      DI_CK(cudaMemcpyAsync(rp.data(), g.row_ptr, ((size_t)nl + 1) * 8, cudaMemcpyDeviceToHost, st));
+    // rows sorted by target (k_rowsort_*; the rows of more than kRsBig links: CUB segmented radix
+    // sort, in calls of at most kSegMax links — its counts are int)
+    {
+      unsigned long long *cnt = reinterpret_cast<unsigned long long *>(cursor);   // reuse
+      int32_t *lst_mid = reinterpret_cast<int32_t *>(cursor) + 128;
+      int32_t *lst_big = lst_mid + nl;   // cursor holds (nl + 1) int64: room for 2 nl int32
+      int32_t *lst_huge = reinterpret_cast<int32_t *>(odeg);   // out-degrees no longer needed
+      DI_CK(cudaMemsetAsync(cnt, 0, 3 * 16 * 8, st));
+      k_rowsort_small<<<grid_for(nl, sms), 256, 0, st>>>(g.row_ptr, nl, craw, g.col, lst_mid, lst_big,
+                                                         lst_huge, cnt);
+      if (options().build_trace) {
+        cudaStreamSynchronize(st);
+        btrace("rs_small");
+      }
+      unsigned long long hc[48];
+      DI_CK(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
       DI_CK(cudaStreamSynchronize(st));
+      const int64_t nmid = (int64_t)hc[0], nbig = (int64_t)hc[16], nhuge = (int64_t)hc[32];
+      if (options().build_trace)
+        fprintf(stderr, "[di build] rows: %lld mid, %lld big, %lld huge\n", (long long)nmid,
+                (long long)nbig, (long long)nhuge);
+      if (nmid > 0)
+        k_rowsort_mid<<<(unsigned)((nmid + 7) / 8), 256, 0, st>>>(g.row_ptr, lst_mid, nmid, craw, g.col);
+      if (options().build_trace) {
+        cudaStreamSynchronize(st);
+        btrace("rs_mid");
+      }
+      if (nbig > 0)
+        k_rowsort_big<<<(unsigned)nbig, 256, 0, st>>>(g.row_ptr, lst_big, b, craw, g.col);
+      if (options().build_trace) {
+        cudaStreamSynchronize(st);
+        btrace("rs_big");
+      }
+
+      if (nhuge > 0) {   // few rows: their offsets on the host, grouped into calls
+        std::vector<int32_t> hr((size_t)nhuge);
+        DI_CK(cudaMemcpyAsync(hr.data(), lst_huge, (size_t)nhuge * 4, cudaMemcpyDeviceToHost, st));
+        std::vector<int64_t> rp((size_t)nl + 1);
+        DI_CK(cudaMemcpyAsync(rp.data(), g.row_ptr, ((size_t)nl + 1) * 8, cudaMemcpyDeviceToHost, st));
+        DI_CK(cudaStreamSynchronize(st));
+        std::sort(hr.begin(), hr.end());
+        std::vector<int32_t> ob, oe;
+        int32_t *doff = lst_mid;   // the mid list is consumed (stream order): offsets go there
+        size_t k = 0;
+        while (k < hr.size()) {
+          const int64_t base = rp[hr[k]];
+          ob.clear();
+          oe.clear();
+          while (k < hr.size() && rp[hr[k] + 1] - base <= kSegMax) {
+            ob.push_back((int32_t)(rp[hr[k]] - base));
+            oe.push_back((int32_t)(rp[hr[k] + 1] - base));
+            k++;
+          }
+          if (ob.empty()) return (set_error("di_graph_upload: a row of more than 2^30 links"), DI_EINVAL);
+          const int ns = (int)ob.size();
+          DI_CK(cudaMemcpyAsync(doff, ob.data(), (size_t)ns * 4, cudaMemcpyHostToDevice, st));
+          DI_CK(cudaMemcpyAsync(doff + ns, oe.data(), (size_t)ns * 4, cudaMemcpyHostToDevice, st));
+          size_t tb = cub_tmp;
+          DI_CK(cub::DeviceSegmentedRadixSort::SortKeys(tmp, tb, craw + base, g.col + base,
+                                                        (int)(oe.back()), ns, doff, doff + ns, 0, b + 1,
+                                                        st));
+          DI_CK(cudaStreamSynchronize(st));   // doff is reused by the next call
+        }
+      }
     }
-    int64_t r0 = 0;
-    while (r0 < nl) {
-      int64_t r1 = nl;
-      if (L > kSegMax) {   // the largest r1 with rp[r1] - rp[r0] <= kSegMax (at least one row)
-        r1 = std::upper_bound(rp.begin() + r0 + 1, rp.end(), rp[r0] + kSegMax) - rp.begin() - 1;
-        if (r1 <= r0) r1 = r0 + 1;
-      }
-      const int64_t base = L > kSegMax ? rp[r0] : 0, cnt = (L > kSegMax ? rp[r1] : L) - base;
-      if (cnt > 0) {
-        if (cnt > INT32_MAX) return (set_error("di_graph_upload: a row of more than 2^31 links"), DI_EINVAL);
-        cub::TransformInputIterator<int, MinusBase, const int64_t *> b0(g.row_ptr + r0, MinusBase{base});
-        cub::TransformInputIterator<int, MinusBase, const int64_t *> b1(g.row_ptr + r0 + 1, MinusBase{base});
-        size_t tb = cub_tmp;
-        DI_CK(cub::DeviceSegmentedSort::SortKeys(tmp, tb, craw + base, g.col + base, (int)cnt,
-                                                 (int)(r1 - r0), b0, b1, st));
-      }
-      r0 = r1;
+    if (options().build_trace) {
+      cudaStreamSynchronize(st);
+      btrace("rs_sort");
     }
     int *any_loop = reinterpret_cast<int *>(small);
     DI_CK(cudaMemsetAsync(any_loop, 0, 4, st));
