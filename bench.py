@@ -455,12 +455,18 @@ def e2e_pipelined(di, src_p, dst_p, n, dev, args, use_async, use_graph):
     q = queue.Queue(maxsize=1)
     err = []
 
+    T0 = time.perf_counter()
+
     def producer():
         try:
             torch.cuda.set_device(dev)
             for k in range(steps):
                 s_ = streams[k % 3]
-                q.put((k, di.Graph(src_p, dst_p, n, stream=s_)))
+                t_ = (time.perf_counter() - T0) * 1e3
+                gk = di.Graph(src_p, dst_p, n, stream=s_)
+                print(f"[bench] pipelined upload {k}: {t_:.1f} -> {(time.perf_counter() - T0) * 1e3:.1f} ms",
+                      file=sys.stderr, flush=True)
+                q.put((k, gk))
         except Exception as e:   # surfaced by the consumer
             err.append(e)
             q.put((None, None))
@@ -474,6 +480,7 @@ def e2e_pipelined(di, src_p, dst_p, n, dev, args, use_async, use_graph):
         k, g = q.get()
         if g is None:
             raise err[0]
+        t_s = (time.perf_counter() - T0) * 1e3
         g.set_stream(solve_streams[k % 3])   # the solve on a high-priority stream
         with torch.cuda.stream(g.stream):
             # host loop: a new handle's CUDA-graph loop would be captured and instantiated while the
@@ -483,6 +490,8 @@ def e2e_pipelined(di, src_p, dst_p, n, dev, args, use_async, use_graph):
             H_host.copy_(H, non_blocking=True)
             g.stream.synchronize()
         assert st["converged"] == 1
+        print(f"[bench] pipelined solve {k}: {t_s:.1f} -> {(time.perf_counter() - T0) * 1e3:.1f} ms "
+              f"(device {st['solve_ms']:.1f})", file=sys.stderr, flush=True)
         g.free()
         del H
         if k == 1:    # steady state from here: step 0 warms the pool; its upload is not overlapped

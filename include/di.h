@@ -219,7 +219,7 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
  *   "remote_tier"    0        >= 0      U: hot remote targets per range (0: half the L2 over G)
  *   "long_lanes"     1        0..1      U: DI_ASYNC long rows (> 256 links) with lane-consecutive
  *                                          targets (0: int4 groups per lane)
- *   "row_sort"       1        0..1      U: one-GPU build without DI_DEDUP / DI_DROP_SELF_LOOPS /
+ *   "row_sort"       0        0..1      U: one-GPU build without DI_DEDUP / DI_DROP_SELF_LOOPS /
  *                                          DI_BUILD_CSC by a counting sort on sources and a
  *                                          segmented sort of the rows (0: 64-bit key radix sort)
  * DI_EINVAL for an unknown name or a value out of range (integers must be integral). */

@@ -336,6 +336,7 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
     g->remote_tier = o.remote_tier;
     g->long_lanes = o.long_lanes;
     g->row_sort = o.row_sort;
+    g->line_spread = o.line_spread;
   }
   di_status s = build_graph(*g, src, dst, n_links, flags);
   if (s == DI_OK) s = alloc_state(*g);
@@ -362,7 +363,7 @@ const OptDesc kOpts[] = {
     {"cycle_grid_div", 1, 4096, true}, {"cycle_times", 0, 1, true}, {"p2p", 0, 1, true},
     {"p2p_force", 0, 1, true},      {"build_trace", 0, 1, true},
     {"remote_compact", 0, 1, true}, {"remote_tier", 0, 2147483647.0, true},
-    {"long_lanes", 0, 1, true},     {"row_sort", 0, 1, true},
+    {"long_lanes", 0, 1, true},     {"row_sort", 0, 1, true},      {"line_spread", 1, 16, true},
 };
 }  // namespace
 
@@ -395,6 +396,11 @@ di_status di_set_option(const char *name, double value) {
   else if (n == "remote_tier") o.remote_tier = (int64_t)value;
   else if (n == "long_lanes") o.long_lanes = iv;
   else if (n == "row_sort") o.row_sort = iv;
+  else if (n == "line_spread") {
+    if (iv != 1 && iv != 2 && iv != 4 && iv != 8 && iv != 16)
+      return fail(DI_EINVAL, "di_set_option: line_spread must be 1, 2, 4, 8 or 16");
+    o.line_spread = iv;
+  }
   return DI_OK;
 }
 
@@ -419,6 +425,7 @@ di_status di_get_option(const char *name, double *value) {
   else if (n == "remote_tier") *value = (double)o.remote_tier;
   else if (n == "long_lanes") *value = o.long_lanes;
   else if (n == "row_sort") *value = o.row_sort;
+  else if (n == "line_spread") *value = o.line_spread;
   else return fail(DI_EINVAL, "di_get_option: unknown option '" + n + "'");
   return DI_OK;
 }

@@ -111,7 +111,8 @@ struct Options {
   int remote_compact = 1;    // "remote_compact": hot remote accumulator + cold records (P2P)
   int64_t remote_tier = 0;   // "remote_tier": hot remote targets per range (0: auto)
   int long_lanes = 1;        // "long_lanes": k_cycle long rows with lane-consecutive targets
-  int row_sort = 1;          // "row_sort": one-GPU build by counting sort + segmented row sort
+  int row_sort = 0;          // "row_sort": one-GPU build by counting sort + segmented row sort
+  int line_spread = 16;      // "line_spread": nodes of one rank class per 16-node line (1, 2, 4, 8, 16)
 };
 Options options();           // a snapshot of the current options
 
@@ -291,9 +292,10 @@ struct Graph {
   unsigned long long *ctop = nullptr;
   int32_t *ccol = nullptr;        // the CSR columns encoded for the compact path (dist.cu)
   bool R_ready = false;           // R (global-size accumulator) allocated: bulk / ring / send-recv
-  int cur_par = 0, cur_compact = 0;
+  int cur_par = 0, cur_compact = 0;  // solve_dist -> launch_cycle: inbox parity, compact path
   int long_lanes = 1;             // option long_lanes
-  int row_sort = 1;               // option row_sort  // solve_dist -> launch_cycle: inbox parity, compact path
+  int row_sort = 0;               // option row_sort
+  int line_spread = 16;           // option line_spread
 };
 
 // ---------------------------------------------------------------- device memory

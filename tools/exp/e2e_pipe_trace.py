@@ -6,7 +6,7 @@ import torch
 import digen
 import paper_1204_6255_b200 as di
 di.set_option("row_sort", 0)
-GL = len(sys.argv) > 1 and sys.argv[1] == "graph"
+GL = "graph" in sys.argv[1:]
 src, dst, n = digen.make("c4")
 sp, dp = torch.from_numpy(src).pin_memory(), torch.from_numpy(dst).pin_memory()
 dev = torch.device("cuda", 0)
@@ -15,6 +15,17 @@ ups = [torch.cuda.Stream(dev, priority=lo) for _ in range(3)]
 sols = [torch.cuda.Stream(dev, priority=hi) for _ in range(3)]
 H = torch.empty(n, dtype=torch.float64).pin_memory()
 q = queue.Queue(maxsize=1)
+if "--serial-first" in sys.argv:   # as in bench.py: serial e2e steps before the pipeline
+    for k in range(8):
+        g = di.Graph(sp, dp, n)
+        g.solve(d=0.85, tol=1e-10, asynchronous=True, graph_loop=True)
+        H.copy_(g.history())
+        g.free()
+    torch.cuda.synchronize()
+if "--trim" in sys.argv:
+    from cuda import cudart
+    err, pool = cudart.cudaDeviceGetDefaultMemPool(0)
+    print("trim", cudart.cudaMemPoolTrimTo(pool, 0), flush=True)
 T0 = time.perf_counter()
 def ts(): return (time.perf_counter() - T0) * 1e3
 def producer():
