@@ -236,20 +236,11 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistAr
       red_add_f64_hint(a.F + j, v, fpol);
     }
   };
-#ifdef DI_COLD_UNROLL_DIST
-  if (DIST) {   // experiment: the four targets unrolled in the partitioned kernel
-    one(0, q.x);
-    one(1, q.y);
-    one(2, q.z);
-    one(3, q.w);
-  } else
-#endif
-  {
   // not unrolled: the COLD kernel's code must stay small enough for the instruction cache (with
-  // the four targets unrolled at every call site, half the stall samples were no_instruction)
+  // the four targets unrolled at every call site, half the stall samples of the single-GPU kernel
+  // were no_instruction; unrolled, the partitioned kernel took 1801 instead of 1118 us per cycle)
 #pragma unroll 1
-    for (int c = 0; c < 4; c++) one(c, c == 0 ? q.x : (c == 1 ? q.y : (c == 2 ? q.z : q.w)));
-  }
+  for (int c = 0; c < 4; c++) one(c, c == 0 ? q.x : (c == 1 ? q.y : (c == 2 ? q.z : q.w)));
   if (__any_sync(0xffffffffu, pending != 0u))
     cold_retry(DIST ? x.bd.world : a.cold_nbins, cs.cptr, cs.fptr, cs.tptr, cs.cnt, cs.base, q,
                pending, bins, v, lane, DIST ? (int32_t)(a.n + cs.rsum) : 0);
