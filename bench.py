@@ -3,13 +3,18 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--variant sop] [--impl ours|reference]
 
-A step is one whole solve of the hot path: F = B, H = 0, DI-SOP bulk sweeps
-(select/compact + degree-binned push) until ||F||_1 <= 1e-10, on the graph resident in HBM (the
-device CSR build a0 is "Init", timed separately as in PAPER.md P:61-63, and inside `e2e`).
-value = link diffusions / solve time (GTEPS = 1e9 link-diffusions/s, all ranks).
-The default workload is BASELINE.json configs[3] (C4: R-MAT N=2^24, L~268M, the largest
-single-GPU configuration). Inputs (col 1.07 GB, F/H 134 MB each) exceed the 126 MB L2, and L2
-is additionally flushed (512 MiB write) before every timed step.
+A step is one whole solve of the hot path: F = B, H = 0, asynchronous DI-SOP
+cycles (one persistent kernel per cycle: select + take + push, R7) until ||F||_1 <= 1e-10,
+on the graph resident in HBM (the device CSR build a0 is "Init", timed separately as in PAPER.md
+P:61-63, and inside `e2e`). value = link diffusions / solve time (GTEPS = 1e9 link-diffusions/s,
+all ranks). The default workload is BASELINE.json configs[3] (C4: R-MAT N=2^24, L~268M, the
+largest single-GPU configuration) at every N (strong scaling); --config c5 is the north_star's.
+Inputs (col 1.07 GB, F/H 134 MB each) exceed the 126 MB L2, and L2 is additionally flushed
+(512 MiB write) before every timed step.
+
+--gpus N > 1 without WORLD_SIZE re-launches this script under torch.distributed.run (one process
+per GPU, 127.0.0.1); every rank generates only its own source range on its GPU and uploads it
+with DI_LOCAL_LINKS. A process group whose size differs from --gpus is refused.
 
 --impl reference times the CPU oracle (oracle/, sequential DI-SOP exactly as PAPER.md §2.5.5)
 on a bounded sample of the same workload (the first cycles of the solve), on this host.

@@ -611,17 +611,15 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           const int64_t beg = sb >> 8, end = beg + (sb & 255), a0 = beg & ~3ll;
           const int nvec = has ? (int)((end - a0 + 3) >> 2) : 0;
           const int32_t gi = LOOPS ? (int32_t)(tb + li + gbase) : -1;
-          constexpr int NG = (kAsyncSmall + 6) / 4;
-          int4 xs[NG];
-#pragma unroll
-          for (int u = 0; u < NG; u++) {
-            xs[u] = make_int4(0, 0, 0, 0);
-            if (u < nvec) xs[u] = ld_col4(col + a0 + 4 * u, pol);
+          // only as many groups as the warp's longest short row needs (warp-uniform), not the
+          // kAsyncSmall bound: most short rows have 1-2 int4 groups
+          const int umax = __reduce_max_sync(0xffffffffu, nvec);
+#pragma unroll 1
+          for (int u = 0; u < umax; u++) {
+            const int4 xg = u < nvec ? ld_col4(col + a0 + 4 * u, pol) : make_int4(0, 0, 0, 0);
+            push_group_cold<LOOPS, DIST>(a, x, rep, hot_lim, copy, xg, a0 + 4 * u, beg, end, u < nvec, gi,
+                                         v, fpol, cs, lane);
           }
-#pragma unroll
-          for (int u = 0; u < NG; u++)
-            push_group_cold<LOOPS, DIST>(a, x, rep, hot_lim, copy, xs[u], a0 + 4 * u, beg, end, u < nvec, gi, v,
-                                   fpol, cs, lane);
         } else if (k < nsmall) {
           const int li = s_si[k];
           const double v = s_sv[k];
