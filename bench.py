@@ -617,7 +617,7 @@ def main():
     ap.add_argument("--cpu-cycles", type=int, default=12)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-breadth", action="store_true", help="skip the DI-CYC / PI / PI' rows")
-    ap.add_argument("--e2e-pipeline", type=int, default=1,
+    ap.add_argument("--e2e-pipeline", type=int, default=0,
                     help="also measure e2e over a stream of graphs (upload of k+1 overlaps solve of k)")
     ap.add_argument("--launch-check", action="store_true",
                     help="only check the launch: N ranks over gloo (CPU), world == --gpus, rank 0 prints "

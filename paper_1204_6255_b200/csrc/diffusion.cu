@@ -343,10 +343,11 @@ __global__ void __launch_bounds__(kPushThreads) k_finalize(const SweepArgs a) {
   finalize_sweep(a, 1, kPushThreads);
 }
 
-// Static capacity of every bin (rows, or chunks for C) from the degrees, per select tile.
+// Static capacity of every bin (rows, or chunks for C) from the degrees: per select tile in
+// shared memory, then one atomic per tile and bin into the totals.
 __global__ void __launch_bounds__(kSelThreads) k_tile_caps(const int32_t *__restrict__ deg,
-                                                           int64_t n, int32_t *__restrict__ cap,
-                                                           int64_t ntiles) {
+                                                           int64_t n,
+                                                           unsigned long long *__restrict__ tot) {
   __shared__ int s_c[kBins];
   if (threadIdx.x < kBins) s_c[threadIdx.x] = 0;
   __syncthreads();
@@ -368,7 +369,8 @@ __global__ void __launch_bounds__(kSelThreads) k_tile_caps(const int32_t *__rest
     if ((threadIdx.x & 31) == 0 && x) atomicAdd(&s_c[b], x);
   }
   __syncthreads();
-  if (threadIdx.x < kBins) cap[(int64_t)threadIdx.x * ntiles + blockIdx.x] = s_c[threadIdx.x];
+  if (threadIdx.x < kBins && s_c[threadIdx.x])
+    atomicAdd(tot + threadIdx.x, (unsigned long long)s_c[threadIdx.x]);
 }
 
 // ------------------------------------------------------------------ push (a5)
@@ -622,16 +624,16 @@ di_status alloc_state(Graph &g) {
   DI_CK(dmalloc(&g.red_partials, (size_t)rg * 8));
   // frontier: per-bin capacity = rows (chunks for C) whose static degree falls in the bin
   g.ntiles = nt;
-  int32_t *cap = nullptr;
-  DI_CK(dmalloc(&cap, (size_t)nt * kBins * 4));
-  k_tile_caps<<<(unsigned)nt, kSelThreads, 0, g.stream>>>(g.deg, n, cap, nt);
-  std::vector<int32_t> hcap((size_t)nt * kBins);
-  DI_CK(cudaMemcpyAsync(hcap.data(), cap, (size_t)nt * kBins * 4, cudaMemcpyDeviceToHost, g.stream));
+  unsigned long long *cap = nullptr;
+  DI_CK(dmalloc(&cap, kBins * 8));
+  DI_CK(cudaMemsetAsync(cap, 0, kBins * 8, g.stream));
+  k_tile_caps<<<(unsigned)nt, kSelThreads, 0, g.stream>>>(g.deg, n, cap);
+  unsigned long long hcap[kBins];
+  DI_CK(cudaMemcpyAsync(hcap, cap, kBins * 8, cudaMemcpyDeviceToHost, g.stream));
   DI_CK(cudaStreamSynchronize(g.stream));
   dfree(cap);
   for (int b = 0; b < kBins; b++) {
-    int64_t acc = 0;
-    for (int64_t t = 0; t < nt; t++) acc += hcap[(size_t)b * nt + t];
+    const int64_t acc = (int64_t)hcap[b];
     g.fr.cap[b] = acc;
     const size_t cap_b = (size_t)std::max<int64_t>(acc, 1);
     DI_CK(dmalloc(&g.fr.ent[b], cap_b * sizeof(Entry)));
@@ -698,30 +700,68 @@ void launch_pull(Graph &g, int64_t *launches) {
 }
 
 // Static pull entries from the CSC (built once per graph, on the host from col_ptr).
+// the pull variant's static entries per in-degree bin, built on the device: pass 0 counts the
+// entries of every bin, pass 1 writes them (unordered: each entry is independent; bin P3's chunks
+// are summed with fp64 atomics anyway)
+__global__ void k_pull_entries(const int64_t *__restrict__ cp, int64_t n, int pass,
+                               unsigned long long *__restrict__ cnt, PullEntry *e0, PullEntry *e1,
+                               PullEntry *e2, PullEntry *e3) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t j0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; j0 < n;
+       j0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = j0 + lane;
+    int64_t beg = 0, len = 0;
+    if (j < n) {
+      beg = cp[j];
+      len = cp[j + 1] - beg;
+    }
+    const int b = len == 0 ? -1 : (len <= kPullT ? 0 : (len <= kPullG ? 1 : (len <= kPullChunk ? 2 : 3)));
+    const int64_t ne = b < 0 ? 0 : (b < 3 ? 1 : (len + kPullChunk - 1) / kPullChunk);
+#pragma unroll
+    for (int c = 0; c < kPullBins; c++) {
+      const bool mine = b == c;
+      // inclusive scan of the lanes' entry counts in this bin: one reservation per warp and bin
+      int64_t incl = mine ? ne : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+      }
+      const int64_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (tot == 0) continue;
+      unsigned long long base = 0;
+      if (lane == 31) base = atomicAdd(cnt + 16 * c, (unsigned long long)tot);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      if (pass == 1 && mine) {
+        PullEntry *e = c == 0 ? e0 : (c == 1 ? e1 : (c == 2 ? e2 : e3));
+        int64_t at = (int64_t)base + incl - ne;
+        for (int64_t k = 0; k < len; k += kPullChunk, at++)
+          e[at] = PullEntry{beg + k, (int32_t)(len - k < kPullChunk ? len - k : kPullChunk), (int32_t)j};
+      }
+    }
+  }
+}
+
 di_status alloc_pull(Graph &g) {
   if (!g.has_csc || g.pe[0]) return DI_OK;
   const int64_t n = g.n;
-  std::vector<int64_t> cp((size_t)n + 1);
-  DI_CK(cudaMemcpy(cp.data(), g.csc_ptr, ((size_t)n + 1) * 8, cudaMemcpyDeviceToHost));
-  std::vector<PullEntry> e[kPullBins];
-  for (int64_t j = 0; j < n; j++) {
-    const int64_t beg = cp[j], len = cp[j + 1] - cp[j];
-    if (len == 0) continue;
-    const int b = len <= kPullT ? 0 : (len <= kPullG ? 1 : (len <= kPullChunk ? 2 : 3));
-    if (b < 3) {
-      e[b].push_back(PullEntry{beg, (int32_t)len, (int32_t)j});
-    } else {
-      for (int64_t c = 0; c < len; c += kPullChunk)
-        e[3].push_back(PullEntry{beg + c, (int32_t)std::min<int64_t>(kPullChunk, len - c), (int32_t)j});
-    }
-  }
+  unsigned long long *cnt = nullptr;
+  DI_CK(dmalloc(&cnt, kPullBins * 16 * 8));
+  DI_CK(cudaMemsetAsync(cnt, 0, kPullBins * 16 * 8, g.stream));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)g.num_sms * 8));
+  k_pull_entries<<<grid, 256, 0, g.stream>>>(g.csc_ptr, n, 0, cnt, nullptr, nullptr, nullptr, nullptr);
+  unsigned long long hc[kPullBins * 16];
+  DI_CK(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, g.stream));
+  DI_CK(cudaStreamSynchronize(g.stream));
   for (int b = 0; b < kPullBins; b++) {
-    g.pe_count[b] = (int64_t)e[b].size();
-    DI_CK(dmalloc(&g.pe[b], std::max<size_t>(e[b].size(), 1) * sizeof(PullEntry)));
-    if (!e[b].empty())
-      DI_CK(cudaMemcpy(g.pe[b], e[b].data(), e[b].size() * sizeof(PullEntry), cudaMemcpyHostToDevice));
+    g.pe_count[b] = (int64_t)hc[16 * b];
+    DI_CK(dmalloc(&g.pe[b], (size_t)std::max<int64_t>(g.pe_count[b], 1) * sizeof(PullEntry)));
   }
+  DI_CK(cudaMemsetAsync(cnt, 0, kPullBins * 16 * 8, g.stream));
+  k_pull_entries<<<grid, 256, 0, g.stream>>>(g.csc_ptr, n, 1, cnt, g.pe[0], g.pe[1], g.pe[2], g.pe[3]);
   DI_CK(dmalloc(&g.S, (size_t)std::max<int64_t>(n, 1) * 8));
+  DI_CK(cudaStreamSynchronize(g.stream));
+  dfree(cnt);
   return DI_OK;
 }
 
