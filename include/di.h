@@ -206,6 +206,7 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
  *                                          0 off; 1 on): pushes to targets beyond the first tier
  *                                          are binned by target slice and applied slice by slice
  *   "cold_tier"      0        >= 0      U: first-tier size in nodes (0: half the L2 in bytes)
+ *   "cold_shift"     0        0..30     U: cold-bin slices of 2^shift nodes (0: about the L2 in F)
  *   "cycle_grid_div" 1        1..4096   U: DI_ASYNC grid divided by k (emulated-rank studies)
  *   "cycle_times"    0        0..1      U: per-CTA start/end times of each cycle, summary on stderr
  *   "p2p"            1        0..1      U: peer-memory inboxes for the partitioned exchange

@@ -160,7 +160,7 @@ __device__ __forceinline__ bool cold_put(ColdRec *const *cptr, int32_t *cnt, con
 }
 
 // the records of an int4 group that found their chunk full (warp-collective; rare: once per
-// kColdChunk records of a bin and warp); bins packed 5 bits per target. Scalar and shared-memory
+// kColdChunk records of a bin and warp); bins packed 6 bits per target. Scalar and shared-memory
 // arguments only: a reference to the kernel's parameter block would make the compiler copy it
 // to the stack.
 __device__ __noinline__ void cold_retry(int nbins, ColdRec *const *cptr, int32_t *const *fptr,
@@ -172,7 +172,7 @@ __device__ __noinline__ void cold_retry(int nbins, ColdRec *const *cptr, int32_t
     cold_refill(nbins, fptr, tptr, cnt, base, lane);
     for (int c = 0; c < 4; c++)
       if ((pending >> c) & 1u)
-        if (cold_put(cptr, cnt, base, (int)((bins >> (5 * c)) & 31u), jj[c], v)) pending &= ~(1u << c);
+        if (cold_put(cptr, cnt, base, (int)((bins >> (6 * c)) & 63u), jj[c], v)) pending &= ~(1u << c);
   }
 }
 
@@ -221,14 +221,14 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistAr
         while ((int64_t)gj >= cs.b[pp + 1]) pp++;
         if (!cold_put(cs.cptr, cs.cnt, cs.base, pp, gj, v)) {
           pending |= 1u << c;
-          bins |= (unsigned)pp << (5 * c);
+          bins |= (unsigned)pp << (6 * c);
         }
       }
     } else if ((int64_t)j >= a.cold_lo) {
       const int bb = (int)(((int64_t)j - a.cold_lo) >> a.cold_shift);
       if (!cold_put(cs.cptr, cs.cnt, cs.base, bb, j, v)) {
         pending |= 1u << c;
-        bins |= (unsigned)bb << (5 * c);
+        bins |= (unsigned)bb << (6 * c);
       }
     } else if (j < hot_lim) {
       red_add_f64(rep + (int64_t)(copy * kRepl + j) * kRepStride, v);
@@ -301,9 +301,9 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   int32_t *ccb = s_ccb[warp], *cce = s_cce[warp];
   const int cnb = DIST ? x.bd.world : a.cold_nbins;
   if (COLD) {
-    if (lane < NCB) {
-      ccb[lane] = kColdChunk;   // slots taken in the current chunk (full: none yet)
-      cce[lane] = -1;           // its start inside the bin's region (-1: none)
+    for (int b = lane; b < NCB; b += 32) {
+      ccb[b] = kColdChunk;   // slots taken in the current chunk (full: none yet)
+      cce[b] = -1;           // its start inside the bin's region (-1: none)
     }
     const int b = threadIdx.x;
     if (b < NCB) {
@@ -877,7 +877,14 @@ static int cycle_grid(const Graph &g);
 static di_status prepare_cold(Graph &g) {
   if (g.cold_rec || g.partitioned || !(g.cold_lo < g.n)) return DI_OK;
   const int64_t ncold = g.n - g.cold_lo;
-  int s = kColdMinShift;
+  // auto: slices of about the L2's size in F (C5: 2^24 nodes = 134 MB, 8 bins). Fewer, larger bins
+  // won over L2-resident slices: every warp keeps one open chunk per bin, whose partly written
+  // lines sit in the L2 beside the first tier (31 bins x 4736 warps ~ 19 MB of them); C5 623.7 /
+  // 592.6 / 584.3 / 629.3 / 755.0 / 979.7 ms with 2^22 ... 2^27-node slices
+  // (profiles/r2/c5_cold_shift.txt). The option cold_shift forces the slice size.
+  int s = g.cold_shift_opt > 0 ? g.cold_shift_opt : kColdMinShift;
+  if (g.cold_shift_opt <= 0)
+    while ((8ll << s) < g.l2_bytes) s++;
   while ((((ncold + (1ll << s) - 1) >> s)) > kColdBins) s++;
   g.cold_shift = s;
   g.cold_nbins = (int)((ncold + (1ll << s) - 1) >> s);

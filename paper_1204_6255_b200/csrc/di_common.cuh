@@ -50,7 +50,7 @@ constexpr double kReplShare = 0.0005;
 // an L2 miss, ~22 G random REDs/s into 1 GB) is appended as a 16-B record to the bin of its
 // slice of 2^shift nodes (at most kColdBins slices), then applied slice by slice after the cycle
 // (k_cold_apply: the slice's F lines stay in L2 while its records stream through).
-constexpr int kColdBins = 32;
+constexpr int kColdBins = 64;
 constexpr int kColdChunk = 64;          // records per warp chunk (one 1 KB run of a bin)
 constexpr double kColdF_L2 = 2.0;
 constexpr double kColdHotL2 = 0.5;
@@ -113,6 +113,7 @@ struct Options {
   int long_lanes = 1;        // "long_lanes": k_cycle long rows with lane-consecutive targets
   int row_sort = 0;          // "row_sort": one-GPU build by counting sort + segmented row sort
   int line_spread = 16;      // "line_spread": nodes of one rank class per 16-node line (1, 2, 4, 8, 16)
+  int cold_shift = 0;        // "cold_shift": cold-bin slices of 2^shift nodes (0: auto, <= kColdBins bins)
 };
 Options options();           // a snapshot of the current options
 
@@ -296,6 +297,7 @@ struct Graph {
   int long_lanes = 1;             // option long_lanes
   int row_sort = 0;               // option row_sort
   int line_spread = 16;           // option line_spread
+  int cold_shift_opt = 0;         // option cold_shift
 };
 
 // ---------------------------------------------------------------- device memory
