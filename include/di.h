@@ -223,6 +223,9 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
  *   "row_sort"       0        0..1      U: one-GPU build without DI_DEDUP / DI_DROP_SELF_LOOPS /
  *                                          DI_BUILD_CSC by a counting sort on sources and a
  *                                          segmented sort of the rows (0: 64-bit key radix sort)
+ *   "line_spread"    16       1,2,4,8,16 U: nodes of one rank class per 16-node L2 line of the
+ *                                          relabelling (16: hot nodes packed; smaller spreads the
+ *                                          hot set over more lines)
  * DI_EINVAL for an unknown name or a value out of range (integers must be integral). */
 di_status di_set_option(const char *name, double value);
 di_status di_get_option(const char *name, double *value);

@@ -19,6 +19,8 @@ from paper_1204_6255_b200.dist import assemble, run_local_group
 G = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1] != "--one-gpu" else 8
 cfg = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else "c5"
 check = "--check" in sys.argv
+if "--remote-tier" in sys.argv:
+    di.set_option("remote_tier", int(sys.argv[sys.argv.index("--remote-tier") + 1]))
 D, TOL = 0.85, 1e-10
 n = digen.CONFIGS[cfg].n
 ranges = digen.node_ranges(n, G)
@@ -64,6 +66,7 @@ def rank(r, grp):
 res = run_local_group(G, rank, timeout=3000)
 st = res[0][2]
 cyc = max(1, st["sweeps"])
+print("remote_tier", di.get_option("remote_tier"))
 print("%s on %d emulated ranks: build %.1f s, %d cycles, %.2f eq-iter, residual %.3e, converged %d" %
       (cfg, G, max(x[3] for x in res), st["sweeps"], st["equivalent_iterations"], st["residual_l1"], st["converged"]), flush=True)
 for r, x in enumerate(res):
