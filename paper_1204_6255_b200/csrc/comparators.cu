@@ -280,22 +280,6 @@ __global__ void k_fill(double *x, double v, int64_t n) {
     x[i] = v;
 }
 
-std::vector<PullEntry> row_entries(const std::vector<int64_t> &ptr, int64_t n, int b) {
-  std::vector<PullEntry> e;
-  for (int64_t j = 0; j < n; j++) {
-    const int64_t beg = ptr[j], len = ptr[j + 1] - ptr[j];
-    if (len == 0) continue;
-    const int bb = len <= kPullT ? 0 : (len <= kPullG ? 1 : (len <= kPullChunk ? 2 : 3));
-    if (bb != b) continue;
-    if (b < 3)
-      e.push_back(PullEntry{beg, (int32_t)len, (int32_t)j});
-    else
-      for (int64_t c = 0; c < len; c += kPullChunk)
-        e.push_back(PullEntry{beg + c, (int32_t)std::min<int64_t>(kPullChunk, len - c), (int32_t)j});
-  }
-  return e;
-}
-
 di_status fail_cmp(const std::string &msg) {
   set_error(msg);
   return DI_ECUDA;
@@ -311,16 +295,9 @@ di_status run_comparator(Graph &g, double d, double tol, int variant, int64_t ma
   const int64_t n = g.n;
   const int grid = g.num_sms * 4;
   // lazily built static out-row entries (PI') and work buffers
-  if (variant == DI_PI_PUSH && !g.re[0]) {
-    std::vector<int64_t> rp((size_t)n + 1);
-    DI_CK(cudaMemcpy(rp.data(), g.row_ptr, ((size_t)n + 1) * 8, cudaMemcpyDeviceToHost));
-    for (int b = 0; b < kPullBins; b++) {
-      std::vector<PullEntry> e = row_entries(rp, n, b);
-      g.re_count[b] = (int64_t)e.size();
-      DI_CK(dmalloc(&g.re[b], std::max<size_t>(e.size(), 1) * sizeof(PullEntry)));
-      if (!e.empty())
-        DI_CK(cudaMemcpy(g.re[b], e.data(), e.size() * sizeof(PullEntry), cudaMemcpyHostToDevice));
-    }
+  if (variant == DI_PI_PUSH && !g.re[0]) {   // (the same size bins as the pull's, over the CSR)
+    di_status bs = build_bin_entries(g, g.row_ptr, n, g.re, g.re_count);
+    if (bs != DI_OK) return bs;
   }
   if (!g.aux) DI_CK(dmalloc(&g.aux, (size_t)n * 8));
   if (!g.S) DI_CK(dmalloc(&g.S, (size_t)n * 8));

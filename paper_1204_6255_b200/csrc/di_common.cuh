@@ -352,6 +352,7 @@ void launch_cycle(Graph &g, int64_t *launches);
 void launch_cycle_test(Graph &g, double *rec_T, double *rec_v, int64_t *launches);
 di_status prepare_cycle(Graph &g, bool async);
 di_status alloc_pull(Graph &g);
+di_status build_bin_entries(Graph &g, const int64_t *ptr, int64_t n, PullEntry **out, int64_t *counts);
 di_status alloc_dist(Graph &g);
 int64_t cycle_warps(const Graph &g);
 // dist.cu

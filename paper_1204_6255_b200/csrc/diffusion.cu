@@ -742,26 +742,32 @@ __global__ void k_pull_entries(const int64_t *__restrict__ cp, int64_t n, int pa
   }
 }
 
-di_status alloc_pull(Graph &g) {
-  if (!g.has_csc || g.pe[0]) return DI_OK;
-  const int64_t n = g.n;
+// static work entries of the rows of `ptr` (n rows) per bin, on the device
+di_status build_bin_entries(Graph &g, const int64_t *ptr, int64_t n, PullEntry **out, int64_t *counts) {
   unsigned long long *cnt = nullptr;
   DI_CK(dmalloc(&cnt, kPullBins * 16 * 8));
   DI_CK(cudaMemsetAsync(cnt, 0, kPullBins * 16 * 8, g.stream));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)g.num_sms * 8));
-  k_pull_entries<<<grid, 256, 0, g.stream>>>(g.csc_ptr, n, 0, cnt, nullptr, nullptr, nullptr, nullptr);
+  k_pull_entries<<<grid, 256, 0, g.stream>>>(ptr, n, 0, cnt, nullptr, nullptr, nullptr, nullptr);
   unsigned long long hc[kPullBins * 16];
   DI_CK(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, g.stream));
   DI_CK(cudaStreamSynchronize(g.stream));
   for (int b = 0; b < kPullBins; b++) {
-    g.pe_count[b] = (int64_t)hc[16 * b];
-    DI_CK(dmalloc(&g.pe[b], (size_t)std::max<int64_t>(g.pe_count[b], 1) * sizeof(PullEntry)));
+    counts[b] = (int64_t)hc[16 * b];
+    DI_CK(dmalloc(&out[b], (size_t)std::max<int64_t>(counts[b], 1) * sizeof(PullEntry)));
   }
   DI_CK(cudaMemsetAsync(cnt, 0, kPullBins * 16 * 8, g.stream));
-  k_pull_entries<<<grid, 256, 0, g.stream>>>(g.csc_ptr, n, 1, cnt, g.pe[0], g.pe[1], g.pe[2], g.pe[3]);
-  DI_CK(dmalloc(&g.S, (size_t)std::max<int64_t>(n, 1) * 8));
+  k_pull_entries<<<grid, 256, 0, g.stream>>>(ptr, n, 1, cnt, out[0], out[1], out[2], out[3]);
   DI_CK(cudaStreamSynchronize(g.stream));
   dfree(cnt);
+  return DI_OK;
+}
+
+di_status alloc_pull(Graph &g) {
+  if (!g.has_csc || g.pe[0]) return DI_OK;
+  di_status s = build_bin_entries(g, g.csc_ptr, g.n, g.pe, g.pe_count);
+  if (s != DI_OK) return s;
+  DI_CK(dmalloc(&g.S, (size_t)std::max<int64_t>(g.n, 1) * 8));
   return DI_OK;
 }
 

@@ -972,7 +972,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   std::vector<size_t> s12(G), r12(G);
   const size_t hw = (size_t)hdr_words(G);
   double xbytes = 0.0, xdense = 0.0;
-  int64_t xentries = 0, ndense = 0, np2p = 0;
+  int64_t ndense = 0, np2p = 0;   // (entries sent are counted on the device: Scalars::x_entries)
   // exchange choice: sparse lists unless the last sparse sweep's lists
   // (12 B per entry, all ranks) outweighed the dense reduction (8 B per remote node per rank);
   // after kDenseRun dense sweeps one sparse sweep measures the lists again
@@ -1103,7 +1103,6 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
         dense_run = 0;
       }
       if (!dense && p2p) {  // the records are already in the owners' inboxes: apply ours
-        for (int p = 0; p < G; p++) xentries += (p == me) ? 0 : g.ghdr_h[(size_t)me * hw + 8 + p];
         k_apply_inbox<<<g.num_sms * 4, 256, 0, g.stream>>>(g.F, g.lo, g.inbox[me], g.icap, par,
                                                           g.ghdr, G, me, g.sc, compact ? g.ccap : 0,
                                                           g.cold_off0, g.fill_off0);
@@ -1119,7 +1118,6 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
         rb[p] = reinterpret_cast<char *>(g.rid) + (size_t)12 * off;
         r12[p] = (size_t)nr * 12;
         off += nr;
-        xentries += ns;
       }
       if (!dense && !p2p &&
           (s = g.comm->exchange(sb.data(), s12.data(), rb.data(), r12.data(), g.stream)) != DI_OK)

@@ -14,8 +14,6 @@
 #include <string>
 
 #include <cub/device/device_segmented_radix_sort.cuh>
-#include <cub/device/device_segmented_sort.cuh>
-#include <cub/iterator/transform_input_iterator.cuh>
 #include <cub/cub.cuh>
 
 #include "comm.cuh"
@@ -379,10 +377,7 @@ __global__ void __launch_bounds__(256) k_rowsort_big(const int64_t *__restrict__
   }
 }
 
-struct MinusBase {
-  int64_t base;
-  __host__ __device__ int operator()(int64_t x) const { return (int)(x - base); }
-};
+
 
 __global__ void k_deg(const int64_t *__restrict__ ptr, int64_t n, int32_t *__restrict__ deg,
                       const int32_t *__restrict__ kloop, int *__restrict__ any_loop) {
