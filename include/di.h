@@ -226,6 +226,18 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
  *   "line_spread"    16       1,2,4,8,16 U: nodes of one rank class per 16-node L2 line of the
  *                                          relabelling (16: hot nodes packed; smaller spreads the
  *                                          hot set over more lines)
+ *   "warm"           -1       -1..65536 U: warm tier of DI_ASYNC on one GPU, skewed graphs with
+ *                                          n >= 8 x (warm + 64): the `warm` ranks after the 64 hot
+ *                                          ones are placed one every 2^warm_shift ids, and every CTA
+ *                                          of the cycle kernel accumulates its pushes to them and to
+ *                                          the hot ids in shared memory (as many as fit without
+ *                                          lowering occupancy), flushed into F when the CTA leaves
+ *                                          the cycle (-1: as many as fit, 4032 on B200; 0: off)
+ *   "warm_flush"     0        >= 0      U: the cycle kernel's CTAs also flush the warm tier into F
+ *                                          every k of their tiles (0: only when they leave the cycle)
+ *   "warm_shift"     0        0..30     U: warm ranks one every 2^k ids (0: auto, the warm ids
+ *                                          spanning about the first eighth of the range or of the
+ *                                          first tier)
  * DI_EINVAL for an unknown name or a value out of range (integers must be integral). */
 di_status di_set_option(const char *name, double value);
 di_status di_get_option(const char *name, double *value);

@@ -72,18 +72,50 @@ constexpr int kCopies = kRepCopies;
 constexpr int64_t kHubMin = 8192;
 constexpr int64_t kHubItem = 16384;
 
+// Warm tier: a push to one of the warm ids is an fp64 add into the CTA's
+// shared-memory accumulator (a CAS loop: sm_100a has no native shared fp64 add) instead of an L2
+// RED; k_cycle flushes the accumulators into F when the CTA leaves the cycle. The warm ids are the
+// hot ids [0, hot) (slots nw + j) and the ids hot + k * 2^shift, k < nw (slot k): the relabelling
+// puts the warm ranks one every 2^shift ids (graph_build.cu k_place), so that every tile of the
+// cycle keeps about the same work (warm rows are long: placed together they made one CTA the
+// straggler of every cycle). On C4 the 4096 hottest ids take ~15 % of the link targets: that many
+// fewer random requests reach the L2, whose request rate bounds the push
+// (profiles/micro_redkind.txt).
+struct WarmT {
+  double *s;       // nw + hot accumulators (dynamic shared memory)
+  int32_t hot;     // hot ids in the tier (0: off)
+  uint32_t mask;   // 2^shift - 1
+  uint32_t lim;    // nw << shift (0: off)
+  int shift, nw;
+};
+
+__device__ __forceinline__ bool warm_take(const WarmT &w, int32_t j, double v) {
+  if (j < w.hot) {
+    atomicAdd(w.s + w.nw + j, v);
+    return true;
+  }
+  const uint32_t u = (uint32_t)(j - w.hot);
+  if ((u & w.mask) == 0u && u < w.lim) {
+    atomicAdd(w.s + (u >> w.shift), v);
+    return true;
+  }
+  return false;
+}
+
 template <bool LOOPS>
 __device__ __forceinline__ void red_group_rep(double *__restrict__ F, double *__restrict__ rep,
                                               int hot_shift, int32_t hot_lim, int copy, int4 x,
                                               int64_t p0, int64_t beg, int64_t end, int32_t gi,
-                                              double v, uint64_t fpol) {
+                                              double v, uint64_t fpol, const WarmT &w) {
   const int32_t jj[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
   for (int c = 0; c < 4; c++) {
     const int64_t p = p0 + c;
     if (p >= beg && p < end && (!LOOPS || jj[c] != gi)) {
       const int32_t j = jj[c];
-      if (j < hot_lim)   // one of the hot ids 0..hot_lim-1 (0 when off)
+      if (warm_take(w, j, v))   // warm tier: the CTA's shared-memory accumulator
+        ;
+      else if (j < hot_lim)   // one of the hot ids 0..hot_lim-1 (0 when off)
         red_add_f64(rep + (int64_t)(copy * kRepl + j) * kRepStride, v);
       else
         red_add_f64_hint(F + j, v, fpol);
@@ -97,9 +129,9 @@ template <bool LOOPS, bool DIST>
 __device__ __forceinline__ void push_group(const SweepArgs &a, const DistArgs &x, double *rep,
                                            int hot_shift, int32_t hot_lim, int copy, int4 q,
                                            int64_t p0, int64_t beg, int64_t end, int32_t gi,
-                                           double v, uint64_t fpol) {
+                                           double v, uint64_t fpol, const WarmT &w) {
   if (!DIST) {
-    red_group_rep<LOOPS>(a.F, rep, hot_shift, hot_lim, copy, q, p0, beg, end, gi, v, fpol);
+    red_group_rep<LOOPS>(a.F, rep, hot_shift, hot_lim, copy, q, p0, beg, end, gi, v, fpol, w);
     return;
   }
   const int32_t jj[4] = {q.x, q.y, q.z, q.w};
@@ -202,7 +234,7 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistAr
                                                 double *__restrict__ rep, int32_t hot_lim, int copy,
                                                 int4 q, int64_t p0, int64_t beg, int64_t end,
                                                 bool valid, int32_t gi, double v, uint64_t fpol,
-                                                const ColdSm &cs, int lane) {
+                                                const ColdSm &cs, int lane, const WarmT &w) {
   unsigned pending = 0u, bins = 0u;
   auto one = [&](int c, int32_t j) {
     const int64_t p = p0 + c;
@@ -230,6 +262,7 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistAr
         pending |= 1u << c;
         bins |= (unsigned)bb << (6 * c);
       }
+    } else if (warm_take(w, j, v)) {
     } else if (j < hot_lim) {
       red_add_f64(rep + (int64_t)(copy * kRepl + j) * kRepStride, v);
     } else {
@@ -276,6 +309,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   __shared__ bool s_last;
   __shared__ double s_red[NW][4];
   __shared__ long long s_ired[NW][3];
+  extern __shared__ double s_warm[];   // warm tier accumulators (dynamic shared memory)
 
   Scalars *sc = a.sc;
   if (sc->stop) return;
@@ -339,6 +373,13 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       s_otab[k] = (int8_t)p;
     }
   }
+  const int nwarm = DIST ? 0 : a.warm;   // slots: nwarm warm-rank ids, then the hot ids
+  const WarmT wt{s_warm, nwarm > 0 ? a.warm_hot : 0, (1u << a.warm_shift) - 1u,
+                 nwarm > 0 ? (uint32_t)nwarm << a.warm_shift : 0u, a.warm_shift, nwarm};
+  const int nslots = nwarm > 0 ? nwarm + a.warm_hot : 0;
+  int tiles_done = 0;
+  for (int k = threadIdx.x; k < nslots; k += kAsyncThreads) s_warm[k] = 0.0;   // (the loop's
+                                                                               //  first barrier)
   const ColdSm cs{ccb, cce, s_cptr, s_fptr, s_tptr, s_db, s_drt, s_dhoff, s_otab, oshift,
                   (COLD && DIST) ? x.hoff[x.bd.world] : 0};
   // the row's own id in the column's numbering (self-loop test): the compact path's columns are
@@ -563,7 +604,9 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
             for (int u = 0; u < 8; u++) {
               const int32_t j = jj[u];
               if (j >= 0 && (!LOOPS || j != gi)) {
-                if (j < hot_lim)
+                if (warm_take(wt, j, v))
+                  ;
+                else if (j < hot_lim)
                   red_add_f64(rep + (int64_t)(copy * kRepl + j) * kRepStride, v);
                 else
                   red_add_f64_hint(F + j, v, fpol);
@@ -585,10 +628,10 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
             const int vi = vb + 32 * k + lane;
             if constexpr (COLD)
               push_group_cold<LOOPS, DIST>(a, x, rep, hot_lim, copy, xq[k], a0 + 4 * (int64_t)vi, beg, end,
-                                     vi < nvec, gi, v, fpol, cs, lane);
+                                     vi < nvec, gi, v, fpol, cs, lane, wt);
             else if (vi < nvec)
               push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, xq[k], a0 + 4 * (int64_t)vi,
-                                      beg, end, gi, v, fpol);
+                                      beg, end, gi, v, fpol, wt);
           }
         }
       }
@@ -618,7 +661,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           for (int u = 0; u < umax; u++) {
             const int4 xg = u < nvec ? ld_col4(col + a0 + 4 * u, pol) : make_int4(0, 0, 0, 0);
             push_group_cold<LOOPS, DIST>(a, x, rep, hot_lim, copy, xg, a0 + 4 * u, beg, end, u < nvec, gi,
-                                         v, fpol, cs, lane);
+                                         v, fpol, cs, lane, wt);
           }
         } else if (k < nsmall) {
           const int li = s_si[k];
@@ -638,7 +681,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           for (int u = 0; u < NG; u++)
             if (u < nvec)
               push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, xs[u], a0 + 4 * u, beg,
-                                      end, gi, v, fpol);
+                                      end, gi, v, fpol, wt);
         }
       }
     }
@@ -664,9 +707,9 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
             if (vb < nvec) x0 = ld_col4(col + a0 + 4 * (int64_t)vb, pol);
             if (vb + 8 < nvec) x1 = ld_col4(col + a0 + 4 * (int64_t)(vb + 8), pol);
             push_group_cold<LOOPS, DIST>(a, x, rep, hot_lim, copy, x0, a0 + 4 * (int64_t)vb, beg, end, vb < nvec,
-                                   gi, v, fpol, cs, lane);
+                                   gi, v, fpol, cs, lane, wt);
             push_group_cold<LOOPS, DIST>(a, x, rep, hot_lim, copy, x1, a0 + 4 * (int64_t)(vb + 8), beg, end,
-                                   vb + 8 < nvec, gi, v, fpol, cs, lane);
+                                   vb + 8 < nvec, gi, v, fpol, cs, lane, wt);
           }
         } else if (k < nmid) {
           const int64_t beg = s_rb[k], end = beg + s_ro[k], a0 = beg & ~3ll;
@@ -678,15 +721,33 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
             int4 x1 = make_int4(0, 0, 0, 0);
             if (vb + 8 < nvec) x1 = ld_col4(col + a0 + 4 * (int64_t)(vb + 8), pol);
             push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, x0, a0 + 4 * (int64_t)vb, beg, end,
-                                 gi, v, fpol);
+                                 gi, v, fpol, wt);
             if (vb + 8 < nvec)
               push_group<LOOPS, DIST>(a, x, rep, hot_shift, hot_lim, copy, x1, a0 + 4 * (int64_t)(vb + 8),
-                                   beg, end, gi, v, fpol);
+                                   beg, end, gi, v, fpol, wt);
           }
         }
       }
     }
     __syncthreads();
+    // option warm_flush = k: the warm accumulators go to F every k tiles of this CTA too (the
+    // barrier above: no push in flight; the next claim's barrier orders the zeroing)
+    if (nslots > 0 && a.warm_flush > 0 && ++tiles_done % a.warm_flush == 0)
+      for (int k = threadIdx.x; k < nslots; k += kAsyncThreads) {
+        const double w = s_warm[k];
+        if (w != 0.0) {
+          s_warm[k] = 0.0;
+          red_add_f64_hint(F + (k < nwarm ? (int64_t)wt.hot + ((int64_t)k << wt.shift) : (int64_t)(k - nwarm)),
+                           w, fpol);
+        }
+      }
+  }
+  // the warm accumulators into F (every push of this CTA is done: the loop ends at a barrier);
+  // before the ticket, so that the cycle's last CTA sees all of the cycle's fluid in F
+  for (int k = threadIdx.x; k < nslots; k += kAsyncThreads) {
+    const double w = s_warm[k];
+    const int64_t j = k < nwarm ? (int64_t)wt.hot + ((int64_t)k << wt.shift) : (int64_t)(k - nwarm);
+    if (w != 0.0) red_add_f64_hint(F + j, w, fpol);
   }
   if (COLD && lane == 0) {  // the warp's open chunks: their fill for the apply kernels
     for (int b = 0; b < cnb; b++)
@@ -871,6 +932,7 @@ static int hot_shift_of(const Graph &g) {
 }
 
 static int cycle_grid(const Graph &g);
+static void warm_init();
 
 // cold bins: the arena of bin regions (cold in-links of the slice + one chunk per warp of the
 // grid), chunk fills and counters; once per graph (the CSR is static)
@@ -918,6 +980,7 @@ static di_status prepare_cold(Graph &g) {
 
 // called by di_solve before any launch or capture (allocations are not capturable)
 di_status prepare_cycle(Graph &g, bool async) {
+  if (async && g.warm_count > 0) warm_init();   // (attributes are set outside any graph capture)
   if (async) {
     di_status cs = prepare_cold(g);
     if (cs != DI_OK) return cs;
@@ -958,6 +1021,56 @@ static int cycle_grid(const Graph &g) {
   // option cycle_grid_div = k (experiments with emulated ranks on one GPU): 1/k of the grid per
   // rank, so the ranks' cycles run side by side at similar rates as they would on k GPUs
   return std::max(1, std::min(g.num_sms * occ, kMaxSlices) / std::max(1, g.grid_div));
+}
+
+// Warm accumulators a CTA of k_cycle<LOOPS, false, false, COLD> can hold without lowering the
+// kernel's occupancy (the SM's shared memory split over its resident CTAs, less each CTA's static
+// shared memory and the per-CTA reservation), in whole 256-id steps; the kernel's dynamic shared
+// memory limit is raised to that once. Cached per instantiation (the device type is fixed).
+template <bool LOOPS, bool COLD>
+static int warm_cap() {
+  static const int cap = [] {
+    auto k = k_cycle<LOOPS, false, false, COLD>;
+    int dev = 0, sm_bytes = 0, resv = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sm_bytes, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) return 0;
+    const int occ = occupancy(k, kAsyncThreads);
+    const int64_t per = (int64_t)sm_bytes / occ - resv - (int64_t)fa.sharedSizeBytes;
+    const int c = per > 0 ? (int)((per / 8) & ~255ll) : 0;
+    if (c > 0 && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, c * 8) != cudaSuccess)
+      return 0;
+    return c;
+  }();
+  return cap;
+}
+
+// the warm tier of k_cycle on this graph: a.warm warm-rank slots (0: off) + the hot ids
+template <bool LOOPS, bool COLD>
+static void set_warm(const Graph &g, SweepArgs &a) {
+  a.warm = 0;
+  a.warm_hot = (int32_t)g.hot_count;
+  a.warm_shift = g.warm_shift;
+  a.warm_flush = g.warm_flush;
+  if (g.partitioned || g.warm_count <= 0) return;
+  a.warm = (int)std::max<int64_t>(0, std::min<int64_t>(g.warm_count, warm_cap<LOOPS, COLD>() - g.hot_count));
+}
+static size_t warm_bytes(const SweepArgs &a) { return a.warm > 0 ? (size_t)(a.warm + a.warm_hot) * 8 : 0; }
+
+// warm ranks k_cycle holds at full occupancy besides the hot ids (graph_build.cu: auto "warm";
+// graphs with self-loops run the LOOPS instantiation, which holds fewer: set_warm clamps)
+int warm_fit(bool cold) {
+  const int c = cold ? warm_cap<false, true>() : warm_cap<false, false>();
+  return std::max(0, c - kHotRanks);
+}
+
+static void warm_init() {
+  warm_cap<false, false>();
+  warm_cap<true, false>();
+  warm_cap<false, true>();
+  warm_cap<true, true>();
 }
 
 // warps of k_cycle's grid (the cold regions reserve one chunk per warp of slack)
@@ -1059,18 +1172,24 @@ void launch_cycle(Graph &g, int64_t *launches) {
     else
       k_cycle<false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
   } else if (cold) {
-    if (g.has_loops)
-      k_cycle<true, false, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
-    else
-      k_cycle<false, false, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+    if (g.has_loops) {
+      set_warm<true, true>(g, a);
+      k_cycle<true, false, false, true><<<grid, kAsyncThreads, warm_bytes(a), g.stream>>>(a, x);
+    } else {
+      set_warm<false, true>(g, a);
+      k_cycle<false, false, false, true><<<grid, kAsyncThreads, warm_bytes(a), g.stream>>>(a, x);
+    }
     k_cold_apply<<<cold_apply_grid(g), 256, 0, g.stream>>>(g.F, g.cold_rec, g.cold_off, g.cold_top,
                                                            g.cold_fill, g.cold_nbins);
     *launches += 1;
   } else {
-    if (g.has_loops)
-      k_cycle<true, false><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
-    else
-      k_cycle<false, false><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
+    if (g.has_loops) {
+      set_warm<true, false>(g, a);
+      k_cycle<true, false><<<grid, kAsyncThreads, warm_bytes(a), g.stream>>>(a, x);
+    } else {
+      set_warm<false, false>(g, a);
+      k_cycle<false, false><<<grid, kAsyncThreads, warm_bytes(a), g.stream>>>(a, x);
+    }
   }
   *launches += 1;
 }

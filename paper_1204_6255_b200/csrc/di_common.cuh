@@ -43,6 +43,10 @@ constexpr int kHotRanks = DI_HOT_RANKS;
 constexpr int kRepCopies = DI_HOT_COPIES;  // copies of each hot accumulator (chosen by warp)
 constexpr int kRepStride = 16;             // doubles between accumulators: one 128-B line each
 constexpr double kReplShare = 0.0005;
+// Warm tier (async.cu): on a skewed graph the kWarmIds ranks after the hot ones are
+// placed one every 2^shift ids, and every CTA of k_cycle accumulates its pushes to them (and to the
+// hot ids) in shared memory, flushed into F once when the CTA leaves the cycle.
+constexpr int kWarmIds = -1;   // option "warm" default: auto (as many as fit in shared memory)
 
 // Cold bins (async.cu): on one GPU, when F is larger than kColdF_L2 times the L2,
 // the relabelling puts a first tier of kColdHotL2 x L2 bytes of nodes (by in-degree) right after
@@ -114,6 +118,10 @@ struct Options {
   int row_sort = 0;          // "row_sort": one-GPU build by counting sort + segmented row sort
   int line_spread = 16;      // "line_spread": nodes of one rank class per 16-node line (1, 2, 4, 8, 16)
   int cold_shift = 0;        // "cold_shift": cold-bin slices of 2^shift nodes (0: auto, <= kColdBins bins)
+  int warm = kWarmIds;       // "warm": ranks after the hot ones accumulated in shared memory by k_cycle
+                             // (skewed graphs; -1 auto, 0 off)
+  int warm_flush = 0;        // "warm_flush": k_cycle flushes them every k tiles of a CTA (0: at its end)
+  int warm_shift = 0;        // "warm_shift": warm ranks every 2^k ids (0: spread over the range / first tier)
 };
 Options options();           // a snapshot of the current options
 
@@ -298,6 +306,11 @@ struct Graph {
   int row_sort = 0;               // option row_sort
   int line_spread = 16;           // option line_spread
   int cold_shift_opt = 0;         // option cold_shift
+  int warm_opt = kWarmIds;        // option warm
+  int64_t warm_count = 0;         // warm tier: ranks hot_count.. placed at hot_count + k << warm_shift
+  int warm_shift = 0;
+  int warm_flush = 0;             // option warm_flush
+  int warm_shift_opt = 0;         // option warm_shift
 };
 
 // ---------------------------------------------------------------- device memory
@@ -355,6 +368,7 @@ di_status alloc_pull(Graph &g);
 di_status build_bin_entries(Graph &g, const int64_t *ptr, int64_t n, PullEntry **out, int64_t *counts);
 di_status alloc_dist(Graph &g);
 int64_t cycle_warps(const Graph &g);
+int warm_fit(bool cold);
 // dist.cu
 di_status solve_dist(Graph &g, double d, const double *B, double tol, int variant,
                      int64_t max_sweeps, uint32_t flags, di_stats *st);

@@ -63,6 +63,8 @@ struct PlaceParams {
   int64_t tier[kMaxWorld];
   int64_t stripes2[kMaxWorld];
   int spread;   // nodes of one rank class per 16-node line (16: no spreading)
+  int64_t warm; // range 0: warm ranks after the hot ones, one every 2^wshift ids (async.cu warm tier)
+  int wshift;
 };
 
 __device__ __forceinline__ int64_t spread_slot(int64_t idx, int64_t len, int G) {
@@ -88,15 +90,30 @@ __global__ void k_place(const int32_t *__restrict__ sorted_old, int64_t n, DistB
     int g = 0;
     while (g + 1 < bd.world && r >= bd.b[g + 1]) g++;
     const int64_t lo = bd.b[g], rr = r - lo, hot = pp.hot[g];
+    const int64_t W = g == 0 ? pp.warm : 0;
     int64_t k;
-    const int64_t tier = pp.tier[g];
+    const int64_t tier = pp.tier[g] > 0 ? pp.tier[g] - W : 0;   // the first tier's non-warm ids
     if (rr < hot) {
       k = lo + rr;
-    } else if (rr < hot + tier) {   // first tier: striped inside the prefix
-      k = lo + hot + stripe_pos(rr - hot, tier, pp.stripes2[g], pp.spread);
+    } else if (rr < hot + W) {      // warm ranks: offsets 0, S, 2S, ... after the hot ids
+      k = lo + hot + ((rr - hot) << pp.wshift);
     } else {
-      const int64_t m = bd.b[g + 1] - lo - hot - tier, q = rr - hot - tier;
-      k = lo + hot + tier + stripe_pos(q, m, pp.stripes[g], pp.spread);
+      // c = offset among the non-warm ids after the hot ones, then skip the warm offsets
+      const int64_t q2 = rr - W - hot;
+      int64_t c;
+      if (q2 < tier) {              // first tier: striped inside the prefix
+        c = stripe_pos(q2, tier, pp.stripes2[g], pp.spread);
+      } else {
+        const int64_t m = bd.b[g + 1] - lo - hot - tier - W;
+        c = tier + stripe_pos(q2 - tier, m, pp.stripes[g], pp.spread);
+      }
+      if (W > 0 && pp.wshift == 0) {   // warm ranks contiguous after the hot ones
+        c += W;
+      } else if (W > 0) {
+        const int64_t S1 = (1ll << pp.wshift) - 1, kq = c / S1;
+        c = kq < W ? c + kq + 1 : c + W;
+      }
+      k = lo + hot + c;
     }
     const int32_t o = sorted_old[r];
     new_of[o] = (int32_t)k;
@@ -690,6 +707,10 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     bool skewed = !g.partitioned && g.hot_acc && L > 0 &&
                   (double)top > g.repl_share * (double)L && n > 4 * kHotRanks;
     g.hot_count = skewed ? kHotRanks : 0;
+    // warm tier (k_cycle's shared-memory accumulators, async.cu): the warm_count ranks after the
+    // hot ones, one every 2^warm_shift ids of the first tier (or of the rest of the range); auto:
+    // as many as k_cycle's CTAs hold in shared memory at full occupancy (C4: 4032)
+    const int64_t prefix = g.hot_count;
     // cold bins (single GPU, F several times the L2): a first tier of ~kColdHotL2 of the L2 in
     // nodes takes the prefix after the hot ids; targets beyond it are "cold" (async.cu)
     int l2 = 0;
@@ -699,16 +720,37 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     int64_t tier = 0;
     if (!g.partitioned && g.cold_mode != 0 &&
         (g.cold_mode == 1 || (double)n * 8.0 > kColdF_L2 * (double)l2)) {
-      tier = std::min<int64_t>(n - g.hot_count, (int64_t)(kColdHotL2 * (double)l2 / 8.0));
-      if (g.cold_tier > 0) tier = std::min<int64_t>(n - g.hot_count, g.cold_tier);
+      tier = std::min<int64_t>(n - prefix, (int64_t)(kColdHotL2 * (double)l2 / 8.0));
+      if (g.cold_tier > 0) tier = std::min<int64_t>(n - prefix, g.cold_tier);
       if (tier < 0) tier = 0;
     }
-    g.cold_lo = (tier > 0 && g.hot_count + tier < n) ? g.hot_count + tier : n;
+    g.cold_lo = (tier > 0 && prefix + tier < n) ? prefix + tier : n;
+    {
+      const int64_t w = g.warm_opt < 0 ? (int64_t)warm_fit(g.cold_lo < n) : (int64_t)g.warm_opt;
+      g.warm_count = (skewed && w > 0 && n >= 8 * (w + g.hot_count)) ? w : 0;
+    }
+    g.warm_shift = 0;
+    if (g.warm_count > 0) {
+      const int64_t region = g.cold_lo < n ? tier : n - prefix;
+      // auto spacing: the warm ids span about the first eighth of the region (C4: every 512 ids).
+      // Fluid pushed to a warm id waits in shared memory until the CTA leaves the cycle, so the
+      // earlier the warm ids come in the cycle the less fluid waits (C4, 4032 warm ranks, one every
+      // 2^11 / 2^10 / 2^9 / 2^8 / 2^7 ids: 57.4 / 55.7 / 52.9 / 55.0 / 54.1 ms; contiguous, their
+      // long rows made the first tiles the stragglers of every cycle: 300 ms)
+      while (((g.warm_count << (g.warm_shift + 1)) << 3) <= region) g.warm_shift++;
+      if (g.warm_shift_opt > 0) {
+        g.warm_shift = g.warm_shift_opt;
+        while (g.warm_shift > 0 && (g.warm_count << g.warm_shift) > region) g.warm_shift--;
+      }
+      if ((g.warm_count << g.warm_shift) > region) g.warm_count = 0;
+    }
     PlaceParams pp;
     pp.spread = g.line_spread;
+    pp.warm = g.warm_count;
+    pp.wshift = g.warm_shift;
     for (int r = 0; r < world; r++) {
       const int64_t m = bd.b[r + 1] - bd.b[r];
-      pp.hot[r] = (r == 0) ? g.hot_count : 0;
+      pp.hot[r] = (r == 0) ? prefix : 0;
       pp.tier[r] = (r == 0 && g.cold_lo < n) ? tier : 0;
       // partitioned: the hot remote targets of every range first (compact remote accumulator,
       // dist.cu); the same on every rank (bounds, world and the L2 size of this GPU type)
@@ -719,9 +761,11 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
         g.rtier[r] = std::max<int64_t>(0, std::min<int64_t>(m, want));
         pp.tier[r] = g.rtier[r] < m ? g.rtier[r] : 0;
       }
-      pp.stripes2[r] = prime_at_most(std::max<int64_t>(1, pp.tier[r] >> 10));
+      const int64_t wr = r == 0 ? pp.warm : 0;   // (warm ids sit inside the first tier if any)
+      const int64_t t1 = pp.tier[r] > 0 ? pp.tier[r] - wr : 0;
+      pp.stripes2[r] = prime_at_most(std::max<int64_t>(1, t1 >> 10));
       pp.stripes[r] = g.stripes > 0 ? (int64_t)g.stripes
-                                     : prime_at_most(std::max<int64_t>(1, (m - pp.hot[r] - pp.tier[r]) >> 10));
+                                     : prime_at_most(std::max<int64_t>(1, (m - pp.hot[r] - t1 - wr) >> 10));
     }
     k_place<<<grid_for(n, sms), 256, 0, st>>>(sorted, n, bd, pp, g.new_of, g.old_of);
     g.reordered = true;

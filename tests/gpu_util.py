@@ -64,3 +64,12 @@ def frontier_reference(res, deg, d, bins):
         off.append(off[-1] + len(out_ids[-1]))
     return (np.concatenate(out_ids).astype(np.int32), np.concatenate(out_v),
             np.concatenate(out_c), np.array(off, dtype=np.int64))
+
+
+def warm_shift(W, region):
+    """Spacing of the warm tier's ids (graph_build.cu, option warm_shift = 0): the largest s with
+    8 * W * 2^s <= region (the warm ids span about the first eighth of the region)."""
+    s = 0
+    while W and ((W << (s + 1)) << 3) <= region:
+        s += 1
+    return s

@@ -3,7 +3,7 @@ import numpy as np
 import pytest
 
 import digen
-from gpu_util import csr_reference, need_gpu, upload
+from gpu_util import csr_reference, need_gpu, upload, warm_shift
 
 pytestmark = pytest.mark.gpu
 
@@ -66,8 +66,14 @@ def test_reorder_relabelling(name):
     indeg = np.bincount(dst, minlength=n)
     ranked = np.argsort(-indeg, kind="stable")           # rank r -> caller id
     # placement (graph_build.cu k_place): on a skewed graph (top in-degree > 0.05 % of the links, kReplShare)
-    # the 64 hottest ranks come first; the rest in P stripes, P = largest prime <= (n - hot)/1024
-    hot = 64 if (indeg.max() > 0.0005 * len(src) and n > 256) else 0
+    # the 64 hottest ranks come first; when n >= 8 * (W + 64) the next W ranks (warm tier, option warm:
+    # auto = 4032 on a B200, what k_cycle's shared memory holds) go one every S ids after them (S = 2^s,
+    # the largest with 8 * W * S <= n - 64); the rest in P stripes over the remaining ids in order,
+    # P = largest prime <= (n - hot - W)/1024
+    skewed = indeg.max() > 0.0005 * len(src) and n > 256
+    hot = 64 if skewed else 0
+    W = 4032 if (skewed and n >= 8 * (4032 + 64)) else 0
+    S = 1 << warm_shift(W, n - hot)
 
     def prime_at_most(x):
         if x < 2:
@@ -77,12 +83,16 @@ def test_reorder_relabelling(name):
                 return p
         return 1
 
-    P = prime_at_most(max(1, (n - hot) >> 10))
-    m = n - hot
+    m = n - hot - W
+    P = prime_at_most(max(1, m >> 10))
     r = np.arange(m)
     M, rem = m // P, m % P
     s_ = r % P
-    k = np.concatenate([np.arange(hot), hot + s_ * M + np.minimum(s_, rem) + r // P])
+    c = s_ * M + np.minimum(s_, rem) + r // P
+    if W:
+        kq = c // (S - 1)
+        c = np.where(kq < W, c + kq + 1, c + W)
+    k = np.concatenate([np.arange(hot), hot + np.arange(W) * S, hot + c])
     expect = np.empty(n, np.int64)
     expect[k] = ranked
     assert np.array_equal(old_of, expect.astype(np.int32))

@@ -5,7 +5,7 @@ import pytest
 import digen
 import oracle
 from conftest import load_pins
-from gpu_util import l1, need_gpu, upload
+from gpu_util import l1, need_gpu, upload, warm_shift
 from oracle import definition as defn
 
 pytestmark = pytest.mark.gpu
@@ -612,3 +612,46 @@ def test_hot_accumulators_pi_push():
     Xs, _, _ = oracle.di(src, dst, n, d=D, tol=1e-15, variant="sop")
     assert l1(x, Xs / Xs.sum()) <= 1e-10
     g.free()
+
+
+@pytest.mark.parametrize("warm", [0, 128, 4032, 60000])
+def test_warm_tier(warm):
+    """Warm tier (option warm): k_cycle accumulates its pushes to the `warm` hottest
+    ids in each CTA's shared memory and flushes them into F when the CTA leaves the cycle — a delay
+    of that fluid to the cycle's end, which any diffusion order allows. Placement: the
+    warm ranks one every 2^s ids after the 64 hot ids (checked through the relabelling); 60000 is
+    above what fits in shared memory, so ids past the capacity take the plain RED. The gate against
+    the oracle on C2 (R-MAT, skewed), a skewed graph with hub rows and a self-loop on a hot node
+    (LOOPS instantiation), DI-SOP and DI-CYC, host loop and graph loop, cold bins forced on too."""
+    need_gpu()
+    import paper_1204_6255_b200 as di
+    src, dst, n = digen.make("c2")
+    rng = np.random.default_rng(12)
+    n2 = 4096 * 16
+    s2 = rng.integers(0, n2, 6 * n2).astype(np.int32)
+    t2 = rng.integers(0, n2, 6 * n2).astype(np.int32)
+    m = len(s2)
+    for hub, share, out in ((77, 0.04, 30000), (5000, 0.02, 9000), (123, 0.01, 100)):
+        k = int(share * m)
+        tgt = rng.choice(n2, out, replace=False).astype(np.int32)
+        s2 = np.concatenate([s2, rng.integers(0, n2, k).astype(np.int32), np.full(out, hub, np.int32), [77]])
+        t2 = np.concatenate([t2, np.full(k, hub, np.int32), tgt, [77]]).astype(np.int32)
+    s2 = s2.astype(np.int32)
+    for (s_, t_, nn) in ((src, dst, n), (s2, t2, n2)):
+        indeg = np.bincount(t_, minlength=nn)
+        for cold in (0, 1):
+            with di.option("warm", warm), di.option("cold_bins", cold), di.option("cold_tier", nn // 8):
+                g = upload(s_, t_, nn)
+            if warm >= 128 and nn >= 8 * (warm + 64):   # hot ids, then warm ranks every S ids (ties: stable)
+                old_of = g.test_perm()
+                ranked = np.argsort(-indeg, kind="stable").astype(np.int32)
+                sh = warm_shift(warm, nn // 8 if cold else nn - 64)
+                assert np.array_equal(old_of[:64], ranked[:64])
+                assert np.array_equal(old_of[64 + (np.arange(warm) << sh)], ranked[64:64 + warm])
+            for variant in ("sop", "cyc"):
+                Ho, _, _ = oracle.di(s_, t_, nn, d=D, tol=1e-10, variant=variant)
+                for graph_loop in (False, True):
+                    st = g.solve(d=D, tol=1e-10, variant=variant, asynchronous=True, graph_loop=graph_loop)
+                    assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
+                    assert l1(g.history().cpu().numpy(), Ho) <= 1e-9, (nn, cold, variant, graph_loop)
+            g.free()
