@@ -284,9 +284,11 @@ def run_ours(args):
                 "whole_solve_counted_GBps": round(counted / (tot_ms * 1e-3) / 1e9, 1),
                 # the unit that binds the push: scattered fp64 REDs at L2, against the
                 # in-L2 ceiling measured by tools/micro/atomics.cu (profiles/micro_atomics.txt)
+                # (with the warm tier, part of the link updates are shared-memory adds:
+                # this is link updates per second, of which the L2 sees the rest)
                 "l2_red": {"achieved_G_per_s": round(sum(s["link_diffusions"] for s in pstats) / world
                                                      / (push_ms * 1e-3) / 1e9, 1) if push_ms > 0 else None,
-                           "peak_G_per_s": RED_PEAK, "unit": "G fp64 RED/s"}}
+                           "peak_G_per_s": RED_PEAK, "unit": "G link updates/s (fp64 REDs + warm-tier adds)"}}
 
     gl_ms = round(statistics.median(ptimes), 3)       # the profiled host-loop solve, for reference
     # warm number (report cold and warm): the same solve without the L2 flush

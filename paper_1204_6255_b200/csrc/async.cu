@@ -25,11 +25,14 @@
 namespace di {
 namespace {
 
-constexpr int kAsyncThreads = 256;
+#ifndef DI_ASYNC_THREADS
+#define DI_ASYNC_THREADS 256
+#endif
+constexpr int kAsyncThreads = DI_ASYNC_THREADS;
 #ifndef DI_CYC_ITEMS
 #define DI_CYC_ITEMS 2
 #endif
-constexpr int kCycItems = DI_CYC_ITEMS;               // consecutive nodes per thread (even)
+constexpr int kCycItems = DI_CYC_ITEMS;               // consecutive nodes per thread (1 or even)
 constexpr int kCycTile = kAsyncThreads * kCycItems;   // nodes per tile
 #ifndef DI_ASYNC_SMALL
 #define DI_ASYNC_SMALL 16
@@ -81,6 +84,7 @@ constexpr int64_t kHubItem = 16384;
 // straggler of every cycle). On C4 the 4096 hottest ids take ~15 % of the link targets: that many
 // fewer random requests reach the L2, whose request rate bounds the push
 // (profiles/micro_redkind.txt).
+template <bool ON>   // ON = false: the instantiations without a warm tier (no code for it)
 struct WarmT {
   double *s;       // nw + hot accumulators (dynamic shared memory)
   int32_t hot;     // hot ids in the tier (0: off)
@@ -89,7 +93,9 @@ struct WarmT {
   int shift, nw;
 };
 
-__device__ __forceinline__ bool warm_take(const WarmT &w, int32_t j, double v) {
+template <bool ON>
+__device__ __forceinline__ bool warm_take(const WarmT<ON> &w, int32_t j, double v) {
+  if constexpr (!ON) return false;
   if (j < w.hot) {
     atomicAdd(w.s + w.nw + j, v);
     return true;
@@ -102,11 +108,11 @@ __device__ __forceinline__ bool warm_take(const WarmT &w, int32_t j, double v) {
   return false;
 }
 
-template <bool LOOPS>
+template <bool LOOPS, bool WON>
 __device__ __forceinline__ void red_group_rep(double *__restrict__ F, double *__restrict__ rep,
                                               int hot_shift, int32_t hot_lim, int copy, int4 x,
                                               int64_t p0, int64_t beg, int64_t end, int32_t gi,
-                                              double v, uint64_t fpol, const WarmT &w) {
+                                              double v, uint64_t fpol, const WarmT<WON> &w) {
   const int32_t jj[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
   for (int c = 0; c < 4; c++) {
@@ -125,11 +131,11 @@ __device__ __forceinline__ void red_group_rep(double *__restrict__ F, double *__
 
 // DIST: targets are global internal ids; a target outside this rank's range gets a RED into the
 // remote accumulator (push_remote, sweep.cuh).
-template <bool LOOPS, bool DIST>
+template <bool LOOPS, bool DIST, bool WON>
 __device__ __forceinline__ void push_group(const SweepArgs &a, const DistArgs &x, double *rep,
                                            int hot_shift, int32_t hot_lim, int copy, int4 q,
                                            int64_t p0, int64_t beg, int64_t end, int32_t gi,
-                                           double v, uint64_t fpol, const WarmT &w) {
+                                           double v, uint64_t fpol, const WarmT<WON> &w) {
   if (!DIST) {
     red_group_rep<LOOPS>(a.F, rep, hot_shift, hot_lim, copy, q, p0, beg, end, gi, v, fpol, w);
     return;
@@ -229,12 +235,12 @@ constexpr int kOwnerTab = 1024;   // owner lookup buckets (partitioned COLD cycl
 // RED into F, cold targets a record of their slice's bin. Partitioned (DIST): local targets a RED
 // into F, hot remote targets (the first rt[p] ids of owner p's range) a RED into the compact
 // accumulator, colder remote targets a record into owner p's inbox.
-template <bool LOOPS, bool DIST>
+template <bool LOOPS, bool DIST, bool WON>
 __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistArgs &x,
                                                 double *__restrict__ rep, int32_t hot_lim, int copy,
                                                 int4 q, int64_t p0, int64_t beg, int64_t end,
                                                 bool valid, int32_t gi, double v, uint64_t fpol,
-                                                const ColdSm &cs, int lane, const WarmT &w) {
+                                                const ColdSm &cs, int lane, const WarmT<WON> &w) {
   unsigned pending = 0u, bins = 0u;
   auto one = [&](int c, int32_t j) {
     const int64_t p = p0 + c;
@@ -283,7 +289,7 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistAr
 // a.rec_v instead of pushing, so that the select-and-take step of this kernel can be compared bit
 // for bit with the oracle's bulk sweep on a frozen F (no push: nothing changes F during the cycle)
 // COLD: cold bins on (single GPU, F several times the L2)
-template <bool LOOPS, bool DIST, bool TEST = false, bool COLD = false>
+template <bool LOOPS, bool DIST, bool TEST = false, bool COLD = false, bool WARM = false>
 __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const SweepArgs a, const DistArgs x) {
   constexpr int NW = kAsyncThreads / 32;
   constexpr int NCB = COLD ? kColdBins : 1;
@@ -373,10 +379,10 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       s_otab[k] = (int8_t)p;
     }
   }
-  const int nwarm = DIST ? 0 : a.warm;   // slots: nwarm warm-rank ids, then the hot ids
-  const WarmT wt{s_warm, nwarm > 0 ? a.warm_hot : 0, (1u << a.warm_shift) - 1u,
+  const int nwarm = (WARM && !DIST) ? a.warm : 0;   // slots: nwarm warm-rank ids, then the hot ids
+  const WarmT<WARM> wt{s_warm, nwarm > 0 ? a.warm_hot : 0, (1u << a.warm_shift) - 1u,
                  nwarm > 0 ? (uint32_t)nwarm << a.warm_shift : 0u, a.warm_shift, nwarm};
-  const int nslots = nwarm > 0 ? nwarm + a.warm_hot : 0;
+  const int nslots = (WARM && nwarm > 0) ? nwarm + a.warm_hot : 0;
   int tiles_done = 0;
   for (int k = threadIdx.x; k < nslots; k += kAsyncThreads) s_warm[k] = 0.0;   // (the loop's
                                                                                //  first barrier)
@@ -440,7 +446,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
     double f[kCycItems];
     int64_t rb[kCycItems + 1];
     int kl[kCycItems];
-    if (base + kCycItems <= a.n) {  // vectorised: 2 x double2 (F, L2 only: REDs land there) and
+    if (kCycItems % 2 == 0 && base + kCycItems <= a.n) {  // vectorised: 2 x double2 (F, L2 only: REDs land there) and
                                     // 2 x longlong2 (row extents) + the next row's start
 #pragma unroll
       for (int h = 0; h < kCycItems / 2; h++) {
@@ -462,7 +468,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         rb[j] = (i < a.n) ? a.row_ptr[i] : 0;
         kl[j] = (LOOPS && i < a.n) ? a.kloop[i] : 0;
       }
-      rb[kCycItems] = base < a.n ? a.row_ptr[a.n] : 0;
+      rb[kCycItems] = base < a.n ? a.row_ptr[min(base + kCycItems, a.n)] : 0;
     }
     // the selection test for the thread's nodes first, then all their exchanges in flight together
     // (one round trip per tile instead of one per selected node)
@@ -1023,14 +1029,14 @@ static int cycle_grid(const Graph &g) {
   return std::max(1, std::min(g.num_sms * occ, kMaxSlices) / std::max(1, g.grid_div));
 }
 
-// Warm accumulators a CTA of k_cycle<LOOPS, false, false, COLD> can hold without lowering the
+// Warm accumulators a CTA of k_cycle<LOOPS, false, false, false, true> can hold without lowering the
 // kernel's occupancy (the SM's shared memory split over its resident CTAs, less each CTA's static
 // shared memory and the per-CTA reservation), in whole 256-id steps; the kernel's dynamic shared
 // memory limit is raised to that once. Cached per instantiation (the device type is fixed).
-template <bool LOOPS, bool COLD>
+template <bool LOOPS>
 static int warm_cap() {
   static const int cap = [] {
-    auto k = k_cycle<LOOPS, false, false, COLD>;
+    auto k = k_cycle<LOOPS, false, false, false, true>;
     int dev = 0, sm_bytes = 0, resv = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sm_bytes, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
@@ -1048,29 +1054,25 @@ static int warm_cap() {
 }
 
 // the warm tier of k_cycle on this graph: a.warm warm-rank slots (0: off) + the hot ids
-template <bool LOOPS, bool COLD>
+template <bool LOOPS>
 static void set_warm(const Graph &g, SweepArgs &a) {
   a.warm = 0;
   a.warm_hot = (int32_t)g.hot_count;
   a.warm_shift = g.warm_shift;
   a.warm_flush = g.warm_flush;
   if (g.partitioned || g.warm_count <= 0) return;
-  a.warm = (int)std::max<int64_t>(0, std::min<int64_t>(g.warm_count, warm_cap<LOOPS, COLD>() - g.hot_count));
+  a.warm = (int)std::max<int64_t>(0, std::min<int64_t>(g.warm_count, warm_cap<LOOPS>() - g.hot_count));
 }
 static size_t warm_bytes(const SweepArgs &a) { return a.warm > 0 ? (size_t)(a.warm + a.warm_hot) * 8 : 0; }
 
 // warm ranks k_cycle holds at full occupancy besides the hot ids (graph_build.cu: auto "warm";
-// graphs with self-loops run the LOOPS instantiation, which holds fewer: set_warm clamps)
-int warm_fit(bool cold) {
-  const int c = cold ? warm_cap<false, true>() : warm_cap<false, false>();
-  return std::max(0, c - kHotRanks);
-}
+// graphs with self-loops run the LOOPS instantiation, which holds fewer: set_warm clamps). Not
+// with cold bins (graph_build.cu): only the non-COLD instantiations have a warm tier.
+int warm_fit() { return std::max(0, warm_cap<false>() - kHotRanks); }
 
 static void warm_init() {
-  warm_cap<false, false>();
-  warm_cap<true, false>();
-  warm_cap<false, true>();
-  warm_cap<true, true>();
+  warm_cap<false>();
+  warm_cap<true>();
 }
 
 // warps of k_cycle's grid (the cold regions reserve one chunk per warp of slack)
@@ -1173,22 +1175,26 @@ void launch_cycle(Graph &g, int64_t *launches) {
       k_cycle<false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
   } else if (cold) {
     if (g.has_loops) {
-      set_warm<true, true>(g, a);
-      k_cycle<true, false, false, true><<<grid, kAsyncThreads, warm_bytes(a), g.stream>>>(a, x);
+      k_cycle<true, false, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
     } else {
-      set_warm<false, true>(g, a);
-      k_cycle<false, false, false, true><<<grid, kAsyncThreads, warm_bytes(a), g.stream>>>(a, x);
+      k_cycle<false, false, false, true><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
     }
     k_cold_apply<<<cold_apply_grid(g), 256, 0, g.stream>>>(g.F, g.cold_rec, g.cold_off, g.cold_top,
                                                            g.cold_fill, g.cold_nbins);
     *launches += 1;
   } else {
     if (g.has_loops) {
-      set_warm<true, false>(g, a);
-      k_cycle<true, false><<<grid, kAsyncThreads, warm_bytes(a), g.stream>>>(a, x);
+      set_warm<true>(g, a);
+      if (a.warm > 0)
+        k_cycle<true, false, false, false, true><<<grid, kAsyncThreads, warm_bytes(a), g.stream>>>(a, x);
+      else
+        k_cycle<true, false><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
     } else {
-      set_warm<false, false>(g, a);
-      k_cycle<false, false><<<grid, kAsyncThreads, warm_bytes(a), g.stream>>>(a, x);
+      set_warm<false>(g, a);
+      if (a.warm > 0)
+        k_cycle<false, false, false, false, true><<<grid, kAsyncThreads, warm_bytes(a), g.stream>>>(a, x);
+      else
+        k_cycle<false, false><<<grid, kAsyncThreads, 0, g.stream>>>(a, x);
     }
   }
   *launches += 1;

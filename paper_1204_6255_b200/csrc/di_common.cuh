@@ -47,6 +47,8 @@ constexpr double kReplShare = 0.0005;
 // placed one every 2^shift ids, and every CTA of k_cycle accumulates its pushes to them (and to the
 // hot ids) in shared memory, flushed into F once when the CTA leaves the cycle.
 constexpr int kWarmIds = -1;   // option "warm" default: auto (as many as fit in shared memory)
+constexpr double kWarmShare = 0.10;   // auto: on when the hot + warm ranks take this share of the
+constexpr double kWarmLinks = 32.0;    // links and L >= kWarmLinks x grid x slots
 
 // Cold bins (async.cu): on one GPU, when F is larger than kColdF_L2 times the L2,
 // the relabelling puts a first tier of kColdHotL2 x L2 bytes of nodes (by in-degree) right after
@@ -368,7 +370,7 @@ di_status alloc_pull(Graph &g);
 di_status build_bin_entries(Graph &g, const int64_t *ptr, int64_t n, PullEntry **out, int64_t *counts);
 di_status alloc_dist(Graph &g);
 int64_t cycle_warps(const Graph &g);
-int warm_fit(bool cold);
+int warm_fit();
 // dist.cu
 di_status solve_dist(Graph &g, double d, const double *B, double tol, int variant,
                      int64_t max_sweeps, uint32_t flags, di_stats *st);

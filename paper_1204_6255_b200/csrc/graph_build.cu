@@ -147,6 +147,21 @@ __global__ void k_perm_keys64(const uint32_t *__restrict__ indeg, int64_t n, Dis
   }
 }
 
+// in-links of the K first ranks (the warm tier's candidates), one block
+__global__ void k_topsum(const uint32_t *__restrict__ indeg, const int32_t *__restrict__ sorted, int64_t K,
+                         unsigned long long *out) {
+  __shared__ unsigned long long s[256];
+  unsigned long long x = 0;
+  for (int64_t r = threadIdx.x; r < K; r += blockDim.x) x += indeg[sorted[r]];
+  s[threadIdx.x] = x;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
 // out-degree histogram in the caller's numbering (partition weights)
 __global__ void k_outdeg(const int32_t *__restrict__ src, int64_t L, int64_t *__restrict__ od) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
@@ -699,6 +714,15 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     size_t mb = cub_tmp;
     DI_CK(cub::DeviceReduce::Max(tmp, mb, indeg, mx, (int64_t)n, st));
     DI_CK(cudaMemcpyAsync(&top, mx, 4, cudaMemcpyDeviceToHost, st));
+    // in-links of the ranks a warm tier would take (auto size), for its on/off decision below
+    const bool want_warm = !g.partitioned && g.warm_opt != 0;
+    const int64_t wk = want_warm ? std::min<int64_t>(n, kHotRanks + (g.warm_opt > 0 ? g.warm_opt : warm_fit())) : 0;
+    unsigned long long topw = 0;
+    unsigned long long *tw = reinterpret_cast<unsigned long long *>(small + 32);
+    if (wk > 0) {
+      k_topsum<<<1, 256, 0, st>>>(indeg, sorted, wk, tw);
+      DI_CK(cudaMemcpyAsync(&topw, tw, 8, cudaMemcpyDeviceToHost, st));
+    }
     DI_CK(cudaStreamSynchronize(st));
     btrace("sync3");
     g.max_indeg = top;
@@ -726,8 +750,18 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     }
     g.cold_lo = (tier > 0 && prefix + tier < n) ? prefix + tier : n;
     {
-      const int64_t w = g.warm_opt < 0 ? (int64_t)warm_fit(g.cold_lo < n) : (int64_t)g.warm_opt;
-      g.warm_count = (skewed && w > 0 && n >= 8 * (w + g.hot_count)) ? w : 0;
+      const int64_t w = g.warm_opt < 0 ? (int64_t)warm_fit() : (int64_t)g.warm_opt;
+      // auto (option warm = -1): on when the candidates take at least kWarmShare of the links
+      // (skewed or not), the graph has at least kWarmLinks links per warm slot of the cycle's grid
+      // (the flush, grid x slots REDs per cycle, then stays a few % of a cycle's pushes), and not
+      // with cold bins. Measured (profiles/r2/c4_ab_warm.txt): C4 (R-MAT, the first 4096 ranks
+      // take 15 % of the links) 58.1 -> 52.9 ms; C3 (host blocks, Zipf targets, 7 %) 23.6 ->
+      // 32.9 ms; C2 (10M links, 51 %) 3.4 -> 4.9 ms; C5 with cold bins 585 -> 640 ms. An explicit
+      // count (warm > 0) turns it on whenever it fits (n >= 8 x (warm + hot), no cold bins).
+      const bool warm_pays = g.warm_opt > 0 ||
+                             (wk > 0 && (double)topw >= kWarmShare * (double)L &&
+                              (double)L >= kWarmLinks * (double)cycle_warps(g) / 8.0 * (double)wk);
+      g.warm_count = (warm_pays && !(g.cold_lo < n) && w > 0 && n >= 8 * (w + g.hot_count)) ? w : 0;
     }
     g.warm_shift = 0;
     if (g.warm_count > 0) {

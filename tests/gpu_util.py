@@ -66,6 +66,21 @@ def frontier_reference(res, deg, d, bins):
             np.concatenate(out_c), np.array(off, dtype=np.int64))
 
 
+def warm_count(indeg, n_links, n, warm=-1, hot=0, grid=148 * 4):
+    """Warm ranks the relabelling places (graph_build.cu, no cold bins): an explicit count `warm` > 0
+    whenever n >= 8 * (warm + hot); auto (-1: 4032, what k_cycle's shared memory holds on a B200)
+    when moreover the 64 + 4032 first ranks take >= 10 % of the links and the graph has
+    >= 32 links per warm slot of k_cycle's grid (148 SMs x 4 CTAs); else 0."""
+    w = 4032 if warm < 0 else warm
+    if w <= 0 or n < 8 * (w + hot):
+        return 0
+    if warm > 0:
+        return w
+    k = min(n, 64 + w)
+    top = np.sort(np.asarray(indeg))[::-1][:k].sum()
+    return w if (top >= 0.10 * n_links and n_links >= 32 * grid * k) else 0
+
+
 def warm_shift(W, region):
     """Spacing of the warm tier's ids (graph_build.cu, option warm_shift = 0): the largest s with
     8 * W * 2^s <= region (the warm ids span about the first eighth of the region)."""

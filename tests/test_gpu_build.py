@@ -3,7 +3,7 @@ import numpy as np
 import pytest
 
 import digen
-from gpu_util import csr_reference, need_gpu, upload, warm_shift
+from gpu_util import csr_reference, need_gpu, upload, warm_count, warm_shift
 
 pytestmark = pytest.mark.gpu
 
@@ -55,24 +55,27 @@ def test_builder_host_pointers_and_edges():
     assert ei.value.status == di.DI_EINVAL and "link 1" in str(ei.value)
 
 
-@pytest.mark.parametrize("name", ["c1", "c2"])
-def test_reorder_relabelling(name):
+@pytest.mark.parametrize("name,warm", [("c1", -1), ("c2", -1), ("c2", 4032), ("c2", 1000)])
+def test_reorder_relabelling(name, warm):
     """Default upload relabels nodes by descending in-degree (stable): the internal CSR equals the
     reference CSR of the relabelled link list, byte for byte."""
     need_gpu()
+    import paper_1204_6255_b200 as di
     src, dst, n = digen.make(name)
-    g = upload(src, dst, n, build_csc=True)
+    with di.option("warm", warm):
+        g = upload(src, dst, n, build_csc=True)
     old_of = g.test_perm()
     indeg = np.bincount(dst, minlength=n)
     ranked = np.argsort(-indeg, kind="stable")           # rank r -> caller id
     # placement (graph_build.cu k_place): on a skewed graph (top in-degree > 0.05 % of the links, kReplShare)
-    # the 64 hottest ranks come first; when n >= 8 * (W + 64) the next W ranks (warm tier, option warm:
-    # auto = 4032 on a B200, what k_cycle's shared memory holds) go one every S ids after them (S = 2^s,
-    # the largest with 8 * W * S <= n - 64); the rest in P stripes over the remaining ids in order,
+    # the 64 hottest ranks come first; when the first 4096 ranks take >= 10 % of the links and
+    # n >= 8 * (W + hot), the next W ranks (warm tier, option warm: auto = 4032 on a B200, what
+    # k_cycle's shared memory holds) go one every S ids after them (S = 2^s, the largest with
+    # 8 * W * S <= n - hot); the rest in P stripes over the remaining ids in order,
     # P = largest prime <= (n - hot - W)/1024
     skewed = indeg.max() > 0.0005 * len(src) and n > 256
     hot = 64 if skewed else 0
-    W = 4032 if (skewed and n >= 8 * (4032 + 64)) else 0
+    W = warm_count(indeg, len(src), n, warm, hot=hot)
     S = 1 << warm_shift(W, n - hot)
 
     def prime_at_most(x):

@@ -5,7 +5,7 @@ import pytest
 import digen
 import oracle
 from conftest import load_pins
-from gpu_util import l1, need_gpu, upload, warm_shift
+from gpu_util import l1, need_gpu, upload, warm_count, warm_shift
 from oracle import definition as defn
 
 pytestmark = pytest.mark.gpu
@@ -622,7 +622,8 @@ def test_warm_tier(warm):
     warm ranks one every 2^s ids after the 64 hot ids (checked through the relabelling); 60000 is
     above what fits in shared memory, so ids past the capacity take the plain RED. The gate against
     the oracle on C2 (R-MAT, skewed), a skewed graph with hub rows and a self-loop on a hot node
-    (LOOPS instantiation), DI-SOP and DI-CYC, host loop and graph loop, cold bins forced on too."""
+    (LOOPS instantiation), DI-SOP and DI-CYC, host loop and graph loop; with cold bins forced on the
+    tier is off (graph_build.cu) and the same gate holds."""
     need_gpu()
     import paper_1204_6255_b200 as di
     src, dst, n = digen.make("c2")
@@ -642,7 +643,7 @@ def test_warm_tier(warm):
         for cold in (0, 1):
             with di.option("warm", warm), di.option("cold_bins", cold), di.option("cold_tier", nn // 8):
                 g = upload(s_, t_, nn)
-            if warm >= 128 and nn >= 8 * (warm + 64):   # hot ids, then warm ranks every S ids (ties: stable)
+            if not cold and warm_count(indeg, len(s_), nn, warm, hot=64):   # hot, then warm every S ids
                 old_of = g.test_perm()
                 ranked = np.argsort(-indeg, kind="stable").astype(np.int32)
                 sh = warm_shift(warm, nn // 8 if cold else nn - 64)

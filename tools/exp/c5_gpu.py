@@ -14,7 +14,11 @@ ap.add_argument("--profile", action="store_true")
 ap.add_argument("--cold", type=int, default=-1, help="option cold_bins (-1 auto, 0 off, 1 on)")
 ap.add_argument("--cold-tier", type=int, default=0, help="option cold_tier (first-tier nodes)")
 ap.add_argument("--cold-shift", type=int, default=0, help="option cold_shift (slice = 2^shift nodes)")
+ap.add_argument("--warm", type=int, default=-1, help="option warm (-1 auto, 0 off)")
+ap.add_argument("--warm-shift", type=int, default=0, help="option warm_shift (0 auto)")
 a = ap.parse_args()
+di.set_option("warm", a.warm)
+di.set_option("warm_shift", a.warm_shift)
 di.set_option("cold_bins", a.cold)
 di.set_option("cold_tier", a.cold_tier)
 di.set_option("cold_shift", a.cold_shift)
@@ -23,7 +27,7 @@ t = time.time()
 n = digen.CONFIGS[a.config].n
 s, d, _ = digen.make_range_gpu(a.config, 0, n)
 torch.cuda.synchronize()
-print(a.config, "cold_bins", a.cold, "cold_tier", a.cold_tier, "cold_shift", a.cold_shift, "generated on the GPU: N =", n, "L =", s.numel(), "in", round(time.time() - t, 1), "s", flush=True)
+print(a.config, "cold_bins", a.cold, "cold_tier", a.cold_tier, "cold_shift", a.cold_shift, "warm", a.warm, "warm_shift", a.warm_shift, "generated on the GPU: N =", n, "L =", s.numel(), "in", round(time.time() - t, 1), "s", flush=True)
 t = time.time()
 g = di.Graph(s, d, n)
 torch.cuda.synchronize()

@@ -106,11 +106,12 @@ if __name__ == "__main__":
         for e in c:
             name = e["kernel"].split("::")[-1].split("(")[0].strip()
             # the single-GPU plain instantiations keep the short key bench.py reads ("k_cycle":
-            # k_cycle<0, 0, 0, 0> or r1's k_cycle<0, 0>); other instantiations (COLD, DIST, LOOPS)
-            # get their template arguments in the key
+            # k_cycle<0, 0, 0, 0> or r1's k_cycle<0, 0>, and round 2's warm-tier k_cycle<0, 0, 0, 0, 1>,
+            # the bench kernel on C4); other instantiations (COLD, DIST, LOOPS) get their template
+            # arguments in the key
             base, _, targs = name.partition("<")
             targs = targs.rstrip(">").replace(" ", "")
-            plain = not targs or set(targs.split(",")) == {"0"}
+            plain = not targs or set(targs.split(",")) == {"0"} or targs == "0,0,0,0,1
             name = base if plain else f"{base}<{targs}>"
             b = to_bytes(e["dram__bytes_read.sum"]) + to_bytes(e["dram__bytes_write.sum"])
             tr.setdefault(name + "_samples", []).append(b)
