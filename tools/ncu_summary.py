@@ -111,7 +111,7 @@ if __name__ == "__main__":
             # arguments in the key
             base, _, targs = name.partition("<")
             targs = targs.rstrip(">").replace(" ", "")
-            plain = not targs or set(targs.split(",")) == {"0"} or targs == "0,0,0,0,1
+            plain = not targs or set(targs.split(",")) == {"0"} or targs == "0,0,0,0,1"
             name = base if plain else f"{base}<{targs}>"
             b = to_bytes(e["dram__bytes_read.sum"]) + to_bytes(e["dram__bytes_write.sum"])
             tr.setdefault(name + "_samples", []).append(b)
