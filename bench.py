@@ -23,6 +23,7 @@ Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -349,6 +350,9 @@ def run_ours(args):
     g.free()
     torch.cuda.empty_cache()
     E2E_WARM = 3                                         # pool growth on the first host-pointer builds
+    gc.disable()   # no collector pause of the harness inside a timed step (re-enabled below)
+    if args.build_trace:
+        di.set_option("build_trace", 1)
     for k in range(args.e2e_steps + E2E_WARM):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -372,6 +376,7 @@ def run_ours(args):
             e2e_ms.append(dt)
             e2e_up.append(round((t1 - t0) * 1e3, 1))
             e2e_links += st["link_diffusions"]
+    gc.enable()
     e2e_val = e2e_links / (sum(e2e_ms) * 1e-3) / 1e9 if e2e_ms else None
     e2e_serial = e2e_val
     e2e_pipe = None
@@ -621,6 +626,8 @@ def main():
     ap.add_argument("--no-breadth", action="store_true", help="skip the DI-CYC / PI / PI' rows")
     ap.add_argument("--e2e-pipeline", type=int, default=0,
                     help="also measure e2e over a stream of graphs (upload of k+1 overlaps solve of k)")
+    ap.add_argument("--build-trace", action="store_true",
+                    help="diagnostic: the library's build_trace option during the e2e uploads (stderr)")
     ap.add_argument("--launch-check", action="store_true",
                     help="only check the launch: N ranks over gloo (CPU), world == --gpus, rank 0 prints "
                          "one JSON line (tests/test_bench_launch.py)")

@@ -57,6 +57,28 @@ cudaError_t dmalloc_bytes(void **p, size_t bytes) {
   return e;
 }
 
+// Pinned host mirrors of the per-graph Scalars from a process-wide slab (cudaMallocHost /
+// cudaFreeHost per upload cost ms and cudaFreeHost synchronises the device): slabs of 64 mirrors,
+// never returned to the driver, handed out and back under a mutex.
+static std::mutex g_pin_mu;
+static std::vector<Scalars *> g_pin_free;
+cudaError_t pinned_scalars_get(Scalars **out) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  if (g_pin_free.empty()) {
+    Scalars *slab = nullptr;
+    cudaError_t e = cudaMallocHost(&slab, 64 * sizeof(Scalars));
+    if (e != cudaSuccess) return e;
+    for (int k = 63; k >= 0; k--) g_pin_free.push_back(slab + k);
+  }
+  *out = g_pin_free.back();
+  g_pin_free.pop_back();
+  return cudaSuccess;
+}
+void pinned_scalars_put(Scalars *p) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back(p);
+}
+
 void dfree(void *p) {
   if (p) cudaFreeAsync(p, alloc_stream());
 }
@@ -128,7 +150,7 @@ void free_graph(Graph *g) {
   if (g->cmp_partials) dfree(g->cmp_partials);
   if (g->loop_exec) cudaGraphExecDestroy(g->loop_exec);
   if (g->loop_graph) cudaGraphDestroy(g->loop_graph);
-  if (g->sc_host) cudaFreeHost(g->sc_host);
+  if (g->sc_host) pinned_scalars_put(g->sc_host);
   free_dist(*g);
   if (g->group) {
     std::lock_guard<std::mutex> lk(g->group->m);
@@ -343,8 +365,11 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
     g->warm_shift_opt = o.warm_shift;
   }
   di_status s = build_graph(*g, src, dst, n_links, flags);
+  btrace("built");
   if (s == DI_OK) s = alloc_state(*g);
+  btrace("state");
   if (s == DI_OK) s = alloc_pull(*g);
+  btrace("pull");
   if (s == DI_OK && partitioned) s = alloc_dist(*g);
   if (s != DI_OK) {
     free_graph(g);

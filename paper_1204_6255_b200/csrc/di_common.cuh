@@ -333,6 +333,8 @@ inline cudaError_t dmalloc(T **p, size_t bytes) {
   return dmalloc_bytes(reinterpret_cast<void **>(p), bytes);
 }
 void dfree(void *p);
+cudaError_t pinned_scalars_get(Scalars **out);   // pinned host mirror of a graph's Scalars
+void pinned_scalars_put(Scalars *p);
 cudaError_t dmemset(void *p, int v, size_t bytes);
 
 // ---------------------------------------------------------------- error plumbing
@@ -348,6 +350,7 @@ void set_error(const std::string &msg);
 
 // ---------------------------------------------------------------- launchers
 // graph_build.cu
+void btrace(const char *what);   // option build_trace: host timestamp of a build phase (stderr)
 di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t n_links,
                       uint32_t flags);
 // diffusion.cu

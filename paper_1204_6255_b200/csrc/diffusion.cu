@@ -615,7 +615,7 @@ di_status alloc_state(Graph &g) {
   DI_CK(dmemset(g.F, 0, (size_t)n * 8));
   DI_CK(dmalloc(&g.sc, sizeof(Scalars)));
   DI_CK(dmemset(g.sc, 0, sizeof(Scalars)));
-  DI_CK(cudaMallocHost(&g.sc_host, sizeof(Scalars)));
+  DI_CK(pinned_scalars_get(&g.sc_host));
   memset(g.sc_host, 0, sizeof(Scalars));
   DI_CK(dmalloc(&g.partials, (size_t)nt * 4 * 8));
   DI_CK(dmalloc(&g.ipartials, (size_t)nt * 4 * 8));

@@ -431,6 +431,8 @@ __global__ void k_swap_keys(const uint64_t *__restrict__ in, int64_t L, int b,
 }
 
 // option build_trace = 1: host timestamps of the build phases on stderr (diagnostics)
+}  // namespace
+
 void btrace(const char *what) {
   const bool on = options().build_trace != 0;
   if (!on) return;
@@ -440,6 +442,8 @@ void btrace(const char *what) {
   fprintf(stderr, "[di build] %-8s %8.2f ms\n", what,
           std::chrono::duration<double, std::milli>(now - t0).count());
 }
+
+namespace {
 
 int grid_for(int64_t n, int sms) {
   int64_t g = (n + 255) / 256;
