@@ -56,6 +56,8 @@ constexpr double kWarmLinks = 32.0;    // links and L >= kWarmLinks x grid x slo
 // an L2 miss, ~22 G random REDs/s into 1 GB) is appended as a 16-B record to the bin of its
 // slice of 2^shift nodes (at most kColdBins slices), then applied slice by slice after the cycle
 // (k_cold_apply: the slice's F lines stay in L2 while its records stream through).
+constexpr int kPipeChunks = 8;                // pipelined host upload: source-id chunks (graph_build.cu)
+constexpr int64_t kPipeMinLinks = 1ll << 22;  // ... for link lists of at least this many links
 constexpr int kColdBins = 64;
 constexpr int kColdChunk = 64;          // records per warp chunk (one 1 KB run of a bin)
 constexpr double kColdF_L2 = 2.0;

@@ -144,3 +144,46 @@ def test_builder_row_sort_option(row_sort):
                 for k in ("row_ptr", "col", "deg", "kloop"):
                     assert np.array_equal(got[k], r2[k]), (nn, reorder, k)
                 g.free()
+
+
+def test_pipelined_host_upload():
+    """Host link lists of >= 2^22 links take the pipelined upload (graph_build.cu: targets copied
+    first and validated / counted while the sources follow in 8 chunks, keys made and sorted per
+    chunk, sorted chunks merged): the CSR, CSC and relabelling are byte-identical to the upload of
+    the same list from device memory (one key sort), with and without dedup / self-loop removal;
+    a bad id anywhere is reported at its (first) link index like the one-shot path."""
+    need_gpu()
+    import paper_1204_6255_b200 as di
+    rng = np.random.default_rng(21)
+    n = 1 << 20
+    L = 5_000_003   # ragged chunks
+    src = (rng.zipf(1.6, L) % n).astype(np.int32)
+    dst = (rng.zipf(1.4, L) % n).astype(np.int32)
+    src[:1000] = dst[:1000]                        # self-loops
+    src[1000:3000], dst[1000:3000] = src[5000:7000], dst[5000:7000]   # duplicates
+    for kw in ({}, {"dedup": True, "drop_self_loops": True}, {"build_csc": True}):
+        gh = di.Graph(src, dst, n, **kw)            # host arrays: DI_HOST_PTRS
+        gd = upload(src, dst, n, **kw)              # device tensors
+        a, b = gh.test_csr(csc=kw.get("build_csc", False)), gd.test_csr(csc=kw.get("build_csc", False))
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (kw, k)
+        assert np.array_equal(gh.test_perm(), gd.test_perm())
+        gh.free()
+        gd.free()
+    ref = csr_reference(src, dst, n)
+    g = di.Graph(src, dst, n, reorder=False)
+    got = g.test_csr()
+    for k in ("row_ptr", "col", "deg", "kloop"):
+        assert np.array_equal(got[k], ref[k]), k
+    g.free()
+    for bad in ((3_000_000, None), (4_500_001, 4_000_000)):
+        s2, d2 = src.copy(), dst.copy()
+        s2[bad[0]] = -1 if bad[1] else s2[bad[0]]
+        if bad[1] is None:
+            d2[bad[0]] = n
+        else:
+            d2[bad[1]] = n + 5
+        first = bad[0] if bad[1] is None else bad[1]
+        with pytest.raises(di.DIError) as ei:
+            di.Graph(s2, d2, n)
+        assert ei.value.status == di.DI_EINVAL and f"link {first} " in str(ei.value), str(ei.value)
