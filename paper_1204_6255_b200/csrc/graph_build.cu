@@ -41,12 +41,13 @@ __global__ void k_validate(const int32_t *__restrict__ src, const int32_t *__res
 // Pipelined host upload (one GPU, DESIGN.md §6 "upload"): the target ids arrive first and are
 // validated (and counted for the relabelling) while the source ids are still being copied
 __global__ void k_validate_dst(const int32_t *__restrict__ dst, int64_t L, int64_t n,
-                               unsigned long long *__restrict__ bad, uint32_t *__restrict__ indeg) {
+                               unsigned long long *__restrict__ bad, uint32_t *__restrict__ indeg,
+                               int64_t k0) {   // (dst: the chunk starting at link k0)
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int32_t t = dst[k];
     if (t < 0 || t >= n)
-      atomicMin(bad, (unsigned long long)k);
+      atomicMin(bad, (unsigned long long)(k0 + k));
     else if (indeg)
       atomicAdd(indeg + t, 1u);
   }
@@ -629,7 +630,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   // chunk of sources (the build's kernels stay on st and wait for them)
   struct PipeRes {
     cudaStream_t cp = nullptr;
-    cudaEvent_t ev[kPipeChunks + 1] = {};
+    cudaEvent_t ev[2 * kPipeChunks] = {};   // target chunks, then source chunks
     ~PipeRes() {   // (before the arena is released: declared after it)
       if (cp) cudaStreamSynchronize(cp);
       for (auto e : ev)
@@ -642,14 +643,14 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     if (pipe) {
       DI_CK(cudaStreamCreateWithFlags(&pr.cp, cudaStreamNonBlocking));
       for (auto &e : pr.ev) DI_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      DI_CK(cudaMemcpyAsync(hd, dst, (size_t)L * 4, cudaMemcpyHostToDevice, pr.cp));
-      DI_CK(cudaEventRecord(pr.ev[0], pr.cp));
-      for (int c = 0; c < kPipeChunks; c++) {
-        const int64_t k0 = std::min<int64_t>(L, c * chunk), k1 = std::min<int64_t>(L, k0 + chunk);
-        if (k1 > k0)
-          DI_CK(cudaMemcpyAsync(hs + k0, src + k0, (size_t)(k1 - k0) * 4, cudaMemcpyHostToDevice, pr.cp));
-        DI_CK(cudaEventRecord(pr.ev[c + 1], pr.cp));
-      }
+      for (int h = 0; h < 2; h++)   // the targets, then the sources, chunk by chunk
+        for (int c = 0; c < kPipeChunks; c++) {
+          const int64_t k0 = std::min<int64_t>(L, c * chunk), k1 = std::min<int64_t>(L, k0 + chunk);
+          if (k1 > k0)
+            DI_CK(cudaMemcpyAsync((h ? hs : hd) + k0, (h ? src : dst) + k0, (size_t)(k1 - k0) * 4,
+                                  cudaMemcpyHostToDevice, pr.cp));
+          DI_CK(cudaEventRecord(pr.ev[h * kPipeChunks + c], pr.cp));
+        }
     } else if (L > 0) {
       DI_CK(cudaMemcpyAsync(hs, src, (size_t)L * 4, cudaMemcpyHostToDevice, st));
       DI_CK(cudaMemcpyAsync(hd, dst, (size_t)L * 4, cudaMemcpyHostToDevice, st));
@@ -680,9 +681,13 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   const int64_t s_lo = local ? g.local_lo : 0, s_hi = local ? g.local_hi : n;
   // a range outside [0, n) fails on every rank, in the collective below
   const bool bad_range = local && !(s_lo >= 0 && s_lo < s_hi && s_hi <= n);
-  if (pipe) {   // the targets only (the sources are validated chunk by chunk, below)
-    DI_CK(cudaStreamWaitEvent(st, pr.ev[0], 0));
-    k_validate_dst<<<grid_for(L, sms), 256, 0, st>>>(d_dev, L, n, badb, indeg);
+  if (pipe) {   // the targets, chunk by chunk as they land (the sources: below)
+    for (int c = 0; c < kPipeChunks; c++) {
+      const int64_t k0 = std::min<int64_t>(L, c * chunk), k1 = std::min<int64_t>(L, k0 + chunk);
+      DI_CK(cudaStreamWaitEvent(st, pr.ev[c], 0));
+      if (k1 > k0)
+        k_validate_dst<<<grid_for(k1 - k0, sms), 256, 0, st>>>(d_dev + k0, k1 - k0, n, badb, indeg, k0);
+    }
   } else if (L > 0 && !bad_range) {
     k_validate<<<grid_for(L, sms), 256, 0, st>>>(s_dev, d_dev, L, n, s_lo, s_hi, badb, indeg);
   }
@@ -936,7 +941,7 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
     static_assert((kPipeChunks & (kPipeChunks - 1)) == 0, "kPipeChunks: a power of two");
     for (int c = 0; c < kPipeChunks; c++) {
       const int64_t k0 = std::min<int64_t>(L, c * chunk), k1 = std::min<int64_t>(L, k0 + chunk);
-      DI_CK(cudaStreamWaitEvent(st, pr.ev[c + 1], 0));
+      DI_CK(cudaStreamWaitEvent(st, pr.ev[kPipeChunks + c], 0));
       k_make_keys_chunk<<<grid_for(k1 - k0, sms), 256, 0, st>>>(s_dev, d_dev, k0, k1, n, b, g.new_of, ka, badb);
       size_t tb = cub_tmp;
       DI_CK(cub::DeviceRadixSort::SortKeys(tmp, tb, ka + k0, kb + k0, (int64_t)(k1 - k0), 0, 2 * b, st));
