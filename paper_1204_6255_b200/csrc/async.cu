@@ -867,6 +867,11 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
 // in L2), each a RED into F; the last block rewinds the bins. Chunks past their fill are skipped.
 // The grid is co-resident (at most the resident blocks of the device) and the blocks meet at a
 // barrier between two bins, so that the whole grid works on one slice of F at a time.
+#ifndef DI_APPLY_UNROLL
+#define DI_APPLY_UNROLL 4
+#endif
+constexpr int kApplyUnroll = DI_APPLY_UNROLL;
+
 __global__ void __launch_bounds__(256) k_cold_apply(double *__restrict__ F, const ColdRec *__restrict__ rec,
                                                     const int64_t *__restrict__ off,
                                                     unsigned long long *top,
@@ -890,14 +895,26 @@ __global__ void __launch_bounds__(256) k_cold_apply(double *__restrict__ F, cons
     const int64_t base = off[b];
     const int64_t per = (m + gridDim.x - 1) / gridDim.x;
     const int64_t r0 = (int64_t)blockIdx.x * per, r1 = r0 + per < m ? r0 + per : m;
-    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-      const int64_t gr = base + r;   // regions are chunk-aligned
-      if ((int)(r % kColdChunk) >= __ldg(fill + gr / kColdChunk)) continue;
-      int4 q;
-      asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
-                   : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
-                   : "l"(rec + gr), "l"(pol));
-      red_add_f64(F + q.x, __hiloint2double(q.w, q.z));
+    // kApplyUnroll records per thread in flight (loads first, then the REDs): the apply is
+    // latency-bound on the record loads (ncu C5: 10 % issue active, long_scoreboard stalls)
+    constexpr int U = kApplyUnroll;
+    for (int64_t rb = r0 + threadIdx.x; rb < r1; rb += (int64_t)U * blockDim.x) {
+      int4 q[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t r = rb + (int64_t)u * blockDim.x;
+        const int64_t gr = base + r;   // regions are chunk-aligned
+        ok[u] = r < r1 && (int)(r % kColdChunk) < __ldg(fill + gr / kColdChunk);
+        q[u] = make_int4(0, 0, 0, 0);
+        if (ok[u])
+          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                       : "=r"(q[u].x), "=r"(q[u].y), "=r"(q[u].z), "=r"(q[u].w)
+                       : "l"(rec + gr), "l"(pol));
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++)
+        if (ok[u]) red_add_f64(F + q[u].x, __hiloint2double(q[u].w, q[u].z));
     }
   }
   __syncthreads();
