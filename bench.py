@@ -351,32 +351,34 @@ def run_ours(args):
     torch.cuda.empty_cache()
     E2E_WARM = 3                                         # pool growth on the first host-pointer builds
     gc.disable()   # no collector pause of the harness inside a timed step (re-enabled below)
-    if args.build_trace:
-        di.set_option("build_trace", 1)
-    for k in range(args.e2e_steps + E2E_WARM):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        gh = di.Graph(src_p, dst_p, n, stream=stream, **part)  # DI_HOST_PTRS: H2D inside
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        st = gh.solve(d=D, tol=TOL, variant=args.variant, mode=args.mode, blocks=args.blocks,
-                      asynchronous=use_async, dist_async=dist_async,
-                      graph_loop=use_graph)
-        t2 = time.perf_counter()
-        H = gh.history()
-        H_host.copy_(H, non_blocking=True)
-        torch.cuda.synchronize()
-        dt = (time.perf_counter() - t0) * 1e3
-        print(f"[bench] e2e step {k}: upload {(t1 - t0) * 1e3:.1f} ms, solve {(t2 - t1) * 1e3:.1f} ms "
-              f"(device {st['solve_ms']:.1f}), H to host {(time.perf_counter() - t2) * 1e3:.1f} ms",
-              file=sys.stderr, flush=True)
-        gh.free()
-        del H
-        if k >= E2E_WARM:
-            e2e_ms.append(dt)
-            e2e_up.append(round((t1 - t0) * 1e3, 1))
-            e2e_links += st["link_diffusions"]
-    gc.enable()
+    try:
+        if args.build_trace:
+            di.set_option("build_trace", 1)
+        for k in range(args.e2e_steps + E2E_WARM):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            gh = di.Graph(src_p, dst_p, n, stream=stream, **part)  # DI_HOST_PTRS: H2D inside
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            st = gh.solve(d=D, tol=TOL, variant=args.variant, mode=args.mode, blocks=args.blocks,
+                          asynchronous=use_async, dist_async=dist_async,
+                          graph_loop=use_graph)
+            t2 = time.perf_counter()
+            H = gh.history()
+            H_host.copy_(H, non_blocking=True)
+            torch.cuda.synchronize()
+            dt = (time.perf_counter() - t0) * 1e3
+            print(f"[bench] e2e step {k}: upload {(t1 - t0) * 1e3:.1f} ms, solve {(t2 - t1) * 1e3:.1f} ms "
+                  f"(device {st['solve_ms']:.1f}), H to host {(time.perf_counter() - t2) * 1e3:.1f} ms",
+                  file=sys.stderr, flush=True)
+            gh.free()
+            del H
+            if k >= E2E_WARM:
+                e2e_ms.append(dt)
+                e2e_up.append(round((t1 - t0) * 1e3, 1))
+                e2e_links += st["link_diffusions"]
+    finally:
+        gc.enable()
     e2e_val = e2e_links / (sum(e2e_ms) * 1e-3) / 1e9 if e2e_ms else None
     e2e_serial = e2e_val
     e2e_pipe = None
