@@ -47,6 +47,12 @@ constexpr int kCycTile = kAsyncThreads * kCycItems;   // nodes per tile
 // sequential cycle: 1024-node tiles x 4 CTAs/SM: C4 43 cycles / 60.2 ms, C2 3.6 ms; 3 CTAs/SM:
 // 42 / 58.7 ms, C2 3.2 ms; 512-node tiles (2 nodes per thread) x 4 CTAs/SM: C4 42 / 58.2 ms,
 // C3 25.8 -> 24.2 ms, C2 3.0 ms at the same per-link rate (tools/exp/async.py)
+#ifndef DI_LL_BATCH
+#define DI_LL_BATCH 8     // long rows (option long_lanes): column loads in flight per lane
+#endif
+#ifndef DI_LL_PIPE
+#define DI_LL_PIPE 0      // 1: the next batch's loads issued before the current batch's REDs
+#endif
 #ifndef DI_ASYNC_MINB
 #define DI_ASYNC_MINB 4
 #endif
@@ -599,15 +605,34 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
           // lane-consecutive targets: lane l takes links beg + 32u + l, so the 32 REDs of one
           // instruction go to 32 consecutive (sorted) targets of the row, which share L2 lines
           // where the row is dense in the hot ids; scalar coalesced loads, no masked lanes
-          for (int64_t p0 = beg; p0 < end; p0 += 32 * 8) {
-            int32_t jj[8];
+          constexpr int NB = DI_LL_BATCH;   // loads in flight per lane
+#if DI_LL_PIPE
+          // software-pipelined: the next batch's column loads are issued before this batch's REDs
+          int32_t nx[NB];
 #pragma unroll
-            for (int u = 0; u < 8; u++) {
+          for (int u = 0; u < NB; u++) {
+            const int64_t p = beg + 32 * u + lane;
+            nx[u] = p < end ? ld_col(col + p, pol) : -1;
+          }
+#endif
+          for (int64_t p0 = beg; p0 < end; p0 += 32 * NB) {
+            int32_t jj[NB];
+#if DI_LL_PIPE
+#pragma unroll
+            for (int u = 0; u < NB; u++) {
+              jj[u] = nx[u];
+              const int64_t p = p0 + 32 * (NB + u) + lane;
+              nx[u] = p < end ? ld_col(col + p, pol) : -1;
+            }
+#else
+#pragma unroll
+            for (int u = 0; u < NB; u++) {
               const int64_t p = p0 + 32 * u + lane;
               jj[u] = p < end ? ld_col(col + p, pol) : -1;
             }
+#endif
 #pragma unroll
-            for (int u = 0; u < 8; u++) {
+            for (int u = 0; u < NB; u++) {
               const int32_t j = jj[u];
               if (j >= 0 && (!LOOPS || j != gi)) {
                 if (warm_take(wt, j, v))
