@@ -655,4 +655,17 @@ def test_warm_tier(warm):
                     st = g.solve(d=D, tol=1e-10, variant=variant, asynchronous=True, graph_loop=graph_loop)
                     assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
                     assert l1(g.history().cpu().numpy(), Ho) <= 1e-9, (nn, cold, variant, graph_loop)
+            if nn == n2:   # stopped after k cycles: the flushed accumulators leave F = B + P.H - H
+                P = defn.sparse_P(s_, t_, nn, D)
+                B = defn.uniform_B(nn, D)
+                out = np.bincount(s_, minlength=nn)
+                for k in (1, 2, 5):
+                    st = g.solve(d=D, tol=1e-300, max_sweeps=k, asynchronous=True)
+                    assert st["sweeps"] == k
+                    H = g.history().cpu().numpy()
+                    _, F = g.residual(return_F=True)
+                    F = F.cpu().numpy()
+                    assert np.all(F >= 0) and np.abs(F - (B + P @ H - H)).max() <= 1e-15, (warm, cold, k)
+                    cons = F.sum() + (1 - D) * H[out > 0].sum() + H[out == 0].sum()
+                    assert abs(cons - (1 - D)) <= 1e-14, (warm, cold, k)
             g.free()
