@@ -235,6 +235,10 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
  *                                          the cycle (-1: as many as fit, 4032 on B200; 0: off)
  *   "warm_flush"     0        >= 0      U: the cycle kernel's CTAs also flush the warm tier into F
  *                                          every k of their tiles (0: only when they leave the cycle)
+ *   "dist_parts"     1        1..64     U: partitioned DI_ASYNC solves run each rank's cycle in k
+ *                                          parts of its tiles, every part followed by the exchange
+ *                                          (remote fluid arrives within the cycle; the threshold
+ *                                          r/L is taken per part; di_stats.sweeps counts parts)
  *   "warm_shift"     0        0..30     U: warm ranks one every 2^k ids (0: auto, the warm ids
  *                                          spanning about the first eighth of the range or of the
  *                                          first tier)

@@ -363,6 +363,7 @@ di_status di_graph_upload(const int32_t *src, const int32_t *dst, int64_t n_link
     g->warm_opt = o.warm;
     g->warm_flush = o.warm_flush;
     g->warm_shift_opt = o.warm_shift;
+    g->dist_parts = o.dist_parts;
   }
   di_status s = build_graph(*g, src, dst, n_links, flags);
   btrace("built");
@@ -394,7 +395,7 @@ const OptDesc kOpts[] = {
     {"remote_compact", 0, 1, true}, {"remote_tier", 0, 2147483647.0, true},
     {"long_lanes", 0, 1, true},     {"row_sort", 0, 1, true},      {"line_spread", 1, 16, true},
     {"cold_shift", 0, 30, true},     {"warm", -1, 65536, true},      {"warm_flush", 0, 1 << 20, true},
-    {"warm_shift", 0, 30, true},
+    {"warm_shift", 0, 30, true},     {"dist_parts", 1, 64, true},
 };
 }  // namespace
 
@@ -431,6 +432,7 @@ di_status di_set_option(const char *name, double value) {
   else if (n == "warm") o.warm = iv;
   else if (n == "warm_flush") o.warm_flush = iv;
   else if (n == "warm_shift") o.warm_shift = iv;
+  else if (n == "dist_parts") o.dist_parts = iv;
   else if (n == "line_spread") {
     if (iv != 1 && iv != 2 && iv != 4 && iv != 8 && iv != 16)
       return fail(DI_EINVAL, "di_set_option: line_spread must be 1, 2, 4, 8 or 16");
@@ -463,6 +465,7 @@ di_status di_get_option(const char *name, double *value) {
   else if (n == "warm") *value = o.warm;
   else if (n == "warm_flush") *value = o.warm_flush;
   else if (n == "warm_shift") *value = o.warm_shift;
+  else if (n == "dist_parts") *value = o.dist_parts;
   else if (n == "line_spread") *value = o.line_spread;
   else if (n == "cold_shift") *value = o.cold_shift;
   else return fail(DI_EINVAL, "di_get_option: unknown option '" + n + "'");

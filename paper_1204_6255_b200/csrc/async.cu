@@ -400,8 +400,9 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
 
   for (;;) {
     if (threadIdx.x == 0) {
-      const int64_t c = (int64_t)atomicAdd(&sc->tile_next, 1u);
-      int64_t tl = c;
+      // (option dist_parts: this launch takes the claims [claim_lo, claim_hi) of the rank's cycle)
+      const int64_t c = (int64_t)atomicAdd(&sc->tile_next, 1u) + a.claim_lo;
+      int64_t tl = (a.claim_hi >= 0 && c >= a.claim_hi) ? a.ntiles : c;
       int it = -1;
       if (c > 0 && a.n_hub > 0) {  // claims 1..n_hub: hub items; then tiles 1, 2, ...
         if (c <= a.n_hub) {
@@ -1201,6 +1202,14 @@ void launch_cycle(Graph &g, int64_t *launches) {
     a.n_hub = g.n_hub;
   }
   const int grid = cycle_grid(g);
+  if (dist && g.dist_parts > 1 && g.cur_part >= 0) {   // this sweep: part cur_part of the cycle
+    // (at most one part per tile: an empty part selects nothing and would trip the starvation
+    //  guard into a threshold-0 sweep every other time)
+    const int64_t T = a.ntiles, K = std::min<int64_t>(g.dist_parts, std::max<int64_t>(T, 1)),
+                  p = g.cur_part % K;
+    a.claim_lo = T * p / K;
+    a.claim_hi = T * (p + 1) / K;
+  }
   if (dist && g.cur_compact) {  // hot remote accumulator + cold records into the owners' inboxes
     x.ipar = g.cur_par;
     x.compact = 1;

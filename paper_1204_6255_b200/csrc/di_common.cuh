@@ -126,6 +126,7 @@ struct Options {
                              // (skewed graphs; -1 auto, 0 off)
   int warm_flush = 0;        // "warm_flush": k_cycle flushes them every k tiles of a CTA (0: at its end)
   int warm_shift = 0;        // "warm_shift": warm ranks every 2^k ids (0: spread over the range / first tier)
+  int dist_parts = 1;        // "dist_parts": partitioned DI_ASYNC: each cycle in k parts, an exchange after each
 };
 Options options();           // a snapshot of the current options
 
@@ -315,6 +316,8 @@ struct Graph {
   int warm_shift = 0;
   int warm_flush = 0;             // option warm_flush
   int warm_shift_opt = 0;         // option warm_shift
+  int dist_parts = 1, cur_part = -1;  // option dist_parts; the part solve_dist launches next
+                                      // (-1: whole cycles, every other caller)
 };
 
 // ---------------------------------------------------------------- device memory

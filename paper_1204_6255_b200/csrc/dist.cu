@@ -989,6 +989,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
   double push_ms = 0.0, select_ms = 0.0, xchg_ms = 0.0;
   int64_t push_launches = 0;
   int64_t batch = 4;
+  int64_t part_ctr = 0;   // option dist_parts: the part of the rank's cycle each sweep takes
   double r_prev = g.sc_host->r;
   while (!converged && launched < max_sweeps) {
     // ---- batched sweeps through peer memory: no host synchronisation inside a batch
@@ -1001,6 +1002,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       for (int64_t j = 0; j < k; j++) {
         if (!async) launch_select(g, 0, &launches);
         g.cur_par = par;   // the cold regions written by this cycle
+        g.cur_part = (int)(part_ctr++ % g.dist_parts);
         if (async)
           launch_cycle(g, &launches);
         else if (g.has_loops)
@@ -1045,6 +1047,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
       if (!async) launch_select(g, 0, &launches);
       if (prof) DI_CK(cudaEventRecord(pe[1], g.stream));
       g.cur_par = par;
+      g.cur_part = (int)(part_ctr++ % g.dist_parts);
       if (async)
         launch_cycle(g, &launches);   // the asynchronous cycle on this rank's range (R7)
       else if (g.has_loops)
@@ -1149,6 +1152,7 @@ di_status solve_dist(Graph &g, double d, const double *B, double tol, int varian
     DI_CK(cudaStreamSynchronize(g.stream));
     g.sc_host->stop = 0;
   }
+  g.cur_part = -1;   // (other callers of launch_cycle take whole cycles)
   if (launched == 0 && !converged) {
     if ((s = global_sum_F(g, 0, &launches)) != DI_OK) return s;
     DI_CK(cudaMemcpyAsync(g.sc_host, g.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, g.stream));

@@ -46,6 +46,7 @@ struct SweepArgs {
   int64_t cold_hot_tiles;   // tiles holding first-tier ids (interleaved over the cycle)
   int cold_shift, cold_nbins;
   int long_lanes;           // k_cycle long rows: lane-consecutive targets (option long_lanes)
+  int64_t claim_lo, claim_hi;   // k_cycle: claims [claim_lo, claim_hi) (claim_hi < 0: all)
   int warm;                 // k_cycle warm tier: warm-rank slots in shared memory (0: off), the
   int warm_hot, warm_shift; //   ids warm_hot + k << warm_shift (k < warm), and the hot ids
   int warm_flush;           //   flushed every warm_flush tiles of a CTA too (0: at its end only)
@@ -401,6 +402,8 @@ inline SweepArgs sweep_args(Graph &g, int test_mode, int blk = 0, int blocks = 1
   a.cold_hot_tiles = 0;
   a.long_lanes = 0;
   a.warm = 0;
+  a.claim_lo = 0;
+  a.claim_hi = -1;
   a.warm_hot = 0;
   a.warm_shift = 0;
   a.warm_flush = 0;

@@ -576,3 +576,39 @@ def test_compact_remote_cold_records(G):
         for s in sts:
             assert s["exchange_bytes"] == 12 * s["exchange_entries"] + 16 * s["exchange_cold"]
             assert s["p2p_exchanges"] == s["sweeps"]
+
+
+@pytest.mark.parametrize("G,parts", [(2, 2), (4, 3), (8, 4)])
+def test_dist_parts(G, parts):
+    """Option dist_parts: each rank's asynchronous cycle runs in `parts` launches over
+    consecutive claim windows of its tiles, the exchange after each, so remote fluid arrives within
+    the cycle. Pins, random graphs with loops and duplicates vs the dense solve, and C1 to the
+    north_star gate against the oracle, with the compact remote path (a small remote tier: cold
+    records) and the plain one."""
+    need_gpu()
+    import paper_1204_6255_b200 as di
+    with di.option("dist_parts", parts), di.option("remote_tier", 5):
+        for name, n, links, X in load_pins():
+            if n < G:
+                continue
+            src = np.array([s for s, _ in links], dtype=np.int32)
+            dst = np.array([t for _, t in links], dtype=np.int32)
+            (H, F, st, sts, _), = run(src, dst, n, G, [dict(d=D, tol=1e-16, asynchronous=True)])
+            assert st["converged"] == 1 and l1(H, [float(x) for x in X]) <= 1e-14, (name, st, l1(H, [float(x) for x in X]))
+        for seed in range(8):
+            src, dst, n = digen.small_random(seed, n_max=3000 if seed % 2 else 200)
+            if n < G:
+                continue
+            X = defn.solve_dense(src, dst, n, D) if n <= 64 else oracle.di(src, dst, n, d=D, tol=1e-15)[0]
+            for H, F, st, sts, _ in run(src, dst, n, G, [dict(d=D, tol=1e-15, variant=v, asynchronous=True)
+                                                          for v in ("sop", "cyc")]):
+                same_stats(sts)
+                assert st["converged"] == 1 and l1(H, X) <= 1e-13 * max(1, n / 64), seed
+    src, dst, n = digen.make("c1", seed=2)
+    Ho, _, _ = oracle.di(src, dst, n, d=D, tol=1e-10, variant="sop")
+    for rt in (0, 300):
+        with di.option("dist_parts", parts), di.option("remote_tier", rt):
+            (H, F, st, sts, _), = run(src, dst, n, G, [dict(d=D, tol=1e-10, asynchronous=True)])
+        same_stats(sts)
+        assert st["converged"] == 1 and st["residual_l1"] <= 1e-10
+        assert l1(H, Ho) <= 1e-9

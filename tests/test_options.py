@@ -8,7 +8,8 @@ DEFAULTS = {"red_hint": 1, "push_occ": 4, "auto_ratio": 0.35, "stripes": 0, "hot
             "repl_share": 0.0005, "cold_bins": -1, "cold_tier": 0, "cold_shift": 0,
             "cycle_grid_div": 1, "cycle_times": 0, "p2p": 1, "p2p_force": 0, "build_trace": 0,
             "remote_compact": 1, "remote_tier": 0, "long_lanes": 1, "row_sort": 0, "line_spread": 16,
-            "warm": -1, "warm_flush": 0, "warm_shift": 0}
+            "warm": -1, "warm_flush": 0, "warm_shift": 0,
+            "dist_parts": 1}
 
 
 def test_defaults_documented_and_settable():

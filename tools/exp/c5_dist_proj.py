@@ -19,6 +19,8 @@ from paper_1204_6255_b200.dist import assemble, run_local_group
 G = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1] != "--one-gpu" else 8
 cfg = sys.argv[2] if len(sys.argv) > 2 and not sys.argv[2].startswith("--") else "c5"
 check = "--check" in sys.argv
+if "--parts" in sys.argv:
+    di.set_option("dist_parts", int(sys.argv[sys.argv.index("--parts") + 1]))
 if "--remote-tier" in sys.argv:
     di.set_option("remote_tier", int(sys.argv[sys.argv.index("--remote-tier") + 1]))
 D, TOL = 0.85, 1e-10
