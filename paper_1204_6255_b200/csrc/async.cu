@@ -7,9 +7,10 @@
 //   - CTAs take tiles of kCycTile (512) consecutive nodes in increasing order from a global
 //     counter (hub items of the hottest rows are claimed right after tile 0, see below);
 //   - a node is selected against the cycle's threshold t = r/L (r once per cycle) and
-//     its fluid is TAKEN with an atomic exchange F_i <- 0, so fluid that other CTAs push into
-//     F_i concurrently is never lost: it is either in the exchanged value or stays in F_i for
-//     the next visit (any diffusion order keeps F = B + P.H - H);
+//     the fluid f the test read is TAKEN with a RED F_i -= f, so fluid that other CTAs push into
+//     F_i concurrently is never lost: it stays in F_i for the next visit (any diffusion
+//     order keeps F = B + P.H - H); (round 1 took it with an atomic exchange F_i <- 0, which the
+//     record mode of di_test_cycle still uses);
 //   - the CTA pushes the tile's rows immediately from shared-memory lists: rows of <= 16 links
 //     a lane each (32 per warp claim), 17-256 links by 8-lane groups (front of the row list),
 //     longer rows as 1024-link chunks claimed by the CTA's warps (back of the row list).
@@ -47,6 +48,10 @@ constexpr int kCycTile = kAsyncThreads * kCycItems;   // nodes per tile
 // sequential cycle: 1024-node tiles x 4 CTAs/SM: C4 43 cycles / 60.2 ms, C2 3.6 ms; 3 CTAs/SM:
 // 42 / 58.7 ms, C2 3.2 ms; 512-node tiles (2 nodes per thread) x 4 CTAs/SM: C4 42 / 58.2 ms,
 // C3 25.8 -> 24.2 ms, C2 3.0 ms at the same per-link rate (tools/exp/async.py)
+#ifndef DI_TAKE_SUB
+#define DI_TAKE_SUB 1   // a selected node's fluid taken as F_i -= f (a RED) (0: an atomic exchange;
+                        // C4 52.8 -> 52.7 ms, C3 23.6 -> 22.9 ms: no round trip to wait for)
+#endif
 #ifndef DI_LL_BATCH
 #define DI_LL_BATCH 8     // long rows (option long_lanes): column loads in flight per lane
 #endif
@@ -496,8 +501,21 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       if (f[j] > thr) o4[j] = o;                                // strict '>'
     }
 #pragma unroll
-    for (int j = 0; j < kCycItems; j++)
+    for (int j = 0; j < kCycItems; j++) {
+#if DI_TAKE_SUB
+      // take exactly the fluid the test saw: F_i -= f (a RED, nothing to wait for); fluid that
+      // arrived since the read stays in F_i for the next visit
+      T04[j] = 0.0;
+      if (o4[j] >= 0 && !TEST) {
+        T04[j] = f[j];
+        red_add_f64(F + base + j, -f[j]);
+      } else if (o4[j] >= 0) {
+        T04[j] = take_fluid(F + base + j);
+      }
+#else
       T04[j] = (o4[j] >= 0) ? take_fluid(F + base + j) : 0.0;  // >= f[j]: only REDs add meanwhile
+#endif
+    }
 #pragma unroll
     for (int j = 0; j < kCycItems; j++) {
       if (o4[j] < 0) {
