@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
     if (threadIdx.x == 0) {
       // (option dist_parts: this launch takes the claims [claim_lo, claim_hi) of the rank's cycle)
       const int64_t c = (int64_t)atomicAdd(&sc->tile_next, 1u) + a.claim_lo;
-      int64_t tl = (a.claim_hi >= 0 && c >= a.claim_hi) ? a.ntiles : c;
+      int64_t tl = c;
       int it = -1;
       if (c > 0 && a.n_hub > 0) {  // claims 1..n_hub: hub items; then tiles 1, 2, ...
         if (c <= a.n_hub) {
@@ -416,6 +416,10 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
         } else {
           tl = c - a.n_hub;
         }
+      }
+      if (a.claim_hi >= 0 && c >= a.claim_hi) {   // past this launch's window
+        tl = a.ntiles;
+        it = -1;
       }
       if (COLD && it < 0 && tl < a.ntiles) {
         // the first-tier (hot) tiles are spread evenly over the cycle instead of all coming
