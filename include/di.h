@@ -79,7 +79,7 @@ typedef enum {
                                   DI_PROFILE; single GPU)                                        */
 #define DI_ASYNC        0x100u /* asynchronous cycles: one persistent kernel per cycle takes tiles
                                   of nodes in increasing order, selects against the cycle's r with
-                                  the live F (fluid taken by atomic exchange) and pushes at once:
+                                  the live F (the fluid read is taken by a RED F_i -= f) and pushes at once:
                                   the paper's cyclic order up to the concurrency of the
                                   grid; push only; on a partitioned graph every rank runs its
                                   range's cycle and the remote fluid is exchanged once per cycle;
