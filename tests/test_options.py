@@ -26,7 +26,9 @@ def test_defaults_documented_and_settable():
 
 
 @pytest.mark.parametrize("name,value", [("nope", 1), ("red_hint", 2), ("push_occ", 0), ("cold_bins", 3),
-                                        ("line_spread", 3), ("stripes", 1.5), ("auto_ratio", float("nan"))])
+                                        ("line_spread", 3), ("stripes", 1.5), ("auto_ratio", float("nan")),
+                                        ("warm", -2), ("warm", 70000), ("dist_parts", 0),
+                                        ("dist_parts", 65), ("warm_shift", 31)])
 def test_bad_options_refused(name, value):
     with pytest.raises(di.DIError) as ei:
         di.set_option(name, value)
