@@ -538,7 +538,9 @@ di_status build_graph(Graph &g, const int32_t *src, const int32_t *dst, int64_t 
   // in-degrees and relabels, then makes and sorts the keys of every chunk as soon as it has landed;
   // the sorted chunks are merged at the end. The PCIe copy (~55 GB/s: 39 ms for C4's 2.1 GB) then
   // hides most of the build (serial: copy, then 19 ms of relabelling, key sort and CSR).
-  const bool pipe = host && world == 1 && !rowsort && L >= kPipeMinLinks;
+  // (CUB's DeviceMerge counts are int and its output offsets overflow past 2^31 - 1 keys: longer
+  //  lists, e.g. C5's 2.16e9 links, take the one-sort path)
+  const bool pipe = host && world == 1 && !rowsort && L >= kPipeMinLinks && L <= (int64_t)INT32_MAX;
   const int64_t chunk = pipe ? (L + kPipeChunks - 1) / kPipeChunks : 0;
 
   btrace("start");
