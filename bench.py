@@ -267,7 +267,13 @@ def run_ours(args):
     sel_ms = sum(s["select_ms"] for s in pstats)
     ptot_ms = sum(ptimes)
     achieved = push_bytes / (push_ms * 1e-3) / 1e9 if push_ms > 0 else 0.0
-    tr = ncu_traffic("k_cycle" if use_async else "k_push")
+    # the instantiation this run's cycles use: the partitioned compact path (N > 1), cold bins
+    # (C5 on one GPU: F > 2 x L2), else the plain / warm-tier kernel (profiles/ncu_traffic.json keys)
+    # (template arguments LOOPS, DIST, TEST, COLD, WARM; round-1 captures carry the first four)
+    keys = ((["k_cycle<0,1,0,1,0>", "k_cycle<0,1,0,1>"] if world > 1 else
+             ["k_cycle<0,0,0,1,0>", "k_cycle<0,0,0,1>"] if 8 * n > 2 * 126 * (1 << 20) else ["k_cycle"])
+            if use_async else ["k_push"])
+    tr = next((v for v in (ncu_traffic(k) for k in keys) if v is not None), None)
     counted = sum(s["counted_bytes"] for s in stats) / world
     kname = ("k_cycle (a2-a6 fused: asynchronous select + push of one cycle)" if use_async else
              "k_push (a5: diffusion of the frontier's fluid)" if args.mode == "push" else
