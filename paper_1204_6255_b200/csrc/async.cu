@@ -215,8 +215,11 @@ __device__ __forceinline__ bool cold_put(ColdRec *const *cptr, int32_t *cnt, con
 __device__ __noinline__ void cold_retry(int nbins, ColdRec *const *cptr, int32_t *const *fptr,
                                         unsigned long long *const *tptr, int32_t *cnt,
                                         int32_t *base, int4 q, unsigned pending, unsigned bins,
-                                        double v, int lane, int32_t dec) {
-  const int32_t jj[4] = {q.x - dec, q.y - dec, q.z - dec, q.w - dec};   // (dec: column encoding)
+                                        double v, int lane, int32_t dec, int32_t cw) {
+  // the records' ids from the columns: q - dec on one GPU; partitioned, the owner-local id
+  // q - dec - owner * cw (the column encoding, dist.cu k_encode_col)
+  int32_t jj[4] = {q.x - dec, q.y - dec, q.z - dec, q.w - dec};
+  for (int c = 0; c < 4; c++) jj[c] -= (int32_t)((bins >> (6 * c)) & 63u) * cw;
   while (__any_sync(0xffffffffu, pending != 0u)) {
     cold_refill(nbins, fptr, tptr, cnt, base, lane);
     for (int c = 0; c < 4; c++)
@@ -230,16 +233,12 @@ struct ColdSm {   // the warp's chunk state and the block's per-bin pointers (sh
   ColdRec *const *cptr;
   int32_t *const *fptr;
   unsigned long long *const *tptr;
-  // partitioned: range bounds, hot-prefix sizes and accumulator offsets per owner, and the owner
-  // of every 2^oshift-id bucket (shared memory: per-lane indexed loads from the parameter block
-  // serialise in the constant cache)
-  const int64_t *b, *rt, *hoff;
-  const int8_t *otab;
-  int oshift;
+  // partitioned: a cold target's column is n + rsum + p * cw + (its id in owner p's range)
+  // (dist.cu k_encode_col): the owner is one fp32 multiply (and at most one correction) away
+  uint32_t cw;    // owner window (the largest range)
+  float cinv;     // 1 / cw
   int64_t rsum;   // hot remote slots (sum of rt)
 };
-
-constexpr int kOwnerTab = 1024;   // owner lookup buckets (partitioned COLD cycles)
 
 // COLD push of one int4 group (warp-collective: every lane calls it; `valid` = the lane has a
 // group). One GPU: hot ids to the replicated accumulators, first-tier targets (j < cold_lo) a
@@ -265,10 +264,17 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistAr
       } else if (e < (uint32_t)(a.n + cs.rsum)) {
         red_add_f64_hint(x.racc + (e - (uint32_t)a.n), v, fpol);
       } else {
-        const int32_t gj = (int32_t)(e - (uint32_t)(a.n + cs.rsum));
-        int pp = cs.otab[gj >> cs.oshift];   // owner of the bucket's first id, then forward
-        while ((int64_t)gj >= cs.b[pp + 1]) pp++;
-        if (!cold_put(cs.cptr, cs.cnt, cs.base, pp, gj, v)) {
+        const uint32_t u = e - (uint32_t)(a.n + cs.rsum);
+        int pp = (int)((float)u * cs.cinv);   // the owner, within one of the quotient
+        int32_t lj = (int32_t)(u - (uint32_t)pp * cs.cw);
+        if (lj < 0) {
+          pp--;
+          lj += (int32_t)cs.cw;
+        } else if (lj >= (int32_t)cs.cw) {
+          pp++;
+          lj -= (int32_t)cs.cw;
+        }
+        if (!cold_put(cs.cptr, cs.cnt, cs.base, pp, lj, v)) {
           pending |= 1u << c;
           bins |= (unsigned)pp << (6 * c);
         }
@@ -293,7 +299,7 @@ __device__ __forceinline__ void push_group_cold(const SweepArgs &a, const DistAr
   for (int c = 0; c < 4; c++) one(c, c == 0 ? q.x : (c == 1 ? q.y : (c == 2 ? q.z : q.w)));
   if (__any_sync(0xffffffffu, pending != 0u))
     cold_retry(DIST ? x.bd.world : a.cold_nbins, cs.cptr, cs.fptr, cs.tptr, cs.cnt, cs.base, q,
-               pending, bins, v, lane, DIST ? (int32_t)(a.n + cs.rsum) : 0);
+               pending, bins, v, lane, DIST ? (int32_t)(a.n + cs.rsum) : 0, DIST ? (int32_t)cs.cw : 0);
 }
 
 // TEST (di_test_cycle, include/di_test.h): the selection records (T, v) per node in a.rec_T /
@@ -308,10 +314,6 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   __shared__ ColdRec *s_cptr[NCB];
   __shared__ int32_t *s_fptr[NCB];
   __shared__ unsigned long long *s_tptr[NCB];
-  constexpr int NDW = (COLD && DIST) ? kMaxWorld + 1 : 1;
-  constexpr int NOT = (COLD && DIST) ? kOwnerTab + 1 : 1;
-  __shared__ int64_t s_db[NDW], s_drt[NDW], s_dhoff[NDW];
-  __shared__ int8_t s_otab[NOT];
   __shared__ int64_t s_rb[kCycTile];   // long rows of the tile: first link
   __shared__ int32_t s_ro[kCycTile];   // #links
   __shared__ double s_rv[kCycTile];    // v = T d / o
@@ -373,23 +375,6 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
       }
     }
   }
-  int oshift = 0;
-  if (COLD && DIST) {
-    const int G = x.bd.world;
-    const int64_t N = x.bd.b[G];
-    while ((N >> oshift) >= kOwnerTab) oshift++;
-    for (int k = threadIdx.x; k <= G; k += blockDim.x) {
-      s_db[k] = k < G ? x.bd.b[k] : INT64_MAX;   // b[G] = +inf: the forward scan stops there
-      s_drt[k] = k < G ? x.rt[k] : 0;
-      s_dhoff[k] = x.hoff[k];
-    }
-    for (int k = threadIdx.x; k <= kOwnerTab; k += blockDim.x) {
-      const int64_t id = (int64_t)k << oshift;
-      int p = 0;
-      while (p + 1 < G && id >= x.bd.b[p + 1]) p++;
-      s_otab[k] = (int8_t)p;
-    }
-  }
   const int nwarm = (WARM && !DIST) ? a.warm : 0;   // slots: nwarm warm-rank ids, then the hot ids
   const WarmT<WARM> wt{s_warm, nwarm > 0 ? a.warm_hot : 0, (1u << a.warm_shift) - 1u,
                  nwarm > 0 ? (uint32_t)nwarm << a.warm_shift : 0u, a.warm_shift, nwarm};
@@ -397,8 +382,8 @@ __global__ void __launch_bounds__(kAsyncThreads, DI_ASYNC_MINB) k_cycle(const Sw
   int tiles_done = 0;
   for (int k = threadIdx.x; k < nslots; k += kAsyncThreads) s_warm[k] = 0.0;   // (the loop's
                                                                                //  first barrier)
-  const ColdSm cs{ccb, cce, s_cptr, s_fptr, s_tptr, s_db, s_drt, s_dhoff, s_otab, oshift,
-                  (COLD && DIST) ? x.hoff[x.bd.world] : 0};
+  const ColdSm cs{ccb, cce, s_cptr, s_fptr, s_tptr, (COLD && DIST) ? (uint32_t)x.cwin : 1u,
+                  (COLD && DIST) ? 1.0f / (float)x.cwin : 1.0f, (COLD && DIST) ? x.hoff[x.bd.world] : 0};
   // the row's own id in the column's numbering (self-loop test): the compact path's columns are
   // encoded with local ids, the others hold global ids
   const int64_t gbase = (COLD && DIST) ? 0 : a.lo;

@@ -302,6 +302,7 @@ struct Graph {
   int64_t rtier[kMaxWorld] = {0}; // hot remote targets at the start of every range
   double *racc = nullptr;         // their accumulator, sum of rtier
   int64_t ccap = 0;               // cold records per (sender, parity) inbox region
+  int64_t cwin = 0;               // owner window of the cold-target column encoding (dist.cu)
   size_t cold_off0 = 0, fill_off0 = 0;
   unsigned long long *ctop = nullptr;
   int32_t *ccol = nullptr;        // the CSR columns encoded for the compact path (dist.cu)

@@ -346,7 +346,7 @@ __global__ void k_apply_inbox(double *__restrict__ F, int64_t lo, const char *__
          k += (int64_t)gridDim.x * blockDim.x) {
       if ((int)(k % kColdChunk) >= fill[k / kColdChunk]) continue;
       const int4 r = *reinterpret_cast<const int4 *>(rec + k);
-      red_add_f64(F + ((int64_t)r.x - lo), __hiloint2double(r.w, r.z));
+      red_add_f64(F + r.x, __hiloint2double(r.w, r.z));   // (cold records carry the local id)
     }
   }
   for (int q = 0; q < world; q++) {
@@ -538,7 +538,7 @@ __global__ void k_cold_remote_count(const int32_t *__restrict__ col, int64_t L, 
 // (R = sum of rt): the push then needs two compares, and an owner lookup only for cold targets.
 __global__ void k_encode_col(const int32_t *__restrict__ col, int64_t L, int64_t lo, int64_t n,
                              DistBounds bd, const int64_t *rt, const int64_t *hoff, int64_t R,
-                             int32_t *__restrict__ out) {
+                             int64_t W, int32_t *__restrict__ out) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < L;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = col[k];
@@ -549,7 +549,7 @@ __global__ void k_encode_col(const int32_t *__restrict__ col, int64_t L, int64_t
       int p = 0;
       while (p + 1 < bd.world && j >= bd.b[p + 1]) p++;
       const int64_t off = j - bd.b[p];
-      e = off < rt[p] ? n + hoff[p] + off : n + R + j;
+      e = off < rt[p] ? n + hoff[p] + off : n + R + p * W + off;   // (owner p, its local id)
     }
     out[k] = (int32_t)e;
   }
@@ -624,8 +624,13 @@ di_status alloc_dist(Graph &g) {
       for (int p = 0; p < G; p++)
         if (p != q) mx = std::max<int64_t>(mx, all[(size_t)q * G + p]);
     g.ccap = (mx + kColdChunk - 1) / kColdChunk * kColdChunk;
-    // the encoded columns (the encoding must fit int32: n + R + N < 2^31; the same on every rank)
-    if ((double)g.n_global + (double)rsum + (double)g.n_global >= 2147483647.0) {
+    // the encoded columns: local ids, hot remote slots, then owner windows of W = the largest
+    // range (a cold target's owner is one multiply away in k_cycle, no table lookup); the
+    // encoding must fit int32 on every rank: W + R + G W < 2^31
+    int64_t W = 1;
+    for (int p = 0; p < G; p++) W = std::max<int64_t>(W, g.bounds.b[p + 1] - g.bounds.b[p]);
+    g.cwin = W;
+    if ((double)W + (double)rsum + (double)G * (double)W >= 2147483647.0) {
       g.ccap = 0;   // no compact path on this graph
     } else {
       int64_t hoff[kMaxWorld + 1];
@@ -640,7 +645,7 @@ di_status alloc_dist(Graph &g) {
       DI_CK(cudaMemsetAsync(g.ccol + g.l, 0, 8 * 4, g.stream));
       if (g.l > 0)
         k_encode_col<<<g.num_sms * 8, 256, 0, g.stream>>>(g.col, g.l, g.lo, g.n, g.bounds, dv,
-                                                           dv + kMaxWorld + 1, rsum, g.ccol);
+                                                           dv + kMaxWorld + 1, rsum, W, g.ccol);
       DI_CK(cudaStreamSynchronize(g.stream));
       dfree(dv);
     }

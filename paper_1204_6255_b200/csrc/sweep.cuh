@@ -330,6 +330,7 @@ struct DistArgs {
   int64_t rt[kMaxWorld];
   int64_t hoff[kMaxWorld + 1];
   int64_t ccap;               // cold records per (sender, parity) region of an inbox
+  int64_t cwin;               // cold targets encoded n + sum(rt) + p * cwin + (j - b[p])
   size_t cold_off0, fill_off0;  // byte offsets of the cold regions / their chunk fills in an inbox
   unsigned long long *ctop;   // [2 * kMaxWorld] one line each
   int64_t *coldcnt;           // [world] (view into the sweep header, after sendcnt)
@@ -360,6 +361,7 @@ inline DistArgs dist_args(Graph &g) {
     x.hoff[p + 1] = x.hoff[p] + x.rt[p];
   }
   x.ccap = g.ccap;
+  x.cwin = g.cwin;
   x.cold_off0 = g.cold_off0;
   x.fill_off0 = g.fill_off0;
   x.ctop = g.ctop;
