@@ -23,6 +23,7 @@ if "--parts" in sys.argv:
     di.set_option("dist_parts", int(sys.argv[sys.argv.index("--parts") + 1]))
 if "--remote-tier" in sys.argv:
     di.set_option("remote_tier", int(sys.argv[sys.argv.index("--remote-tier") + 1]))
+ALPHA = float(sys.argv[sys.argv.index("--alpha") + 1]) if "--alpha" in sys.argv else 1.0   # F4 threshold scale
 D, TOL = 0.85, 1e-10
 n = digen.CONFIGS[cfg].n
 ranges = digen.node_ranges(n, G)
@@ -59,6 +60,8 @@ def rank(r, grp):
         torch.cuda.synchronize()
         tb = time.time() - t0
         del s, t
+        if ALPHA != 1.0:
+            gr.set_threshold_scale(ALPHA)
         st = gr.solve(d=D, tol=TOL, asynchronous=True)
         out = ((gr.lo, gr.hi), gr.history().cpu().numpy() if check else None, st, tb, gr.n_links)
         gr.free()
@@ -68,7 +71,7 @@ def rank(r, grp):
 res = run_local_group(G, rank, timeout=3000)
 st = res[0][2]
 cyc = max(1, st["sweeps"])
-print("remote_tier", di.get_option("remote_tier"))
+print("remote_tier", di.get_option("remote_tier"), "alpha", ALPHA)
 print("%s on %d emulated ranks: build %.1f s, %d cycles, %.2f eq-iter, residual %.3e, converged %d" %
       (cfg, G, max(x[3] for x in res), st["sweeps"], st["equivalent_iterations"], st["residual_l1"], st["converged"]), flush=True)
 for r, x in enumerate(res):
