@@ -12,6 +12,7 @@ import bench
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c5")
+ap.add_argument("--skip0", action="store_true", help="no GPU-drawn graph first: the host-drawn upload populates a fresh pool")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 stream = torch.cuda.current_stream(dev)
@@ -32,12 +33,13 @@ def solves(g, tag, k=2, **kw):
 
 n = digen.CONFIGS[a.config].n
 # [0] the tool's path: links drawn on the GPU
-s, d, _ = digen.make_range_gpu(a.config, 0, n)
-g = di.Graph(s, d, n)
-del s, d
-solves(g, "[0] GPU-drawn links, device upload")
-g.free()
-torch.cuda.empty_cache()
+if not a.skip0:
+    s, d, _ = digen.make_range_gpu(a.config, 0, n)
+    g = di.Graph(s, d, n)
+    del s, d
+    solves(g, "[0] GPU-drawn links, device upload")
+    g.free()
+    torch.cuda.empty_cache()
 # [1] bench.py's path: links drawn on the host, copied, device upload
 t = time.time()
 src, dst, n = digen.make(a.config, seed=1)
