@@ -198,12 +198,13 @@ def run_ours(args):
     else:
         src, dst, n, gen_s = make_graph(args.config, args.seed)
         L = len(src)
-        # Where the graph's arrays land in device memory changes the solve time by a few per cent
-        # (profiles/r2/c5_bench_vs_tool.txt, bench_spacer_ab.txt): C5 runs in 583-587 ms when the
-        # library's arrays take the lowest device addresses (links drawn on the GPU, or uploaded
-        # from the host) and in 603-624 ms with the 17.3 GB link list below them; C4 (2.1 GB of
-        # links) is 1.2 % faster the plain way. So a link list of more than 4 GiB goes above a
-        # spacer that is released before the upload; --no-spacer keeps the plain order
+        # The physical memory behind the graph's arrays changes the solve time by a few per cent
+        # (profiles/r2/c5_bench_vs_tool.txt, bench_spacer_ab.txt, placement_sweep.txt): C5 runs in
+        # 583-591 ms when the library's pool is carved from memory torch had used and released (links
+        # drawn on the GPU, or this spacer) and in 603-624 ms when it follows the 17.3 GB link list
+        # in never-used memory; C4 (2.1 GB of links) is 1.2 % faster the plain way. So a link list
+        # of more than 4 GiB is preceded by a spacer that is released before the upload;
+        # --no-spacer keeps the plain order
         spacer = None
         if not args.no_spacer and 8 * L > (4 << 30):
             spacer = torch.empty(int(torch.cuda.mem_get_info(dev)[0] * 0.5), dtype=torch.uint8, device=dev)
