@@ -172,6 +172,7 @@ def run_ours(args):
 
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
+    used_spacer = False
     if world > 1:
         # every rank draws only the links of its own source range (equal node ranges; the R-MAT
         # ids are Feistel-relabelled) on its GPU, and uploads them with DI_LOCAL_LINKS: no rank
@@ -210,6 +211,7 @@ def run_ours(args):
             spacer = torch.empty(int(torch.cuda.mem_get_info(dev)[0] * 0.5), dtype=torch.uint8, device=dev)
         s_d = torch.from_numpy(src).to(dev)
         t_d = torch.from_numpy(dst).to(dev)
+        used_spacer = spacer is not None
         if spacer is not None:
             del spacer
             torch.cuda.empty_cache()
@@ -432,7 +434,9 @@ def run_ours(args):
                                    + (", asynchronous cycles meeting every 4 (F2)" if dist_async else
                                       ", one exchange per cycle")) if world > 1
                    else "single GPU",
-                   "init_build_ms": round(init_ms, 1), "generator_s": round(gen_s, 1)},
+                   "init_build_ms": round(init_ms, 1), "generator_s": round(gen_s, 1),
+                   "link_tensors": "allocated above a spacer released before the upload" if used_spacer
+                   else "plain allocation order"},
         "time_to_tol_ms": round(ms_per_step, 3),
         "warm_ms_per_step": warm_ms,
         "sweeps": stats[-1]["sweeps"], "equivalent_iterations": round(stats[-1]["equivalent_iterations"], 2),
